@@ -1,0 +1,469 @@
+"""Plain, slow CPU oracle of NoScope's per-frame cascade and CBO threshold sweep.
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this module.  It shares no
+code with the CUDA path (paper_1703_02529_b200/) and never imports it.
+
+Each function is the plain definition written out from PAPER.md (P:n = line n
+of /root/reference/PAPER.md); where the paper is silent the reading adopted is
+SURVEY.md §8(c) O1-O10 / R-1..R-20, listed again in DESIGN.md "Readings".
+Arithmetic: integers are exact (Python/numpy int64); floating point is fp64
+unless the definition fixes another precision (the fp32 normalisation O6 and
+fp32 logit comparisons O7, the bf16 roundings of the CNN's activations).
+
+Parity status per function: every function below is
+pinned by tests/test_oracle_*.py against closed forms, library routines or
+brute force, except cnn_logits on random weights, which is pinned by closed
+forms on special weights plus an independent torch-fp64 re-derivation of the
+layer algebra (tests/test_oracle_cnn.py).
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+# Disposition codes (O4; SPEC dd_step S:227-235)
+SKIPPED, SUPPRESSED, FIRED = 0, 1, 2
+# Per-frame route codes (ABI route_out): 0 skip, 1 suppressed, 2 neg, 3 pos, 4 uncertain
+R_SKIP, R_SUPP, R_NEG, R_POS, R_UNC = 0, 1, 2, 3, 4
+
+
+# --------------------------------------------------------------------------
+# O1 Downsample — P:834-837 "resizes them for downstream processing";
+#    area averaging S:74; reading R-1 (integer box filter, round half up)
+# --------------------------------------------------------------------------
+def downsample(frames: np.ndarray, out_h: int, out_w: int) -> np.ndarray:
+    """frames uint8 [N, H, W, 3] -> uint8 [N, out_h, out_w, 3].
+
+    G[i][j][c] = floor((2*S + n) / (2*n)), S = sum of F over rows
+    [floor(iH/h), floor((i+1)H/h)) x cols [floor(jW/w), floor((j+1)W/w)),
+    n = #rows * #cols.  h > H or w > W is an error."""
+    N, H, W, C = frames.shape
+    if out_h > H or out_w > W:
+        raise ValueError("downsample target larger than source (S:75)")
+    out = np.empty((N, out_h, out_w, C), dtype=np.uint8)
+    f = frames.astype(np.int64)
+    for i in range(out_h):
+        r0, r1 = (i * H) // out_h, ((i + 1) * H) // out_h
+        for j in range(out_w):
+            q0, q1 = (j * W) // out_w, ((j + 1) * W) // out_w
+            n = (r1 - r0) * (q1 - q0)
+            S = f[:, r0:r1, q0:q1, :].sum(axis=(1, 2))          # [N, C] exact
+            out[:, i, j, :] = ((2 * S + n) // (2 * n)).astype(np.uint8)
+    return out
+
+
+# --------------------------------------------------------------------------
+# O3 Scores — P:575-585 "computes the Mean Square Error (MSE) between them";
+#    blocked: "subdivides each image into a grid and computes the metric on
+#    every grid block ... trains a logistic regression (LR) classifier to weigh
+#    each block"; readings R-2 (raw u8, all channels), R-3 (logit, no sigmoid)
+# --------------------------------------------------------------------------
+def ssd(a: np.ndarray, b: np.ndarray) -> int:
+    """Exact sum of squared differences over all elements (integer)."""
+    d = a.astype(np.int64) - b.astype(np.int64)
+    return int((d * d).sum())
+
+
+def mse(a: np.ndarray, b: np.ndarray) -> float:
+    """MSE = (double)SSD / (double)count (correctly rounded ratio)."""
+    return float(ssd(a, b)) / float(a.size)
+
+
+def block_bounds(n: int, g: int):
+    """Block k covers [k*floor(n/g), (k+1)*floor(n/g)); the last takes the
+    remainder."""
+    step = n // g
+    return [(k * step, (k + 1) * step if k < g - 1 else n) for k in range(g)]
+
+
+def blocked_mse(a: np.ndarray, b: np.ndarray, g: int) -> np.ndarray:
+    """a, b: [h, w, 3].  Returns float64 [g*g] block MSEs in row-major block order."""
+    h, w = a.shape[0], a.shape[1]
+    out = np.empty(g * g, dtype=np.float64)
+    for bi, (r0, r1) in enumerate(block_bounds(h, g)):
+        for bj, (c0, c1) in enumerate(block_bounds(w, g)):
+            blk_a, blk_b = a[r0:r1, c0:c1], b[r0:r1, c0:c1]
+            out[bi * g + bj] = float(ssd(blk_a, blk_b)) / float(blk_a.size)
+    return out
+
+
+def lr_logit(m: np.ndarray, w: np.ndarray, bias) -> float:
+    """z = b; z = z + w_k*m_k for k in order, each product and sum rounded
+    to fp64 separately (plain Python floats: no fused multiply-add)."""
+    z = float(np.float32(bias))
+    for k in range(len(m)):
+        z = z + float(np.float32(w[k])) * float(m[k])
+    return z
+
+
+def score_frame(G: np.ndarray, A: np.ndarray, metric: int, grid: int = 1,
+                lr_w=None, lr_b=0.0) -> float:
+    if metric == 0:
+        return mse(G, A)
+    return lr_logit(blocked_mse(G, A, grid), lr_w, lr_b)
+
+
+# --------------------------------------------------------------------------
+# O2/O4 Difference detector over one unit — P:554-563 (reference image / an
+#   earlier frame t_diff back), P:587-593 and P:678-679 ("fire if the frame's
+#   MSE ... is higher than delta_diff"), P:601-610 (check every t_skip frames);
+#   readings R-4 (strict >), R-8 (fixed lag k, tau<k forced fire), R-10.
+# --------------------------------------------------------------------------
+@dataclasses.dataclass
+class DDConfig:
+    mode: int = 0            # 0 reference image, 1 earlier frame t-k
+    metric: int = 0          # 0 global MSE, 1 blocked MSE + LR
+    out_w: int = 50
+    out_h: int = 50
+    grid: int = 1
+    t_diff_frames: int = 1   # k
+    t_skip_frames: int = 1
+    delta_diff: float = 0.0
+    ref_image: np.ndarray | None = None    # uint8 [out_h, out_w, 3]
+    lr_w: np.ndarray | None = None         # float32 [grid*grid]
+    lr_b: float = 0.0
+
+
+def diff_detect(small: np.ndarray, cfg: DDConfig):
+    """small: uint8 [N, h, w, 3] downsampled frames of ONE unit (tau = 0..N-1).
+
+    Returns (score float64[N], disposition uint8[N]).  Skipped frames carry
+    score -inf, forced fires (mode 1, tau < k) +inf."""
+    N = small.shape[0]
+    score = np.empty(N, dtype=np.float64)
+    disp = np.empty(N, dtype=np.uint8)
+    k = cfg.t_diff_frames
+    for tau in range(N):
+        if tau % cfg.t_skip_frames != 0:
+            score[tau], disp[tau] = -math.inf, SKIPPED
+            continue
+        if cfg.mode == 1 and tau < k:
+            score[tau], disp[tau] = math.inf, FIRED
+            continue
+        anchor = cfg.ref_image if cfg.mode == 0 else small[tau - k]
+        s = score_frame(small[tau], anchor, cfg.metric, cfg.grid, cfg.lr_w, cfg.lr_b)
+        score[tau] = s
+        disp[tau] = FIRED if s > cfg.delta_diff else SUPPRESSED
+    return score, disp
+
+
+# --------------------------------------------------------------------------
+# O5 Compaction — batches for the specialized NN
+# --------------------------------------------------------------------------
+def compact(disp: np.ndarray) -> np.ndarray:
+    """Ascending int32 indices t with disp[t] == FIRED."""
+    return np.array([t for t in range(len(disp)) if disp[t] == FIRED], dtype=np.int32)
+
+
+# --------------------------------------------------------------------------
+# O6 Specialized CNN — P:437-456 ("AlexNet ... filter doubling ... ReLU ...
+#   softmax"), P:449-453 (layers 2/4, filters 32/64, dense 32..256),
+#   P:866-869 (mean-centre, range [-1, 1]); readings R-11, R-12, R-13.
+# --------------------------------------------------------------------------
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """Round float64 values to the nearest bf16 (8 significant bits), ties to
+    even, returned as float64.  Normal range only (activations never reach
+    bf16 subnormals or overflow)."""
+    x = np.asarray(x, dtype=np.float64)
+    m, e = np.frexp(x)                      # x = m * 2^e, |m| in [0.5, 1)
+    return np.ldexp(np.rint(m * 256.0), e - 8)
+
+
+def normalize_input(G: np.ndarray, chan_mean) -> np.ndarray:
+    """x = bf16_RNE(clamp(((float)G - mu_c) / 127.5f, -1, 1)) in fp32 IEEE."""
+    g = G.astype(np.float32)
+    mu = np.asarray(chan_mean, dtype=np.float32)
+    x = (g - mu) / np.float32(127.5)
+    x = np.minimum(np.maximum(x, np.float32(-1.0)), np.float32(1.0))
+    return bf16_round(x.astype(np.float64))
+
+
+def bf16_bits_to_f64(bits) -> np.ndarray:
+    return (np.asarray(bits, dtype=np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
+
+
+def conv3x3_same(x: np.ndarray, w: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """x [n, H, W, Cin] f64, w [Cout, 3, 3, Cin] f64, b [Cout] -> [n, H, W, Cout]
+    acc = b + sum_{dy,dx,ci} w[co,dy,dx,ci] * x[y+dy-1, x+dx-1, ci] (zero pad 1),
+    accumulated in fp64 (a library matmul per tap)."""
+    n, H, W, _ = x.shape
+    xp = np.zeros((n, H + 2, W + 2, x.shape[3]), dtype=np.float64)
+    xp[:, 1:H + 1, 1:W + 1, :] = x
+    acc = np.broadcast_to(b.astype(np.float64), (n, H, W, w.shape[0])).copy()
+    for dy in range(3):
+        for dx in range(3):
+            acc += xp[:, dy:dy + H, dx:dx + W, :] @ w[:, dy, dx, :].T
+    return acc
+
+
+def maxpool2x2_floor(x: np.ndarray) -> np.ndarray:
+    """2x2 stride-2 max pool, floor (50->25->12->6->3)."""
+    n, H, W, C = x.shape
+    Ho, Wo = H // 2, W // 2
+    v = x[:, :2 * Ho, :2 * Wo, :].reshape(n, Ho, 2, Wo, 2, C)
+    return v.max(axis=(2, 4))
+
+
+def cnn_logits(small: np.ndarray, arch, weights: dict, batch: int = 256) -> np.ndarray:
+    """small uint8 [n, in_h, in_w, 3] -> fp32 logits z [n].
+
+    Per layer l: 3x3 same conv (fp64 acc + bias) -> ReLU -> 2x2 maxpool ->
+    round to bf16.  Flatten (h, w, c) -> FC1 (fp64 acc + bias) -> ReLU ->
+    bf16 -> FC2 (fp64 acc) + b2 -> z = (float)z.  c = sigmoid(z) is the
+    paper's confidence (2-class softmax == sigmoid of the logit gap)."""
+    n = small.shape[0]
+    out = np.empty(n, dtype=np.float32)
+    conv_w = [bf16_bits_to_f64(w) for w in weights["conv_w"]]
+    conv_b = [np.asarray(b, dtype=np.float32).astype(np.float64) for b in weights["conv_b"]]
+    fc1_w = bf16_bits_to_f64(weights["fc1_w"])
+    fc1_b = np.asarray(weights["fc1_b"], dtype=np.float32).astype(np.float64)
+    fc2_w = bf16_bits_to_f64(weights["fc2_w"])
+    fc2_b = float(np.asarray(weights["fc2_b"], dtype=np.float32)[0])
+    for s in range(0, n, batch):
+        x = normalize_input(small[s:s + batch], arch.chan_mean)
+        for l in range(arch.n_conv):
+            a = conv3x3_same(x, conv_w[l], conv_b[l])
+            a = np.maximum(a, 0.0)
+            x = bf16_round(maxpool2x2_floor(a))
+        f = x.reshape(x.shape[0], -1)                          # (h, w, c) order
+        h1 = bf16_round(np.maximum(f @ fc1_w.T + fc1_b, 0.0))
+        z = h1 @ fc2_w + fc2_b
+        out[s:s + batch] = z.astype(np.float32)
+    return out
+
+
+def sigmoid(z):
+    return 1.0 / (1.0 + np.exp(-np.asarray(z, dtype=np.float64)))
+
+
+# --------------------------------------------------------------------------
+# O7 Routing — P:377-380 / P:458-462: "no object" if c < c_low, "object" if
+#   c > c_high, else call the reference NN; reading R-5 (strict confident
+#   decisions, equality -> uncertain, compared on fp32 logits).
+# --------------------------------------------------------------------------
+def route(z: np.ndarray, lo: float, hi: float) -> np.ndarray:
+    if not lo <= hi:
+        raise ValueError("c_low must not exceed c_high (S:280)")
+    out = np.empty(len(z), dtype=np.uint8)
+    lo32, hi32 = np.float32(lo), np.float32(hi)
+    for i, zi in enumerate(np.asarray(z, dtype=np.float32)):
+        if zi < lo32:
+            out[i] = R_NEG
+        elif zi > hi32:
+            out[i] = R_POS
+        else:
+            out[i] = R_UNC
+    return out
+
+
+# --------------------------------------------------------------------------
+# O8 Labels — P:559-563 ("returns the same labels that it output for the
+#   previous frame"), P:554-558 (reference image contains no objects),
+#   P:601-610 (skipped frames); readings R-9, R-10.
+# --------------------------------------------------------------------------
+def resolve_labels(disp: np.ndarray, fired_route: np.ndarray, labeller: np.ndarray,
+                   mode: int, k: int, t_skip: int) -> np.ndarray:
+    """disp uint8[N]; fired_route uint8[N] (route code for fired frames, else
+    ignored); labeller uint8[N] (reference answer, read only for uncertain
+    frames).  One forward loop; every pointer is strictly backward."""
+    N = len(disp)
+    L = np.zeros(N, dtype=np.uint8)
+    for t in range(N):
+        d = disp[t]
+        if d == SKIPPED:
+            L[t] = L[t - (t % t_skip)]
+        elif d == SUPPRESSED:
+            L[t] = 0 if mode == 0 else L[t - k]
+        else:
+            r = fired_route[t]
+            L[t] = 0 if r == R_NEG else 1 if r == R_POS else labeller[t]
+    return L
+
+
+def cascade(frames_hw3: np.ndarray, cfg: DDConfig, arch, weights, lo: float, hi: float,
+            truth: np.ndarray):
+    """Whole per-unit cascade: downsample -> DD -> compaction ->
+    CNN -> routing -> stand-in labeller (ground truth) -> labels.
+
+    Returns dict with small, score, disp, idx, logits (fired only), route
+    (per-frame code), labels."""
+    small = downsample(frames_hw3, cfg.out_h, cfg.out_w)
+    score, disp = diff_detect(small, cfg)
+    idx = compact(disp)
+    z = cnn_logits(small[idx], arch, weights) if len(idx) else np.zeros(0, np.float32)
+    r_fired = route(z, lo, hi)
+    route_pf = np.where(disp == SKIPPED, R_SKIP, R_SUPP).astype(np.uint8)
+    route_pf[idx] = r_fired
+    labels = resolve_labels(disp, route_pf, truth, cfg.mode, cfg.t_diff_frames,
+                            cfg.t_skip_frames)
+    return dict(small=small, score=score, disp=disp, idx=idx, logits=z,
+                route=route_pf, labels=labels)
+
+
+# --------------------------------------------------------------------------
+# O9 CBO threshold sweep — P:627-637 (objective), P:685-701 (cost model,
+#   formula P:696), P:747-779 (sort by delta, sweep prefixes, move c_low up /
+#   c_high down until FN*/FP*); readings R-6, R-7, R-14, R-15, R-16, R-17.
+# --------------------------------------------------------------------------
+def build_records(score: np.ndarray, y: np.ndarray, mode: int, k: int):
+    """Default record builder (S:439 approximation): a_i = label the cascade
+    would inherit if frame i is not fired, computed from reference labels y:
+    skipped -> y[last checked]; mode 0 -> 0; mode 1 -> y[i-k] (0 if i<k)."""
+    N = len(score)
+    a = np.zeros(N, dtype=np.uint8)
+    last_checked = 0
+    for i in range(N):
+        if score[i] == -math.inf:
+            a[i] = y[last_checked]
+        else:
+            last_checked = i
+            a[i] = 0 if (mode == 0 or i < k) else y[i - k]
+    return a
+
+
+def sweep_tables(s, z, y, a, delta, u):
+    """Direct per-threshold counts (O9).  Returns dict of uint64 tables:
+    F[j], FPnf[j], FNnf[j], FPf[j][h], FNf[j][l], GE[j][l] = #(fired, z >= u_l),
+    GT[j][h] = #(fired, z > u_h), plus checked and total counts."""
+    s = np.asarray(s, np.float64); z = np.asarray(z, np.float32)
+    y = np.asarray(y, np.uint8); a = np.asarray(a, np.uint8)
+    nd, m = len(delta), len(u)
+    T = {k: np.zeros((nd, m), np.uint64) for k in ("FPf", "FNf", "GE", "GT")}
+    for k in ("F", "FPnf", "FNnf"):
+        T[k] = np.zeros(nd, np.uint64)
+    for j in range(nd):
+        fired = s > delta[j]
+        nf = ~fired
+        T["F"][j] = fired.sum()
+        T["FPnf"][j] = (nf & (a == 1) & (y == 0)).sum()
+        T["FNnf"][j] = (nf & (a == 0) & (y == 1)).sum()
+        for t in range(m):
+            T["FPf"][j, t] = (fired & (z > u[t]) & (y == 0)).sum()
+            T["FNf"][j, t] = (fired & (z < u[t]) & (y == 1)).sum()
+            T["GE"][j, t] = (fired & (z >= u[t])).sum()
+            T["GT"][j, t] = (fired & (z > u[t])).sum()
+    T["checked"] = int((s != -math.inf).sum())
+    T["total"] = len(s)
+    return T
+
+
+def triple_counts(T, j, l, h):
+    """FP, FN, F, U of triple (delta_j, u_l, u_h), l <= h."""
+    fp = int(T["FPnf"][j]) + int(T["FPf"][j, h])
+    fn = int(T["FNnf"][j]) + int(T["FNf"][j, l])
+    U = int(T["GE"][j, l]) - int(T["GT"][j, h])     # #(fired, u_l <= z <= u_h)
+    return fp, fn, int(T["F"][j]), U
+
+
+def cost_ps(checked, F, U, t_mse, t_snn, t_full):
+    """N x (f_s T_MSE + f_s f_m T_SNN + f_s f_m f_c T_Full) in integer
+    picoseconds: f_s = checked/N, f_s f_m = F/N, f_s f_m f_c = U/N."""
+    return checked * t_mse + F * t_snn + U * t_full
+
+
+def sweep_best(T, timing, fp_limit, fn_limit):
+    """argmin over feasible (j, l <= h) of the key (cost, U, j, -l, h); if none
+    is feasible, the best-effort triple minimising (max violation, cost, U, j,
+    -l, h) with feasible=False (R-14)."""
+    nd, m = T["FPf"].shape
+    best, best_key = None, None
+    fb, fb_key = None, None
+    for j in range(nd):
+        for l in range(m):
+            for h in range(l, m):
+                fp, fn, F, U = triple_counts(T, j, l, h)
+                c = cost_ps(T["checked"], F, U, *timing)
+                rec = dict(j=j, l=l, h=h, fp=fp, fn=fn, F=F, U=U, cost=c)
+                if fp <= fp_limit and fn <= fn_limit:
+                    key = (c, U, j, -l, h)
+                    if best_key is None or key < best_key:
+                        best, best_key = rec, key
+                else:
+                    viol = max(fp - fp_limit, fn - fn_limit, 0)
+                    key = (viol, c, U, j, -l, h)
+                    if fb_key is None or key < fb_key:
+                        fb, fb_key = rec, key
+    if best is not None:
+        best["feasible"] = True
+        return best
+    fb["feasible"] = False
+    return fb
+
+
+def sweep(s, z, y, a, delta, u, timing, fp_limit, fn_limit):
+    T = sweep_tables(s, z, y, a, delta, u)
+    return T, sweep_best(T, timing, fp_limit, fn_limit)
+
+
+def sweep_brute_force(s, z, y, a, delta, u, timing, fp_limit, fn_limit):
+    """Pure-Python brute force over ALL triples and ALL records (tiny inputs):
+    simulate the cascade per triple and count errors directly."""
+    t_mse, t_snn, t_full = timing
+    checked = sum(1 for v in s if v != -math.inf)
+    best, best_key, fb, fb_key = None, None, None, None
+    for j in range(len(delta)):
+        for l in range(len(u)):
+            for h in range(l, len(u)):
+                fp = fn = F = U = 0
+                for i in range(len(s)):
+                    if s[i] > delta[j]:
+                        F += 1
+                        zi = np.float32(z[i])
+                        if zi < u[l]:
+                            out = 0
+                        elif zi > u[h]:
+                            out = 1
+                        else:
+                            out = int(y[i]); U += 1
+                    else:
+                        out = int(a[i])
+                    fp += int(out == 1 and y[i] == 0)
+                    fn += int(out == 0 and y[i] == 1)
+                c = checked * t_mse + F * t_snn + U * t_full
+                rec = dict(j=j, l=l, h=h, fp=fp, fn=fn, F=F, U=U, cost=c)
+                if fp <= fp_limit and fn <= fn_limit:
+                    key = (c, U, j, -l, h)
+                    if best_key is None or key < best_key:
+                        best, best_key = rec, key
+                else:
+                    key = (max(fp - fp_limit, fn - fn_limit, 0), c, U, j, -l, h)
+                    if fb_key is None or key < fb_key:
+                        fb, fb_key = rec, key
+    if best is not None:
+        best["feasible"] = True
+        return best
+    fb["feasible"] = False
+    return fb
+
+
+def sweep_greedy_paper(s, z, y, a, delta, u, timing, fp_limit, fn_limit):
+    """The paper's own procedure: for each delta prefix, start with
+    thresholds at the extremes, move c_low up while FN stays within FN*, move
+    c_high down while FP stays within FP*; if they cross, meet at the candidate
+    in [h_min, l_max] minimising U (R-15).  Used as an equivalence pin."""
+    t_mse, t_snn, t_full = timing
+    T = sweep_tables(s, z, y, a, delta, u)
+    m = len(u)
+    cands = []
+    for j in range(len(delta)):
+        if T["FPnf"][j] + T["FPf"][j, m - 1] > fp_limit or T["FNnf"][j] + T["FNf"][j, 0] > fn_limit:
+            continue                                   # infeasible even at the extremes
+        l = 0
+        while l + 1 < m and int(T["FNnf"][j]) + int(T["FNf"][j, l + 1]) <= fn_limit:
+            l += 1
+        h = m - 1
+        while h - 1 >= 0 and int(T["FPnf"][j]) + int(T["FPf"][j, h - 1]) <= fp_limit:
+            h -= 1
+        if l > h:
+            best_k = min(range(h, l + 1), key=lambda t: (triple_counts(T, j, t, t)[3], -t, t))
+            l = h = best_k
+        fp, fn, F, U = triple_counts(T, j, l, h)
+        cands.append(((cost_ps(T["checked"], F, U, t_mse, t_snn, t_full), U, j, -l, h),
+                      dict(j=j, l=l, h=h, fp=fp, fn=fn, F=F, U=U,
+                           cost=cost_ps(T["checked"], F, U, t_mse, t_snn, t_full))))
+    if not cands:
+        return None
+    return min(cands, key=lambda c: c[0])[1]
