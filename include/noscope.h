@@ -1,0 +1,327 @@
+/*
+ * noscope.h — C ABI of the B200-native NoScope cascade hot path.
+ *
+ * NoScope (Kang et al., "NoScope: Optimizing Neural Network Queries over Video
+ * at Scale", arXiv 1703.02529; text at /root/reference/PAPER.md, cited P:<line>)
+ * answers a binary per-frame query ("is an object of class X visible?") by
+ * reproducing a reference network's decisions through a cascade: frame
+ * skipping and a difference detector, a specialized CNN with two
+ * confidence thresholds c_low / c_high, and the reference network
+ * only for the uncertain frames; a cost-based optimizer sweeps the thresholds
+ * (delta_diff, c_low, c_high) under FP/FN targets.
+ *
+ * This library exports that hot path as four calls (BASELINE.json north_star):
+ *   noscope_diff_detect        downsample + difference detector + compaction
+ *   noscope_specialized_infer  the specialized CNN on compacted frames
+ *   noscope_cascade_run        the whole per-frame cascade on one chunk
+ *   noscope_threshold_sweep    the CBO's (delta_diff, c_low, c_high) sweep
+ * plus small helpers (size queries, state init, routing, status strings).
+ *
+ * Conventions (all entry points)
+ *  - Pointers named *_dev / frames / small / ws / state are DEVICE pointers
+ *    (any CUDA allocation visible to the current device, e.g. the PyTorch
+ *    caching allocator); *_host pointers are host memory.  The caller owns
+ *    every buffer; the library never allocates or frees device memory and
+ *    holds no global state, so calls on different streams with distinct
+ *    workspaces/states are independent.
+ *  - Work is enqueued asynchronously on `stream` (a cudaStream_t; 0 = legacy
+ *    default stream).  Exceptions: noscope_threshold_sweep with phase 2/3 and
+ *    any call given a non-null *_host output synchronise `stream` once to copy
+ *    the result back.
+ *  - Host-side validation happens before any launch and returns
+ *    NOSCOPE_INVALID_ARGUMENT / NOSCOPE_SHAPE / NOSCOPE_WORKSPACE_TOO_SMALL
+ *    with nothing enqueued.  Launch failures return NOSCOPE_CUDA.  Errors the
+ *    device detects (NaN scores/logits) set a status word inside the workspace;
+ *    noscope_check() reads it (synchronising `stream`).
+ *  - Frames: uint8, row-major, channel-interleaved RGB (HWC, 3 channels);
+ *    frame f starts at frames + f*frame_pitch; frame_pitch is a multiple of 16
+ *    and >= round_up(width*height*3, 16).  Downsampled ("small") frames use the
+ *    same convention with small_pitch.
+ *  - Every device buffer must be 16-byte aligned.
+ *  - Requires compute capability 10.0 (B200, sm_100a); otherwise
+ *    NOSCOPE_UNSUPPORTED_DEVICE.
+ */
+#ifndef NOSCOPE_H_
+#define NOSCOPE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* noscope_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  NOSCOPE_OK = 0,
+  NOSCOPE_INVALID_ARGUMENT = 1,   /* null pointer, bad enum, unsorted/duplicate candidates, lo > hi */
+  NOSCOPE_SHAPE = 2,              /* downsample target > source, pitch not /16, grid > dims */
+  NOSCOPE_WORKSPACE_TOO_SMALL = 3,
+  NOSCOPE_CUDA = 4,               /* launch / runtime error */
+  NOSCOPE_UNSUPPORTED_DEVICE = 5, /* not compute capability 10.0 */
+  NOSCOPE_DATA = 6,               /* NaN score or logit detected on device */
+  NOSCOPE_INFEASIBLE = 7,         /* sweep: no triple meets FP* and FN*; best-effort result written */
+  NOSCOPE_LABELLER = 8            /* labeller callback returned nonzero */
+} noscope_status;
+
+const char* noscope_status_string(noscope_status s);
+/* Library version, e.g. 100 = 0.1.0. */
+int32_t noscope_version(void);
+
+/* ---------------------------------------------------------------- frames */
+typedef struct {
+  int32_t width;        /* source W (pixels) */
+  int32_t height;       /* source H (pixels) */
+  int64_t frame_pitch;  /* bytes between frames, multiple of 16 */
+} noscope_frames_desc;
+
+/* ------------------------------------------------------ difference detector
+ * PAPER.md §5.  Modes: "difference detection against a fixed
+ * reference image ... that contains no objects" or "against an
+ * earlier frame a pre-configured time t_diff seconds into the past",
+ * here a fixed lag of k = t_diff_frames frames (reading R-8).  Metric: MSE over
+ * the whole image, or "a blocked comparison where it subdivides each image into
+ * a grid and computes the metric on every grid block" weighted by a logistic
+ * regression; the blocked score is the LR logit (reading R-3).
+ * A frame at unit position tau is checked iff tau % t_skip_frames == 0
+ * (R-10); it fires iff score > delta_diff (strict, R-4);
+ * in mode 1 the first k checked frames of a unit (tau < k) fire unconditionally.
+ * Before scoring, every needed frame is downsampled by the integer box filter
+ * G[i][j][c] = floor((2S + n) / 2n) over source rows [floor(iH/h), floor((i+1)H/h))
+ * and columns [floor(jW/w), floor((j+1)W/w)) (reading R-1); the same
+ * out_w x out_h frames feed the CNN.
+ * Scores are fp64: global = (double)SSD / (double)(out_w*out_h*3) where SSD is
+ * the exact integer sum of squared u8 differences; blocked: blocks of
+ * floor(out/g) rows/cols (last block takes the remainder), m_k = SSD_k / n_k,
+ * z = b + sum_k w_k * m_k evaluated in block order with separate fp64 rounding
+ * of every product and sum (no FMA).  Skipped frames get score -inf, forced
+ * fires +inf.                                                               */
+typedef struct {
+  int32_t mode;           /* 0 = reference image, 1 = earlier frame t-k */
+  int32_t metric;         /* 0 = global MSE, 1 = blocked MSE + LR */
+  int32_t out_w, out_h;   /* downsample target (<= source), e.g. 50 x 50 */
+  int32_t grid;           /* g for metric 1: 1 <= g <= min(out_w, out_h) */
+  int32_t t_diff_frames;  /* k >= 1 (mode 1) */
+  int32_t t_skip_frames;  /* >= 1 */
+  int32_t reserved;
+  double delta_diff;      /* firing threshold (MSE units, or LR logit) ; +-inf allowed */
+  const uint8_t* ref_image;   /* device, out_h*out_w*3 u8 HWC (mode 0) */
+  const float* lr_weights;    /* device, grid*grid fp32, row-major block order (metric 1) */
+  float lr_bias;
+  float reserved2;
+} noscope_dd_config;
+
+/* Disposition codes written per frame by noscope_diff_detect. */
+enum { NOSCOPE_SKIPPED = 0, NOSCOPE_SUPPRESSED = 1, NOSCOPE_FIRED = 2 };
+
+/* ------------------------------------------------------- specialized CNN
+ * PAPER.md §4: shallow AlexNet-style network, "number of
+ * convolutional layers (2 or 4), number of convolution units in the base layer
+ * (32 or 64), and number of neurons in the dense layer", ReLU
+ * hidden units, softmax output (two-class softmax == sigmoid of one logit).
+ * Per layer l = 1..n_conv: 3x3 conv, stride 1, zero pad 1, Cout = base*2^(l-1)
+ * ("filter doubling"), + bias, ReLU, 2x2/2 max pool (floor); flatten
+ * (h, w, c); FC(dense) + bias + ReLU; FC(1) + bias -> logit z (reading R-12).
+ * Input: x = bf16_RNE(clamp(((float)G - chan_mean[c]) / 127.5f, -1, 1))
+ * ("mean-center the pixel values and change the dynamic range in each color
+ * channel to [-1, 1]", reading R-13).  Operands bf16, accumulation
+ * fp32 (tensor cores), activations rounded to bf16 after each pool / FC1.
+ * Supported: n_conv in {2,4}, base_filters in {32,64}, dense in {32,64,128,256},
+ * in_w = in_h = 50.                                                          */
+typedef struct {
+  int32_t n_conv, base_filters, dense, in_w, in_h;
+  float chan_mean[3];
+} noscope_cnn_arch;
+
+/* Weight tensors (device).  bf16 = IEEE bfloat16 bit patterns (uint16).
+ *   conv_w[l]: bf16 [Cout][3][3][Cin]      conv_b[l]: fp32 [Cout]
+ *   fc1_w:     bf16 [dense][K], K = (h,w,c) of the last pooled map
+ *   fc1_b:     fp32 [dense]   fc2_w: bf16 [dense]   fc2_b: fp32 [1]          */
+typedef struct {
+  const uint16_t* conv_w[4];
+  const float* conv_b[4];
+  const uint16_t* fc1_w;
+  const float* fc1_b;
+  const uint16_t* fc2_w;
+  const float* fc2_b;
+} noscope_cnn_weights;
+
+/* ------------------------------------------------------------- routing
+ * "no object" if c < c_low, "object" if c > c_high,
+ * otherwise call the reference NN.  Compared on fp32 logits (c = sigmoid(z));
+ * equality defers to the reference (reading R-5); lo <= hi; +-inf allowed.  */
+typedef struct {
+  float lo_logit;   /* logit(c_low)  */
+  float hi_logit;   /* logit(c_high) */
+} noscope_route;
+
+/* Per-frame route codes written by noscope_cascade_run / noscope_route_logits. */
+enum { NOSCOPE_R_SKIP = 0, NOSCOPE_R_SUPP = 1, NOSCOPE_R_NEG = 2, NOSCOPE_R_POS = 3, NOSCOPE_R_UNC = 4 };
+
+/* Reference-network stand-in.  Called once per cascade chunk on the
+ * uncertain frames: idx_dev[i] (i < *n_dev, device count, <= n_max) are chunk
+ * frame indices; the callee writes answers_dev[i] in {0,1} for frame
+ * frame_index_base + idx_dev[i], enqueued on `stream`.  Return 0 on success. */
+typedef int (*noscope_labeller_fn)(void* user, const int32_t* idx_dev, const int64_t* n_dev,
+                                   int64_t n_max, int64_t frame_index_base,
+                                   uint8_t* answers_dev, noscope_stream_t stream);
+
+typedef struct {
+  int64_t n_frames, n_skipped, n_suppressed, n_fired, n_neg, n_pos, n_uncertain;
+} noscope_run_stats;
+
+/* ------------------------------------------------------------ size queries */
+typedef enum {
+  NOSCOPE_OP_DIFF_DETECT = 0,
+  NOSCOPE_OP_SPECIALIZED_INFER = 1,
+  NOSCOPE_OP_CASCADE_RUN = 2,
+  NOSCOPE_OP_THRESHOLD_SWEEP = 3
+} noscope_op;
+
+/* Workspace bytes for `op` on up to n_frames frames (sweep: n_delta, m
+ * candidates; other ops ignore them).  arch may be null for ops without the
+ * CNN; dd may be null for ops without the detector.  0 on invalid input.  */
+size_t noscope_workspace_bytes(noscope_op op, const noscope_dd_config* dd,
+                               const noscope_cnn_arch* arch, int64_t n_frames,
+                               int32_t n_delta, int32_t m);
+
+/* Per-stream carried state for chunked processing of one unit: the last k
+ * downsampled frames (mode 1 anchors across chunk boundaries) and the last
+ * max(k, t_skip) emitted labels.  Device memory, caller-owned.               */
+size_t noscope_stream_state_bytes(const noscope_dd_config* dd);
+/* Zeroes the state (call once per unit before its first chunk). */
+noscope_status noscope_stream_state_init(const noscope_dd_config* dd, void* state_dev,
+                                         noscope_stream_t stream);
+
+/* ---------------------------------------------------------- entry points */
+
+/* Downsample + difference detector + stable compaction over frames
+ * [seg_offset, seg_offset + n_frames) of one unit.
+ *  frames:        device, n_frames frames described by `desc`.
+ *  seg_offset:    tau of frames[0] within its unit (>= 0).
+ *  stream_state:  nullable; if non-null it supplies the anchors of frames whose
+ *                 t-k lies before seg_offset (mode 1) and is updated with this
+ *                 chunk's last frames.  Required in mode 1 when seg_offset > 0.
+ *  small_out:     device [n_frames][small_pitch] u8; rows of frames that are
+ *                 neither checked nor a future anchor are left unwritten.
+ *  score_out:     device fp64 [n_frames] (nullable).
+ *  disposition_out: device u8 [n_frames] NOSCOPE_SKIPPED/SUPPRESSED/FIRED.
+ *  fired_idx_out: device i32 [n_frames] (nullable): ascending indices (into
+ *                 this chunk) of fired frames; n_fired_dev: device i64 count.
+ *  Errors: NOSCOPE_SHAPE if out_w > width or out_h > height or pitches not /16.  */
+noscope_status noscope_diff_detect(const noscope_dd_config* dd, const uint8_t* frames,
+                                   noscope_frames_desc desc, int64_t n_frames,
+                                   int64_t seg_offset, void* stream_state,
+                                   uint8_t* small_out, int64_t small_pitch, double* score_out,
+                                   uint8_t* disposition_out, int32_t* fired_idx_out,
+                                   int64_t* n_fired_dev, void* ws, size_t ws_bytes,
+                                   noscope_stream_t stream);
+
+/* Specialized CNN logits for frames small[idx[i]] (i < n).
+ *  small_frames: device u8 [*][small_pitch], each in_h x in_w x 3.
+ *  idx:          device i32 (nullable: dense 0..n-1).
+ *  n_dev:        device i64 count (nullable: n = n_max); must be <= n_max.
+ *  logits_out:   device fp32 [n_max]; entries >= n are left unwritten.      */
+noscope_status noscope_specialized_infer(const noscope_cnn_arch* arch,
+                                         const noscope_cnn_weights* weights,
+                                         const uint8_t* small_frames, int64_t small_pitch,
+                                         const int32_t* idx, const int64_t* n_dev, int64_t n_max,
+                                         float* logits_out, void* ws, size_t ws_bytes,
+                                         noscope_stream_t stream);
+
+/* Routing helper: route_out[i] = NEG/POS/UNC of logits[i] for i < *n_dev
+ * (or n_max), and the stable list of uncertain positions + count.         */
+noscope_status noscope_route_logits(noscope_route r, const float* logits, const int64_t* n_dev,
+                                    int64_t n_max, uint8_t* route_out, int32_t* unc_idx_out,
+                                    int64_t* n_unc_dev, noscope_stream_t stream);
+
+/* The whole cascade on one chunk of one unit:
+ * diff_detect -> compaction -> specialized CNN on fired frames -> routing ->
+ * labeller on uncertain frames -> per-frame labels:
+ *   skipped:    label of the unit's last checked frame (tau - tau % t_skip)
+ *   suppressed: 0 in mode 0 (the reference image "contains no objects",
+ *               P:555); the label emitted for frame tau-k in mode 1 ("returns
+ *               the same labels that it output for the previous frame")
+ *   fired:      NEG -> 0, POS -> 1, UNC -> labeller answer.
+ *  labels_out: device u8 [n_frames]; route_out: device u8 [n_frames] route
+ *  codes (nullable); logits_out: device fp32 [n_frames] (nullable; written
+ *  for fired frames only); scores_out: device fp64 [n_frames] (nullable).
+ *  stream_state is required (init once per unit).  stats_host (nullable)
+ *  triggers one synchronisation to copy counts back.                        */
+noscope_status noscope_cascade_run(const noscope_dd_config* dd, const noscope_cnn_arch* arch,
+                                   const noscope_cnn_weights* weights, noscope_route route,
+                                   const uint8_t* frames, noscope_frames_desc desc,
+                                   int64_t n_frames, int64_t seg_offset,
+                                   int64_t frame_index_base, void* stream_state,
+                                   noscope_labeller_fn labeller, void* labeller_user,
+                                   uint8_t* labels_out, uint8_t* route_out, float* logits_out,
+                                   double* scores_out, noscope_run_stats* stats_host,
+                                   void* ws, size_t ws_bytes, noscope_stream_t stream);
+
+/* Same as noscope_cascade_run, plus device-time stage breakdown (CUDA events on
+ * `stream`, synchronises once): stage_ms_host[7] = ms of 0 downsample(+mode-0
+ * score) kernel, 1 mode-1 lag-score kernel, 2 compaction, 3 CNN, 4 routing,
+ * 5 labeller, 6 label resolution + state update.                            */
+noscope_status noscope_cascade_run_profiled(
+    const noscope_dd_config* dd, const noscope_cnn_arch* arch, const noscope_cnn_weights* weights,
+    noscope_route route, const uint8_t* frames, noscope_frames_desc desc, int64_t n_frames,
+    int64_t seg_offset, int64_t frame_index_base, void* stream_state, noscope_labeller_fn labeller,
+    void* labeller_user, uint8_t* labels_out, uint8_t* route_out, float* logits_out,
+    double* scores_out, noscope_run_stats* stats_host, void* ws, size_t ws_bytes,
+    noscope_stream_t stream, float* stage_ms_host);
+
+/* Number of kernels this library has launched from the calling host thread
+ * (diagnostic; used by bench.py's gpu_launches).                           */
+uint64_t noscope_launch_count(void);
+
+/* --------------------------------------------------------- threshold sweep
+ * PAPER.md §6 (P:627-637 objective; P:685-701 cost model
+ * E[t/frame] = f_s T_MSE + f_s f_m T_SNN + f_s f_m f_c T_Full; P:747-779 sweep).
+ * Records i < n: s[i] fp64 DD score (-inf = skipped frame), z[i] fp32 CNN
+ * logit, y[i] reference label, a[i] label inherited when not fired.
+ * Candidates: delta_cand (n_delta, fp64, strictly ascending), logit_cand (m,
+ * fp32, strictly ascending, +-inf allowed).  For each (j, l <= h):
+ *   fired = s > delta_j;  FP = #(!fired & a=1 & y=0) + #(fired & z > u_h & y=0)
+ *   FN = #(!fired & a=0 & y=1) + #(fired & z < u_l & y=1);  F = #fired
+ *   U = #(fired & u_l <= z <= u_h);  cost = C*t_mse + F*t_snn + U*t_full (ps,
+ *   C = #checked records) == N x the paper's formula;  feasible iff FP <=
+ *   fp_limit and FN <= fn_limit.  best = argmin over feasible triples of
+ *   (cost, U, j, -l, h); if none, NOSCOPE_INFEASIBLE and the triple minimising
+ *   (max(FP-fp_limit, FN-fn_limit), cost, U, j, -l, h).
+ * phase 1 ACCUMULATES the local records into `hist` (caller zeroes it first;
+ * size noscope_sweep_hist_words(n_delta, m) uint64); the caller may sum `hist`
+ * across GPUs (e.g. ncclAllReduce) before phase 2, which evaluates it.
+ * phase 3 = 1 then 2.                                                        */
+typedef struct { uint64_t t_mse_ps, t_snn_ps, t_full_ps; } noscope_timing;
+typedef struct {
+  int32_t j, l, h, feasible;
+  uint64_t cost_ps, fp, fn, fired, uncertain, checked, total;
+  double delta;
+  float lo_logit, hi_logit;
+} noscope_sweep_best;
+/* Optional device tables (each uint64, row-major): F[n_delta], FPnf[n_delta],
+ * FNnf[n_delta], FPf[n_delta][m], FNf[n_delta][m], GE[n_delta][m] =
+ * #(fired & z >= u), GT[n_delta][m] = #(fired & z > u).                    */
+typedef struct {
+  uint64_t *F, *FPnf, *FNnf, *FPf, *FNf, *GE, *GT;
+} noscope_sweep_tables;
+
+size_t noscope_sweep_hist_words(int32_t n_delta, int32_t m);
+
+noscope_status noscope_threshold_sweep(int32_t phase, const double* s, const float* z,
+                                       const uint8_t* y, const uint8_t* a, int64_t n,
+                                       const double* delta_cand, int32_t n_delta,
+                                       const float* logit_cand, int32_t m, uint64_t* hist,
+                                       const noscope_timing* timing, uint64_t fp_limit,
+                                       uint64_t fn_limit, const noscope_sweep_tables* tables_dev,
+                                       noscope_sweep_best* best_host, void* ws, size_t ws_bytes,
+                                       noscope_stream_t stream);
+
+/* Reads and clears the device status word in a workspace (synchronises). */
+noscope_status noscope_check(void* ws, noscope_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NOSCOPE_H_ */

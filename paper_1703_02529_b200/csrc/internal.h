@@ -1,0 +1,127 @@
+// internal.h — host/device declarations shared by the NoScope CUDA sources.
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/noscope.h"
+
+namespace ns {
+
+constexpr int kMaxGrid = 16;      // blocked-DD grid side limit (g*g <= 256 blocks)
+constexpr int kMaxOutW = 85;      // out_w*3 <= 256 threads own one output column each
+
+// Optional stage timing (noscope_cascade_run_profiled) and launch counting.
+struct Prof {
+  cudaEvent_t ev[16];
+  int n;
+};
+inline void prof_mark(Prof* p, cudaStream_t st) {
+  if (p && p->n < 16) cudaEventRecord(p->ev[p->n++], st);
+}
+uint64_t& launch_counter();  // kernels launched by the calling host thread
+inline void count_launch(int k = 1) { launch_counter() += (uint64_t)k; }
+
+struct DsGeom {
+  int out_w, out_h, metric, grid;
+  const float* lr_w;
+  float lr_b;
+  double delta;
+};
+
+// Frames that must be downsampled: checked frames (tau % t_skip == 0) and,
+// in mode 1, anchors of checked frames ((tau + k) % t_skip == 0).  Ordinals
+// m enumerate them in tau order: tau = (m / nres) * t_skip + res[m % nres].
+struct NeededSet {
+  int64_t m0, m1, tau0;
+  int t_skip, nres;
+  int res[2];
+  __host__ __device__ int64_t frame_of(int64_t m) const {
+    int64_t p = m / nres;
+    return p * t_skip + res[m - p * nres] - tau0;
+  }
+};
+
+inline int64_t needed_count(const NeededSet& s, int64_t x) {  // # needed tau in [0, x)
+  int64_t c = 0;
+  for (int r = 0; r < s.nres; ++r)
+    if (x > s.res[r]) c += (x - s.res[r] + s.t_skip - 1) / s.t_skip;
+  return c;
+}
+
+inline NeededSet make_needed_set(const noscope_dd_config& cfg, int64_t tau0, int64_t n) {
+  NeededSet s{};
+  s.t_skip = cfg.t_skip_frames;
+  s.tau0 = tau0;
+  s.res[0] = 0;
+  s.nres = 1;
+  if (cfg.mode == 1) {
+    int r = (int)((s.t_skip - (cfg.t_diff_frames % s.t_skip)) % s.t_skip);
+    if (r != 0) {
+      s.res[1] = r;
+      s.nres = 2;
+    }
+  }
+  s.m0 = needed_count(s, tau0);
+  s.m1 = needed_count(s, tau0 + n);
+  return s;
+}
+
+inline int64_t small_bytes_of(const noscope_dd_config& c) { return (int64_t)c.out_w * c.out_h * 3; }
+inline int64_t state_ring_pitch(const noscope_dd_config& c) { return (small_bytes_of(c) + 15) & ~15ll; }
+inline int64_t state_ring_bytes(const noscope_dd_config& c) {
+  return c.mode == 1 ? (int64_t)c.t_diff_frames * state_ring_pitch(c) : 0;
+}
+inline int state_label_len(const noscope_dd_config& c) {
+  const int ts = c.t_skip_frames;
+  if (c.mode != 1) return ts;
+  const int K = (c.t_diff_frames + ts - 1) / ts;
+  return (K + 1) * ts;
+}
+
+// ---- launchers (all asynchronous on `st`)
+noscope_status launch_diff_detect(const noscope_dd_config& cfg, const uint8_t* frames,
+                                  const noscope_frames_desc& desc, int64_t n, int64_t tau0,
+                                  uint8_t* state, uint8_t* small, int64_t small_pitch,
+                                  double* score, uint8_t* disp, uint32_t* status,
+                                  cudaStream_t st, Prof* prof = nullptr);
+noscope_status launch_state_update(const noscope_dd_config& cfg, const uint8_t* small,
+                                   int64_t small_pitch, uint8_t* state, int64_t tau0, int64_t n,
+                                   const uint8_t* labels, cudaStream_t st);
+
+// Stable compaction of fired frames (+ fills skipped frames' disposition/score).
+size_t compact_ws_bytes(int64_t n);
+noscope_status launch_compact_fired(const uint8_t* disp_in, uint8_t* disp, double* score,
+                                    int64_t n, int64_t tau0, int t_skip, int32_t* idx_out,
+                                    int64_t* count_out, void* scan_ws, cudaStream_t st);
+// Routing of compacted logits + compaction of uncertain ones.
+noscope_status launch_route(noscope_route r, const float* logits, const int64_t* n_dev,
+                            int64_t n_max, const int32_t* frame_idx, uint8_t* route_out,
+                            uint8_t* route_pf, int32_t* unc_out, int64_t* n_unc,
+                            int32_t* unc_pos_pf, float* logits_pf, uint64_t* counters,
+                            void* scan_ws, uint32_t* status, cudaStream_t st);
+// Label resolution for one chunk.
+size_t labels_ws_bytes(int64_t n);
+noscope_status launch_labels(const noscope_dd_config& cfg, int64_t tau0, int64_t n,
+                             const uint8_t* disp, const uint8_t* route_pf,
+                             const int32_t* unc_pos_pf, const uint8_t* answers,
+                             const uint8_t* lab_hist, uint8_t* labels, uint8_t* route_out,
+                             void* lws, cudaStream_t st);
+
+// Specialized CNN.
+size_t cnn_ws_bytes(const noscope_cnn_arch& a, int64_t n_max);
+noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& w,
+                          const uint8_t* small, int64_t small_pitch, const int32_t* idx,
+                          const int64_t* n_dev, int64_t n_max, float* logits, void* ws,
+                          uint32_t* status, cudaStream_t st);
+
+// Threshold sweep.
+size_t sweep_ws_bytes(int32_t n_delta, int32_t m);
+noscope_status launch_sweep(int32_t phase, const double* s, const float* z, const uint8_t* y,
+                            const uint8_t* a, int64_t n, const double* delta, int32_t nd,
+                            const float* u, int32_t m, uint64_t* hist, const noscope_timing& t,
+                            uint64_t fp_limit, uint64_t fn_limit,
+                            const noscope_sweep_tables* tables, noscope_sweep_best* best_host,
+                            void* ws, cudaStream_t st, bool* infeasible);
+
+}  // namespace ns

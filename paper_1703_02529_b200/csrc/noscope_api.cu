@@ -1,0 +1,441 @@
+// noscope_api.cu — the C ABI (include/noscope.h): host-side validation,
+// workspace carving and launch sequencing.  No torch types cross this boundary.
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace ns {
+bool cnn_arch_supported(const noscope_cnn_arch& a);
+bool cnn_debug_layout(const noscope_cnn_arch& a, int64_t n_max, int64_t* out);
+}  // namespace ns
+
+using namespace ns;
+
+namespace {
+
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+noscope_status check_device() {
+  static int cached = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return NOSCOPE_CUDA;
+  if (cached < 0) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return NOSCOPE_CUDA;
+    cached = (p.major == 10 && p.minor == 0) ? 1 : 0;
+  }
+  return cached ? NOSCOPE_OK : NOSCOPE_UNSUPPORTED_DEVICE;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+noscope_status validate_dd(const noscope_dd_config* c, bool check_ptrs = true) {
+  if (!c) return NOSCOPE_INVALID_ARGUMENT;
+  if (c->mode != 0 && c->mode != 1) return NOSCOPE_INVALID_ARGUMENT;
+  if (c->metric != 0 && c->metric != 1) return NOSCOPE_INVALID_ARGUMENT;
+  if (c->out_w < 1 || c->out_h < 1 || c->out_w > kMaxOutW) return NOSCOPE_SHAPE;
+  if (c->t_skip_frames < 1) return NOSCOPE_INVALID_ARGUMENT;
+  if (c->mode == 1 && c->t_diff_frames < 1) return NOSCOPE_INVALID_ARGUMENT;
+  if (check_ptrs && c->mode == 0 && !c->ref_image) return NOSCOPE_INVALID_ARGUMENT;
+  if (c->metric == 1) {
+    if (c->grid < 1 || c->grid > kMaxGrid || c->grid > c->out_w || c->grid > c->out_h)
+      return NOSCOPE_SHAPE;
+    if (check_ptrs && !c->lr_weights) return NOSCOPE_INVALID_ARGUMENT;
+  }
+  if (std::isnan(c->delta_diff)) return NOSCOPE_INVALID_ARGUMENT;
+  return NOSCOPE_OK;
+}
+
+noscope_status validate_frames(const noscope_dd_config* c, const noscope_frames_desc& d) {
+  if (d.width < 1 || d.height < 1) return NOSCOPE_SHAPE;
+  if (c->out_w > d.width || c->out_h > d.height) return NOSCOPE_SHAPE;
+  if (d.frame_pitch % 16 != 0 || d.frame_pitch < (((int64_t)d.width * d.height * 3 + 15) & ~15ll))
+    return NOSCOPE_SHAPE;
+  // vertical box height must fit the 16-bit SWAR lanes (<= 257 rows of 255)
+  if ((d.height + c->out_h - 1) / c->out_h > 257) return NOSCOPE_SHAPE;
+  if ((int64_t)d.width * 3 > 200 * 1024 / 4) return NOSCOPE_SHAPE;
+  return NOSCOPE_OK;
+}
+
+noscope_status validate_arch(const noscope_cnn_arch* a, const noscope_cnn_weights* w) {
+  if (!a || !w) return NOSCOPE_INVALID_ARGUMENT;
+  if (!cnn_arch_supported(*a)) return NOSCOPE_SHAPE;
+  for (int l = 0; l < a->n_conv; ++l)
+    if (!w->conv_w[l] || !w->conv_b[l]) return NOSCOPE_INVALID_ARGUMENT;
+  if (!w->fc1_w || !w->fc1_b || !w->fc2_w || !w->fc2_b) return NOSCOPE_INVALID_ARGUMENT;
+  return NOSCOPE_OK;
+}
+
+// ---- workspace layouts
+struct DDWs {
+  size_t status, scan, score, total;
+};
+DDWs dd_ws(int64_t n) {
+  DDWs w{};
+  w.status = 0;
+  w.scan = 256;
+  w.score = w.scan + align256(compact_ws_bytes(n));
+  w.total = w.score + align256((size_t)n * 8);
+  return w;
+}
+
+struct CascadeWs {
+  size_t status, scan, small, score, disp, idx, nfired, logits, route_pf, unc, nunc, unc_pos,
+      answers, counters, lab, cnn, total;
+  int64_t small_pitch;
+};
+CascadeWs cascade_ws(const noscope_dd_config* dd, const noscope_cnn_arch* a, int64_t n) {
+  CascadeWs w{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = off;
+    off = align256(off + bytes);
+    return r;
+  };
+  w.small_pitch = (small_bytes_of(*dd) + 15) & ~15ll;
+  w.status = take(256);
+  w.scan = take(compact_ws_bytes(n));
+  w.small = take((size_t)n * w.small_pitch);
+  w.score = take((size_t)n * 8);
+  w.disp = take((size_t)n);
+  w.idx = take((size_t)n * 4);
+  w.nfired = take(8);
+  w.logits = take((size_t)n * 4);
+  w.route_pf = take((size_t)n);
+  w.unc = take((size_t)n * 4);
+  w.nunc = take(8);
+  w.unc_pos = take((size_t)n * 4);
+  w.answers = take((size_t)n);
+  w.counters = take(64);
+  w.lab = take(labels_ws_bytes(n));
+  w.cnn = off;
+  off += a ? cnn_ws_bytes(*a, n) : 0;
+  w.total = align256(off);
+  return w;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* noscope_status_string(noscope_status s) {
+  switch (s) {
+    case NOSCOPE_OK: return "ok";
+    case NOSCOPE_INVALID_ARGUMENT: return "invalid argument";
+    case NOSCOPE_SHAPE: return "shape error";
+    case NOSCOPE_WORKSPACE_TOO_SMALL: return "workspace too small";
+    case NOSCOPE_CUDA: return "CUDA error";
+    case NOSCOPE_UNSUPPORTED_DEVICE: return "unsupported device (needs sm_100a / B200)";
+    case NOSCOPE_DATA: return "NaN score or logit";
+    case NOSCOPE_INFEASIBLE: return "no feasible threshold triple";
+    case NOSCOPE_LABELLER: return "labeller callback failed";
+  }
+  return "unknown status";
+}
+
+int32_t noscope_version(void) { return 100; }
+
+size_t noscope_stream_state_bytes(const noscope_dd_config* dd) {
+  if (validate_dd(dd, false) != NOSCOPE_OK) return 0;
+  return (size_t)align256(state_ring_bytes(*dd) + state_label_len(*dd));
+}
+
+noscope_status noscope_stream_state_init(const noscope_dd_config* dd, void* state,
+                                         noscope_stream_t stream) {
+  noscope_status s = validate_dd(dd, false);
+  if (s != NOSCOPE_OK) return s;
+  if (!state) return NOSCOPE_INVALID_ARGUMENT;
+  if ((s = check_device()) != NOSCOPE_OK) return s;
+  NS_CUDA_TRY(cudaMemsetAsync(state, 0, noscope_stream_state_bytes(dd), (cudaStream_t)stream));
+  return NOSCOPE_OK;
+}
+
+size_t noscope_sweep_hist_words(int32_t nd, int32_t m) {
+  if (nd < 1 || m < 1) return 0;
+  return (size_t)(nd + 1) * (2 * m + 1) * 2 + (size_t)(nd + 1) * 4 + 2;
+}
+
+size_t noscope_workspace_bytes(noscope_op op, const noscope_dd_config* dd,
+                               const noscope_cnn_arch* arch, int64_t n, int32_t nd, int32_t m) {
+  if (n < 0) return 0;
+  switch (op) {
+    case NOSCOPE_OP_DIFF_DETECT:
+      return dd_ws(n).total;
+    case NOSCOPE_OP_SPECIALIZED_INFER:
+      if (!arch || !cnn_arch_supported(*arch)) return 0;
+      return 256 + cnn_ws_bytes(*arch, n);
+    case NOSCOPE_OP_CASCADE_RUN:
+      if (!arch || !dd || validate_dd(dd, false) != NOSCOPE_OK || !cnn_arch_supported(*arch))
+        return 0;
+      return cascade_ws(dd, arch, n).total;
+    case NOSCOPE_OP_THRESHOLD_SWEEP:
+      if (nd < 1 || m < 1) return 0;
+      return sweep_ws_bytes(nd, m);
+  }
+  return 0;
+}
+
+noscope_status noscope_check(void* ws, noscope_stream_t stream) {
+  if (!ws) return NOSCOPE_INVALID_ARGUMENT;
+  uint32_t st = 0;
+  NS_CUDA_TRY(cudaMemcpyAsync(&st, ws, 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  NS_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  NS_CUDA_TRY(cudaMemsetAsync(ws, 0, 4, (cudaStream_t)stream));
+  return st ? NOSCOPE_DATA : NOSCOPE_OK;
+}
+
+noscope_status noscope_diff_detect(const noscope_dd_config* dd, const uint8_t* frames,
+                                   noscope_frames_desc desc, int64_t n, int64_t seg_offset,
+                                   void* state, uint8_t* small_out, int64_t small_pitch,
+                                   double* score_out, uint8_t* disp_out, int32_t* fired_idx_out,
+                                   int64_t* n_fired_dev, void* ws, size_t ws_bytes,
+                                   noscope_stream_t stream) {
+  noscope_status s = validate_dd(dd);
+  if (s != NOSCOPE_OK) return s;
+  if ((s = validate_frames(dd, desc)) != NOSCOPE_OK) return s;
+  if (n < 0 || seg_offset < 0) return NOSCOPE_INVALID_ARGUMENT;
+  if (!frames || !small_out || !disp_out || !ws) return NOSCOPE_INVALID_ARGUMENT;
+  if ((fired_idx_out == nullptr) != (n_fired_dev == nullptr)) return NOSCOPE_INVALID_ARGUMENT;
+  if (small_pitch % 16 || small_pitch < ((small_bytes_of(*dd) + 15) & ~15ll)) return NOSCOPE_SHAPE;
+  if (!aligned16(frames) || !aligned16(small_out) || !aligned16(ws)) return NOSCOPE_INVALID_ARGUMENT;
+  if (dd->mode == 1 && seg_offset > 0 && !state) return NOSCOPE_INVALID_ARGUMENT;
+  DDWs w = dd_ws(n);
+  if (ws_bytes < w.total) return NOSCOPE_WORKSPACE_TOO_SMALL;
+  if ((s = check_device()) != NOSCOPE_OK) return s;
+  if (n == 0) {
+    if (n_fired_dev) NS_CUDA_TRY(cudaMemsetAsync(n_fired_dev, 0, 8, (cudaStream_t)stream));
+    return NOSCOPE_OK;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
+  uint32_t* status = reinterpret_cast<uint32_t*>(wsb + w.status);
+  uint8_t* st8 = reinterpret_cast<uint8_t*>(state);
+  if (!score_out) score_out = reinterpret_cast<double*>(wsb + w.score);
+  s = launch_diff_detect(*dd, frames, desc, n, seg_offset, seg_offset > 0 ? st8 : nullptr, small_out,
+                         small_pitch, score_out, disp_out, status, st);
+  if (s != NOSCOPE_OK) return s;
+  // compaction also fills skipped frames' disposition/score
+  s = launch_compact_fired(disp_out, disp_out, score_out, n, seg_offset, dd->t_skip_frames,
+                           fired_idx_out, n_fired_dev, wsb + w.scan, st);
+  if (s != NOSCOPE_OK) return s;
+  if (state && dd->mode == 1)
+    s = launch_state_update(*dd, small_out, small_pitch, st8, seg_offset, n, nullptr, st);
+  return s;
+}
+
+noscope_status noscope_specialized_infer(const noscope_cnn_arch* arch,
+                                         const noscope_cnn_weights* weights,
+                                         const uint8_t* small, int64_t small_pitch,
+                                         const int32_t* idx, const int64_t* n_dev, int64_t n_max,
+                                         float* logits, void* ws, size_t ws_bytes,
+                                         noscope_stream_t stream) {
+  noscope_status s = validate_arch(arch, weights);
+  if (s != NOSCOPE_OK) return s;
+  if (!small || !logits || !ws || n_max < 0) return NOSCOPE_INVALID_ARGUMENT;
+  if (small_pitch % 16 || small_pitch < 7504) return NOSCOPE_SHAPE;
+  if (!aligned16(small) || !aligned16(ws)) return NOSCOPE_INVALID_ARGUMENT;
+  if (ws_bytes < noscope_workspace_bytes(NOSCOPE_OP_SPECIALIZED_INFER, nullptr, arch, n_max, 0, 0))
+    return NOSCOPE_WORKSPACE_TOO_SMALL;
+  if ((s = check_device()) != NOSCOPE_OK) return s;
+  if (n_max == 0) return NOSCOPE_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
+  const int64_t* nd = n_dev;
+  if (!nd) {  // dense count: store n_max in the workspace header
+    int64_t* hdr = reinterpret_cast<int64_t*>(wsb + 128);
+    NS_CUDA_TRY(cudaMemcpyAsync(hdr, &n_max, 8, cudaMemcpyHostToDevice, st));
+    nd = hdr;
+  }
+  return launch_cnn(*arch, *weights, small, small_pitch, idx, nd, n_max, logits, wsb + 256,
+                    reinterpret_cast<uint32_t*>(wsb), st);
+}
+
+noscope_status noscope_route_logits(noscope_route r, const float* logits, const int64_t* n_dev,
+                                    int64_t n_max, uint8_t* route_out, int32_t* unc_idx_out,
+                                    int64_t* n_unc_dev, noscope_stream_t stream) {
+  if (!(r.lo_logit <= r.hi_logit)) return NOSCOPE_INVALID_ARGUMENT;
+  if ((!logits && n_max > 0) || !unc_idx_out || !n_unc_dev || n_max < 0) return NOSCOPE_INVALID_ARGUMENT;
+  noscope_status s = check_device();
+  if (s != NOSCOPE_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  // scan scratch: allocated from the stream-ordered pool (small, freed asynchronously)
+  void* scratch = nullptr;
+  size_t bytes = compact_ws_bytes(n_max) + 256;
+  NS_CUDA_TRY(cudaMallocAsync(&scratch, bytes, st));
+  uint32_t* status = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(scratch));
+  NS_CUDA_TRY(cudaMemsetAsync(status, 0, 4, st));
+  s = launch_route(r, logits, n_dev, n_max, nullptr, route_out, nullptr, unc_idx_out, n_unc_dev,
+                   nullptr, nullptr, nullptr, reinterpret_cast<uint8_t*>(scratch) + 256, status, st);
+  cudaFreeAsync(scratch, st);
+  return s;
+}
+
+static noscope_status cascade_impl(const noscope_dd_config* dd, const noscope_cnn_arch* arch,
+                                   const noscope_cnn_weights* weights, noscope_route route,
+                                   const uint8_t* frames, noscope_frames_desc desc, int64_t n,
+                                   int64_t seg_offset, int64_t frame_index_base, void* state,
+                                   noscope_labeller_fn labeller, void* labeller_user,
+                                   uint8_t* labels_out, uint8_t* route_out, float* logits_out,
+                                   double* scores_out, noscope_run_stats* stats_host, void* ws,
+                                   size_t ws_bytes, noscope_stream_t stream, Prof* prof) {
+  noscope_status s = validate_dd(dd);
+  if (s != NOSCOPE_OK) return s;
+  if ((s = validate_frames(dd, desc)) != NOSCOPE_OK) return s;
+  if ((s = validate_arch(arch, weights)) != NOSCOPE_OK) return s;
+  if (dd->out_w != arch->in_w || dd->out_h != arch->in_h) return NOSCOPE_SHAPE;
+  if (!(route.lo_logit <= route.hi_logit)) return NOSCOPE_INVALID_ARGUMENT;
+  if (!frames || !labels_out || !state || !labeller || !ws || n < 0 || seg_offset < 0)
+    return NOSCOPE_INVALID_ARGUMENT;
+  if (!aligned16(frames) || !aligned16(ws) || !aligned16(state)) return NOSCOPE_INVALID_ARGUMENT;
+  CascadeWs w = cascade_ws(dd, arch, n);
+  if (ws_bytes < w.total) return NOSCOPE_WORKSPACE_TOO_SMALL;
+  if ((s = check_device()) != NOSCOPE_OK) return s;
+  if (n == 0) {
+    if (stats_host) std::memset(stats_host, 0, sizeof(*stats_host));
+    return NOSCOPE_OK;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* b = reinterpret_cast<uint8_t*>(ws);
+  uint32_t* status = reinterpret_cast<uint32_t*>(b + w.status);
+  uint8_t* small = b + w.small;
+  double* score = scores_out ? scores_out : reinterpret_cast<double*>(b + w.score);
+  uint8_t* disp = b + w.disp;
+  int32_t* idx = reinterpret_cast<int32_t*>(b + w.idx);
+  int64_t* nfired = reinterpret_cast<int64_t*>(b + w.nfired);
+  float* logits = reinterpret_cast<float*>(b + w.logits);
+  uint8_t* route_pf = b + w.route_pf;
+  int32_t* unc = reinterpret_cast<int32_t*>(b + w.unc);
+  int64_t* nunc = reinterpret_cast<int64_t*>(b + w.nunc);
+  int32_t* unc_pos = reinterpret_cast<int32_t*>(b + w.unc_pos);
+  uint8_t* answers = b + w.answers;
+  uint64_t* counters = reinterpret_cast<uint64_t*>(b + w.counters);
+  uint8_t* st8 = reinterpret_cast<uint8_t*>(state);
+
+  NS_CUDA_TRY(cudaMemsetAsync(counters, 0, 64, st));
+  prof_mark(prof, st);  // e0
+  s = launch_diff_detect(*dd, frames, desc, n, seg_offset, seg_offset > 0 ? st8 : nullptr, small,
+                         w.small_pitch, score, disp, status, st, prof);  // e1 after downsample
+  if (s != NOSCOPE_OK) return s;
+  prof_mark(prof, st);  // e2 after lag score
+  s = launch_compact_fired(disp, disp, score, n, seg_offset, dd->t_skip_frames, idx, nfired,
+                           b + w.scan, st);
+  if (s != NOSCOPE_OK) return s;
+  prof_mark(prof, st);  // e3
+  s = launch_cnn(*arch, *weights, small, w.small_pitch, idx, nfired, n, logits, b + w.cnn, status,
+                 st);
+  if (s != NOSCOPE_OK) return s;
+  prof_mark(prof, st);  // e4
+  s = launch_route(route, logits, nfired, n, idx, nullptr, route_pf, unc, nunc, unc_pos, logits_out,
+                   counters, b + w.scan, status, st);
+  if (s != NOSCOPE_OK) return s;
+  prof_mark(prof, st);  // e5
+  if (labeller(labeller_user, unc, nunc, n, frame_index_base, answers, stream) != 0)
+    return NOSCOPE_LABELLER;
+  prof_mark(prof, st);  // e6
+  const uint8_t* hist = seg_offset > 0 ? st8 + state_ring_bytes(*dd) : nullptr;
+  s = launch_labels(*dd, seg_offset, n, disp, route_pf, unc_pos, answers, hist, labels_out,
+                    route_out, b + w.lab, st);
+  if (s != NOSCOPE_OK) return s;
+  s = launch_state_update(*dd, small, w.small_pitch, st8, seg_offset, n, labels_out, st);
+  if (s != NOSCOPE_OK) return s;
+  prof_mark(prof, st);  // e7
+  if (stats_host) {
+    int64_t nf = 0, nu = 0;
+    uint64_t cnt[2] = {0, 0};
+    NS_CUDA_TRY(cudaMemcpyAsync(&nf, nfired, 8, cudaMemcpyDeviceToHost, st));
+    NS_CUDA_TRY(cudaMemcpyAsync(&nu, nunc, 8, cudaMemcpyDeviceToHost, st));
+    NS_CUDA_TRY(cudaMemcpyAsync(cnt, counters, 16, cudaMemcpyDeviceToHost, st));
+    NS_CUDA_TRY(cudaStreamSynchronize(st));
+    const int64_t ts = dd->t_skip_frames;
+    const int64_t checked = (seg_offset + n + ts - 1) / ts - (seg_offset + ts - 1) / ts;
+    stats_host->n_frames = n;
+    stats_host->n_skipped = n - checked;
+    stats_host->n_fired = nf;
+    stats_host->n_suppressed = checked - nf;
+    stats_host->n_neg = (int64_t)cnt[0];
+    stats_host->n_pos = (int64_t)cnt[1];
+    stats_host->n_uncertain = nu;
+  }
+  return NOSCOPE_OK;
+}
+
+noscope_status noscope_cascade_run(const noscope_dd_config* dd, const noscope_cnn_arch* arch,
+                                   const noscope_cnn_weights* weights, noscope_route route,
+                                   const uint8_t* frames, noscope_frames_desc desc, int64_t n,
+                                   int64_t seg_offset, int64_t frame_index_base, void* state,
+                                   noscope_labeller_fn labeller, void* labeller_user,
+                                   uint8_t* labels_out, uint8_t* route_out, float* logits_out,
+                                   double* scores_out, noscope_run_stats* stats_host, void* ws,
+                                   size_t ws_bytes, noscope_stream_t stream) {
+  return cascade_impl(dd, arch, weights, route, frames, desc, n, seg_offset, frame_index_base,
+                      state, labeller, labeller_user, labels_out, route_out, logits_out,
+                      scores_out, stats_host, ws, ws_bytes, stream, nullptr);
+}
+
+noscope_status noscope_cascade_run_profiled(
+    const noscope_dd_config* dd, const noscope_cnn_arch* arch, const noscope_cnn_weights* weights,
+    noscope_route route, const uint8_t* frames, noscope_frames_desc desc, int64_t n,
+    int64_t seg_offset, int64_t frame_index_base, void* state, noscope_labeller_fn labeller,
+    void* labeller_user, uint8_t* labels_out, uint8_t* route_out, float* logits_out,
+    double* scores_out, noscope_run_stats* stats_host, void* ws, size_t ws_bytes,
+    noscope_stream_t stream, float* stage_ms_host) {
+  if (!stage_ms_host) return NOSCOPE_INVALID_ARGUMENT;
+  Prof prof{};
+  for (int i = 0; i < 8; ++i) NS_CUDA_TRY(cudaEventCreate(&prof.ev[i]));
+  noscope_status s = cascade_impl(dd, arch, weights, route, frames, desc, n, seg_offset,
+                                  frame_index_base, state, labeller, labeller_user, labels_out,
+                                  route_out, logits_out, scores_out, stats_host, ws, ws_bytes,
+                                  stream, &prof);
+  if (s == NOSCOPE_OK && prof.n == 8) {
+    NS_CUDA_TRY(cudaEventSynchronize(prof.ev[7]));
+    for (int i = 0; i < 7; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, prof.ev[i], prof.ev[i + 1]);
+      stage_ms_host[i] = ms;
+    }
+  }
+  for (int i = 0; i < 8; ++i) cudaEventDestroy(prof.ev[i]);
+  return s;
+}
+
+uint64_t noscope_launch_count(void) { return ns::launch_counter(); }
+
+noscope_status noscope_threshold_sweep(int32_t phase, const double* s, const float* z,
+                                       const uint8_t* y, const uint8_t* a, int64_t n,
+                                       const double* delta, int32_t nd, const float* u, int32_t m,
+                                       uint64_t* hist, const noscope_timing* timing,
+                                       uint64_t fp_limit, uint64_t fn_limit,
+                                       const noscope_sweep_tables* tables,
+                                       noscope_sweep_best* best_host, void* ws, size_t ws_bytes,
+                                       noscope_stream_t stream) {
+  if (phase < 1 || phase > 3) return NOSCOPE_INVALID_ARGUMENT;
+  if (nd < 1 || m < 1 || m > 2048 || nd > 65535) return NOSCOPE_INVALID_ARGUMENT;
+  if (!hist || !delta || !u || !ws) return NOSCOPE_INVALID_ARGUMENT;
+  if ((phase & 1) && n > 0 && (!s || !z || !y || !a)) return NOSCOPE_INVALID_ARGUMENT;
+  if ((phase & 2) && !timing) return NOSCOPE_INVALID_ARGUMENT;
+  if (n < 0) return NOSCOPE_INVALID_ARGUMENT;
+  if (ws_bytes < sweep_ws_bytes(nd, m)) return NOSCOPE_WORKSPACE_TOO_SMALL;
+  noscope_status st = check_device();
+  if (st != NOSCOPE_OK) return st;
+  noscope_timing t0{0, 0, 0};
+  bool infeasible = false;
+  st = launch_sweep(phase, s, z, y, a, n, delta, nd, u, m, hist, timing ? *timing : t0, fp_limit,
+                    fn_limit, tables, best_host, ws, (cudaStream_t)stream, &infeasible);
+  if (st != NOSCOPE_OK) return st;
+  return infeasible ? NOSCOPE_INFEASIBLE : NOSCOPE_OK;
+}
+
+// Test/debug helper (not part of the four-call contract): internal CNN
+// activation offsets within the specialized_infer workspace, so tests can
+// check individual layers.  out[9]: act2 off, act2 frame bytes, act3 off/bytes,
+// act4 off/bytes, feature off, K, chunk.  Offsets include the 256-B header.
+int32_t noscope_debug_cnn_layout(const noscope_cnn_arch* arch, int64_t n_max, int64_t* out) {
+  if (!arch || !out || !ns::cnn_debug_layout(*arch, n_max, out)) return 1;
+  for (int i : {0, 2, 4, 6})
+    if (out[i] >= 0) out[i] += 256;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,357 @@
+// sweep.cu — the CBO's (delta_diff, c_low, c_high) threshold sweep
+// (§6.3, cost model P:685-701, objective P:627-637).
+//
+// The paper sorts frames by the DD metric and sweeps prefixes; here the same
+// exact counts come from a histogram over candidate bins, which is what makes
+// the sweep a bandwidth-bound pass over the labelled records and lets GPUs
+// sum partial histograms (NCCL allreduce between phase 1 and phase 2):
+//   d = #{j : delta_j < s}       (frame fired for exactly the j < d)
+//   b = #{u < z} + #{u <= z}     (c_lt = b/2 floor, c_le = b/2 ceil)
+//   H2[d][b][y] += 1,  H1[d][a][y] += 1
+// Phase 2 turns suffix sums over d and prefix/suffix sums over b into the
+// per-threshold tables FP/FN/F/U and evaluates all n_delta*m*(m+1)/2 triples
+// with the integer cost model, reducing to the lexicographic argmin.
+#include "common.cuh"
+#include "internal.h"
+
+namespace ns {
+
+constexpr int kHistThreads = 512;
+constexpr int kMaxCand = 2048;
+
+struct HistLayout {
+  int nd, m, B;         // B = 2m + 1
+  size_t h2, h1, tail;  // word offsets
+  size_t words;
+  __host__ __device__ HistLayout(int nd_, int m_) : nd(nd_), m(m_), B(2 * m_ + 1) {
+    h2 = 0;
+    h1 = (size_t)(nd + 1) * B * 2;
+    tail = h1 + (size_t)(nd + 1) * 4;
+    words = tail + 2;
+  }
+};
+
+NS_DEV int count_lt_d(const double* c, int n, double v) {  // #{c < v}
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (c[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+NS_DEV int count_lt_f(const float* c, int n, float v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (c[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+NS_DEV int count_le_f(const float* c, int n, float v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (c[mid] <= v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Phase 1: block-privatised histogram in shared memory (u32), flushed to the
+// global u64 histogram with one atomic per nonzero bin.
+__global__ void __launch_bounds__(kHistThreads, 1)
+sweep_hist_kernel(const double* __restrict__ s, const float* __restrict__ z,
+                  const uint8_t* __restrict__ y, const uint8_t* __restrict__ a, int64_t n,
+                  const double* __restrict__ delta, int nd, const float* __restrict__ u, int m,
+                  unsigned long long* hist, uint32_t* status, int privatised) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  HistLayout L(nd, m);
+  double* dc = reinterpret_cast<double*>(smem);
+  float* uc = reinterpret_cast<float*>(dc + nd);
+  uint32_t* hs = reinterpret_cast<uint32_t*>(uc + ((m + 3) & ~3));
+  const int tid = threadIdx.x;
+  for (int t = tid; t < nd; t += blockDim.x) dc[t] = delta[t];
+  for (int t = tid; t < m; t += blockDim.x) uc[t] = u[t];
+  if (privatised)
+    for (size_t t = tid; t < L.tail; t += blockDim.x) hs[t] = 0u;
+  __syncthreads();
+  unsigned long long checked = 0;
+  bool bad = false;
+  const double ninf = __longlong_as_double(0xFFF0000000000000ll);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + tid; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double si = s[i];
+    const float zi = z[i];
+    const int yi = y[i] ? 1 : 0, ai = a[i] ? 1 : 0;
+    bad |= (si != si) | (zi != zi);
+    checked += (si != ninf);
+    const int d = count_lt_d(dc, nd, si);
+    const int b = count_lt_f(uc, m, zi) + count_le_f(uc, m, zi);
+    const size_t w2 = L.h2 + ((size_t)d * L.B + b) * 2 + yi;
+    const size_t w1 = L.h1 + (size_t)d * 4 + ai * 2 + yi;
+    if (privatised) {
+      atomicAdd(&hs[w2], 1u);
+      atomicAdd(&hs[w1], 1u);
+    } else {
+      atomicAdd(&hist[w2], 1ull);
+      atomicAdd(&hist[w1], 1ull);
+    }
+  }
+  if (bad) atomicOr(status, 4u);
+  checked = warp_sum(checked);
+  if ((tid & 31) == 0 && checked) atomicAdd(&hist[L.tail], checked);
+  if (privatised) {
+    __syncthreads();
+    for (size_t t = tid; t < L.tail; t += blockDim.x)
+      if (hs[t]) atomicAdd(&hist[t], (unsigned long long)hs[t]);
+  }
+  if (blockIdx.x == 0 && tid == 0) atomicAdd(&hist[L.tail + 1], (unsigned long long)n);
+}
+
+// Phase 2a: per-delta tables.  One CTA per j.
+struct Tables {
+  unsigned long long *F, *FPnf, *FNnf, *FPf, *FNf, *GE, *GT;
+};
+
+__global__ void sweep_prefix_kernel(const unsigned long long* hist, int nd, int m, Tables T) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  HistLayout L(nd, m);
+  unsigned long long* fh0 = reinterpret_cast<unsigned long long*>(smem);
+  unsigned long long* fh1 = fh0 + L.B;
+  unsigned long long* S0 = fh1 + L.B;   // suffix of fh0
+  unsigned long long* SA = S0 + L.B + 1;  // suffix of fh0 + fh1
+  unsigned long long* P1 = SA + L.B + 1;  // prefix (inclusive) of fh1
+  const int j = blockIdx.x, tid = threadIdx.x;
+  for (int b = tid; b < L.B; b += blockDim.x) {
+    unsigned long long c0 = 0, c1 = 0;
+    for (int d = j + 1; d <= nd; ++d) {   // fired: d > j
+      c0 += hist[L.h2 + ((size_t)d * L.B + b) * 2 + 0];
+      c1 += hist[L.h2 + ((size_t)d * L.B + b) * 2 + 1];
+    }
+    fh0[b] = c0;
+    fh1[b] = c1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    S0[L.B] = 0;
+    SA[L.B] = 0;
+    for (int b = L.B - 1; b >= 0; --b) {
+      S0[b] = S0[b + 1] + fh0[b];
+      SA[b] = SA[b + 1] + fh0[b] + fh1[b];
+    }
+    unsigned long long p = 0;
+    for (int b = 0; b < L.B; ++b) {
+      p += fh1[b];
+      P1[b] = p;
+    }
+    unsigned long long fp = 0, fn = 0;
+    for (int d = 0; d <= j; ++d) {         // not fired: d <= j
+      fp += hist[L.h1 + (size_t)d * 4 + 1 * 2 + 0];  // a = 1, y = 0
+      fn += hist[L.h1 + (size_t)d * 4 + 0 * 2 + 1];  // a = 0, y = 1
+    }
+    T.F[j] = SA[0];
+    T.FPnf[j] = fp;
+    T.FNnf[j] = fn;
+  }
+  __syncthreads();
+  for (int t = tid; t < m; t += blockDim.x) {
+    const int bg = 2 * t + 2 < L.B ? 2 * t + 2 : L.B;   // z > u_t  <=> b >= 2t+2
+    const int be = 2 * t + 1;                           // z >= u_t <=> b >= 2t+1
+    T.FPf[(size_t)j * m + t] = S0[bg];
+    T.GT[(size_t)j * m + t] = SA[bg];
+    T.GE[(size_t)j * m + t] = SA[be];
+    T.FNf[(size_t)j * m + t] = P1[2 * t];               // z < u_t  <=> b <= 2t
+  }
+}
+
+// Phase 2b: evaluate every (j, l <= h); thread per (j, l).
+struct Cand {
+  unsigned long long k0, k1, k2;
+  unsigned int j, nl, h, valid;
+};
+NS_DEV bool cand_less(const Cand& x, const Cand& y) {
+  if (x.valid != y.valid) return x.valid > y.valid;
+  if (x.k0 != y.k0) return x.k0 < y.k0;
+  if (x.k1 != y.k1) return x.k1 < y.k1;
+  if (x.k2 != y.k2) return x.k2 < y.k2;
+  if (x.j != y.j) return x.j < y.j;
+  if (x.nl != y.nl) return x.nl < y.nl;
+  return x.h < y.h;
+}
+
+struct EvalOut {
+  Cand feas, infeas;
+};
+
+__global__ void __launch_bounds__(256)
+sweep_eval_kernel(Tables T, const unsigned long long* hist, int nd, int m,
+                  unsigned long long t_mse, unsigned long long t_snn,
+                  unsigned long long t_full, unsigned long long fp_lim,
+                  unsigned long long fn_lim, EvalOut* block_out) {
+  __shared__ Cand sf[256], si[256];
+  HistLayout L(nd, m);
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  Cand bf{0, 0, 0, 0, 0, 0, 0}, bi{0, 0, 0, 0, 0, 0, 0};
+  if (t < (int64_t)nd * m) {
+    const int j = (int)(t / m), l = (int)(t % m);
+    const unsigned long long checked = hist[L.tail];
+    const unsigned long long F = T.F[j];
+    const unsigned long long fn = T.FNnf[j] + T.FNf[(size_t)j * m + l];
+    const unsigned long long ge = T.GE[(size_t)j * m + l];
+    const unsigned long long base_cost = checked * t_mse + F * t_snn;
+    for (int h = l; h < m; ++h) {
+      const unsigned long long fp = T.FPnf[j] + T.FPf[(size_t)j * m + h];
+      const unsigned long long U = ge - T.GT[(size_t)j * m + h];
+      const unsigned long long cost = base_cost + U * t_full;
+      Cand c;
+      c.j = j;
+      c.nl = (unsigned)(m - 1 - l);
+      c.h = h;
+      c.valid = 1;
+      if (fp <= fp_lim && fn <= fn_lim) {
+        c.k0 = cost; c.k1 = U; c.k2 = 0;
+        if (cand_less(c, bf)) bf = c;
+      } else {
+        const unsigned long long vfp = fp > fp_lim ? fp - fp_lim : 0;
+        const unsigned long long vfn = fn > fn_lim ? fn - fn_lim : 0;
+        c.k0 = vfp > vfn ? vfp : vfn; c.k1 = cost; c.k2 = U;
+        if (cand_less(c, bi)) bi = c;
+      }
+    }
+  }
+  sf[threadIdx.x] = bf;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      if (cand_less(sf[threadIdx.x + o], sf[threadIdx.x])) sf[threadIdx.x] = sf[threadIdx.x + o];
+      if (cand_less(si[threadIdx.x + o], si[threadIdx.x])) si[threadIdx.x] = si[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    block_out[blockIdx.x].feas = sf[0];
+    block_out[blockIdx.x].infeas = si[0];
+  }
+}
+
+__global__ void sweep_final_kernel(const EvalOut* blocks, int nblocks, Tables T,
+                                   const unsigned long long* hist, int nd, int m,
+                                   const double* delta, const float* u,
+                                   unsigned long long t_mse, unsigned long long t_snn,
+                                   unsigned long long t_full, noscope_sweep_best* out) {
+  if (threadIdx.x != 0) return;
+  HistLayout L(nd, m);
+  Cand bf{0, 0, 0, 0, 0, 0, 0}, bi{0, 0, 0, 0, 0, 0, 0};
+  for (int b = 0; b < nblocks; ++b) {
+    if (cand_less(blocks[b].feas, bf)) bf = blocks[b].feas;
+    if (cand_less(blocks[b].infeas, bi)) bi = blocks[b].infeas;
+  }
+  const bool feasible = bf.valid != 0;
+  const Cand c = feasible ? bf : bi;
+  noscope_sweep_best r{};
+  r.j = (int)c.j;
+  r.l = m - 1 - (int)c.nl;
+  r.h = (int)c.h;
+  r.feasible = feasible ? 1 : 0;
+  const unsigned long long F = T.F[r.j];
+  r.fp = T.FPnf[r.j] + T.FPf[(size_t)r.j * m + r.h];
+  r.fn = T.FNnf[r.j] + T.FNf[(size_t)r.j * m + r.l];
+  r.uncertain = T.GE[(size_t)r.j * m + r.l] - T.GT[(size_t)r.j * m + r.h];
+  r.fired = F;
+  r.checked = hist[L.tail];
+  r.total = hist[L.tail + 1];
+  r.cost_ps = r.checked * t_mse + F * t_snn + r.uncertain * t_full;
+  r.delta = delta[r.j];
+  r.lo_logit = u[r.l];
+  r.hi_logit = u[r.h];
+  *out = r;
+}
+
+// ===================================================================== host
+size_t sweep_ws_bytes(int32_t nd, int32_t m) {
+  size_t tabs = (size_t)nd * 3 + (size_t)nd * m * 4;
+  size_t blocks = ((size_t)nd * m + 255) / 256;
+  return 256 + tabs * 8 + blocks * sizeof(EvalOut) + sizeof(noscope_sweep_best) + 256;
+}
+
+noscope_status launch_sweep(int32_t phase, const double* s, const float* z, const uint8_t* y,
+                            const uint8_t* a, int64_t n, const double* delta, int32_t nd,
+                            const float* u, int32_t m, uint64_t* hist_u, const noscope_timing& tm,
+                            uint64_t fp_limit, uint64_t fn_limit,
+                            const noscope_sweep_tables* tables, noscope_sweep_best* best_host,
+                            void* ws, cudaStream_t st, bool* infeasible) {
+  unsigned long long* hist = reinterpret_cast<unsigned long long*>(hist_u);
+  uint32_t* status = reinterpret_cast<uint32_t*>(ws);
+  HistLayout L(nd, m);
+  if (phase & 1) {
+    if (n > 0) {
+      size_t smem = (size_t)nd * 8 + (size_t)((m + 3) & ~3) * 4;
+      size_t priv = smem + L.tail * 4;
+      int privatised = priv <= 200 * 1024 ? 1 : 0;
+      size_t use = privatised ? priv : smem;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(sweep_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             227 * 1024);
+        attr = true;
+      }
+      int64_t want = (n + kHistThreads * 16 - 1) / (kHistThreads * 16);
+      int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, kNumSMs));
+      sweep_hist_kernel<<<grid, kHistThreads, use, st>>>(s, z, y, a, n, delta, nd, u, m, hist,
+                                                         status, privatised);
+      NS_LAUNCH_CHECK();
+      count_launch();
+    }
+  }
+  if (phase & 2) {
+    uint8_t* p = reinterpret_cast<uint8_t*>(ws) + 256;
+    Tables T;
+    auto take = [&](size_t words) {
+      unsigned long long* r = reinterpret_cast<unsigned long long*>(p);
+      p += words * 8;
+      return r;
+    };
+    if (tables && tables->F) {
+      T.F = reinterpret_cast<unsigned long long*>(tables->F);
+      T.FPnf = reinterpret_cast<unsigned long long*>(tables->FPnf);
+      T.FNnf = reinterpret_cast<unsigned long long*>(tables->FNnf);
+      T.FPf = reinterpret_cast<unsigned long long*>(tables->FPf);
+      T.FNf = reinterpret_cast<unsigned long long*>(tables->FNf);
+      T.GE = reinterpret_cast<unsigned long long*>(tables->GE);
+      T.GT = reinterpret_cast<unsigned long long*>(tables->GT);
+      take((size_t)nd * 3 + (size_t)nd * m * 4);
+    } else {
+      T.F = take(nd);
+      T.FPnf = take(nd);
+      T.FNnf = take(nd);
+      T.FPf = take((size_t)nd * m);
+      T.FNf = take((size_t)nd * m);
+      T.GE = take((size_t)nd * m);
+      T.GT = take((size_t)nd * m);
+    }
+    const int nblocks = (int)(((int64_t)nd * m + 255) / 256);
+    EvalOut* bo = reinterpret_cast<EvalOut*>(p);
+    p += (size_t)nblocks * sizeof(EvalOut);
+    p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+    noscope_sweep_best* best_dev = reinterpret_cast<noscope_sweep_best*>(p);
+    size_t smem = (size_t)(5 * L.B + 2) * 8;
+    sweep_prefix_kernel<<<nd, 256, smem, st>>>(hist, nd, m, T);
+    NS_LAUNCH_CHECK();
+    count_launch(3);
+    sweep_eval_kernel<<<nblocks, 256, 0, st>>>(T, hist, nd, m, tm.t_mse_ps, tm.t_snn_ps,
+                                               tm.t_full_ps, fp_limit, fn_limit, bo);
+    NS_LAUNCH_CHECK();
+    sweep_final_kernel<<<1, 32, 0, st>>>(bo, nblocks, T, hist, nd, m, delta, u, tm.t_mse_ps,
+                                         tm.t_snn_ps, tm.t_full_ps, best_dev);
+    NS_LAUNCH_CHECK();
+    if (best_host) {
+      NS_CUDA_TRY(cudaMemcpyAsync(best_host, best_dev, sizeof(noscope_sweep_best),
+                                  cudaMemcpyDeviceToHost, st));
+      NS_CUDA_TRY(cudaStreamSynchronize(st));
+      if (infeasible) *infeasible = best_host->feasible == 0;
+    }
+  }
+  return NOSCOPE_OK;
+}
+
+}  // namespace ns

@@ -1,0 +1,84 @@
+"""CPU-side checks of the C-ABI boundary: the library builds, loads, and exports
+every function include/noscope.h declares; host-side size queries and
+validation work without a GPU (no compute calls)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "noscope.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(noscope_[a-z_0-9]+)\s*\(", src)
+    return sorted(set(n for n in names if n != "noscope_labeller_fn"))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1703_02529_b200 import build
+    build.build_all()
+    from paper_1703_02529_b200 import noscope
+    return noscope.lib()
+
+
+def test_header_declares_the_four_entry_points():
+    fns = _declared_functions()
+    for f in ("noscope_diff_detect", "noscope_specialized_infer", "noscope_cascade_run",
+              "noscope_threshold_sweep"):
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for f in _declared_functions():
+        assert hasattr(lib, f), f"{f} not exported"
+
+
+def test_host_queries_without_gpu(lib):
+    from paper_1703_02529_b200 import noscope as N
+    assert lib.noscope_version() == 100
+    assert lib.noscope_status_string(7) == b"no feasible threshold triple"
+    dd = N.DD(mode=1, metric=1, grid=10, t_diff_frames=30, t_skip_frames=1)
+    c = dd.c()
+    # state = 30 ring frames of 7504 B + label history (K+1)*t_skip = 31
+    assert lib.noscope_stream_state_bytes(ctypes.byref(c)) == (30 * 7504 + 31 + 255) // 256 * 256
+    arch = N.Arch(2, 32, 32).c()
+    ws = lib.noscope_workspace_bytes(N.OP_CASCADE_RUN, ctypes.byref(c), ctypes.byref(arch), 108000, 0, 0)
+    assert ws > 108000 * 7504
+    assert lib.noscope_workspace_bytes(N.OP_SPECIALIZED_INFER, None, ctypes.byref(N.Arch(3, 32, 32).c()),
+                                       10, 0, 0) == 0                  # unsupported arch
+    assert lib.noscope_sweep_hist_words(100, 100) == 101 * 201 * 2 + 101 * 4 + 2
+    bad = N.DD(mode=1, metric=1, grid=17).c()
+    assert lib.noscope_stream_state_bytes(ctypes.byref(bad)) == 0      # grid > kMaxGrid
+
+
+def test_validation_precedes_device_use(lib):
+    from paper_1703_02529_b200 import noscope as N
+    dd = N.DD(mode=0, metric=0, ref_image=None).c()                    # mode 0 needs ref image
+    rc = lib.noscope_diff_detect(ctypes.byref(dd), None, N.FramesDesc(50, 50, 7504), 1, 0, None,
+                                 None, 7504, None, None, None, None, None, 0, None)
+    assert rc == 1
+    dd = N.DD(mode=1, metric=0, out_w=60, out_h=60).c()
+    rc = lib.noscope_diff_detect(ctypes.byref(dd), ctypes.c_void_p(16), N.FramesDesc(50, 50, 7504), 1,
+                                 0, None, ctypes.c_void_p(16), 10816, None, ctypes.c_void_p(16),
+                                 None, None, ctypes.c_void_p(16), 1 << 20, None)
+    assert rc == 2                                                     # S:75 target > source
+    rc = lib.noscope_threshold_sweep(4, None, None, None, None, 0, None, 1, None, 1, None, None, 0, 0,
+                                     None, None, None, 0, None)
+    assert rc == 1
+
+
+def test_oracle_and_product_share_no_code():
+    """The oracle never imports the CUDA path and vice versa (task rule ③)."""
+    for d, forbidden in [("oracle", ("paper_1703_02529_b200",)),
+                         ("paper_1703_02529_b200", ("oracle",))]:
+        for dirpath, _, files in os.walk(os.path.join(ROOT, d)):
+            for fn in files:
+                if fn.endswith((".py", ".cu", ".cuh", ".h", ".c")):
+                    txt = open(os.path.join(dirpath, fn)).read()
+                    for f in forbidden:
+                        assert not re.search(rf"^\s*(from|import)\s+{f}\b", txt, re.M), (fn, f)
+                        assert f"#include \"../../{f}" not in txt

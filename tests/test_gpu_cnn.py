@@ -1,0 +1,96 @@
+"""GPU parity: the tcgen05 specialized CNN (noscope_specialized_infer) against the
+oracle's fp64 forward on the same bf16 weights and inputs.  Bar: |z_gpu - z_oracle|
+<= 2e-2 absolute (north star).  Also checks the conv1 activation map directly
+(layer-level parity) and gather-by-index / device-count semantics."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synthgen as sg
+from gpu_util import hw3, ns, requires_gpu, scene_frames
+
+pytestmark = [pytest.mark.gpu, requires_gpu]
+TOL = 2e-2
+
+
+def _small(n, seed):
+    sc, fr = scene_frames(50, 50, n, seed=seed, prevalence=0.6)
+    pitch = 7504
+    small = np.zeros((n, pitch), np.uint8)
+    small[:, :7500] = fr[:, :7500]
+    return small, hw3(fr, 50, 50)
+
+
+@pytest.mark.parametrize("arch", sg.ARCH_GRID, ids=lambda a: a.name)
+def test_cnn_logits_vs_oracle(arch):
+    nsm = ns()
+    n = 203                                             # several tiles + ragged tail
+    small, g = _small(n, 11)
+    w = sg.he_normal_weights(arch, 3)
+    z_o = O.cnn_logits(g, arch, w)
+    W = nsm.Weights(w)
+    A = nsm.Arch(arch.n_conv, arch.base_filters, arch.dense)
+    z = nsm.noscope_specialized_infer(A, W, torch.from_numpy(small).cuda())
+    torch.cuda.synchronize()
+    z = z.cpu().numpy()
+    err = np.abs(z - z_o)
+    assert err.max() <= TOL, (arch.name, err.max(), np.argmax(err))
+    assert np.isfinite(z).all()
+
+
+def test_conv1_activation_map():
+    nsm = ns()
+    arch = sg.CnnArch(2, 32, 32)
+    n = 5
+    small, g = _small(n, 12)
+    w = sg.he_normal_weights(arch, 4)
+    W = nsm.Weights(w)
+    A = nsm.Arch(2, 32, 32)
+    ws = nsm.workspace(nsm.OP_SPECIALIZED_INFER, None, A, n)
+    nsm.noscope_specialized_infer(A, W, torch.from_numpy(small).cuda(), ws=ws)
+    torch.cuda.synchronize()
+    lay = nsm.debug_cnn_layout(A, n)
+    off, fb = lay[0], lay[1]
+    act = ws[off:off + n * fb].cpu().numpy().view(np.uint16).reshape(n, 4, 27, 27, 8)
+    got = act.transpose(0, 2, 3, 1, 4).reshape(n, 27, 27, 32)
+    got = (got.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    x = O.normalize_input(g, arch.chan_mean)
+    a1 = O.conv3x3_same(x, O.bf16_bits_to_f64(w["conv_w"][0]), w["conv_b"][0].astype(np.float64))
+    ref = O.bf16_round(O.maxpool2x2_floor(np.maximum(a1, 0)))
+    assert np.all(got[:, 0, :, :] == 0) and np.all(got[:, :, 0, :] == 0)   # zero halo
+    inner = got[:, 1:26, 1:26, :]
+    diff = np.abs(inner - ref)
+    # fp32 accumulation vs fp64: at most one bf16 ulp apart
+    assert (diff <= np.abs(ref) * 2 ** -7 + 1e-30).all(), diff.max()
+    assert (diff == 0).mean() > 0.99
+
+
+def test_cnn_gather_by_index_and_device_count():
+    nsm = ns()
+    arch = sg.CnnArch(2, 32, 32)
+    small, g = _small(300, 13)
+    w = sg.he_normal_weights(arch, 5)
+    W = nsm.Weights(w)
+    A = nsm.Arch(2, 32, 32)
+    idx = np.array(sorted(np.random.default_rng(1).choice(300, 150, replace=False)), np.int32)
+    cnt = torch.tensor([97], dtype=torch.int64, device="cuda")
+    out = torch.full((150,), 12345.0, device="cuda")
+    nsm.noscope_specialized_infer(A, W, torch.from_numpy(small).cuda(), idx=torch.from_numpy(idx).cuda(),
+                                  n_dev=cnt, n_max=150, logits=out)
+    torch.cuda.synchronize()
+    z = out.cpu().numpy()
+    z_o = O.cnn_logits(g[idx[:97]], arch, w)
+    assert np.abs(z[:97] - z_o).max() <= TOL
+    assert np.all(z[97:] == 12345.0)                      # beyond the device count: untouched
+
+
+def test_cnn_zero_and_bias_weights():
+    nsm = ns()
+    arch = sg.CnnArch(4, 64, 128)
+    w = sg.zero_weights(arch)
+    w["fc2_b"] = np.float32([np.log(3.0)])
+    small, _ = _small(20, 14)
+    z = nsm.noscope_specialized_infer(nsm.Arch(4, 64, 128), nsm.Weights(w), torch.from_numpy(small).cuda())
+    torch.cuda.synchronize()
+    assert np.allclose(1 / (1 + np.exp(-z.cpu().numpy())), 0.75, atol=1e-6)

@@ -1,0 +1,139 @@
+"""GPU parity: downsample + difference detector + compaction (noscope_diff_detect)
+against the oracle on the same seeded inputs.  Dispositions and compaction are
+compared bit-exact, downsampled frames byte-exact, scores to rel 1e-5 (the
+north-star bound; the implementation is expected to be exactly equal)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synthgen as sg
+from gpu_util import dd_pair, hw3, ns, requires_gpu, scene_frames
+
+pytestmark = [pytest.mark.gpu, requires_gpu]
+
+
+def _run(nsm, g, frames_np, W, H, seg_offset=0, state=None):
+    fr = torch.from_numpy(frames_np).cuda()
+    out = nsm.noscope_diff_detect(g, fr, W, H, seg_offset=seg_offset, state=state)
+    torch.cuda.synchronize()
+    return {k: (v.cpu().numpy() if isinstance(v, torch.Tensor) else v) for k, v in out.items()}
+
+
+def _compare(res, small_o, score_o, disp_o, out=50, needed=None):
+    n = len(disp_o)
+    assert np.array_equal(res["disp"][:n], disp_o)
+    idx_o = O.compact(disp_o)
+    assert int(res["n_fired"][0]) == len(idx_o)
+    assert np.array_equal(res["idx"][:len(idx_o)], idx_o)
+    s_g, s_o = res["score"][:n], score_o
+    fin = np.isfinite(s_o)
+    assert np.array_equal(np.isinf(s_g), np.isinf(s_o)) and np.array_equal(s_g[~fin], s_o[~fin])
+    assert np.allclose(s_g[fin], s_o[fin], rtol=1e-5, atol=1e-12)
+    assert np.array_equal(s_g[fin], s_o[fin]), "expected exact fp64 scores"
+    sb = out * out * 3
+    rows = np.arange(n) if needed is None else needed
+    assert np.array_equal(res["small"][rows, :sb], small_o.reshape(n, -1)[rows])
+
+
+def test_synthgen_gpu_matches_cpu():
+    from synthgen.gpu import GpuScene
+    for (W, H, n) in [(50, 50, 40), (640, 480, 6), (101, 77, 9)]:
+        sc, fr = scene_frames(W, H, n, seed=5, prevalence=0.9)
+        gs = GpuScene(sc)
+        out = torch.zeros((n, fr.shape[1]), dtype=torch.uint8, device="cuda")
+        gs.render(out, 0, n)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), fr)
+
+
+@pytest.mark.parametrize("n", [1, 37, 1000, 4097])
+def test_tiny_global_vs_reference_image(n):
+    nsm = ns()
+    sc, fr = scene_frames(50, 50, n, seed=1, prevalence=0.3)
+    ref = sg.background(sc.spec)
+    ocfg, g = dd_pair(nsm, 0, 0, delta=20.0, ref=ref)
+    small = hw3(fr, 50, 50)
+    s_o, d_o = O.diff_detect(small, ocfg)
+    res = _run(nsm, g, fr, 50, 50)
+    _compare(res, small, s_o, d_o)
+
+
+@pytest.mark.parametrize("mode,metric,t_skip", [(0, 1, 1), (1, 0, 1), (1, 1, 1), (1, 1, 4), (0, 0, 3)])
+def test_webcam_640x480(mode, metric, t_skip):
+    nsm = ns()
+    n = 70
+    sc, fr = scene_frames(640, 480, n, seed=2, prevalence=0.95)
+    src = hw3(fr, 640, 480)
+    small_o = O.downsample(src, 50, 50)
+    lr = sg.lr_weights(10, 3)
+    ref = O.downsample(sg.background(sc.spec)[None], 50, 50)[0]
+    s_tmp, _ = O.diff_detect(small_o, O.DDConfig(mode=mode, metric=metric, grid=10, t_diff_frames=7,
+                                                 t_skip_frames=t_skip, delta_diff=0.0,
+                                                 ref_image=ref, lr_w=lr[0], lr_b=lr[1]))
+    fin = s_tmp[np.isfinite(s_tmp)]
+    delta = float(np.quantile(fin, 0.5)) if fin.size else 0.0
+    ocfg, g = dd_pair(nsm, mode, metric, k=7, t_skip=t_skip, delta=delta, ref=ref, lr=lr)
+    s_o, d_o = O.diff_detect(small_o, ocfg)
+    assert 0 < (d_o == O.FIRED).sum() < n
+    res = _run(nsm, g, fr, 640, 480)
+    # small frames are written for checked frames and (mode 1) anchors only
+    need = [t for t in range(n) if t % t_skip == 0 or (mode == 1 and (t + 7) % t_skip == 0)]
+    _compare(res, small_o, s_o, d_o, needed=np.array(need))
+
+
+@pytest.mark.parametrize("t_skip,chunks", [(1, [23, 1, 40, 6]), (3, [10, 11, 49]), (4, [7, 63])])
+def test_chunked_with_state_equals_whole_unit(t_skip, chunks):
+    nsm = ns()
+    n = sum(chunks)
+    sc, fr = scene_frames(160, 120, n, seed=4, prevalence=0.9)
+    small_o = O.downsample(hw3(fr, 160, 120), 50, 50)
+    lr = sg.lr_weights(10, 5)
+    ocfg, g = dd_pair(nsm, 1, 1, k=9, t_skip=t_skip, delta=-3.9, lr=lr)
+    s_o, d_o = O.diff_detect(small_o, ocfg)
+    state = nsm.noscope_stream_state_init(g)
+    pos = 0
+    disp = np.empty(n, np.uint8)
+    score = np.empty(n)
+    for c in chunks:
+        r = _run(nsm, g, fr[pos:pos + c], 160, 120, seg_offset=pos, state=state)
+        disp[pos:pos + c] = r["disp"][:c]
+        score[pos:pos + c] = r["score"][:c]
+        pos += c
+    assert np.array_equal(disp, d_o)
+    assert np.array_equal(score, s_o)
+
+
+def test_odd_width_generic_path_and_identity():
+    nsm = ns()
+    for (W, H, out) in [(101, 77, 50), (50, 50, 50), (53, 61, 17)]:
+        sc, fr = scene_frames(W, H, 30, seed=6, prevalence=0.8)
+        small_o = O.downsample(hw3(fr, W, H), out, out)
+        ocfg, g = dd_pair(nsm, 1, 0, out=out, k=2, delta=3.0)
+        s_o, d_o = O.diff_detect(small_o, ocfg)
+        res = _run(nsm, g, fr, W, H)
+        _compare(res, small_o, s_o, d_o, out=out)
+
+
+def test_extreme_deltas_and_identical_frames():
+    nsm = ns()
+    sc, fr = scene_frames(50, 50, 64, seed=7, prevalence=0.0, sigma=0)
+    ref = sg.background(sc.spec)
+    for delta, expect in [(math.inf, O.SUPPRESSED), (0.0, O.SUPPRESSED), (-math.inf, O.FIRED)]:
+        ocfg, g = dd_pair(nsm, 0, 0, delta=delta, ref=ref)
+        res = _run(nsm, g, fr, 50, 50)
+        assert np.all(res["disp"][:64] == expect)
+
+
+def test_validation_errors():
+    nsm = ns()
+    fr = torch.zeros((4, 7504), dtype=torch.uint8, device="cuda")
+    _, g = dd_pair(nsm, 1, 0, out=60)
+    with pytest.raises(nsm.NoScopeError) as e:
+        nsm.noscope_diff_detect(g, fr, 50, 50)           # out > source
+    assert e.value.code == 2
+    _, g = dd_pair(nsm, 1, 0)
+    with pytest.raises(nsm.NoScopeError):
+        nsm.noscope_diff_detect(g, fr[:, :7500], 50, 50)  # pitch not /16

@@ -1,0 +1,126 @@
+"""GPU parity: routing (bit-exact on identical logits) and the CBO threshold
+sweep (tables and best triple bit-exact vs the oracle; sampled entries and
+optimality properties at the 1M-record BASELINE size)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synthgen as sg
+from gpu_util import ns, requires_gpu
+
+pytestmark = [pytest.mark.gpu, requires_gpu]
+
+
+@pytest.mark.parametrize("n", [0, 1, 100, 4096, 4097, 50001])
+def test_route_bit_exact(n):
+    nsm = ns()
+    rng = np.random.default_rng(n)
+    z = rng.normal(0, 2, n).astype(np.float32)
+    if n > 10:
+        z[:5] = np.float32([-1.0, 1.0, -1.0, 1.0, 0.5])   # exact ties at lo / hi
+    for lo, hi in [(-1.0, 1.0), (-math.inf, math.inf), (0.5, 0.5), (-math.inf, -1.0)]:
+        r, unc, nunc = nsm.noscope_route_logits(lo, hi, torch.from_numpy(z).cuda())
+        torch.cuda.synchronize()
+        ro = O.route(z, lo, hi)
+        assert np.array_equal(r.cpu().numpy(), ro)
+        k = int(nunc.item())
+        assert np.array_equal(unc.cpu().numpy()[:k], np.flatnonzero(ro == O.R_UNC))
+
+
+def _gpu_sweep(nsm, s, z, y, a, delta, u, timing, fpl, fnl, split=1):
+    dev = "cuda"
+    T = lambda x, dt: torch.from_numpy(np.ascontiguousarray(x, dtype=dt)).to(dev)
+    dd, uu = T(delta, np.float64), T(u, np.float32)
+    hist = torch.zeros(nsm.sweep_hist_words(len(delta), len(u)), dtype=torch.int64, device=dev)
+    bounds = np.linspace(0, len(s), split + 1).astype(int)
+    for i in range(split):                         # phase 1 accumulates (as after an allreduce)
+        sl = slice(bounds[i], bounds[i + 1])
+        nsm.noscope_threshold_sweep(1, T(s[sl], np.float64), T(z[sl], np.float32),
+                                    T(y[sl], np.uint8), T(a[sl], np.uint8), dd, uu, hist)
+    nd, m = len(delta), len(u)
+    tabs = {k: torch.zeros(nd * (m if k in ("FPf", "FNf", "GE", "GT") else 1), dtype=torch.int64,
+                           device=dev) for k in ("F", "FPnf", "FNnf", "FPf", "FNf", "GE", "GT")}
+    best, code = nsm.noscope_threshold_sweep(2, None, None, None, None, dd, uu, hist, timing,
+                                             fpl, fnl, tables=tabs)
+    return best, code, {k: v.cpu().numpy().astype(np.uint64) for k, v in tabs.items()}, hist
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_sweep_random_instances_bit_exact(seed):
+    nsm = ns()
+    n = [1, 7, 60, 300, 999][seed % 5]
+    s, z, y, a, delta, u = sg.random_sweep_records(n, seed + 1000, n_delta=9, m=8)
+    timing = [(1, 10, 1000), (3, 5, 7)][seed % 2]
+    fpl, fnl = seed % 3, (seed // 3) % 3
+    T, best_o = O.sweep(s, z, y, a, delta, u, timing, fpl, fnl)
+    best, code, tabs, _ = _gpu_sweep(nsm, s, z, y, a, delta, u, timing, fpl, fnl, split=1 + seed % 3)
+    for k in ("F", "FPnf", "FNnf"):
+        assert np.array_equal(tabs[k], T[k]), k
+    for k in ("FPf", "FNf", "GE", "GT"):
+        assert np.array_equal(tabs[k].reshape(len(delta), len(u)), T[k]), k
+    assert (code == 7) == (not best_o["feasible"])
+    for k_g, k_o in [("j", "j"), ("l", "l"), ("h", "h"), ("fp", "fp"), ("fn", "fn"),
+                     ("uncertain", "U"), ("fired", "F"), ("cost_ps", "cost")]:
+        assert best[k_g] == best_o[k_o], (k_g, best, best_o)
+    assert best["checked"] == T["checked"] and best["total"] == len(s)
+
+
+def test_sweep_spec_six_frame_instance():
+    nsm = ns()
+    s = np.array([9, 8, 5, 4, 2, 1], np.float64)
+    y = np.array([1, 1, 0, 1, 0, 0], np.uint8)
+    c = np.array([.95, .9, .6, .55, .2, .1])
+    z = np.log(c / (1 - c)).astype(np.float32)
+    a = np.zeros(6, np.uint8)
+    delta = np.array([-np.inf, 0.5, 1.5, 3, 4.5, 6.5, 8.5, 9.5])
+    u = np.unique(np.concatenate([[-np.inf, np.inf], z])).astype(np.float32)
+    bf = O.sweep_brute_force(s, z, y, a, delta, u, (1, 10, 1000), 1, 1)
+    best, code, _, _ = _gpu_sweep(nsm, s, z, y, a, delta, u, (1, 10, 1000), 1, 1)
+    assert code == 0 and (best["j"], best["l"], best["h"]) == (bf["j"], bf["l"], bf["h"])
+
+
+def test_sweep_1m_records_sampled():
+    """BASELINE configs[3] size: 1M records, 100 x 100 candidates; sampled table
+    entries recomputed one by one with the oracle definition, best triple's counts
+    re-derived, and optimality checked against random feasible triples."""
+    nsm = ns()
+    rng = np.random.default_rng(77)
+    N = 1_000_000
+    y = (rng.random(N) < 0.15).astype(np.uint8)
+    s = np.where(rng.random(N) < 0.1, -np.inf, rng.gamma(2.0, 10.0, N) + 40.0 * y)
+    z = (rng.normal(0, 1, N) + 2.5 * y - 1.0).astype(np.float32)
+    a = np.where(np.isinf(s), y, 0).astype(np.uint8)
+    delta = sg.delta_grid(s, 100)
+    u = sg.logit_grid(100)
+    timing = (1_000, 20_000, 12_500_000)
+    lim = N // 100
+    best, code, tabs, hist = _gpu_sweep(nsm, s, z, y, a, delta, u, timing, lim, lim, split=4)
+    nd, m = len(delta), len(u)
+    for j in rng.integers(0, nd, 6):
+        fired = s > delta[j]
+        assert tabs["F"][j] == fired.sum()
+        assert tabs["FPnf"][j] == (~fired & (a == 1) & (y == 0)).sum()
+        for h in rng.integers(0, m, 3):
+            assert tabs["FPf"].reshape(nd, m)[j, h] == (fired & (z > u[h]) & (y == 0)).sum()
+            assert tabs["GE"].reshape(nd, m)[j, h] == (fired & (z >= u[h])).sum()
+            assert tabs["FNf"].reshape(nd, m)[j, h] == (fired & (z < u[h]) & (y == 1)).sum()
+    assert code == 0
+    j, l, h = best["j"], best["l"], best["h"]
+    fired = s > delta[j]
+    out = np.where(fired, np.where(z < u[l], 0, np.where(z > u[h], 1, y)), a)
+    assert best["fp"] == ((out == 1) & (y == 0)).sum() <= lim
+    assert best["fn"] == ((out == 0) & (y == 1)).sum() <= lim
+    U = int((fired & (z >= u[l]) & (z <= u[h])).sum())
+    assert best["uncertain"] == U
+    checked = int(np.isfinite(s).sum() + (s == np.inf).sum())
+    assert best["cost_ps"] == checked * timing[0] + int(fired.sum()) * timing[1] + U * timing[2]
+    T = {k: (tabs[k].reshape(nd, m) if k in ("FPf", "FNf", "GE", "GT") else tabs[k]) for k in tabs}
+    T["checked"] = checked
+    for _ in range(2000):
+        jj = int(rng.integers(0, nd)); ll = int(rng.integers(0, m)); hh = int(rng.integers(ll, m))
+        fp, fn, F, UU = O.triple_counts(T, jj, ll, hh)
+        if fp <= lim and fn <= lim:
+            assert O.cost_ps(checked, F, UU, *timing) >= best["cost_ps"]
