@@ -1,0 +1,502 @@
+#!/usr/bin/env python
+"""Benchmark of the NoScope cascade hot path on B200 (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], the metric's config): one hour of a
+synthetic fixed-angle 640x480 webcam at 30 fps = 108,000 frames (99.5 GB,
+resident in HBM before the timed region), blocked-MSE difference detector
+(10x10 grid, LR weights ~U[0,1], bias -4) against frame t-30, t_skip = 1,
+delta_diff at the 85th percentile of the unit's scores, specialized CNN
+L2/C32/D32 (random He-normal bf16 weights), c_low/c_high at the 30%/70%
+logit quantiles of fired frames, ground-truth stand-in labeller.
+One step = noscope_cascade_run over the whole unit (state re-initialised).
+Inputs (99.5 GB) exceed L2 (126 MB), so no L2 flush is needed between steps.
+
+Multi-GPU (torchrun, one process per GPU): every rank processes its own
+stream's hour (weak scaling); labels are gathered to rank 0 over NCCL inside
+the timed region; time = max over ranks of device-event time.
+
+--impl reference: the CPU oracle (oracle/) on a bounded sample of the same
+workload, on this host's cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+W_SRC, H_SRC, OUT = 640, 480, 50
+UNIT = 108_000
+K_LAG = 30
+GRID = 10
+ARCH = (2, 32, 32)
+CONFIG_NAME = "webcam-1h: 108k 640x480 frames, blocked-MSE (10x10, LR) vs t-30, t_skip=1, CNN L2C32D32"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--frames", type=int, default=UNIT, help="frames per unit (default 1 h)")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-extras", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-frames", type=int, default=192)
+    p.add_argument("--e2e-frames", type=int, default=8192)
+    return p.parse_args()
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained"), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.idx), "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- workload
+def make_weights():
+    import synthgen as sg
+    arch = sg.CnnArch(*ARCH)
+    return arch, sg.he_normal_weights(arch, 3), sg.lr_weights(GRID, 3)
+
+
+def setup_gpu(rank, n_frames, device):
+    """Render the unit on the device (decode stand-in) and pick thresholds."""
+    import torch
+    import synthgen as sg
+    from paper_1703_02529_b200 import noscope as N
+    from synthgen.gpu import GpuScene
+
+    sc = sg.make_scene(sg.SceneSpec(W_SRC, H_SRC, n_frames, seed=2, stream=rank))
+    gs = GpuScene(sc, device=device)
+    pitch = sg.frame_pitch(W_SRC, H_SRC)
+    frames = torch.empty((n_frames, pitch), dtype=torch.uint8, device=device)
+    step = 4096
+    for t0 in range(0, n_frames, step):
+        gs.render(frames[t0:t0 + step], t0, min(step, n_frames - t0))
+    arch_s, w, (lr_w, lr_b) = make_weights()
+    dd = N.DD(mode=1, metric=1, out_w=OUT, out_h=OUT, grid=GRID, t_diff_frames=K_LAG, t_skip_frames=1,
+              delta_diff=0.0, lr_weights=torch.from_numpy(lr_w).to(device), lr_bias=float(lr_b))
+    # delta_diff = 85th percentile of the unit's finite scores
+    state = N.noscope_stream_state_init(dd)
+    probe = N.noscope_diff_detect(dd, frames, W_SRC, H_SRC, state=state, compact=False)
+    sc_t = probe["score"]
+    fin = sc_t[torch.isfinite(sc_t)]
+    dd.delta_diff = float(torch.quantile(fin[:: max(1, fin.numel() // 100000)].float(), 0.85).item())
+    del probe
+    arch = N.Arch(*ARCH)
+    W = N.Weights(w, device=device)
+    state = N.noscope_stream_state_init(dd)
+    det = N.noscope_diff_detect(dd, frames, W_SRC, H_SRC, state=state)
+    nf = int(det["n_fired"].item())
+    z = N.noscope_specialized_infer(arch, W, det["small"], idx=det["idx"][:nf])
+    lo = float(torch.quantile(z.float(), 0.3).item())
+    hi = float(torch.quantile(z.float(), 0.7).item())
+    del det, z
+    torch.cuda.empty_cache()
+    return dict(scene=sc, gs=gs, frames=frames, dd=dd, arch=arch, W=W, lo=lo, hi=hi, w=w,
+                lr=(lr_w, lr_b), pitch=pitch)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1703_02529_b200 import noscope as N
+    from synthgen.gpu import truth_labeller_address
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    n = args.frames
+    S = setup_gpu(rank, n, device)
+    dd, arch, W = S["dd"], S["arch"], S["W"]
+    ws = N.workspace(N.OP_CASCADE_RUN, dd, arch, n, device=device)
+    state = torch.empty(max(1, N.lib().noscope_stream_state_bytes(__import__("ctypes").byref(dd.c()))),
+                        dtype=torch.uint8, device=device)
+    labels = torch.empty(n, dtype=torch.uint8, device=device)
+    gathered = torch.empty(n * world, dtype=torch.uint8, device=device) if world > 1 else None
+    lab_fn = truth_labeller_address()
+    stream = torch.cuda.current_stream()
+    stats = {}
+
+    def step(stage_acc=None):
+        N.lib().noscope_stream_state_init(__import__("ctypes").byref(dd.c()), N._ptr(state), N._stream())
+        stage = [] if stage_acc is not None else None
+        out = N.noscope_cascade_run(dd, arch, W, S["lo"], S["hi"], S["frames"], W_SRC, H_SRC, state,
+                                    lab_fn, S["gs"].truth, ws=ws, labels=labels,
+                                    want_stats=not stats, stage_ms=stage)
+        if "stats" in out:
+            stats.update(out["stats"])
+        if stage_acc is not None:
+            stage_acc.append(stage)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, labels)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    stage_acc = []
+    l0 = N.launch_count()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(stage_acc)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = N.launch_count() - l0 + args.steps      # + the stand-in labeller kernel per step
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_step = ms / args.steps
+    fps = n * world / (ms_step / 1e3)
+    stage = np.mean(np.array(stage_acc), axis=0)   # 7 stages, ms
+
+    hbm, bf16, bf16_sus, peak_kind = measured_peaks()
+    # dominant kernel: dd_downsample_kernel; algorithmic bytes per launch =
+    # frames downsampled x (source frame read + small frame write)
+    ds_bytes = n * (W_SRC * H_SRC * 3 + OUT * OUT * 3)
+    ds_ms = float(stage[0])
+    achieved = ds_bytes / (ds_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_dd_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    nf = stats.get("n_fired", 0)
+    cnn_flops = nf * cnn_flops_per_frame(ARCH)
+    line = {
+        "metric": "cascade frames/sec (diff+CNN+routing)",
+        "value": round(fps, 1),
+        "unit": "frames/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8/int64/f64 (DD), bf16->f32 (CNN)",
+        "data": "synthetic fixed-angle webcam (static textured background, sensor noise, moving "
+                "rectangles), random-init He-normal CNN weights; generated on device before timing",
+        "config": {"workload": CONFIG_NAME, "frames_per_gpu": n, "source": f"{W_SRC}x{H_SRC}x3 u8",
+                   "dd": "mode 1 (t-30), blocked 10x10 + LR, t_skip 1",
+                   "delta_diff": dd.delta_diff, "c_low_logit": S["lo"], "c_high_logit": S["hi"],
+                   "cnn": "L2C32D32", "l2_flush": "not needed: 99.5 GB input per GPU > 126 MB L2",
+                   "parallelism": f"dp{world} (units sharded by stream)"},
+        "roofline": {"bound": "hbm", "kernel": "dd_downsample_kernel", "achieved": round(achieved, 1),
+                     "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                     "peak_source": peak_kind, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": ds_bytes, "avg_launch_ms": round(ds_ms, 4)},
+        "stage_ms": {k: round(float(v), 4) for k, v in zip(
+            ["downsample_score", "lag_score", "compaction", "cnn", "routing", "labeller",
+             "labels_state"], stage)},
+        "run_stats": stats,
+        "cnn": {"frames": nf, "tflops": round(cnn_flops / (stage[3] / 1e3) / 1e12, 2) if stage[3] > 0 else None},
+        "gpu_launches": int(launches),
+    }
+    if rank == 0:
+        with ClockSampler(local) as _:
+            pass
+        line["clocks"] = clk.summary()
+    if not args.no_e2e:
+        line["e2e"] = run_e2e(args, S, device, world)
+    del S["frames"]
+    torch.cuda.empty_cache()
+    if not args.no_extras and rank == 0:
+        line["extras"] = run_extras(device)
+    if rank == 0 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(args, S)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cnn_flops_per_frame(arch):
+    L, Cb, D = arch
+    h, cin, f = 50, 3, 0
+    for l in range(L):
+        cout = Cb * 2 ** l
+        f += 2 * h * h * 9 * cin * cout
+        h //= 2
+        cin = cout
+    K = h * h * cin
+    return f + 2 * K * D + 2 * D
+
+
+def run_e2e(args, S, device, world):
+    """Same metric through the public C ABI with HOST buffers: each step copies
+    the unit's frames from pinned host memory (H2D) chunk by chunk, runs the
+    cascade on each chunk with carried stream state, and reads the labels back
+    (D2H), on two streams so copies overlap compute.  Bounded unit size."""
+    import torch
+    from paper_1703_02529_b200 import noscope as N
+    from synthgen.gpu import truth_labeller_address
+    n = min(args.e2e_frames, args.frames)
+    chunk = 1024
+    pitch = S["pitch"]
+    host = torch.empty((n, pitch), dtype=torch.uint8, pin_memory=True)
+    host.copy_(S["frames"][:n].cpu() if False else S["frames"][:n], non_blocking=False)
+    lab_host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    dev_buf = [torch.empty((chunk, pitch), dtype=torch.uint8, device=device) for _ in range(2)]
+    labels = torch.empty(n, dtype=torch.uint8, device=device)
+    dd, arch, W = S["dd"], S["arch"], S["W"]
+    ws = N.workspace(N.OP_CASCADE_RUN, dd, arch, chunk, device=device)
+    import ctypes
+    state = torch.empty(max(1, N.lib().noscope_stream_state_bytes(ctypes.byref(dd.c()))), dtype=torch.uint8,
+                        device=device)
+    copy_s = torch.cuda.Stream(device=device)
+    comp_s = torch.cuda.current_stream()
+    lab_fn = truth_labeller_address()
+
+    def step():
+        N.lib().noscope_stream_state_init(ctypes.byref(dd.c()), N._ptr(state), N._stream(comp_s))
+        done = [torch.cuda.Event() for _ in range(2)]
+        ready = [torch.cuda.Event() for _ in range(2)]
+        for c, t0 in enumerate(range(0, n, chunk)):
+            b = c & 1
+            m = min(chunk, n - t0)
+            with torch.cuda.stream(copy_s):
+                if c >= 2:
+                    copy_s.wait_event(done[b])
+                dev_buf[b][:m].copy_(host[t0:t0 + m], non_blocking=True)
+                ready[b].record(copy_s)
+            comp_s.wait_event(ready[b])
+            N.noscope_cascade_run(dd, arch, W, S["lo"], S["hi"], dev_buf[b][:m], W_SRC, H_SRC, state,
+                                  lab_fn, S["gs"].truth, seg_offset=t0, frame_index_base=t0, ws=ws,
+                                  labels=labels[t0:t0 + m], stream=comp_s)
+            done[b].record(comp_s)
+        lab_host.copy_(labels, non_blocking=True)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    steps = max(2, args.steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(comp_s)
+    for _ in range(steps):
+        step()
+    e1.record(comp_s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    del host
+    return {"value": round(n * world / (ms / 1e3), 1), "unit": "frames/s",
+            "h2d_bytes_per_step": n * pitch, "d2h_bytes_per_step": n,
+            "frames_per_step": n, "chunk": chunk, "ms_per_step": round(ms, 3)}
+
+
+def run_extras(device):
+    """Secondary measurements of the other BASELINE configs (not the headline)."""
+    import torch
+    import synthgen as sg
+    from paper_1703_02529_b200 import noscope as N
+    out = {}
+    _, bf16, bf16_sus, _ = measured_peaks()
+    # configs[2]: CNN grid, 65,536 frames per arch
+    nG = 65536
+    sc = sg.make_scene(sg.SceneSpec(50, 50, nG, seed=3, prevalence=0.15))
+    gs = __import__("synthgen.gpu", fromlist=["GpuScene"]).GpuScene(sc, device=device)
+    small = torch.empty((nG, 7504), dtype=torch.uint8, device=device)
+    gs.render(small, 0, nG)
+    grid = {}
+    for a in sg.ARCH_GRID:
+        w = sg.he_normal_weights(a, 3)
+        A, Wt = N.Arch(a.n_conv, a.base_filters, a.dense), N.Weights(w, device=device)
+        ws = N.workspace(N.OP_SPECIALIZED_INFER, None, A, nG, device=device)
+        logits = torch.empty(nG, dtype=torch.float32, device=device)
+        for _ in range(2):
+            N.noscope_specialized_infer(A, Wt, small, ws=ws, logits=logits)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        e0.record()
+        for _ in range(reps):
+            N.noscope_specialized_infer(A, Wt, small, ws=ws, logits=logits)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        fl = cnn_flops_per_frame((a.n_conv, a.base_filters, a.dense)) * nG
+        grid[a.name] = {"ms": round(ms, 3), "fps": round(nG / ms * 1e3, 1),
+                        "tflops": round(fl / ms / 1e9, 1), "frac_of_bf16_peak": round(fl / ms / 1e9 / bf16, 4)}
+        del ws
+    out["cnn_grid_65536"] = grid
+    # configs[3]: sweep over 1M labelled records, 100 x 100 candidates
+    rng = np.random.default_rng(4)
+    M = 1_000_000
+    y = (rng.random(M) < 0.15).astype(np.uint8)
+    s = np.where(rng.random(M) < 0.05, -np.inf, rng.gamma(2.0, 10.0, M) + 40.0 * y)
+    z = (rng.normal(0, 1, M) + 2.5 * y - 1.0).astype(np.float32)
+    a_ = np.where(np.isinf(s), y, 0).astype(np.uint8)
+    T = lambda x, dt: torch.from_numpy(np.ascontiguousarray(x, dtype=dt)).to(device)
+    sd, zd, yd, ad = T(s, np.float64), T(z, np.float32), T(y, np.uint8), T(a_, np.uint8)
+    dl, ul = T(sg.delta_grid(s, 100), np.float64), T(sg.logit_grid(100), np.float32)
+    hist = torch.zeros(N.sweep_hist_words(100, 100), dtype=torch.int64, device=device)
+    ws = N.workspace(N.OP_THRESHOLD_SWEEP, None, None, 0, 100, 100, device=device)
+    timing = (1000, 20000, 12_500_000)
+    for _ in range(2):
+        hist.zero_()
+        N.noscope_threshold_sweep(3, sd, zd, yd, ad, dl, ul, hist, timing, M // 100, M // 100, ws=ws)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    reps = 5
+    for _ in range(reps):
+        hist.zero_()
+        best, code = N.noscope_threshold_sweep(3, sd, zd, yd, ad, dl, ul, hist, timing, M // 100, M // 100,
+                                               ws=ws)
+    wall = (time.perf_counter() - t0) / reps
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        N.noscope_threshold_sweep(1, sd, zd, yd, ad, dl, ul, hist)
+    e1.record()
+    torch.cuda.synchronize()
+    h_ms = e0.elapsed_time(e1) / reps
+    out["sweep_1M"] = {"wall_ms_incl_readback": round(wall * 1e3, 3), "hist_ms": round(h_ms, 4),
+                       "records_per_s": round(M / wall, 1), "hist_GBps": round(M * 14 / h_ms / 1e6, 1),
+                       "best": {k: best[k] for k in ("j", "l", "h", "feasible", "cost_ps", "uncertain")}}
+    return out
+
+
+def oracle_sample(S_or_none, frames_n):
+    """Run the CPU oracle cascade on a bounded sample of the webcam workload."""
+    import oracle as O
+    import synthgen as sg
+    t_begin = 50_000
+    sc = sg.make_scene(sg.SceneSpec(W_SRC, H_SRC, UNIT, seed=2, stream=0))
+    fr = sg.render_frames(sc, t_begin, t_begin + frames_n)
+    src = fr[:, :W_SRC * H_SRC * 3].reshape(-1, H_SRC, W_SRC, 3)
+    arch, w, (lr_w, lr_b) = make_weights()
+    delta = S_or_none["dd"].delta_diff if S_or_none else -2.5
+    lo = S_or_none["lo"] if S_or_none else -0.1
+    hi = S_or_none["hi"] if S_or_none else 0.1
+    cfg = O.DDConfig(mode=1, metric=1, out_w=OUT, out_h=OUT, grid=GRID, t_diff_frames=K_LAG,
+                     t_skip_frames=1, delta_diff=delta, lr_w=lr_w, lr_b=lr_b)
+    truth = sc.truth[t_begin:t_begin + frames_n]
+    return src, cfg, arch, w, lo, hi, truth
+
+
+def cpu_baseline(args, S):
+    import oracle as O
+    from threadpoolctl import threadpool_limits
+    src, cfg, arch, w, lo, hi, truth = oracle_sample(S, args.cpu_frames)
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        O.cascade(src, cfg, arch, w, lo, hi, truth)
+        dt = time.perf_counter() - t0
+    return {"value": round(len(src) / dt, 3), "unit": "frames/s", "cores": 1, "kind": "oracle",
+            "sample": f"{len(src)} consecutive frames (t=50000..) of the webcam unit processed as one "
+                      f"unit by the plain CPU oracle (numpy, 1 thread), {dt:.1f} s",
+            "host_cores_available": os.cpu_count()}
+
+
+def run_reference(args):
+    """Reference arm: the oracle as it stands, on a bounded sample per step."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as O
+    from threadpoolctl import threadpool_limits
+    per_step = 32
+    src, cfg, arch, w, lo, hi, truth = oracle_sample(None, per_step)
+    with threadpool_limits(1):
+        for _ in range(args.warmup):
+            O.cascade(src, cfg, arch, w, lo, hi, truth)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            O.cascade(src, cfg, arch, w, lo, hi, truth)
+        dt = (time.perf_counter() - t0) / args.steps
+    v = round(per_step / dt, 3)
+    line = {"impl": "reference", "metric": "cascade frames/sec (diff+CNN+routing)", "value": v,
+            "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64/f64 (numpy oracle)", "data": "synthetic",
+            "config": {"workload": CONFIG_NAME, "sample_frames_per_step": per_step},
+            "cpu_baseline": {"value": v, "unit": "frames/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{per_step} frames of the webcam unit per step"},
+            "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -117,6 +117,10 @@ def lib():
                                       C.POINTER(CnnWeightsC), Route, c_p, FramesDesc, c_i64, c_i64,
                                       c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p,
                                       C.POINTER(RunStats), c_p, c_sz, c_p]
+    L.noscope_cascade_run_profiled.restype = c_i32
+    L.noscope_cascade_run_profiled.argtypes = L.noscope_cascade_run.argtypes + [C.POINTER(c_f32)]
+    L.noscope_launch_count.restype = C.c_uint64
+    L.noscope_launch_count.argtypes = []
     L.noscope_threshold_sweep.restype = c_i32
     L.noscope_threshold_sweep.argtypes = [c_i32, c_p, c_p, c_p, c_p, c_i64, c_p, c_i32, c_p, c_i32,
                                           c_p, C.POINTER(Timing), C.c_uint64, C.c_uint64,
@@ -276,11 +280,13 @@ def noscope_cascade_run(dd: DD, arch: Arch, weights: Weights, lo: float, hi: flo
                         frames: torch.Tensor, width: int, height: int, state: torch.Tensor,
                         labeller, labeller_user, seg_offset=0, frame_index_base=0, ws=None,
                         labels=None, route_out=None, logits_out=None, scores_out=None,
-                        want_stats=False, stream=None):
+                        want_stats=False, stream=None, stage_ms=None):
     """One chunk of one unit through the whole cascade.
 
     labeller: an int function address (e.g. the stand-in from synthgen) or a
-    LABELLER_FN instance; labeller_user: its void* (e.g. a device tensor)."""
+    LABELLER_FN instance; labeller_user: its void* (e.g. a device tensor).
+    stage_ms: optional list; if given, the profiled entry point fills it with
+    the 7 per-stage device times (ms) of noscope_cascade_run_profiled."""
     n, pitch = frames.shape
     dev = frames.device
     if ws is None:
@@ -289,18 +295,26 @@ def noscope_cascade_run(dd: DD, arch: Arch, weights: Weights, lo: float, hi: flo
     stats = RunStats() if want_stats else None
     fn = labeller if isinstance(labeller, int) else C.cast(labeller, c_p).value
     user = labeller_user.data_ptr() if isinstance(labeller_user, torch.Tensor) else labeller_user
-    code = lib().noscope_cascade_run(C.byref(dd.c()), C.byref(arch.c()), C.byref(weights.c()),
-                                     Route(lo, hi), _ptr(frames), FramesDesc(width, height, pitch), n,
-                                     seg_offset, frame_index_base, _ptr(state), C.c_void_p(fn),
-                                     C.c_void_p(user), _ptr(labels), _ptr(route_out),
-                                     _ptr(logits_out), _ptr(scores_out),
-                                     C.byref(stats) if stats is not None else None, _ptr(ws),
-                                     ws.numel(), _stream(stream))
+    args = [C.byref(dd.c()), C.byref(arch.c()), C.byref(weights.c()), Route(lo, hi), _ptr(frames),
+            FramesDesc(width, height, pitch), n, seg_offset, frame_index_base, _ptr(state),
+            C.c_void_p(fn), C.c_void_p(user), _ptr(labels), _ptr(route_out), _ptr(logits_out),
+            _ptr(scores_out), C.byref(stats) if stats is not None else None, _ptr(ws), ws.numel(),
+            _stream(stream)]
+    if stage_ms is None:
+        code = lib().noscope_cascade_run(*args)
+    else:
+        buf = (c_f32 * 7)()
+        code = lib().noscope_cascade_run_profiled(*args, buf)
+        stage_ms[:] = list(buf)
     _check(code, "noscope_cascade_run")
     out = dict(labels=labels[:n], route=route_out, logits=logits_out, scores=scores_out)
     if stats is not None:
         out["stats"] = {f: getattr(stats, f) for f, _ in RunStats._fields_}
     return out
+
+
+def launch_count():
+    return int(lib().noscope_launch_count())
 
 
 def sweep_hist_words(n_delta, m):
