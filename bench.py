@@ -473,7 +473,7 @@ def run_reference(args):
         return
     import oracle as O
     from threadpoolctl import threadpool_limits
-    per_step = 32
+    per_step = 96
     src, cfg, arch, w, lo, hi, truth = oracle_sample(None, per_step)
     with threadpool_limits(1):
         for _ in range(args.warmup):
