@@ -9,7 +9,8 @@
 namespace ns {
 
 constexpr int kMaxGrid = 16;      // blocked-DD grid side limit (g*g <= 256 blocks)
-constexpr int kMaxOutW = 85;      // out_w*3 <= 256 threads own one output column each
+constexpr int kMaxOutW = 53;      // out_w*3 <= 160 box-mean threads own one output column each
+constexpr int kMaxBox = 2048;     // max source pixels per output pixel (exact magic division)
 
 // Optional stage timing (noscope_cascade_run_profiled) and launch counting.
 struct Prof {
@@ -84,7 +85,8 @@ noscope_status launch_diff_detect(const noscope_dd_config& cfg, const uint8_t* f
                                   const noscope_frames_desc& desc, int64_t n, int64_t tau0,
                                   uint8_t* state, uint8_t* small, int64_t small_pitch,
                                   double* score, uint8_t* disp, uint32_t* status,
-                                  cudaStream_t st, Prof* prof = nullptr);
+                                  unsigned* flags, cudaStream_t st, Prof* prof = nullptr);
+size_t dd_flags_bytes();  // workspace for the per-CTA completion flags
 noscope_status launch_state_update(const noscope_dd_config& cfg, const uint8_t* small,
                                    int64_t small_pitch, uint8_t* state, int64_t tau0, int64_t n,
                                    const uint8_t* labels, cudaStream_t st);

@@ -54,8 +54,11 @@ noscope_status validate_frames(const noscope_dd_config* c, const noscope_frames_
   if (d.frame_pitch % 16 != 0 || d.frame_pitch < (((int64_t)d.width * d.height * 3 + 15) & ~15ll))
     return NOSCOPE_SHAPE;
   // vertical box height must fit the 16-bit SWAR lanes (<= 257 rows of 255)
-  if ((d.height + c->out_h - 1) / c->out_h > 257) return NOSCOPE_SHAPE;
-  if ((int64_t)d.width * 3 > 200 * 1024 / 4) return NOSCOPE_SHAPE;
+  const int64_t box_h = (d.height + c->out_h - 1) / c->out_h;
+  const int64_t box_w = (d.width + c->out_w - 1) / c->out_w;
+  if (box_h > 257 || box_h * box_w > kMaxBox) return NOSCOPE_SHAPE;
+  // one band (box_h source rows) per pipeline stage: 4 stages x 2 CTAs must fit smem
+  if (box_h * d.width * 3 + 32 > 24 * 1024) return NOSCOPE_SHAPE;
   return NOSCOPE_OK;
 }
 
@@ -70,20 +73,21 @@ noscope_status validate_arch(const noscope_cnn_arch* a, const noscope_cnn_weight
 
 // ---- workspace layouts
 struct DDWs {
-  size_t status, scan, score, total;
+  size_t status, scan, score, flags, total;
 };
 DDWs dd_ws(int64_t n) {
   DDWs w{};
   w.status = 0;
   w.scan = 256;
   w.score = w.scan + align256(compact_ws_bytes(n));
-  w.total = w.score + align256((size_t)n * 8);
+  w.flags = w.score + align256((size_t)n * 8);
+  w.total = w.flags + align256(dd_flags_bytes());
   return w;
 }
 
 struct CascadeWs {
   size_t status, scan, small, score, disp, idx, nfired, logits, route_pf, unc, nunc, unc_pos,
-      answers, counters, lab, cnn, total;
+      answers, counters, lab, flags, cnn, total;
   int64_t small_pitch;
 };
 CascadeWs cascade_ws(const noscope_dd_config* dd, const noscope_cnn_arch* a, int64_t n) {
@@ -110,6 +114,7 @@ CascadeWs cascade_ws(const noscope_dd_config* dd, const noscope_cnn_arch* a, int
   w.answers = take((size_t)n);
   w.counters = take(64);
   w.lab = take(labels_ws_bytes(n));
+  w.flags = take(dd_flags_bytes());
   w.cnn = off;
   off += a ? cnn_ws_bytes(*a, n) : 0;
   w.total = align256(off);
@@ -214,7 +219,8 @@ noscope_status noscope_diff_detect(const noscope_dd_config* dd, const uint8_t* f
   uint8_t* st8 = reinterpret_cast<uint8_t*>(state);
   if (!score_out) score_out = reinterpret_cast<double*>(wsb + w.score);
   s = launch_diff_detect(*dd, frames, desc, n, seg_offset, seg_offset > 0 ? st8 : nullptr, small_out,
-                         small_pitch, score_out, disp_out, status, st);
+                         small_pitch, score_out, disp_out, status,
+                         reinterpret_cast<unsigned*>(wsb + w.flags), st);
   if (s != NOSCOPE_OK) return s;
   // compaction also fills skipped frames' disposition/score
   s = launch_compact_fired(disp_out, disp_out, score_out, n, seg_offset, dd->t_skip_frames,
@@ -316,9 +322,10 @@ static noscope_status cascade_impl(const noscope_dd_config* dd, const noscope_cn
   NS_CUDA_TRY(cudaMemsetAsync(counters, 0, 64, st));
   prof_mark(prof, st);  // e0
   s = launch_diff_detect(*dd, frames, desc, n, seg_offset, seg_offset > 0 ? st8 : nullptr, small,
-                         w.small_pitch, score, disp, status, st, prof);  // e1 after downsample
+                         w.small_pitch, score, disp, status, reinterpret_cast<unsigned*>(b + w.flags),
+                         st, prof);  // e1 after the fused downsample + score kernel
   if (s != NOSCOPE_OK) return s;
-  prof_mark(prof, st);  // e2 after lag score
+  prof_mark(prof, st);  // e2 (the separate lag-score stage no longer exists: ~0 ms)
   s = launch_compact_fired(disp, disp, score, n, seg_offset, dd->t_skip_frames, idx, nfired,
                            b + w.scan, st);
   if (s != NOSCOPE_OK) return s;
