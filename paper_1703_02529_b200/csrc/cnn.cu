@@ -418,8 +418,8 @@ convN_kernel(ConvNArgs A) {
           uint32_t pk[8];
 #pragma unroll
           for (int j = 0; j < 16; j += 2) {
-            const float v0 = fmaxf(__uint_as_float(r[j]) + A.bias[ch0 + j], 0.0f);
-            const float v1 = fmaxf(__uint_as_float(r[j + 1]) + A.bias[ch0 + j + 1], 0.0f);
+            const float v0 = relu(__uint_as_float(r[j]) + A.bias[ch0 + j]);
+            const float v1 = relu(__uint_as_float(r[j + 1]) + A.bias[ch0 + j + 1]);
             pk[j >> 1] = (uint32_t)f2bf(v0) | ((uint32_t)f2bf(v1) << 16);
           }
           uint4* dst = reinterpret_cast<uint4*>(staging + (size_t)(t * 128 + tid) * 32);
@@ -591,7 +591,7 @@ static bool make_plan(const noscope_cnn_arch& a, int64_t n_max, CnnPlan* P) {
   p.chunk = std::min<int64_t>(kCnnChunk, std::max<int64_t>(128, (n_max + 127) / 128 * 128));
   size_t off = 256;  // status words etc. live before the CNN region (caller offset)
   p.w1_off = off;
-  p.w1_bytes = (size_t)p.C * 32 * 2;
+  p.w1_bytes = (size_t)p.C * 32 * 2;  // [4 kc][C][8]: K = 27 padded to 32
   off = align_up(off + p.w1_bytes, 256);
   int h = 25, cin = p.C;
   for (int l = 1; l < p.L; ++l) {
@@ -717,8 +717,32 @@ noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& 
     cudaFuncSetAttribute(conv1_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     attr = true;
   }
+  const bool fused12 = P.C == 32;  // conv1+conv2 in one kernel (cnn_fused.cu)
   for (int64_t base = 0; base < n_max; base += P.chunk) {
     const int64_t len = std::min<int64_t>(P.chunk, n_max - base);
+    if (fused12) {
+      FusedArgs fa{};
+      fa.small = small;
+      fa.small_pitch = small_pitch;
+      fa.idx = idx;
+      fa.n_dev = n_dev;
+      fa.n_max = n_max;
+      fa.chunk_base = base;
+      fa.chunk_len = len;
+      fa.w1 = ws + P.w1_off;
+      fa.w2 = ws + P.lay[1].w_off;
+      fa.b1 = w.conv_b[0];
+      fa.b2 = w.conv_b[1];
+      fa.mean[0] = a.chan_mean[0];
+      fa.mean[1] = a.chan_mean[1];
+      fa.mean[2] = a.chan_mean[2];
+      fa.to_features = P.L == 2 ? 1 : 0;
+      fa.out = P.L == 2 ? ws + P.feat_off : ws + P.lay[2].in_off;
+      fa.K_feat = P.K;
+      fa.out_frame_bytes = P.L == 2 ? 0 : P.lay[2].in_frame_bytes;
+      noscope_status s = launch_conv12_fused(fa, (int)std::min<int64_t>(len, kNumSMs), st);
+      if (s != NOSCOPE_OK) return s;
+    }
     Conv1Args c1{};
     c1.small = small;
     c1.small_pitch = small_pitch;
@@ -735,11 +759,12 @@ noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& 
     c1.act_out = ws + P.act2_off;
     c1.out_frame_bytes = P.act2_frame_bytes;
     const int g1 = (int)std::min<int64_t>(len, 3 * kNumSMs);
-    if (P.C == 32) conv1_kernel<32><<<g1, kCnnThreads, conv1_smem_bytes<32>(), st>>>(c1);
-    else conv1_kernel<64><<<g1, kCnnThreads, conv1_smem_bytes<64>(), st>>>(c1);
-    NS_LAUNCH_CHECK();
-    count_launch();
-    for (int l = 1; l < P.L; ++l) {
+    if (!fused12) {
+      conv1_kernel<64><<<g1, kCnnThreads, conv1_smem_bytes<64>(), st>>>(c1);
+      NS_LAUNCH_CHECK();
+      count_launch();
+    }
+    for (int l = fused12 ? 2 : 1; l < P.L; ++l) {
       const LayerPlan& L = P.lay[l];
       ConvNArgs c{};
       c.act_in = ws + L.in_off;

@@ -1,0 +1,450 @@
+// cnn_fused.cu — layers 1+2 of the specialized CNN (§4)
+// in one warp-specialised persistent kernel for base_filters = 32: the conv1
+// output (25x25x32 pooled, bf16) is written straight into the shared-memory
+// operand planes of conv2 and never touches HBM.
+//
+// Roles (19 warps):
+//   W0      producer    — cp.async.bulk of the u8 input frames (2-deep ring) and
+//                         the packed weights (once)
+//   W1      conv1 MMA   — one thread issues tcgen05.mma for conv1 with the A
+//                         operand (im2col rows) in TENSOR MEMORY (K = 27 -> 32,
+//                         N = 32); owns the TMEM allocation
+//   W2      conv2 MMA   — one thread issues the shifted-window conv2 tiles
+//                         (A and B from shared memory, K = 9 x 32, N = 64)
+//   W3-W6   builders    — normalisation through a 3x256 lookup table
+//                         of the exact fp32 formula into a zero-haloed bf16 image
+//                         (4 channel slots per pixel), then one im2col row per
+//                         thread (pool-window-major: the 4 rows of a 2x2 pool
+//                         window are adjacent lanes) stored into TMEM with
+//                         tcgen05.st (no shared-memory traffic for A)
+//   W7-W14  epilogue 1  — two 4-warp groups on alternate tiles: TMEM -> bias ->
+//                         ReLU -> bf16 -> 2x2 max across the window's 4 lanes
+//                         (packed bf16x2 shuffles) -> conv2 operand planes
+//                         (double-buffered per frame)
+//   W15-W18 epilogue 2  — TMEM -> bias -> ReLU -> bf16 -> 2x2 max by shuffles ->
+//                         FC feature tiles (L = 2) or the haloed layer-3 map (L = 4)
+// conv2 M tile = 16 conv rows x 8 conv columns: 16 core-matrix groups of 8
+// consecutive pixels at a stride of one image row (SBO = Wp*16 B), so a warp's
+// 32 TMEM lanes hold a 4x8 pixel block and the 2x2 pool is two shuffles.
+// MMAs on one accumulator serialise on the D read-modify-write (measured in
+// tools/umma_bench.cu), so both issuers interleave the K steps of two tiles with
+// independent accumulators (4 TMEM buffers each).
+#include "common.cuh"
+#include "internal.h"
+
+namespace ns {
+
+namespace fz {
+constexpr int kThreads = 19 * 32;
+constexpr int C1 = 32, C2 = 64;
+constexpr int kIn = 50, kInP = 52, kP1 = 25;
+// image row stride in 8-byte cells: 56 cells = 448 B puts two consecutive image
+// rows in opposite bank halves (a half-warp of im2col loads = 2 rows x 8 cells)
+constexpr int kXs = 56;
+constexpr int kInBytes = 7504;
+constexpr int kT1 = 20;                 // conv1 tiles per frame (625 windows x 4 / 128)
+constexpr int kK1 = 32;                 // conv1 K: 27 (tap-major, 3 channels) padded to 32
+constexpr int kA1Cols = kK1 / 2;        // TMEM columns per A tile (bf16 pairs)
+constexpr int kA1Stages = 4;
+constexpr int kNB1 = 4;                 // conv1 accumulators (32 columns each)
+constexpr int kNB2 = 4;                 // conv2 accumulators (64 columns each)
+constexpr int kColA1 = 0;                                 // TMEM column map
+constexpr int kColD1 = kColA1 + kA1Stages * kA1Cols;      // 64
+constexpr int kColD2 = kColD1 + kNB1 * C1;                // 192
+constexpr int kTmemCols = 512;                            // 192 + 256 = 448 -> 512
+constexpr int kWp = 27, kHp = 27;       // conv2 input map with halo
+constexpr int kT2 = 6;                  // conv2 tiles: y blocks {0, 8} x x blocks {0, 8, 16}
+constexpr int kK2 = 9 * C1 / 16;        // 18 K16 steps for conv2
+constexpr int kPlaneRows = kHp * kWp + 1;  // rho = q + 1, q in [-1, 729)
+constexpr int kPlaneBytes = kPlaneRows * 16;  // 11,680
+constexpr int kActBytes = (C1 / 8) * kPlaneBytes;  // 46,720
+constexpr int wBuild0 = 3, wEp1_0 = 7, wEp2_0 = 15;
+// smem offsets (bytes)
+constexpr int oB1 = 0;                                   // conv1 weights [4][32][8]
+constexpr int oB2 = oB1 + (kK1 / 8) * C1 * 16;           // conv2 weights [36][64][8]
+constexpr int oAct = oB2 + 9 * (C1 / 8) * C2 * 16;       // 2 x conv2 operand planes
+constexpr int oIn = oAct + 2 * kActBytes;                // 2 x u8 frames
+constexpr int oX = oIn + 2 * kInBytes;                   // bf16 image [52][52][4]
+constexpr int oLut = oX + kInP * kXs * 8;                // bf16 LUT [3][256]
+constexpr int oBias = oLut + 3 * 256 * 2;                // (32 + 64) x 4
+constexpr int oBar = oBias + (C1 + C2) * 4;
+constexpr int kNumBars = 2 + 2 + 2 * kA1Stages + 2 * kNB1 + 2 + 2 + 2 * kNB2 + 1;
+constexpr int kSmem = oBar + kNumBars * 8 + 16;
+}  // namespace fz
+
+NS_DEV void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+NS_DEV uint16_t f2bf_u(float v) {
+  __nv_bfloat16 h = __float2bfloat16_rn(v);
+  return *reinterpret_cast<uint16_t*>(&h);
+}
+NS_DEV uint32_t pack_bf2(float lo, float hi) {
+  return (uint32_t)f2bf_u(lo) | ((uint32_t)f2bf_u(hi) << 16);
+}
+// D[tmem] (+)= A[tmem] * B[smem]^T (kind::f16, A in tensor memory).
+NS_DEV void umma_bf16_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; "
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }" ::"r"(d),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+NS_DEV void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+NS_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__global__ void __launch_bounds__(fz::kThreads, 1)
+conv12_fused_kernel(FusedArgs A) {
+  using namespace fz;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int64_t n = min(*A.n_dev, A.n_max);
+  const int64_t cnt = min(n - A.chunk_base, A.chunk_len);
+  if (cnt <= 0 || blockIdx.x >= cnt) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + oBar);
+  uint64_t* in_full = bars + 0;                 // [2]
+  uint64_t* in_empty = in_full + 2;             // [2] 128 builder arrivals
+  uint64_t* a1_full = in_empty + 2;             // [kA1Stages] 128 builder arrivals
+  uint64_t* a1_empty = a1_full + kA1Stages;     // [kA1Stages] MMA commit
+  uint64_t* t1_full = a1_empty + kA1Stages;     // [kNB1] MMA commit
+  uint64_t* t1_empty = t1_full + kNB1;          // [kNB1] 128 ep1 arrivals (one ep1 group)
+  uint64_t* act_full = t1_empty + kNB1;         // [2] 256 ep1 arrivals (both groups)
+  uint64_t* act_empty = act_full + 2;           // [2] MMA commit
+  uint64_t* t2_full = act_empty + 2;            // [kNB2] MMA commit
+  uint64_t* t2_empty = t2_full + kNB2;          // [kNB2] 128 ep2 arrivals
+  uint64_t* w_full = t2_empty + kNB2;           // weights loaded
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
+  float* bias1 = reinterpret_cast<float*>(smem + oBias);
+  float* bias2 = bias1 + C1;
+  uint16_t* lut = reinterpret_cast<uint16_t*>(smem + oLut);
+  uint2* X = reinterpret_cast<uint2*>(smem + oX);  // one 8-byte (4 x bf16) cell per pixel
+
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&in_full[s], 1);
+      mbar_init(&in_empty[s], 128);
+      mbar_init(&act_full[s], 256);
+      mbar_init(&act_empty[s], 1);
+    }
+    for (int s = 0; s < kA1Stages; ++s) {
+      mbar_init(&a1_full[s], 128);
+      mbar_init(&a1_empty[s], 1);
+    }
+    for (int s = 0; s < kNB1; ++s) {
+      mbar_init(&t1_full[s], 1);
+      mbar_init(&t1_empty[s], 128);
+    }
+    for (int s = 0; s < kNB2; ++s) {
+      mbar_init(&t2_full[s], 1);
+      mbar_init(&t2_empty[s], 128);
+    }
+    mbar_init(w_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  // zero both conv2 operand buffers once: the halo ring and row q=-1 stay zero,
+  // epilogue 1 only ever writes interior cells
+  for (int e = tid; e < 2 * kActBytes / 16; e += blockDim.x)
+    reinterpret_cast<uint4*>(smem + oAct)[e] = make_uint4(0, 0, 0, 0);
+  for (int e = tid; e < kInP * kXs; e += blockDim.x) X[e] = make_uint2(0, 0);  // zero halo
+  // normalisation LUT: x = bf16_RNE(clamp(((float)g - mu_c) / 127.5f, -1, 1)), exact fp32
+  for (int e = tid; e < 3 * 256; e += blockDim.x) {
+    const int c = e >> 8, g = e & 255;
+    const float mu = c == 0 ? A.mean[0] : (c == 1 ? A.mean[1] : A.mean[2]);
+    const float v = fminf(fmaxf(((float)g - mu) / 127.5f, -1.0f), 1.0f);
+    lut[e] = f2bf_u(v);
+  }
+  for (int e = tid; e < C1; e += blockDim.x) bias1[e] = A.b1[e];
+  for (int e = tid; e < C2; e += blockDim.x) bias2[e] = A.b2[e];
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int64_t my_frames = (cnt - blockIdx.x + gridDim.x - 1) / gridDim.x;
+
+  if (warp == 0) {
+    // ===================================================== producer
+    if (lane == 0) {
+      mbar_arrive_expect_tx(w_full, (kK1 / 8) * C1 * 16 + 9 * (C1 / 8) * C2 * 16);
+      bulk_g2s(smem + oB1, A.w1, (kK1 / 8) * C1 * 16, w_full);
+      bulk_g2s(smem + oB2, A.w2, 9 * (C1 / 8) * C2 * 16, w_full);
+      for (int64_t it = 0; it < my_frames; ++it) {
+        const int s = (int)(it & 1);
+        if (it >= 2) mbar_wait(&in_empty[s], (uint32_t)(((it >> 1) - 1) & 1));
+        const int64_t g = A.chunk_base + blockIdx.x + it * gridDim.x;
+        const int64_t f = A.idx ? (int64_t)A.idx[g] : g;
+        mbar_arrive_expect_tx(&in_full[s], kInBytes);
+        bulk_g2s(smem + oIn + s * kInBytes, A.small + f * A.small_pitch, kInBytes, &in_full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // ===================================================== conv1 MMA issuer (A in TMEM)
+    if (lane == 0) {
+      constexpr uint32_t id1 = idesc_bf16_f32(128, C1);
+      const uint32_t sB1 = smem_u32(smem + oB1);
+      mbar_wait(w_full, 0);
+      uint64_t u1 = 0;
+      for (int64_t it = 0; it < my_frames; ++it) {
+        for (int t = 0; t < kT1; t += 2, u1 += 2) {
+          int a[2], b[2];
+          for (int q = 0; q < 2; ++q) {
+            const uint64_t u = u1 + q;
+            a[q] = (int)(u % kA1Stages);
+            b[q] = (int)(u % kNB1);
+            mbar_wait(&a1_full[a[q]], (uint32_t)((u / kA1Stages) & 1));
+            if (u >= kNB1) mbar_wait(&t1_empty[b[q]], (uint32_t)(((u / kNB1) - 1) & 1));
+          }
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < kK1 / 16; ++kk)
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+              umma_bf16_ts(tmem + kColD1 + b[q] * C1, tmem + kColA1 + a[q] * kA1Cols + kk * 8,
+                           sdesc(sB1 + kk * 2 * C1 * 16, C1 * 16, 128), id1, kk);
+          for (int q = 0; q < 2; ++q) {
+            umma_commit(&a1_empty[a[q]]);
+            umma_commit(&t1_full[b[q]]);
+          }
+        }
+      }
+    }
+  } else if (warp == 2) {
+    // ===================================================== conv2 MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t id2 = idesc_bf16_f32(128, C2);
+      const uint32_t sB2 = smem_u32(smem + oB2), sAct = smem_u32(smem + oAct);
+      mbar_wait(w_full, 0);
+      uint64_t u2 = 0;
+      for (int64_t it = 0; it < my_frames; ++it) {
+        const int pb = (int)(it & 1);
+        mbar_wait(&act_full[pb], (uint32_t)((it >> 1) & 1));
+        for (int t = 0; t < kT2; t += 2, u2 += 2) {
+          int b[2], q0[2];
+          for (int q = 0; q < 2; ++q) {
+            const uint64_t u = u2 + q;
+            b[q] = (int)(u % kNB2);
+            const int yb = ((t + q) / 3) * 8, xb = ((t + q) % 3) * 8;
+            q0[q] = (yb + 1) * kWp + (xb + 1);
+            if (u >= kNB2) mbar_wait(&t2_empty[b[q]], (uint32_t)(((u / kNB2) - 1) & 1));
+          }
+          tc_fence_after();
+          const uint32_t abase = sAct + pb * kActBytes;
+#pragma unroll 1
+          for (int ks = 0; ks < kK2; ++ks) {
+            const int tap = ks >> 1, cg = (ks & 1) * 2;  // 4 channel groups per tap, 2 per step
+            const int shift = (tap / 3 - 1) * kWp + (tap % 3 - 1);
+            const uint64_t bd = sdesc(sB2 + (tap * 4 + cg) * C2 * 16, C2 * 16, 128);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              // 16 groups of 8 pixels, one image row apart: SBO = Wp * 16 bytes
+              const uint64_t ad = sdesc(abase + cg * kPlaneBytes + (uint32_t)(q0[q] + shift + 1) * 16,
+                                        kPlaneBytes, kWp * 16);
+              umma_bf16(tmem + kColD2 + b[q] * C2, ad, bd, id2, ks > 0 ? 1u : 0u);
+            }
+          }
+          for (int q = 0; q < 2; ++q) umma_commit(&t2_full[b[q]]);
+        }
+        umma_commit(&act_empty[pb]);
+      }
+    }
+  } else if (warp < wEp1_0) {
+    // ===================================================== builders
+    const int lg = (warp & 3) * 32;
+    const int bt = lg + lane;  // im2col row = TMEM lane
+    uint64_t u1 = 0;
+    for (int64_t it = 0; it < my_frames; ++it) {
+      const int s = (int)(it & 1);
+      mbar_wait(&in_full[s], (uint32_t)((it >> 1) & 1));
+      nbar_sync(1, 128);  // previous frame's rows are all built: X may be overwritten
+      const uint8_t* in = smem + oIn + s * kInBytes;
+      for (int p = bt; p < kIn * kIn; p += 128) {
+        const int y = p / kIn, x = p - kIn * y;
+        const uint8_t* px = in + 3 * p;
+        X[(y + 1) * kXs + (x + 1)] =
+            make_uint2((uint32_t)lut[px[0]] | ((uint32_t)lut[256 + px[1]] << 16),
+                       (uint32_t)lut[512 + px[2]]);
+      }
+      mbar_arrive(&in_empty[s]);
+      nbar_sync(1, 128);  // X complete
+      for (int t = 0; t < kT1; ++t, ++u1) {
+        const int a = (int)(u1 % kA1Stages);
+        if (u1 >= kA1Stages) mbar_wait(&a1_empty[a], (uint32_t)(((u1 / kA1Stages) - 1) & 1));
+        const int w = t * 32 + (bt >> 2), pq = bt & 3;
+        uint32_t v[16];
+        if (w < kP1 * kP1) {
+          const int yp = w / kP1, xp = w - kP1 * yp;
+          const int y = 2 * yp + (pq >> 1), x = 2 * xp + (pq & 1);
+          const uint2* base = X + y * kXs + x;
+          uint32_t h[27];  // 27 bf16 in (tap, channel) order, one per 32-bit register
+#pragma unroll
+          for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+            for (int kx = 0; kx < 3; ++kx) {
+              const uint2 c = base[ky * kXs + kx];
+              const int k = (ky * 3 + kx) * 3;
+              h[k] = c.x & 0xFFFFu;
+              h[k + 1] = c.x >> 16;
+              h[k + 2] = c.y & 0xFFFFu;
+            }
+#pragma unroll
+          for (int j = 0; j < 13; ++j) v[j] = h[2 * j] | (h[2 * j + 1] << 16);
+          v[13] = h[26];
+          v[14] = 0;
+          v[15] = 0;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = 0;
+        }
+        tc_fence_after();
+        tmem_st16(tmem + ((uint32_t)lg << 16) + kColA1 + a * kA1Cols, v);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&a1_full[a]);
+      }
+    }
+  } else if (warp < wEp2_0) {
+    // ===================================================== epilogue 1 (two groups, alternate tiles)
+    const int grp = (warp - wEp1_0) >> 2;
+    const int lg = (warp & 3) * 32;       // TMEM lane group of this warp
+    const int row = lg + lane;            // im2col row in the tile
+    float b1r[C1];  // conv1 bias in registers (keeps shared-memory bandwidth for the MMAs)
+#pragma unroll
+    for (int c = 0; c < C1; ++c) b1r[c] = bias1[c];
+    const int k4 = lane & 3;  // after the butterfly all 4 lanes of a window hold the max;
+                              // lane k4 stores bytes [8*k4, 8*k4+8) of the window's 32 B
+    uint64_t ut1 = 0;
+    for (int64_t it = 0; it < my_frames; ++it) {
+      const int pb = (int)(it & 1);
+      if (it >= 2) mbar_wait(&act_empty[pb], (uint32_t)(((it >> 1) - 1) & 1));
+      uint8_t* planes = smem + oAct + pb * kActBytes;
+      for (int t = 0; t < kT1; ++t, ++ut1) {
+        if ((t & 1) != grp) continue;
+        const int b = (int)(ut1 % kNB1);
+        mbar_wait(&t1_full[b], (uint32_t)((ut1 / kNB1) & 1));
+        tc_fence_after();
+        const int w = t * 32 + (row >> 2);
+        const bool valid = w < kP1 * kP1;
+        const int yp = w / kP1, xp = w - kP1 * (w / kP1);
+        const int rho = (yp + 1) * kWp + (xp + 1) + 1;
+#pragma unroll
+        for (int cb = 0; cb < C1 / 16; ++cb) {
+          uint32_t r[16];
+          tmem_ld16(tmem + ((uint32_t)lg << 16) + kColD1 + b * C1 + cb * 16, r);
+          tmem_ld_wait();
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            // ReLU output is >= +0, so max over bf16 bit patterns == max over values
+            uint32_t v = relu_bf16x2(__uint_as_float(r[2 * j]) + b1r[cb * 16 + 2 * j],
+                                     __uint_as_float(r[2 * j + 1]) + b1r[cb * 16 + 2 * j + 1]);
+            v = __vmaxu2(v, __shfl_xor_sync(0xffffffffu, v, 1));
+            v = __vmaxu2(v, __shfl_xor_sync(0xffffffffu, v, 2));
+            pk[j] = v;
+          }
+          if (valid) {
+            const uint32_t lo = k4 == 0 ? pk[0] : k4 == 1 ? pk[2] : k4 == 2 ? pk[4] : pk[6];
+            const uint32_t hi = k4 == 0 ? pk[1] : k4 == 1 ? pk[3] : k4 == 2 ? pk[5] : pk[7];
+            *reinterpret_cast<uint2*>(planes + (2 * cb + (k4 >> 1)) * kPlaneBytes + rho * 16 +
+                                      (k4 & 1) * 8) = make_uint2(lo, hi);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&t1_empty[b]);
+      }
+      fence_proxy_async_smem();  // planes written by threads -> read by the tensor core
+      mbar_arrive(&act_full[pb]);
+    }
+  } else {
+    // ===================================================== epilogue 2
+    const int lg = (warp & 3) * 32;
+    const int et = tid - wEp2_0 * 32;  // 0..127
+    // lane -> conv position inside the tile: 4 conv rows x 8 conv columns per warp
+    const int rl = (warp & 3) * 4 + (lane >> 3), cl = lane & 7;
+    const bool pool_lane = ((lane & 1) == 0) && (((lane >> 3) & 1) == 0);
+    uint64_t ut2 = 0;
+    constexpr int kHpool = 12, kHo = kHpool + 2;  // pooled 12x12 (+ halo for layer 3)
+    for (int64_t it = 0; it < my_frames; ++it) {
+      const int64_t i = blockIdx.x + it * gridDim.x;  // chunk-relative frame
+      if (!A.to_features) {   // zero the halo ring of the layer-3 map
+        uint8_t* outf = A.out + i * A.out_frame_bytes;
+        for (int e = et; e < (C2 / 8) * 4 * (kHo - 1); e += 128) {
+          const int cg = e / (4 * (kHo - 1)), h = e % (4 * (kHo - 1));
+          const int side = h / (kHo - 1), s = h % (kHo - 1);
+          const int yy = side == 0 ? 0 : side == 1 ? s : side == 2 ? kHo - 1 : s + 1;
+          const int xx = side == 0 ? s : side == 1 ? kHo - 1 : side == 2 ? s + 1 : 0;
+          *reinterpret_cast<uint4*>(outf + (size_t)cg * kHo * kHo * 16 + (yy * kHo + xx) * 16) =
+              make_uint4(0, 0, 0, 0);
+        }
+      }
+      for (int t = 0; t < kT2; ++t, ++ut2) {
+        const int b = (int)(ut2 % kNB2);
+        mbar_wait(&t2_full[b], (uint32_t)((ut2 / kNB2) & 1));
+        tc_fence_after();
+        const int yb = (t / 3) * 8, xb = (t % 3) * 8;
+        const int yc = yb + rl, xc = xb + cl;                 // conv output position
+        // the second y block re-computes conv rows 8..15: only rows >= 16 are new
+        const bool keep = pool_lane && yc < 24 && (yb == 0 || yc >= 16);
+        const int yp = yc >> 1, xp = xc >> 1;
+#pragma unroll
+        for (int g = 0; g < C2 / 16; ++g) {
+          uint32_t r[16];
+          tmem_ld16(tmem + ((uint32_t)lg << 16) + kColD2 + b * C2 + g * 16, r);
+          tmem_ld_wait();
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint32_t v = relu_bf16x2(__uint_as_float(r[2 * j]) + bias2[g * 16 + 2 * j],
+                                     __uint_as_float(r[2 * j + 1]) + bias2[g * 16 + 2 * j + 1]);
+            v = __vmaxu2(v, __shfl_xor_sync(0xffffffffu, v, 1));   // x pair
+            v = __vmaxu2(v, __shfl_xor_sync(0xffffffffu, v, 8));   // y pair
+            pk[j] = v;
+          }
+          if (keep) {
+            const uint4 o0 = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            const uint4 o1 = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            const int cgo = g * 2;
+            if (A.to_features) {
+              const int64_t kc = ((int64_t)(yp * kHpool + xp) * C2) / 8 + cgo;
+              uint8_t* dst = A.out + (i / 128) * ((int64_t)A.K_feat * 256) + kc * 2048 + (i % 128) * 16;
+              *reinterpret_cast<uint4*>(dst) = o0;
+              *reinterpret_cast<uint4*>(dst + 2048) = o1;
+            } else {
+              uint8_t* dst = A.out + i * A.out_frame_bytes + (size_t)((yp + 1) * kHo + (xp + 1)) * 16;
+              *reinterpret_cast<uint4*>(dst + (size_t)cgo * kHo * kHo * 16) = o0;
+              *reinterpret_cast<uint4*>(dst + (size_t)(cgo + 1) * kHo * kHo * 16) = o1;
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&t2_empty[b]);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
+}
+
+size_t conv12_fused_smem() { return (size_t)fz::kSmem; }
+
+noscope_status launch_conv12_fused(const FusedArgs& a, int grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(conv12_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         fz::kSmem);
+    attr = true;
+  }
+  conv12_fused_kernel<<<grid, fz::kThreads, fz::kSmem, st>>>(a);
+  NS_LAUNCH_CHECK();
+  count_launch();
+  return NOSCOPE_OK;
+}
+
+}  // namespace ns

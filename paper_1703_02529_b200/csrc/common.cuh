@@ -34,13 +34,16 @@ NS_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 NS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  // try_wait with a suspend-time hint: the waiting thread sleeps in hardware
+  // until the phase completes (or ~0.5 ms pass) instead of re-issuing the
+  // check, so idle roles do not steal issue slots from the working warps.
   uint32_t addr = smem_u32(bar), done;
   do {
     asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; "
         "selp.u32 %0, 1, 0, p; }"
         : "=r"(done)
-        : "r"(addr), "r"(parity)
+        : "r"(addr), "r"(parity), "r"(500000u)
         : "memory");
   } while (!done);
 }
@@ -149,6 +152,16 @@ NS_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "memory");
 }
 NS_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ReLU that always yields +0 for non-positive inputs (so bf16 bit patterns of
+// ReLU outputs order like their values — used by the integer max pools).
+NS_DEV float relu(float x) { return __int_as_float(max(__float_as_int(x), 0)); }
+// bf16x2 {lo, hi} = (bf16_RNE(max(lo, 0)), bf16_RNE(max(hi, 0))) in one instruction.
+NS_DEV uint32_t relu_bf16x2(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
 
 // ---------------------------------------------------------------- reductions
 template <typename T>

@@ -111,6 +111,25 @@ noscope_status launch_labels(const noscope_dd_config& cfg, int64_t tau0, int64_t
                              void* lws, cudaStream_t st);
 
 // Specialized CNN.
+// Fused conv1+conv2 (base_filters = 32), cnn_fused.cu.
+struct FusedArgs {
+  const uint8_t* small;
+  int64_t small_pitch;
+  const int32_t* idx;
+  const int64_t* n_dev;
+  int64_t n_max, chunk_base, chunk_len;
+  const uint8_t* w1;   // packed [4][32][8]
+  const uint8_t* w2;   // packed [36][64][8]
+  const float* b1;
+  const float* b2;
+  float mean[3];
+  int to_features;     // 1: FC feature tiles, 0: haloed 12x12x64 map (layer-3 input)
+  uint8_t* out;
+  int K_feat;          // feature length (to_features)
+  int64_t out_frame_bytes;  // haloed map bytes per frame (!to_features)
+};
+size_t conv12_fused_smem();
+noscope_status launch_conv12_fused(const FusedArgs& a, int grid, cudaStream_t st);
 size_t cnn_ws_bytes(const noscope_cnn_arch& a, int64_t n_max);
 noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& w,
                           const uint8_t* small, int64_t small_pitch, const int32_t* idx,

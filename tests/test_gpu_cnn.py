@@ -40,20 +40,22 @@ def test_cnn_logits_vs_oracle(arch):
 
 
 def test_conv1_activation_map():
+    """Layer-level parity of conv1 (the base_filters = 64 path materialises the
+    haloed conv1 map in the workspace; base_filters = 32 keeps it on chip)."""
     nsm = ns()
-    arch = sg.CnnArch(2, 32, 32)
+    arch = sg.CnnArch(2, 64, 32)
     n = 5
     small, g = _small(n, 12)
     w = sg.he_normal_weights(arch, 4)
     W = nsm.Weights(w)
-    A = nsm.Arch(2, 32, 32)
+    A = nsm.Arch(2, 64, 32)
     ws = nsm.workspace(nsm.OP_SPECIALIZED_INFER, None, A, n)
     nsm.noscope_specialized_infer(A, W, torch.from_numpy(small).cuda(), ws=ws)
     torch.cuda.synchronize()
     lay = nsm.debug_cnn_layout(A, n)
     off, fb = lay[0], lay[1]
-    act = ws[off:off + n * fb].cpu().numpy().view(np.uint16).reshape(n, 4, 27, 27, 8)
-    got = act.transpose(0, 2, 3, 1, 4).reshape(n, 27, 27, 32)
+    act = ws[off:off + n * fb].cpu().numpy().view(np.uint16).reshape(n, 8, 27, 27, 8)
+    got = act.transpose(0, 2, 3, 1, 4).reshape(n, 27, 27, 64)
     got = (got.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
     x = O.normalize_input(g, arch.chan_mean)
     a1 = O.conv3x3_same(x, O.bf16_bits_to_f64(w["conv_w"][0]), w["conv_b"][0].astype(np.float64))
