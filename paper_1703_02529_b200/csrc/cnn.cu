@@ -702,6 +702,10 @@ noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& 
   uint8_t* ws = reinterpret_cast<uint8_t*>(ws_v);
   // pack weights into the canonical UMMA layouts
   pack(w.conv_w[0], P.C, 27, 32, P.C, ws + P.w1_off, st);
+  if (P.C == 32) {  // fused path: bias folded into K columns 27/28 of conv1
+    noscope_status sb = pack_conv12_bias(w.conv_b[0], ws + P.w1_off, st);
+    if (sb != NOSCOPE_OK) return sb;
+  }
   for (int l = 1; l < P.L; ++l) {
     const LayerPlan& L = P.lay[l];
     pack(w.conv_w[l], L.cout, 9 * L.cin, 9 * L.cin, L.pass_n, ws + L.w_off, st);

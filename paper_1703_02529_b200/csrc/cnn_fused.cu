@@ -38,20 +38,27 @@ namespace fz {
 constexpr int kThreads = 19 * 32;
 constexpr int C1 = 32, C2 = 64;
 constexpr int kIn = 50, kInP = 52, kP1 = 25;
-// image row stride in 8-byte cells: 56 cells = 448 B puts two consecutive image
-// rows in opposite bank halves (a half-warp of im2col loads = 2 rows x 8 cells)
-constexpr int kXs = 56;
+// The zero-haloed bf16 image is stored column-polyphase: X[x & 1][y][x >> 1]
+// (8-byte cells).  im2col lanes are consecutive pool windows (x stride 2), so a
+// tap's loads are consecutive cells of one parity plane; the 40-cell row stride
+// (320 B = 64 mod 128) keeps a half-warp that wraps to the next row conflict-free.
+constexpr int kXs = 40;
+constexpr int kXPlane = kInP * kXs;   // cells per parity plane
 constexpr int kInBytes = 7504;
-constexpr int kT1 = 20;                 // conv1 tiles per frame (625 windows x 4 / 128)
-constexpr int kK1 = 32;                 // conv1 K: 27 (tap-major, 3 channels) padded to 32
+// conv1 tiles: group G of 128 pool windows x 4 window members (dy, dx): tile
+// 4G + q holds member q of windows 128G .. 128G+127, one window per TMEM lane,
+// so the 2x2 max pool is an element-wise max of 4 accumulators in one thread.
+constexpr int kG1 = 5;                  // window groups per frame (625 windows)
+constexpr int kT1 = 4 * kG1;            // 20 conv1 tiles per frame
+constexpr int kK1 = 32;                 // conv1 K: 27 (tap-major, 3 channels) + bias hi/lo + pad
 constexpr int kA1Cols = kK1 / 2;        // TMEM columns per A tile (bf16 pairs)
 constexpr int kA1Stages = 4;
-constexpr int kNB1 = 4;                 // conv1 accumulators (32 columns each)
-constexpr int kNB2 = 4;                 // conv2 accumulators (64 columns each)
+constexpr int kNG1 = 2;                 // conv1 accumulator groups (4 x 32 columns each)
+constexpr int kNB2 = 3;                 // conv2 accumulators (64 columns each)
 constexpr int kColA1 = 0;                                 // TMEM column map
 constexpr int kColD1 = kColA1 + kA1Stages * kA1Cols;      // 64
-constexpr int kColD2 = kColD1 + kNB1 * C1;                // 192
-constexpr int kTmemCols = 512;                            // 192 + 256 = 448 -> 512
+constexpr int kColD2 = kColD1 + kNG1 * 4 * C1;            // 320
+constexpr int kTmemCols = 512;                            // 320 + 192 = 512
 constexpr int kWp = 27, kHp = 27;       // conv2 input map with halo
 constexpr int kT2 = 6;                  // conv2 tiles: y blocks {0, 8} x x blocks {0, 8, 16}
 constexpr int kK2 = 9 * C1 / 16;        // 18 K16 steps for conv2
@@ -65,10 +72,10 @@ constexpr int oB2 = oB1 + (kK1 / 8) * C1 * 16;           // conv2 weights [36][6
 constexpr int oAct = oB2 + 9 * (C1 / 8) * C2 * 16;       // 2 x conv2 operand planes
 constexpr int oIn = oAct + 2 * kActBytes;                // 2 x u8 frames
 constexpr int oX = oIn + 2 * kInBytes;                   // bf16 image [52][52][4]
-constexpr int oLut = oX + kInP * kXs * 8;                // bf16 LUT [3][256]
+constexpr int oLut = oX + 2 * kXPlane * 8;               // bf16 LUT [3][256]
 constexpr int oBias = oLut + 3 * 256 * 2;                // (32 + 64) x 4
 constexpr int oBar = oBias + (C1 + C2) * 4;
-constexpr int kNumBars = 2 + 2 + 2 * kA1Stages + 2 * kNB1 + 2 + 2 + 2 * kNB2 + 1;
+constexpr int kNumBars = 2 + 2 + 2 * kA1Stages + 2 * kNG1 + 2 + 2 + 2 * kNB2 + 1;
 constexpr int kSmem = oBar + kNumBars * 8 + 16;
 }  // namespace fz
 
@@ -113,9 +120,9 @@ conv12_fused_kernel(FusedArgs A) {
   uint64_t* in_empty = in_full + 2;             // [2] 128 builder arrivals
   uint64_t* a1_full = in_empty + 2;             // [kA1Stages] 128 builder arrivals
   uint64_t* a1_empty = a1_full + kA1Stages;     // [kA1Stages] MMA commit
-  uint64_t* t1_full = a1_empty + kA1Stages;     // [kNB1] MMA commit
-  uint64_t* t1_empty = t1_full + kNB1;          // [kNB1] 128 ep1 arrivals (one ep1 group)
-  uint64_t* act_full = t1_empty + kNB1;         // [2] 256 ep1 arrivals (both groups)
+  uint64_t* t1_full = a1_empty + kA1Stages;     // [kNG1] MMA commit after a group's 4 tiles
+  uint64_t* t1_empty = t1_full + kNG1;          // [kNG1] 128 ep1 arrivals (one ep1 group)
+  uint64_t* act_full = t1_empty + kNG1;         // [2] 256 ep1 arrivals (both groups)
   uint64_t* act_empty = act_full + 2;           // [2] MMA commit
   uint64_t* t2_full = act_empty + 2;            // [kNB2] MMA commit
   uint64_t* t2_empty = t2_full + kNB2;          // [kNB2] 128 ep2 arrivals
@@ -137,7 +144,7 @@ conv12_fused_kernel(FusedArgs A) {
       mbar_init(&a1_full[s], 128);
       mbar_init(&a1_empty[s], 1);
     }
-    for (int s = 0; s < kNB1; ++s) {
+    for (int s = 0; s < kNG1; ++s) {
       mbar_init(&t1_full[s], 1);
       mbar_init(&t1_empty[s], 128);
     }
@@ -153,7 +160,7 @@ conv12_fused_kernel(FusedArgs A) {
   // epilogue 1 only ever writes interior cells
   for (int e = tid; e < 2 * kActBytes / 16; e += blockDim.x)
     reinterpret_cast<uint4*>(smem + oAct)[e] = make_uint4(0, 0, 0, 0);
-  for (int e = tid; e < kInP * kXs; e += blockDim.x) X[e] = make_uint2(0, 0);  // zero halo
+  for (int e = tid; e < 2 * kXPlane; e += blockDim.x) X[e] = make_uint2(0, 0);  // zero halo
   // normalisation LUT: x = bf16_RNE(clamp(((float)g - mu_c) / 127.5f, -1, 1)), exact fp32
   for (int e = tid; e < 3 * 256; e += blockDim.x) {
     const int c = e >> 8, g = e & 255;
@@ -191,28 +198,30 @@ conv12_fused_kernel(FusedArgs A) {
       constexpr uint32_t id1 = idesc_bf16_f32(128, C1);
       const uint32_t sB1 = smem_u32(smem + oB1);
       mbar_wait(w_full, 0);
-      uint64_t u1 = 0;
+      uint64_t u1 = 0;  // global conv1 tile sequence; group = u1 / 4, member = u1 % 4
       for (int64_t it = 0; it < my_frames; ++it) {
         for (int t = 0; t < kT1; t += 2, u1 += 2) {
-          int a[2], b[2];
+          const uint64_t ug = u1 >> 2;           // global window-group sequence
+          const int gb = (int)(ug % kNG1);
+          if ((u1 & 3) == 0 && ug >= kNG1)       // group's accumulators drained by epilogue 1?
+            mbar_wait(&t1_empty[gb], (uint32_t)(((ug / kNG1) - 1) & 1));
+          int a[2];
           for (int q = 0; q < 2; ++q) {
             const uint64_t u = u1 + q;
             a[q] = (int)(u % kA1Stages);
-            b[q] = (int)(u % kNB1);
             mbar_wait(&a1_full[a[q]], (uint32_t)((u / kA1Stages) & 1));
-            if (u >= kNB1) mbar_wait(&t1_empty[b[q]], (uint32_t)(((u / kNB1) - 1) & 1));
           }
           tc_fence_after();
+          const uint64_t bd0 = sdesc(sB1, C1 * 16, 128);
 #pragma unroll
           for (int kk = 0; kk < kK1 / 16; ++kk)
 #pragma unroll
             for (int q = 0; q < 2; ++q)
-              umma_bf16_ts(tmem + kColD1 + b[q] * C1, tmem + kColA1 + a[q] * kA1Cols + kk * 8,
-                           sdesc(sB1 + kk * 2 * C1 * 16, C1 * 16, 128), id1, kk);
-          for (int q = 0; q < 2; ++q) {
-            umma_commit(&a1_empty[a[q]]);
-            umma_commit(&t1_full[b[q]]);
-          }
+              umma_bf16_ts(tmem + kColD1 + (gb * 4 + (int)((u1 + q) & 3)) * C1,
+                           tmem + kColA1 + a[q] * kA1Cols + kk * 8,
+                           bd0 + (uint64_t)((kk * 2 * C1 * 16) >> 4), id1, kk);
+          for (int q = 0; q < 2; ++q) umma_commit(&a1_empty[a[q]]);
+          if (((u1 + 1) & 3) == 3) umma_commit(&t1_full[gb]);  // group complete
         }
       }
     }
@@ -236,19 +245,24 @@ conv12_fused_kernel(FusedArgs A) {
             if (u >= kNB2) mbar_wait(&t2_empty[b[q]], (uint32_t)(((u / kNB2) - 1) & 1));
           }
           tc_fence_after();
+          // Descriptors = base + (byte offset >> 4) in the start-address field; all
+          // K-step offsets are compile-time constants, so the fully unrolled issue
+          // loop is one add + one tcgen05.mma per step (a per-step descriptor build
+          // made the single issuing thread the bottleneck).
           const uint32_t abase = sAct + pb * kActBytes;
-#pragma unroll 1
+          // 16 groups of 8 pixels, one image row apart: SBO = Wp * 16 bytes
+          const uint64_t ad0 = sdesc(abase + (uint32_t)(q0[0] + 1) * 16, kPlaneBytes, kWp * 16);
+          const uint64_t ad1 = sdesc(abase + (uint32_t)(q0[1] + 1) * 16, kPlaneBytes, kWp * 16);
+          const uint64_t bd0 = sdesc(sB2, C2 * 16, 128);
+          const uint32_t d0 = tmem + kColD2 + b[0] * C2, d1 = tmem + kColD2 + b[1] * C2;
+#pragma unroll
           for (int ks = 0; ks < kK2; ++ks) {
             const int tap = ks >> 1, cg = (ks & 1) * 2;  // 4 channel groups per tap, 2 per step
             const int shift = (tap / 3 - 1) * kWp + (tap % 3 - 1);
-            const uint64_t bd = sdesc(sB2 + (tap * 4 + cg) * C2 * 16, C2 * 16, 128);
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              // 16 groups of 8 pixels, one image row apart: SBO = Wp * 16 bytes
-              const uint64_t ad = sdesc(abase + cg * kPlaneBytes + (uint32_t)(q0[q] + shift + 1) * 16,
-                                        kPlaneBytes, kWp * 16);
-              umma_bf16(tmem + kColD2 + b[q] * C2, ad, bd, id2, ks > 0 ? 1u : 0u);
-            }
+            const uint64_t aoff = (uint64_t)((cg * kPlaneBytes + shift * 16) >> 4);
+            const uint64_t bd = bd0 + (uint64_t)(((tap * 4 + cg) * C2 * 16) >> 4);
+            umma_bf16(d0, ad0 + aoff, bd, id2, ks > 0 ? 1u : 0u);
+            umma_bf16(d1, ad1 + aoff, bd, id2, ks > 0 ? 1u : 0u);
           }
           for (int q = 0; q < 2; ++q) umma_commit(&t2_full[b[q]]);
         }
@@ -268,7 +282,7 @@ conv12_fused_kernel(FusedArgs A) {
       for (int p = bt; p < kIn * kIn; p += 128) {
         const int y = p / kIn, x = p - kIn * y;
         const uint8_t* px = in + 3 * p;
-        X[(y + 1) * kXs + (x + 1)] =
+        X[((x + 1) & 1) * kXPlane + (y + 1) * kXs + ((x + 1) >> 1)] =
             make_uint2((uint32_t)lut[px[0]] | ((uint32_t)lut[256 + px[1]] << 16),
                        (uint32_t)lut[512 + px[2]]);
       }
@@ -277,18 +291,21 @@ conv12_fused_kernel(FusedArgs A) {
       for (int t = 0; t < kT1; ++t, ++u1) {
         const int a = (int)(u1 % kA1Stages);
         if (u1 >= kA1Stages) mbar_wait(&a1_empty[a], (uint32_t)(((u1 / kA1Stages) - 1) & 1));
-        const int w = t * 32 + (bt >> 2), pq = bt & 3;
+        // tile t = 4G + q: window w = 128G + row, window member q = (dy, dx)
+        const int w = (t >> 2) * 128 + bt, pq = t & 3;
         uint32_t v[16];
         if (w < kP1 * kP1) {
           const int yp = w / kP1, xp = w - kP1 * yp;
-          const int y = 2 * yp + (pq >> 1), x = 2 * xp + (pq & 1);
-          const uint2* base = X + y * kXs + x;
+          const int y = 2 * yp + (pq >> 1), dx = pq & 1;
+          // padded column x + kx = 2*xp + dx + kx -> parity (dx+kx)&1, half (dx+kx)>>1
+          const uint2* even = X + ((dx & 1) ? kXPlane : 0) + y * kXs + xp;       // kx = 0, 2
+          const uint2* odd = X + ((dx & 1) ? 0 : kXPlane) + y * kXs + xp + dx;   // kx = 1
           uint32_t h[27];  // 27 bf16 in (tap, channel) order, one per 32-bit register
 #pragma unroll
           for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
             for (int kx = 0; kx < 3; ++kx) {
-              const uint2 c = base[ky * kXs + kx];
+              const uint2 c = kx == 1 ? odd[ky * kXs] : even[ky * kXs + (kx >> 1)];
               const int k = (ky * 3 + kx) * 3;
               h[k] = c.x & 0xFFFFu;
               h[k + 1] = c.x >> 16;
@@ -296,8 +313,10 @@ conv12_fused_kernel(FusedArgs A) {
             }
 #pragma unroll
           for (int j = 0; j < 13; ++j) v[j] = h[2 * j] | (h[2 * j + 1] << 16);
-          v[13] = h[26];
-          v[14] = 0;
+          // K 27 and 28 = 1.0: the packed weights carry the bias there as a bf16
+          // hi/lo pair, so the accumulator comes out as bias + sum (no epilogue add)
+          v[13] = h[26] | (0x3F80u << 16);
+          v[14] = 0x3F80u;
           v[15] = 0;
         } else {
 #pragma unroll
@@ -311,53 +330,54 @@ conv12_fused_kernel(FusedArgs A) {
       }
     }
   } else if (warp < wEp2_0) {
-    // ===================================================== epilogue 1 (two groups, alternate tiles)
+    // ===================================================== epilogue 1 (two groups, alternate window groups)
     const int grp = (warp - wEp1_0) >> 2;
     const int lg = (warp & 3) * 32;       // TMEM lane group of this warp
-    const int row = lg + lane;            // im2col row in the tile
-    float b1r[C1];  // conv1 bias in registers (keeps shared-memory bandwidth for the MMAs)
-#pragma unroll
-    for (int c = 0; c < C1; ++c) b1r[c] = bias1[c];
-    const int k4 = lane & 3;  // after the butterfly all 4 lanes of a window hold the max;
-                              // lane k4 stores bytes [8*k4, 8*k4+8) of the window's 32 B
-    uint64_t ut1 = 0;
+    const int row = lg + lane;            // window within the group
+    uint64_t ug = 0;                      // global window-group sequence
     for (int64_t it = 0; it < my_frames; ++it) {
       const int pb = (int)(it & 1);
       if (it >= 2) mbar_wait(&act_empty[pb], (uint32_t)(((it >> 1) - 1) & 1));
       uint8_t* planes = smem + oAct + pb * kActBytes;
-      for (int t = 0; t < kT1; ++t, ++ut1) {
-        if ((t & 1) != grp) continue;
-        const int b = (int)(ut1 % kNB1);
-        mbar_wait(&t1_full[b], (uint32_t)((ut1 / kNB1) & 1));
+      for (int G = 0; G < kG1; ++G, ++ug) {
+        const int gb = (int)(ug % kNG1);
+        if (gb != grp) continue;
+        mbar_wait(&t1_full[gb], (uint32_t)((ug / kNG1) & 1));
         tc_fence_after();
-        const int w = t * 32 + (row >> 2);
+        const int w = G * 128 + row;
         const bool valid = w < kP1 * kP1;
         const int yp = w / kP1, xp = w - kP1 * (w / kP1);
         const int rho = (yp + 1) * kWp + (xp + 1) + 1;
+        const uint32_t tb = tmem + ((uint32_t)lg << 16) + kColD1 + gb * 4 * C1;
 #pragma unroll
         for (int cb = 0; cb < C1 / 16; ++cb) {
-          uint32_t r[16];
-          tmem_ld16(tmem + ((uint32_t)lg << 16) + kColD1 + b * C1 + cb * 16, r);
+          // 2x2 max pool = element-wise max over the window's 4 accumulators
+          // (bias already accumulated; max, ReLU and RNE commute: all monotone)
+          uint32_t r0[16], r1[16], r2[16], r3[16];
+          tmem_ld16(tb + 0 * C1 + cb * 16, r0);
+          tmem_ld16(tb + 1 * C1 + cb * 16, r1);
+          tmem_ld16(tb + 2 * C1 + cb * 16, r2);
+          tmem_ld16(tb + 3 * C1 + cb * 16, r3);
           tmem_ld_wait();
           uint32_t pk[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            // ReLU output is >= +0, so max over bf16 bit patterns == max over values
-            uint32_t v = relu_bf16x2(__uint_as_float(r[2 * j]) + b1r[cb * 16 + 2 * j],
-                                     __uint_as_float(r[2 * j + 1]) + b1r[cb * 16 + 2 * j + 1]);
-            v = __vmaxu2(v, __shfl_xor_sync(0xffffffffu, v, 1));
-            v = __vmaxu2(v, __shfl_xor_sync(0xffffffffu, v, 2));
-            pk[j] = v;
+            const float m0 = fmaxf(fmaxf(__uint_as_float(r0[2 * j]), __uint_as_float(r1[2 * j])),
+                                   fmaxf(__uint_as_float(r2[2 * j]), __uint_as_float(r3[2 * j])));
+            const float m1 =
+                fmaxf(fmaxf(__uint_as_float(r0[2 * j + 1]), __uint_as_float(r1[2 * j + 1])),
+                      fmaxf(__uint_as_float(r2[2 * j + 1]), __uint_as_float(r3[2 * j + 1])));
+            pk[j] = relu_bf16x2(m0, m1);
           }
           if (valid) {
-            const uint32_t lo = k4 == 0 ? pk[0] : k4 == 1 ? pk[2] : k4 == 2 ? pk[4] : pk[6];
-            const uint32_t hi = k4 == 0 ? pk[1] : k4 == 1 ? pk[3] : k4 == 2 ? pk[5] : pk[7];
-            *reinterpret_cast<uint2*>(planes + (2 * cb + (k4 >> 1)) * kPlaneBytes + rho * 16 +
-                                      (k4 & 1) * 8) = make_uint2(lo, hi);
+            *reinterpret_cast<uint4*>(planes + (2 * cb) * kPlaneBytes + rho * 16) =
+                make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            *reinterpret_cast<uint4*>(planes + (2 * cb + 1) * kPlaneBytes + rho * 16) =
+                make_uint4(pk[4], pk[5], pk[6], pk[7]);
           }
         }
         tc_fence_before();
-        mbar_arrive(&t1_empty[b]);
+        mbar_arrive(&t1_empty[gb]);
       }
       fence_proxy_async_smem();  // planes written by threads -> read by the tensor core
       mbar_arrive(&act_full[pb]);
@@ -433,6 +453,26 @@ conv12_fused_kernel(FusedArgs A) {
 }
 
 size_t conv12_fused_smem() { return (size_t)fz::kSmem; }
+
+// conv1 packed weights [4 kc][32][8]: K index 27 <- bf16(bias), 28 <- bf16(bias -
+// bf16(bias)); with A[., 27] = A[., 28] = 1.0 the tensor core accumulates the
+// fp32 bias to ~2^-17 relative (fused path only; conv1_kernel adds it in fp32).
+__global__ void pack_conv1_bias_kernel(const float* __restrict__ b, uint16_t* __restrict__ out) {
+  const int n = threadIdx.x;
+  if (n >= fz::C1) return;
+  const float v = b[n];
+  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+  const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+  out[(3 * fz::C1 + n) * 8 + 3] = *reinterpret_cast<const uint16_t*>(&hi);
+  out[(3 * fz::C1 + n) * 8 + 4] = *reinterpret_cast<const uint16_t*>(&lo);
+}
+
+noscope_status pack_conv12_bias(const float* b1, uint8_t* w1_packed, cudaStream_t st) {
+  pack_conv1_bias_kernel<<<1, 32, 0, st>>>(b1, reinterpret_cast<uint16_t*>(w1_packed));
+  NS_LAUNCH_CHECK();
+  count_launch();
+  return NOSCOPE_OK;
+}
 
 noscope_status launch_conv12_fused(const FusedArgs& a, int grid, cudaStream_t st) {
   static bool attr = false;

@@ -129,6 +129,7 @@ struct FusedArgs {
   int64_t out_frame_bytes;  // haloed map bytes per frame (!to_features)
 };
 size_t conv12_fused_smem();
+noscope_status pack_conv12_bias(const float* b1, uint8_t* w1_packed, cudaStream_t st);
 noscope_status launch_conv12_fused(const FusedArgs& a, int grid, cudaStream_t st);
 size_t cnn_ws_bytes(const noscope_cnn_arch& a, int64_t n_max);
 noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& w,
