@@ -226,7 +226,7 @@ def run_ours(args):
     stage = np.mean(np.array(stage_acc), axis=0)   # 7 stages, ms
 
     hbm, bf16, bf16_sus, peak_kind = measured_peaks()
-    # dominant kernel: dd_downsample_kernel; algorithmic bytes per launch =
+    # dominant kernel: dd_kernel (fused downsample + DD score); algorithmic bytes per launch =
     # frames downsampled x (source frame read + small frame write)
     ds_bytes = n * (W_SRC * H_SRC * 3 + OUT * OUT * 3)
     ds_ms = float(stage[0])
@@ -259,12 +259,12 @@ def run_ours(args):
                    "delta_diff": dd.delta_diff, "c_low_logit": S["lo"], "c_high_logit": S["hi"],
                    "cnn": "L2C32D32", "l2_flush": "not needed: 99.5 GB input per GPU > 126 MB L2",
                    "parallelism": f"dp{world} (units sharded by stream)"},
-        "roofline": {"bound": "hbm", "kernel": "dd_downsample_kernel", "achieved": round(achieved, 1),
+        "roofline": {"bound": "hbm", "kernel": "dd_kernel", "achieved": round(achieved, 1),
                      "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
                      "peak_source": peak_kind, "traffic": traffic,
                      "algorithmic_bytes_per_launch": ds_bytes, "avg_launch_ms": round(ds_ms, 4)},
         "stage_ms": {k: round(float(v), 4) for k, v in zip(
-            ["downsample_score", "lag_score", "compaction", "cnn", "routing", "labeller",
+            ["dd_kernel", "dd_tail", "compaction", "cnn", "routing", "labeller",
              "labels_state"], stage)},
         "run_stats": stats,
         "cnn": {"frames": nf, "tflops": round(cnn_flops / (stage[3] / 1e3) / 1e12, 2) if stage[3] > 0 else None},

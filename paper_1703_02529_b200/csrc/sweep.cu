@@ -31,6 +31,13 @@ struct HistLayout {
   }
 };
 
+// Smallest power of two P with P >= n + 1 (so a P-step search can return n).
+__host__ __device__ inline int pow2_above(int n) {
+  int p = 1;
+  while (p < n + 1) p <<= 1;
+  return p;
+}
+
 NS_DEV int count_lt_d(const double* c, int n, double v) {  // #{c < v}
   int lo = 0, hi = n;
   while (lo < hi) {
@@ -66,34 +73,90 @@ sweep_hist_kernel(const double* __restrict__ s, const float* __restrict__ z,
   extern __shared__ __align__(16) uint8_t smem[];
   HistLayout L(nd, m);
   double* dc = reinterpret_cast<double*>(smem);
-  float* uc = reinterpret_cast<float*>(dc + nd);
-  uint32_t* hs = reinterpret_cast<uint32_t*>(uc + ((m + 3) & ~3));
+  const int pd = pow2_above(nd), pu = pow2_above(m);
+  float* uc = reinterpret_cast<float*>(dc + pd);
+  uint32_t* hs = reinterpret_cast<uint32_t*>(uc + pu);
   const int tid = threadIdx.x;
-  for (int t = tid; t < nd; t += blockDim.x) dc[t] = delta[t];
-  for (int t = tid; t < m; t += blockDim.x) uc[t] = u[t];
+  for (int t = tid; t < pd; t += blockDim.x) dc[t] = t < nd ? delta[t] : __longlong_as_double(0x7FF0000000000000ll);
+  for (int t = tid; t < pu; t += blockDim.x) uc[t] = t < m ? u[t] : __int_as_float(0x7F800000);
   if (privatised)
     for (size_t t = tid; t < L.tail; t += blockDim.x) hs[t] = 0u;
   __syncthreads();
   unsigned long long checked = 0;
   bool bad = false;
   const double ninf = __longlong_as_double(0xFFF0000000000000ll);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + tid; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double si = s[i];
-    const float zi = z[i];
-    const int yi = y[i] ? 1 : 0, ai = a[i] ? 1 : 0;
-    bad |= (si != si) | (zi != zi);
-    checked += (si != ninf);
-    const int d = count_lt_d(dc, nd, si);
-    const int b = count_lt_f(uc, m, zi) + count_le_f(uc, m, zi);
-    const size_t w2 = L.h2 + ((size_t)d * L.B + b) * 2 + yi;
-    const size_t w1 = L.h1 + (size_t)d * 4 + ai * 2 + yi;
-    if (privatised) {
-      atomicAdd(&hs[w2], 1u);
-      atomicAdd(&hs[w1], 1u);
-    } else {
-      atomicAdd(&hist[w2], 1ull);
-      atomicAdd(&hist[w1], 1ull);
+  // Each thread takes kU records per step (all loads issued before the searches,
+  // coalesced: record = chunk base + r * blockDim + tid), so the dependent
+  // binary-search chains of independent records overlap.
+  // The next step's records are prefetched into registers before the current
+  // step's searches run (software pipelining: loads overlap the search work).
+  constexpr int kU = 8;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x * kU;
+  double sv[kU], sn[kU];
+  float zv[kU], zn[kU];
+  uint32_t ya[kU], yn[kU];
+  auto load = [&](int64_t base, double (&sx)[kU], float (&zx)[kU], uint32_t (&yx)[kU]) {
+#pragma unroll
+    for (int r = 0; r < kU; ++r) {
+      const int64_t i = base + (int64_t)r * blockDim.x + tid;
+      if (i < n) {
+        sx[r] = __ldcs(s + i);
+        zx[r] = __ldcs(z + i);
+        yx[r] = (uint32_t)__ldcs(y + i) | ((uint32_t)__ldcs(a + i) << 8);
+      } else {
+        sx[r] = 0.0;
+        zx[r] = 0.0f;
+        yx[r] = 0x10000u;  // no record
+      }
+    }
+  };
+  int64_t base = (int64_t)blockIdx.x * blockDim.x * kU;
+  if (base < n) load(base, sn, zn, yn);
+  for (; base < n; base += step) {
+#pragma unroll
+    for (int r = 0; r < kU; ++r) {
+      sv[r] = sn[r];
+      zv[r] = zn[r];
+      ya[r] = yn[r];
+    }
+    if (base + step < n) load(base + step, sn, zn, yn);
+    // Branch-free binary searches over the +inf-padded power-of-two grids, all
+    // 2*kU searches advanced one level at a time (independent smem chains).
+    int dj[kU], lj[kU];
+#pragma unroll
+    for (int r = 0; r < kU; ++r) dj[r] = lj[r] = 0;
+    for (int st = pd >> 1; st > 0; st >>= 1) {
+#pragma unroll
+      for (int r = 0; r < kU; ++r) dj[r] += (dc[dj[r] + st - 1] < sv[r]) ? st : 0;
+    }
+    for (int st = pu >> 1; st > 0; st >>= 1) {
+#pragma unroll
+      for (int r = 0; r < kU; ++r) lj[r] += (uc[lj[r] + st - 1] < zv[r]) ? st : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < kU; ++r) {
+      if (ya[r] & 0x10000u) continue;
+      const double si = sv[r];
+      const float zi = zv[r];
+      const int yi = (ya[r] & 0xFFu) ? 1 : 0, ai = (ya[r] & 0xFF00u) ? 1 : 0;
+      bad |= (si != si) | (zi != zi);
+      checked += (si != ninf);
+      const int d = dj[r];
+      const int lt = lj[r];
+      const int b = 2 * lt + ((lt < m && uc[lt] == zi) ? 1 : 0);  // #{u<z} + #{u<=z}
+      const size_t w2 = L.h2 + ((size_t)d * L.B + b) * 2 + yi;
+      const size_t w1 = L.h1 + (size_t)d * 4 + ai * 2 + yi;
+      // H1 is only ever read at (a, y) = (1, 0) and (0, 1) (the not-fired FP and
+      // FN counts), so records with a == y skip that atomic (shared-memory
+      // atomics are this kernel's throughput limit).
+      const bool h1 = ai != yi;
+      if (privatised) {
+        atomicAdd(&hs[w2], 1u);
+        if (h1) atomicAdd(&hs[w1], 1u);
+      } else {
+        atomicAdd(&hist[w2], 1ull);
+        if (h1) atomicAdd(&hist[w1], 1ull);
+      }
     }
   }
   if (bad) atomicOr(status, 4u);
@@ -285,7 +348,7 @@ noscope_status launch_sweep(int32_t phase, const double* s, const float* z, cons
   HistLayout L(nd, m);
   if (phase & 1) {
     if (n > 0) {
-      size_t smem = (size_t)nd * 8 + (size_t)((m + 3) & ~3) * 4;
+      size_t smem = (size_t)pow2_above(nd) * 8 + (size_t)pow2_above(m) * 4;
       size_t priv = smem + L.tail * 4;
       int privatised = priv <= 200 * 1024 ? 1 : 0;
       size_t use = privatised ? priv : smem;
