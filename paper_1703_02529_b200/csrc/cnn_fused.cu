@@ -79,8 +79,6 @@ constexpr int kNumBars = 2 + 2 + 2 * kA1Stages + 2 * kNG1 + 2 + 2 + 2 * kNB2 + 1
 constexpr int kSmem = oBar + kNumBars * 8 + 16;
 }  // namespace fz
 
-NS_DEV void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
 NS_DEV uint16_t f2bf_u(float v) {
   __nv_bfloat16 h = __float2bfloat16_rn(v);
   return *reinterpret_cast<uint16_t*>(&h);
@@ -390,20 +388,18 @@ conv12_fused_kernel(FusedArgs A) {
     const int rl = (warp & 3) * 4 + (lane >> 3), cl = lane & 7;
     const bool pool_lane = ((lane & 1) == 0) && (((lane >> 3) & 1) == 0);
     uint64_t ut2 = 0;
-    constexpr int kHpool = 12, kHo = kHpool + 2;  // pooled 12x12 (+ halo for layer 3)
+    // pooled 12x12; layer-3 input in the stacked layout (internal.h): row pitch
+    // 13, 169 rows per frame, 14 leading guard rows
+    constexpr int kHpool = 12, kWqo = 13, kPo = 13 * 13, kGo = 14;
+    if (!A.to_features && blockIdx.x == 0) {  // zero the leading / trailing guards
+      for (int e = et; e < (C2 / 8) * (kGo + kWqo); e += 128) {
+        const int c = e / (kGo + kWqo), k = e % (kGo + kWqo);
+        const int64_t row = k < kGo ? k : kGo + cnt * kPo + (k - kGo);
+        *reinterpret_cast<uint4*>(A.out + ((int64_t)c * A.out_rows + row) * 16) = make_uint4(0, 0, 0, 0);
+      }
+    }
     for (int64_t it = 0; it < my_frames; ++it) {
       const int64_t i = blockIdx.x + it * gridDim.x;  // chunk-relative frame
-      if (!A.to_features) {   // zero the halo ring of the layer-3 map
-        uint8_t* outf = A.out + i * A.out_frame_bytes;
-        for (int e = et; e < (C2 / 8) * 4 * (kHo - 1); e += 128) {
-          const int cg = e / (4 * (kHo - 1)), h = e % (4 * (kHo - 1));
-          const int side = h / (kHo - 1), s = h % (kHo - 1);
-          const int yy = side == 0 ? 0 : side == 1 ? s : side == 2 ? kHo - 1 : s + 1;
-          const int xx = side == 0 ? s : side == 1 ? kHo - 1 : side == 2 ? s + 1 : 0;
-          *reinterpret_cast<uint4*>(outf + (size_t)cg * kHo * kHo * 16 + (yy * kHo + xx) * 16) =
-              make_uint4(0, 0, 0, 0);
-        }
-      }
       for (int t = 0; t < kT2; ++t, ++ut2) {
         const int b = (int)(ut2 % kNB2);
         mbar_wait(&t2_full[b], (uint32_t)((ut2 / kNB2) & 1));
@@ -437,9 +433,18 @@ conv12_fused_kernel(FusedArgs A) {
               *reinterpret_cast<uint4*>(dst) = o0;
               *reinterpret_cast<uint4*>(dst + 2048) = o1;
             } else {
-              uint8_t* dst = A.out + i * A.out_frame_bytes + (size_t)((yp + 1) * kHo + (xp + 1)) * 16;
-              *reinterpret_cast<uint4*>(dst + (size_t)cgo * kHo * kHo * 16) = o0;
-              *reinterpret_cast<uint4*>(dst + (size_t)(cgo + 1) * kHo * kHo * 16) = o1;
+              const int64_t orow = kGo + i * kPo + (yp + 1) * kWqo + xp;
+              const uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                uint4* pl = reinterpret_cast<uint4*>(A.out + (int64_t)(cgo + hh) * A.out_rows * 16);
+                pl[orow] = hh ? o1 : o0;
+                if (xp == kHpool - 1) pl[orow + 1] = z;       // separator column
+                if (yp == 0) {                                 // separator row above
+                  pl[orow - kWqo] = z;
+                  if (xp == kHpool - 1) pl[orow - kWqo + 1] = z;
+                }
+              }
             }
           }
         }

@@ -102,6 +102,27 @@ NS_DEV void tmem_dealloc(uint32_t taddr) {  // whole warp
 }
 NS_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 NS_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// Runtime-sized TMEM allocation (power of two >= 32 columns), whole warp.
+NS_DEV void tmem_alloc_rt(uint32_t* dst, uint32_t cols) {
+  switch (cols) {
+    case 32: tmem_alloc<32>(dst); break;
+    case 64: tmem_alloc<64>(dst); break;
+    case 128: tmem_alloc<128>(dst); break;
+    case 256: tmem_alloc<256>(dst); break;
+    default: tmem_alloc<512>(dst); break;
+  }
+}
+NS_DEV void tmem_dealloc_rt(uint32_t taddr, uint32_t cols) {
+  switch (cols) {
+    case 32: tmem_dealloc<32>(taddr); break;
+    case 64: tmem_dealloc<64>(taddr); break;
+    case 128: tmem_dealloc<128>(taddr); break;
+    case 256: tmem_dealloc<256>(taddr); break;
+    default: tmem_dealloc<512>(taddr); break;
+  }
+}
+// Named barrier over `n` threads (multiple of 32).
+NS_DEV void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // D[tmem] (+)= A[smem] * B[smem]^T, bf16 inputs, fp32 accumulate.
 NS_DEV void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,

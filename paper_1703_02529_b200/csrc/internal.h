@@ -123,12 +123,52 @@ struct FusedArgs {
   const float* b1;
   const float* b2;
   float mean[3];
-  int to_features;     // 1: FC feature tiles, 0: haloed 12x12x64 map (layer-3 input)
+  int to_features;     // 1: FC feature tiles, 0: stacked 12x12x64 map (layer-3 input)
   uint8_t* out;
   int K_feat;          // feature length (to_features)
-  int64_t out_frame_bytes;  // haloed map bytes per frame (!to_features)
+  int64_t out_rows;    // rows per channel-group plane of the stacked map (!to_features)
 };
 size_t conv12_fused_smem();
+
+// Generic conv layer (cnn_gemm.cu): batched implicit GEMM over the "stacked"
+// activation layout.  A map of H x W pixels x Cin channels for a chunk of F
+// frames is stored as Cin/8 planes [cg][R rows][8 ch] (bf16, 16 B per row):
+//   row(f, y, x) = G + f*P + (y + 1)*Wq + x,  Wq = W + 1, P = (H + 1)*Wq, G = Wq + 1,
+// with every other row zero: one zero row above each frame and one zero column
+// right of each row are the 3x3 conv's zero padding on all four sides (the
+// column right of row y-1 is the left neighbour of row y).
+struct ConvGGeom {
+  int cin_real, cin_eff, cout, H, W;
+  int N, passes, steps;      // MMA N (<= 256) per pass over Cout; K16 steps
+  int MT, nacc, nA, bstages; // M tiles per unit, accumulator sets, A buffers, B ring depth
+  int S, rows_blk;           // unit stride in rows; rows loaded per unit per plane
+  int64_t R;                 // rows per plane of the layer input (chunk)
+  uint32_t tmem_cols;
+  size_t oB, oStage, oWin, oBias, oBar, smem;
+};
+bool make_convg_geom(int cin_real, int cout, int H, int64_t chunk, ConvGGeom* g);
+inline int64_t sl_rows(int H, int W, int64_t frames, int64_t slack) {
+  const int64_t Wq = W + 1;
+  return (Wq + 1) + frames * (H + 1) * Wq + slack;
+}
+struct ConvGArgs {
+  ConvGGeom g;
+  const uint8_t* in;       // stacked input planes
+  const uint8_t* wpack;    // [passes][steps][2][N][8] bf16
+  const float* bias;
+  int to_features;
+  uint8_t* out;            // stacked output planes (R_out rows) or FC feature tiles
+  int64_t out_rows;
+  int K_feat;
+  const int64_t* n_dev;
+  int64_t n_max, chunk_base, chunk_len;
+};
+noscope_status launch_convg(const ConvGArgs& a, cudaStream_t st);
+noscope_status pack_convg(const uint16_t* w, const ConvGGeom& g, uint8_t* out, cudaStream_t st);
+// u8 frames (gathered by idx) -> normalised bf16 stacked 50x50 map, 8 channels (3 real)
+noscope_status launch_prep_sl(const uint8_t* small, int64_t pitch, const int32_t* idx,
+                              const int64_t* n_dev, int64_t n_max, int64_t chunk_base,
+                              int64_t chunk_len, const float mean[3], uint8_t* out, cudaStream_t st);
 noscope_status pack_conv12_bias(const float* b1, uint8_t* w1_packed, cudaStream_t st);
 noscope_status launch_conv12_fused(const FusedArgs& a, int grid, cudaStream_t st);
 size_t cnn_ws_bytes(const noscope_cnn_arch& a, int64_t n_max);

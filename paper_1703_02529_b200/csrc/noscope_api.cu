@@ -436,11 +436,12 @@ noscope_status noscope_threshold_sweep(int32_t phase, const double* s, const flo
 
 // Test/debug helper (not part of the four-call contract): internal CNN
 // activation offsets within the specialized_infer workspace, so tests can
-// check individual layers.  out[9]: act2 off, act2 frame bytes, act3 off/bytes,
-// act4 off/bytes, feature off, K, chunk.  Offsets include the 256-B header.
+// check individual layers.  out[19]: per conv layer l = 0..3 {offset of its
+// stacked input map (-1: not materialised), rows per plane, H, channels}, then
+// feature-tile offset, K, chunk.  Offsets include the 256-B header.
 int32_t noscope_debug_cnn_layout(const noscope_cnn_arch* arch, int64_t n_max, int64_t* out) {
   if (!arch || !out || !ns::cnn_debug_layout(*arch, n_max, out)) return 1;
-  for (int i : {0, 2, 4, 6})
+  for (int i : {0, 4, 8, 12, 16})
     if (out[i] >= 0) out[i] += 256;
   return 0;
 }

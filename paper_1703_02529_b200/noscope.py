@@ -352,6 +352,6 @@ def noscope_check(ws, stream=None):
 
 
 def debug_cnn_layout(arch: Arch, n_max: int):
-    out = (c_i64 * 9)()
+    out = (c_i64 * 19)()
     _check(lib().noscope_debug_cnn_layout(C.byref(arch.c()), n_max, out), "debug_cnn_layout")
     return list(out)
