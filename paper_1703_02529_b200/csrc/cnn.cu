@@ -6,8 +6,9 @@
 //   base_filters = 32: conv1+conv2 fused in one kernel (cnn_fused.cu; the conv1
 //     map never leaves the SM), then conv3/conv4 (L = 4) on the generic layer
 //     kernel (cnn_gemm.cu);
-//   base_filters = 64: input normalisation into the stacked layout, then every
-//     conv layer on the generic layer kernel (conv1 packs two taps per K16 step).
+//   base_filters = 64: conv1 on the same fused kernel without the conv2 stage
+//     (two N = 32 halves per A tile), its pooled map written to HBM in the
+//     stacked layout, then conv2..convL on the generic layer kernel.
 //   The last conv layer writes the FC feature tiles; fc_kernel does FC1 + ReLU
 //   + FC2.
 // FC: features (h, w, c) in the canonical A layout [tile][K/8][128][8] ->
@@ -151,7 +152,7 @@ fc_kernel(FcArgs A) {
 // =================================================================== host plan
 struct CnnPlan {
   int L, C, D, K;
-  bool fused;                 // conv1+conv2 in cnn_fused.cu (base_filters = 32)
+  bool fused;                 // conv2 fused into the conv1 kernel (base_filters = 32)
   int first_g;                // first layer on the generic kernel
   size_t w1_off, w2_off;      // fused: packed conv1 [4][32][8], conv2 [36][64][8]
   ConvGGeom g[4];             // generic layers first_g .. L-1
@@ -169,12 +170,12 @@ static bool make_plan(const noscope_cnn_arch& a, int64_t n_max, CnnPlan* P) {
   p.C = a.base_filters;
   p.D = a.dense;
   p.fused = p.C == 32;
-  p.first_g = p.fused ? 2 : 0;
+  p.first_g = p.fused ? 2 : 1;
   p.chunk = std::min<int64_t>(kCnnChunk, std::max<int64_t>(128, (n_max + 127) / 128 * 128));
   size_t off = 256;  // status words etc. live before the CNN region (caller offset)
+  p.w1_off = off;
+  off = align_up(off + (size_t)p.C * 32 * 2, 256);
   if (p.fused) {
-    p.w1_off = off;
-    off = align_up(off + (size_t)p.C * 32 * 2, 256);
     p.w2_off = off;
     off = align_up(off + (size_t)2 * p.C * 9 * p.C * 2, 256);
   }
@@ -255,13 +256,11 @@ noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& 
   if (n_max <= 0) return NOSCOPE_OK;
   uint8_t* ws = reinterpret_cast<uint8_t*>(ws_v);
   // pack weights into the canonical UMMA layouts
-  if (P.fused) {
-    pack(w.conv_w[0], P.C, 27, 32, P.C, ws + P.w1_off, st);
-    pack(w.conv_w[1], 2 * P.C, 9 * P.C, 9 * P.C, 2 * P.C, ws + P.w2_off, st);
-    NS_LAUNCH_CHECK();
-    noscope_status sb = pack_conv12_bias(w.conv_b[0], ws + P.w1_off, st);  // bias in K 27/28
-    if (sb != NOSCOPE_OK) return sb;
-  }
+  pack(w.conv_w[0], P.C, 27, 32, P.C, ws + P.w1_off, st);
+  if (P.fused) pack(w.conv_w[1], 2 * P.C, 9 * P.C, 9 * P.C, 2 * P.C, ws + P.w2_off, st);
+  NS_LAUNCH_CHECK();
+  noscope_status sb = pack_conv12_bias(w.conv_b[0], P.C, ws + P.w1_off, st);  // bias in K 27/28
+  if (sb != NOSCOPE_OK) return sb;
   for (int l = P.first_g; l < P.L; ++l) {
     noscope_status s = pack_convg(w.conv_w[l], P.g[l], ws + P.gw_off[l], st);
     if (s != NOSCOPE_OK) return s;
@@ -276,33 +275,28 @@ noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& 
   }
   for (int64_t base = 0; base < n_max; base += P.chunk) {
     const int64_t len = std::min<int64_t>(P.chunk, n_max - base);
-    if (P.fused) {
-      FusedArgs fa{};
-      fa.small = small;
-      fa.small_pitch = small_pitch;
-      fa.idx = idx;
-      fa.n_dev = n_dev;
-      fa.n_max = n_max;
-      fa.chunk_base = base;
-      fa.chunk_len = len;
-      fa.w1 = ws + P.w1_off;
-      fa.w2 = ws + P.w2_off;
-      fa.b1 = w.conv_b[0];
-      fa.b2 = w.conv_b[1];
-      fa.mean[0] = a.chan_mean[0];
-      fa.mean[1] = a.chan_mean[1];
-      fa.mean[2] = a.chan_mean[2];
-      fa.to_features = P.L == 2 ? 1 : 0;
-      fa.out = P.L == 2 ? ws + P.feat_off : ws + P.in_off[2];
-      fa.K_feat = P.K;
-      fa.out_rows = P.L == 2 ? 0 : P.g[2].R;
-      noscope_status s = launch_conv12_fused(fa, (int)std::min<int64_t>(len, kNumSMs), st);
-      if (s != NOSCOPE_OK) return s;
-    } else {
-      noscope_status s = launch_prep_sl(small, small_pitch, idx, n_dev, n_max, base, len,
-                                        a.chan_mean, ws + P.in_off[0], st);
-      if (s != NOSCOPE_OK) return s;
-    }
+    FusedArgs fa{};
+    fa.C1 = P.C;
+    fa.small = small;
+    fa.small_pitch = small_pitch;
+    fa.idx = idx;
+    fa.n_dev = n_dev;
+    fa.n_max = n_max;
+    fa.chunk_base = base;
+    fa.chunk_len = len;
+    fa.w1 = ws + P.w1_off;
+    fa.w2 = P.fused ? ws + P.w2_off : nullptr;
+    fa.b1 = w.conv_b[0];
+    fa.b2 = P.fused ? w.conv_b[1] : nullptr;
+    fa.mean[0] = a.chan_mean[0];
+    fa.mean[1] = a.chan_mean[1];
+    fa.mean[2] = a.chan_mean[2];
+    fa.to_features = (P.fused && P.L == 2) ? 1 : 0;
+    fa.out = fa.to_features ? ws + P.feat_off : ws + P.in_off[P.first_g];
+    fa.K_feat = P.K;
+    fa.out_rows = fa.to_features ? 0 : P.g[P.first_g].R;
+    noscope_status s = launch_conv12_fused(fa, (int)std::min<int64_t>(len, kNumSMs), st);
+    if (s != NOSCOPE_OK) return s;
     for (int l = P.first_g; l < P.L; ++l) {
       ConvGArgs c{};
       c.g = P.g[l];

@@ -1,28 +1,31 @@
-// cnn_fused.cu — layers 1+2 of the specialized CNN (§4)
-// in one warp-specialised persistent kernel for base_filters = 32: the conv1
-// output (25x25x32 pooled, bf16) is written straight into the shared-memory
-// operand planes of conv2 and never touches HBM.
+// cnn_fused.cu — layer 1 (+ layer 2) of the specialized CNN (§4,
+// P:437-456) in one warp-specialised persistent kernel, two variants:
+//   <1, true>  base_filters = 32: conv1 + conv2 fused; the conv1 output (25x25x32
+//              pooled, bf16) is written straight into the shared-memory operand
+//              planes of conv2 and never touches HBM;
+//   <2, false> base_filters = 64: conv1 only, as two N = 32 halves on the same
+//              TMEM A tile; the pooled 25x25x64 map goes to HBM in the stacked
+//              layout (internal.h) for the generic layer kernel (cnn_gemm.cu).
 //
 // Roles (19 warps):
 //   W0      producer    — cp.async.bulk of the u8 input frames (2-deep ring) and
 //                         the packed weights (once)
 //   W1      conv1 MMA   — one thread issues tcgen05.mma for conv1 with the A
 //                         operand (im2col rows) in TENSOR MEMORY (K = 27 -> 32,
-//                         N = 32); owns the TMEM allocation
+//                         N = 32 per half); owns the TMEM allocation
 //   W2      conv2 MMA   — one thread issues the shifted-window conv2 tiles
 //                         (A and B from shared memory, K = 9 x 32, N = 64)
 //   W3-W6   builders    — normalisation through a 3x256 lookup table
 //                         of the exact fp32 formula into a zero-haloed bf16 image
 //                         (4 channel slots per pixel), then one im2col row per
-//                         thread (pool-window-major: the 4 rows of a 2x2 pool
-//                         window are adjacent lanes) stored into TMEM with
-//                         tcgen05.st (no shared-memory traffic for A)
-//   W7-W14  epilogue 1  — two 4-warp groups on alternate tiles: TMEM -> bias ->
-//                         ReLU -> bf16 -> 2x2 max across the window's 4 lanes
-//                         (packed bf16x2 shuffles) -> conv2 operand planes
-//                         (double-buffered per frame)
+//                         thread stored into TMEM with tcgen05.st (no
+//                         shared-memory traffic for A)
+//   W7-W14  epilogue 1  — two 4-warp groups on alternate (window group, half):
+//                         element-wise max of the window's 4 member accumulators
+//                         -> ReLU -> bf16 -> conv2 operand planes (double-buffered
+//                         per frame) or the stacked map in HBM
 //   W15-W18 epilogue 2  — TMEM -> bias -> ReLU -> bf16 -> 2x2 max by shuffles ->
-//                         FC feature tiles (L = 2) or the haloed layer-3 map (L = 4)
+//                         FC feature tiles (L = 2) or the stacked layer-3 map (L = 4)
 // conv2 M tile = 16 conv rows x 8 conv columns: 16 core-matrix groups of 8
 // consecutive pixels at a stride of one image row (SBO = Wp*16 B), so a warp's
 // 32 TMEM lanes hold a 4x8 pixel block and the 2x2 pool is two shuffles.
@@ -36,7 +39,8 @@ namespace ns {
 
 namespace fz {
 constexpr int kThreads = 19 * 32;
-constexpr int C1 = 32, C2 = 64;
+constexpr int C1 = 32, C2 = 64;   // conv1 channels per half, conv2 channels (fused variant)
+constexpr int kC1Max = 64;        // conv1 channels of the widest variant (2 halves)
 constexpr int kIn = 50, kInP = 52, kP1 = 25;
 // The zero-haloed bf16 image is stored column-polyphase: X[x & 1][y][x >> 1]
 // (8-byte cells).  im2col lanes are consecutive pool windows (x stride 2), so a
@@ -68,13 +72,13 @@ constexpr int kActBytes = (C1 / 8) * kPlaneBytes;  // 46,720
 constexpr int wBuild0 = 3, wEp1_0 = 7, wEp2_0 = 15;
 // smem offsets (bytes)
 constexpr int oB1 = 0;                                   // conv1 weights [4][32][8]
-constexpr int oB2 = oB1 + (kK1 / 8) * C1 * 16;           // conv2 weights [36][64][8]
+constexpr int oB2 = oB1 + (kK1 / 8) * kC1Max * 16;       // conv2 weights [36][64][8]
 constexpr int oAct = oB2 + 9 * (C1 / 8) * C2 * 16;       // 2 x conv2 operand planes
 constexpr int oIn = oAct + 2 * kActBytes;                // 2 x u8 frames
 constexpr int oX = oIn + 2 * kInBytes;                   // bf16 image [52][52][4]
 constexpr int oLut = oX + 2 * kXPlane * 8;               // bf16 LUT [3][256]
-constexpr int oBias = oLut + 3 * 256 * 2;                // (32 + 64) x 4
-constexpr int oBar = oBias + (C1 + C2) * 4;
+constexpr int oBias = oLut + 3 * 256 * 2;                // (64 + 64) x 4
+constexpr int oBar = oBias + (kC1Max + C2) * 4;
 constexpr int kNumBars = 2 + 2 + 2 * kA1Stages + 2 * kNG1 + 2 + 2 + 2 * kNB2 + 1;
 constexpr int kSmem = oBar + kNumBars * 8 + 16;
 }  // namespace fz
@@ -104,9 +108,14 @@ NS_DEV void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
 }
 NS_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// kHalves = conv1 channels / 32 (each half is one N = 32 MMA on the shared A
+// tile); kConv2 = conv2 fused (base_filters = 32) or the conv1 map written to
+// HBM in the stacked layout for the generic layer kernel (base_filters = 64).
+template <int kHalves, bool kConv2>
 __global__ void __launch_bounds__(fz::kThreads, 1)
 conv12_fused_kernel(FusedArgs A) {
   using namespace fz;
+  constexpr int C1t = C1 * kHalves;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int64_t n = min(*A.n_dev, A.n_max);
   const int64_t cnt = min(n - A.chunk_base, A.chunk_len);
@@ -126,8 +135,7 @@ conv12_fused_kernel(FusedArgs A) {
   uint64_t* t2_empty = t2_full + kNB2;          // [kNB2] 128 ep2 arrivals
   uint64_t* w_full = t2_empty + kNB2;           // weights loaded
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
-  float* bias1 = reinterpret_cast<float*>(smem + oBias);
-  float* bias2 = bias1 + C1;
+  float* bias1 = reinterpret_cast<float*>(smem + oBias);   // conv1 bias is folded into K
   uint16_t* lut = reinterpret_cast<uint16_t*>(smem + oLut);
   uint2* X = reinterpret_cast<uint2*>(smem + oX);  // one 8-byte (4 x bf16) cell per pixel
 
@@ -166,8 +174,9 @@ conv12_fused_kernel(FusedArgs A) {
     const float v = fminf(fmaxf(((float)g - mu) / 127.5f, -1.0f), 1.0f);
     lut[e] = f2bf_u(v);
   }
-  for (int e = tid; e < C1; e += blockDim.x) bias1[e] = A.b1[e];
-  for (int e = tid; e < C2; e += blockDim.x) bias2[e] = A.b2[e];
+  float* bias2 = bias1 + kC1Max;
+  if (kConv2)
+    for (int e = tid; e < C2; e += blockDim.x) bias2[e] = A.b2[e];
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -178,9 +187,9 @@ conv12_fused_kernel(FusedArgs A) {
   if (warp == 0) {
     // ===================================================== producer
     if (lane == 0) {
-      mbar_arrive_expect_tx(w_full, (kK1 / 8) * C1 * 16 + 9 * (C1 / 8) * C2 * 16);
-      bulk_g2s(smem + oB1, A.w1, (kK1 / 8) * C1 * 16, w_full);
-      bulk_g2s(smem + oB2, A.w2, 9 * (C1 / 8) * C2 * 16, w_full);
+      mbar_arrive_expect_tx(w_full, (kK1 / 8) * C1t * 16 + (kConv2 ? 9 * (C1 / 8) * C2 * 16 : 0));
+      bulk_g2s(smem + oB1, A.w1, (kK1 / 8) * C1t * 16, w_full);
+      if (kConv2) bulk_g2s(smem + oB2, A.w2, 9 * (C1 / 8) * C2 * 16, w_full);
       for (int64_t it = 0; it < my_frames; ++it) {
         const int s = (int)(it & 1);
         if (it >= 2) mbar_wait(&in_empty[s], (uint32_t)(((it >> 1) - 1) & 1));
@@ -196,13 +205,12 @@ conv12_fused_kernel(FusedArgs A) {
       constexpr uint32_t id1 = idesc_bf16_f32(128, C1);
       const uint32_t sB1 = smem_u32(smem + oB1);
       mbar_wait(w_full, 0);
-      uint64_t u1 = 0;  // global conv1 tile sequence; group = u1 / 4, member = u1 % 4
+      // B1 = [4 kc][C1t][8]: half h = rows 32h.., K chunk kk*2 at kk*2*C1t*16 B
+      const uint64_t bd0 = sdesc(sB1, C1t * 16, 128);
+      uint64_t u1 = 0;  // global conv1 tile sequence; window group = u1 / 4, member = u1 % 4
       for (int64_t it = 0; it < my_frames; ++it) {
         for (int t = 0; t < kT1; t += 2, u1 += 2) {
           const uint64_t ug = u1 >> 2;           // global window-group sequence
-          const int gb = (int)(ug % kNG1);
-          if ((u1 & 3) == 0 && ug >= kNG1)       // group's accumulators drained by epilogue 1?
-            mbar_wait(&t1_empty[gb], (uint32_t)(((ug / kNG1) - 1) & 1));
           int a[2];
           for (int q = 0; q < 2; ++q) {
             const uint64_t u = u1 + q;
@@ -210,22 +218,31 @@ conv12_fused_kernel(FusedArgs A) {
             mbar_wait(&a1_full[a[q]], (uint32_t)((u / kA1Stages) & 1));
           }
           tc_fence_after();
-          const uint64_t bd0 = sdesc(sB1, C1 * 16, 128);
 #pragma unroll
-          for (int kk = 0; kk < kK1 / 16; ++kk)
+          for (int h = 0; h < kHalves; ++h) {
+            const uint64_t ugh = ug * kHalves + h;  // (window group, half) sequence
+            const int gb = (int)(ugh % kNG1);
+            if ((u1 & 3) == 0 && ugh >= kNG1) {    // accumulators drained by epilogue 1?
+              mbar_wait(&t1_empty[gb], (uint32_t)(((ugh / kNG1) - 1) & 1));
+              tc_fence_after();
+            }
 #pragma unroll
-            for (int q = 0; q < 2; ++q)
-              umma_bf16_ts(tmem + kColD1 + (gb * 4 + (int)((u1 + q) & 3)) * C1,
-                           tmem + kColA1 + a[q] * kA1Cols + kk * 8,
-                           bd0 + (uint64_t)((kk * 2 * C1 * 16) >> 4), id1, kk);
+            for (int kk = 0; kk < kK1 / 16; ++kk)
+#pragma unroll
+              for (int q = 0; q < 2; ++q)
+                umma_bf16_ts(tmem + kColD1 + (gb * 4 + (int)((u1 + q) & 3)) * C1,
+                             tmem + kColA1 + a[q] * kA1Cols + kk * 8,
+                             bd0 + (uint64_t)((kk * 2 * C1t * 16 + h * C1 * 16) >> 4), id1, kk);
+          }
           for (int q = 0; q < 2; ++q) umma_commit(&a1_empty[a[q]]);
-          if (((u1 + 1) & 3) == 3) umma_commit(&t1_full[gb]);  // group complete
+          if (((u1 + 1) & 3) == 3)                 // window group complete (all halves)
+            for (int h = 0; h < kHalves; ++h) umma_commit(&t1_full[(int)((ug * kHalves + h) % kNG1)]);
         }
       }
     }
   } else if (warp == 2) {
     // ===================================================== conv2 MMA issuer
-    if (lane == 0) {
+    if (kConv2 && lane == 0) {
       constexpr uint32_t id2 = idesc_bf16_f32(128, C2);
       const uint32_t sB2 = smem_u32(smem + oB2), sAct = smem_u32(smem + oAct);
       mbar_wait(w_full, 0);
@@ -328,59 +345,90 @@ conv12_fused_kernel(FusedArgs A) {
       }
     }
   } else if (warp < wEp2_0) {
-    // ===================================================== epilogue 1 (two groups, alternate window groups)
+    // ===================================================== epilogue 1 (two groups, alternate (window group, half))
     const int grp = (warp - wEp1_0) >> 2;
     const int lg = (warp & 3) * 32;       // TMEM lane group of this warp
     const int row = lg + lane;            // window within the group
-    uint64_t ug = 0;                      // global window-group sequence
+    uint64_t ugh = 0;                     // global (window group, half) sequence
+    // !kConv2: conv1 map -> HBM, stacked layout of a 25x25 map (internal.h):
+    // row pitch 26, 676 rows per frame, 27 leading guard rows
+    constexpr int kWq1 = kP1 + 1, kPf1 = (kP1 + 1) * (kP1 + 1), kG1r = kP1 + 2;
+    if (!kConv2 && blockIdx.x == 0) {
+      const int e0 = (warp - wEp1_0) * 32 + lane;
+      for (int e = e0; e < (C1t / 8) * (kG1r + kWq1); e += 256) {
+        const int c = e / (kG1r + kWq1), k = e % (kG1r + kWq1);
+        const int64_t r = k < kG1r ? k : kG1r + cnt * kPf1 + (k - kG1r);
+        *reinterpret_cast<uint4*>(A.out + ((int64_t)c * A.out_rows + r) * 16) = make_uint4(0, 0, 0, 0);
+      }
+    }
     for (int64_t it = 0; it < my_frames; ++it) {
       const int pb = (int)(it & 1);
-      if (it >= 2) mbar_wait(&act_empty[pb], (uint32_t)(((it >> 1) - 1) & 1));
+      if (kConv2 && it >= 2) mbar_wait(&act_empty[pb], (uint32_t)(((it >> 1) - 1) & 1));
       uint8_t* planes = smem + oAct + pb * kActBytes;
-      for (int G = 0; G < kG1; ++G, ++ug) {
-        const int gb = (int)(ug % kNG1);
-        if (gb != grp) continue;
-        mbar_wait(&t1_full[gb], (uint32_t)((ug / kNG1) & 1));
-        tc_fence_after();
-        const int w = G * 128 + row;
-        const bool valid = w < kP1 * kP1;
-        const int yp = w / kP1, xp = w - kP1 * (w / kP1);
-        const int rho = (yp + 1) * kWp + (xp + 1) + 1;
-        const uint32_t tb = tmem + ((uint32_t)lg << 16) + kColD1 + gb * 4 * C1;
+      const int64_t i = blockIdx.x + it * gridDim.x;  // chunk-relative frame
+      for (int G = 0; G < kG1; ++G) {
+        for (int h = 0; h < kHalves; ++h, ++ugh) {
+          const int gb = (int)(ugh % kNG1);
+          if (gb != grp) continue;
+          mbar_wait(&t1_full[gb], (uint32_t)((ugh / kNG1) & 1));
+          tc_fence_after();
+          const int w = G * 128 + row;
+          const bool valid = w < kP1 * kP1;
+          const int yp = w / kP1, xp = w - kP1 * (w / kP1);
+          const int rho = (yp + 1) * kWp + (xp + 1) + 1;
+          const uint32_t tb = tmem + ((uint32_t)lg << 16) + kColD1 + gb * 4 * C1;
 #pragma unroll
-        for (int cb = 0; cb < C1 / 16; ++cb) {
-          // 2x2 max pool = element-wise max over the window's 4 accumulators
-          // (bias already accumulated; max, ReLU and RNE commute: all monotone)
-          uint32_t r0[16], r1[16], r2[16], r3[16];
-          tmem_ld16(tb + 0 * C1 + cb * 16, r0);
-          tmem_ld16(tb + 1 * C1 + cb * 16, r1);
-          tmem_ld16(tb + 2 * C1 + cb * 16, r2);
-          tmem_ld16(tb + 3 * C1 + cb * 16, r3);
-          tmem_ld_wait();
-          uint32_t pk[8];
+          for (int cb = 0; cb < C1 / 16; ++cb) {
+            // 2x2 max pool = element-wise max over the window's 4 accumulators
+            // (bias already accumulated; max, ReLU and RNE commute: all monotone)
+            uint32_t r0[16], r1[16], r2[16], r3[16];
+            tmem_ld16(tb + 0 * C1 + cb * 16, r0);
+            tmem_ld16(tb + 1 * C1 + cb * 16, r1);
+            tmem_ld16(tb + 2 * C1 + cb * 16, r2);
+            tmem_ld16(tb + 3 * C1 + cb * 16, r3);
+            tmem_ld_wait();
+            uint32_t pk[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float m0 = fmaxf(fmaxf(__uint_as_float(r0[2 * j]), __uint_as_float(r1[2 * j])),
-                                   fmaxf(__uint_as_float(r2[2 * j]), __uint_as_float(r3[2 * j])));
-            const float m1 =
-                fmaxf(fmaxf(__uint_as_float(r0[2 * j + 1]), __uint_as_float(r1[2 * j + 1])),
-                      fmaxf(__uint_as_float(r2[2 * j + 1]), __uint_as_float(r3[2 * j + 1])));
-            pk[j] = relu_bf16x2(m0, m1);
+            for (int j = 0; j < 8; ++j) {
+              const float m0 = fmaxf(fmaxf(__uint_as_float(r0[2 * j]), __uint_as_float(r1[2 * j])),
+                                     fmaxf(__uint_as_float(r2[2 * j]), __uint_as_float(r3[2 * j])));
+              const float m1 =
+                  fmaxf(fmaxf(__uint_as_float(r0[2 * j + 1]), __uint_as_float(r1[2 * j + 1])),
+                        fmaxf(__uint_as_float(r2[2 * j + 1]), __uint_as_float(r3[2 * j + 1])));
+              pk[j] = relu_bf16x2(m0, m1);
+            }
+            if (valid) {
+              const uint4 o0 = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              const uint4 o1 = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+              if (kConv2) {
+                *reinterpret_cast<uint4*>(planes + (2 * cb) * kPlaneBytes + rho * 16) = o0;
+                *reinterpret_cast<uint4*>(planes + (2 * cb + 1) * kPlaneBytes + rho * 16) = o1;
+              } else {
+                const int64_t orow = kG1r + i * kPf1 + (yp + 1) * kWq1 + xp;
+                const uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                  uint4* pl = reinterpret_cast<uint4*>(A.out + (int64_t)(h * 4 + 2 * cb + hh) * A.out_rows * 16);
+                  pl[orow] = hh ? o1 : o0;
+                  if (xp == kP1 - 1) pl[orow + 1] = z;          // separator column
+                  if (yp == 0) {                                 // separator row above
+                    pl[orow - kWq1] = z;
+                    if (xp == kP1 - 1) pl[orow - kWq1 + 1] = z;
+                  }
+                }
+              }
+            }
           }
-          if (valid) {
-            *reinterpret_cast<uint4*>(planes + (2 * cb) * kPlaneBytes + rho * 16) =
-                make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            *reinterpret_cast<uint4*>(planes + (2 * cb + 1) * kPlaneBytes + rho * 16) =
-                make_uint4(pk[4], pk[5], pk[6], pk[7]);
-          }
+          tc_fence_before();
+          mbar_arrive(&t1_empty[gb]);
         }
-        tc_fence_before();
-        mbar_arrive(&t1_empty[gb]);
       }
-      fence_proxy_async_smem();  // planes written by threads -> read by the tensor core
-      mbar_arrive(&act_full[pb]);
+      if (kConv2) {
+        fence_proxy_async_smem();  // planes written by threads -> read by the tensor core
+        mbar_arrive(&act_full[pb]);
+      }
     }
-  } else {
+  } else if (kConv2) {
     // ===================================================== epilogue 2
     const int lg = (warp & 3) * 32;
     const int et = tid - wEp2_0 * 32;  // 0..127
@@ -459,37 +507,44 @@ conv12_fused_kernel(FusedArgs A) {
 
 size_t conv12_fused_smem() { return (size_t)fz::kSmem; }
 
-// conv1 packed weights [4 kc][32][8]: K index 27 <- bf16(bias), 28 <- bf16(bias -
+// conv1 packed weights [4 kc][C][8]: K index 27 <- bf16(bias), 28 <- bf16(bias -
 // bf16(bias)); with A[., 27] = A[., 28] = 1.0 the tensor core accumulates the
-// fp32 bias to ~2^-17 relative (fused path only; conv1_kernel adds it in fp32).
-__global__ void pack_conv1_bias_kernel(const float* __restrict__ b, uint16_t* __restrict__ out) {
+// fp32 bias to ~2^-17 relative.
+__global__ void pack_conv1_bias_kernel(const float* __restrict__ b, int C, uint16_t* __restrict__ out) {
   const int n = threadIdx.x;
-  if (n >= fz::C1) return;
+  if (n >= C) return;
   const float v = b[n];
   const __nv_bfloat16 hi = __float2bfloat16_rn(v);
   const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
-  out[(3 * fz::C1 + n) * 8 + 3] = *reinterpret_cast<const uint16_t*>(&hi);
-  out[(3 * fz::C1 + n) * 8 + 4] = *reinterpret_cast<const uint16_t*>(&lo);
+  out[(3 * C + n) * 8 + 3] = *reinterpret_cast<const uint16_t*>(&hi);
+  out[(3 * C + n) * 8 + 4] = *reinterpret_cast<const uint16_t*>(&lo);
 }
 
-noscope_status pack_conv12_bias(const float* b1, uint8_t* w1_packed, cudaStream_t st) {
-  pack_conv1_bias_kernel<<<1, 32, 0, st>>>(b1, reinterpret_cast<uint16_t*>(w1_packed));
+noscope_status pack_conv12_bias(const float* b1, int C, uint8_t* w1_packed, cudaStream_t st) {
+  pack_conv1_bias_kernel<<<1, 64, 0, st>>>(b1, C, reinterpret_cast<uint16_t*>(w1_packed));
+  NS_LAUNCH_CHECK();
+  count_launch();
+  return NOSCOPE_OK;
+}
+
+template <int kHalves, bool kConv2>
+static noscope_status launch_variant(const FusedArgs& a, int grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(conv12_fused_kernel<kHalves, kConv2>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, fz::kSmem);
+    attr = true;
+  }
+  conv12_fused_kernel<kHalves, kConv2><<<grid, fz::kThreads, fz::kSmem, st>>>(a);
   NS_LAUNCH_CHECK();
   count_launch();
   return NOSCOPE_OK;
 }
 
 noscope_status launch_conv12_fused(const FusedArgs& a, int grid, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(conv12_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         fz::kSmem);
-    attr = true;
-  }
-  conv12_fused_kernel<<<grid, fz::kThreads, fz::kSmem, st>>>(a);
-  NS_LAUNCH_CHECK();
-  count_launch();
-  return NOSCOPE_OK;
+  if (a.C1 == 32) return launch_variant<1, true>(a, grid, st);
+  if (a.C1 == 64) return launch_variant<2, false>(a, grid, st);
+  return NOSCOPE_INVALID_ARGUMENT;
 }
 
 }  // namespace ns

@@ -1,9 +1,9 @@
 // cnn_gemm.cu — one 3x3 conv + bias + ReLU + 2x2 max-pool layer of the
 // specialized CNN (§4: "convolutional layers ... max
 // pooling ... the number of filters doubles") as a batched implicit GEMM on
-// tcgen05 tensor cores.  Used for every layer that is not inside the fused
-// conv1+conv2 kernel (cnn_fused.cu): conv1/conv2 of base_filters = 64 and
-// conv3/conv4 of the 4-layer networks.
+// tcgen05 tensor cores.  Used for every layer after the fused conv1(+conv2)
+// kernel (cnn_fused.cu): conv2 of base_filters = 64 and conv3/conv4 of the
+// 4-layer networks.
 //
 // Data layout: the "stacked" map (internal.h) puts all frames of a chunk one
 // after another in one row space with a shared zero separator row/column, so a
@@ -20,14 +20,20 @@
 // an owned window are inside the unit (neighbouring units overlap by Wq + 1
 // rows, recomputed).
 //
+// K order: channel-group pair major, tap minor (s = cgp * 9 + tap), so both
+// operands stream like an ordinary GEMM: A arrives one channel-group pair at a
+// time (the unit's rows of 2 planes, re-read by the 9 taps), B one K16 step at a
+// time; the ring depths are sized to cover L2 latency (weights are re-streamed
+// per unit, so B is the bandwidth term).
+//
 // Roles (11 warps, persistent, one CTA per SM):
-//   W10   A producer  — cp.async.bulk of the unit's rows (one copy per channel
-//                       group plane), nA-deep
-//   W0    B producer  — weight K-step slabs [2][N][8] through a bstages ring
+//   W10   A producer  — cp.async.bulk of the unit's rows of 2 channel-group planes
+//                       per A stage
+//   W0    B producer  — weight K-step slabs [2][N][8] through the B ring
 //   W1    MMA issuer  — per pass over Cout: steps x MT tcgen05.mma (M=128, N,
 //                       K=16), the MT tiles interleaved on independent
 //                       accumulators; owns TMEM
-//   W2-W9 epilogue    — TMEM -> +bias -> ReLU -> bf16 -> smem staging (16-channel
+//   W2-W9 epilogue    — TMEM -> +bias -> ReLU -> bf16 -> smem staging (32-channel
 //                       slabs, double-buffered) -> 2x2 max of the owned windows
 //                       -> next layer's stacked map (separators written as zeros)
 //                       or the FC feature tiles
@@ -39,8 +45,9 @@ namespace ns {
 namespace gm {
 constexpr int kThreads = 11 * 32;
 constexpr int kEpi = 256;       // epilogue threads (W2-W9)
-constexpr int kMaxWin = 1024;   // owned pool windows per unit (<= S/4 + 2*rows/Wq)
-constexpr int kNumBars = 2 + 2 + 8 + 8 + 2 + 2;
+constexpr int kMaxWin = 256;    // owned pool windows per unit (<= S/4 + Wq)
+constexpr int kMaxA = 8, kMaxB = 24;
+constexpr int kNumBars = 2 * kMaxA + 2 * kMaxB + 2 + 2;
 }  // namespace gm
 
 static size_t al(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -48,34 +55,35 @@ static size_t al(size_t v, size_t a) { return (v + a - 1) / a * a; }
 bool make_convg_geom(int cin_real, int cout, int H, int64_t chunk, ConvGGeom* out) {
   ConvGGeom g{};
   g.cin_real = cin_real;
-  g.cin_eff = cin_real < 8 ? 8 : cin_real;
-  if (g.cin_eff != 8 && g.cin_eff % 16) return false;
+  g.cin_eff = cin_real;
+  if (cin_real % 16) return false;
   g.cout = cout;
   g.H = H;
   g.W = H;
+  // N = 256 per pass when Cout allows: B (re-streamed weights) is the traffic
+  // term, and two 128-row tiles x 256 columns use all 512 TMEM columns.
   g.N = std::min(cout, 256);
-  if (cout % g.N || g.N % 16) return false;
+  if (cout % g.N || g.N % 32) return false;
   g.passes = cout / g.N;
-  // K16 steps: (tap, channel-group pair); Cin = 8 packs two taps per step
-  g.steps = g.cin_eff == 8 ? 5 : 9 * (g.cin_eff / 16);
-  if (g.N == 256) { g.MT = 2; g.nacc = 1; }
-  else if (g.N == 128) { g.MT = 2; g.nacc = 2; }
-  else { g.MT = 4; g.nacc = 512 / (4 * g.N) >= 2 ? 2 : 1; }
+  g.steps = 9 * (g.cin_eff / 16);   // K16 steps: (channel-group pair, tap)
+  g.MT = 2;
+  g.nacc = 512 / (g.MT * g.N) >= 2 ? 2 : 1;
   const int Wq = g.W + 1;
   g.S = 128 * g.MT - Wq - 1;
   if (g.S <= 0) return false;
-  g.rows_blk = 128 * g.MT + 2 * Wq + 3;   // [c0 - Wq - 1, c0 + 128 MT + Wq + 2)
+  g.rows_blk = 128 * g.MT + 2 * Wq + 2;   // [c0 - Wq - 1, c0 + 128 MT + Wq + 1)
   g.R = sl_rows(g.H, g.W, chunk, 128 * g.MT + Wq + 8);
   uint32_t tc = 32;
   while ((int)tc < g.nacc * g.MT * g.N) tc <<= 1;
   g.tmem_cols = tc;
-  const size_t ablk = (size_t)(g.cin_eff / 8) * g.rows_blk * 16;
-  auto layout = [&](int nA, int bst) {
-    size_t o = al((size_t)nA * ablk, 1024);
+  const size_t astage = (size_t)2 * g.rows_blk * 16;   // two channel-group planes
+  const size_t bstage = (size_t)g.N * 32;
+  auto layout = [&](int na, int nb) {
+    size_t o = al((size_t)na * astage, 1024);
     g.oB = o;
-    o = al(o + (size_t)bst * g.N * 32, 128);
+    o = al(o + (size_t)nb * bstage, 128);
     g.oStage = o;
-    o += (size_t)2 * 128 * g.MT * 32;
+    o += (size_t)2 * 128 * g.MT * 64;   // staging: 2 x rows x 32 bf16
     g.oWin = o;
     o += (size_t)gm::kMaxWin * 8;
     g.oBias = o;
@@ -85,11 +93,10 @@ bool make_convg_geom(int cin_real, int cout, int H, int64_t chunk, ConvGGeom* ou
     return o + 1024;  // alignment slack
   };
   const size_t kMax = 227 * 1024;
-  g.nA = 2;
-  g.bstages = 6;
-  g.smem = layout(2, 6);
-  if (g.smem > kMax) { g.nA = 1; g.smem = layout(1, 6); }
-  if (g.smem > kMax) { g.bstages = 4; g.smem = layout(1, 4); }
+  g.nA = 4;
+  g.bstages = gm::kMaxB;
+  while (layout(g.nA, g.bstages) > kMax && g.bstages > 4) --g.bstages;
+  g.smem = layout(g.nA, g.bstages);
   if (g.smem > kMax) return false;
   *out = g;
   return true;
@@ -109,16 +116,8 @@ __global__ void pack_convg_kernel(const uint16_t* __restrict__ w, ConvGGeom g,
     const int64_t r3 = r2 >> 1;
     const int s = (int)(r3 % g.steps), p = (int)(r3 / g.steps);
     const int co = p * g.N + n;
-    int tap, ch;
-    if (g.cin_eff == 8) {
-      tap = 2 * s + h;
-      ch = e;
-    } else {
-      const int cpt = g.cin_eff / 16;
-      tap = s / cpt;
-      ch = ((s % cpt) * 2 + h) * 8 + e;
-    }
-    out[t] = (tap < 9 && ch < g.cin_real) ? w[((int64_t)co * 9 + tap) * g.cin_real + ch] : 0;
+    const int tap = s % 9, ch = ((s / 9) * 2 + h) * 8 + e;
+    out[t] = w[((int64_t)co * 9 + tap) * g.cin_real + ch];
   }
 }
 
@@ -126,58 +125,6 @@ noscope_status pack_convg(const uint16_t* w, const ConvGGeom& g, uint8_t* out, c
   const int64_t total = (int64_t)g.cout * g.steps * 16;
   const int grid = (int)std::min<int64_t>((total + 255) / 256, 4 * kNumSMs);
   pack_convg_kernel<<<grid, 256, 0, st>>>(w, g, reinterpret_cast<uint16_t*>(out));
-  NS_LAUNCH_CHECK();
-  count_launch();
-  return NOSCOPE_OK;
-}
-
-NS_DEV uint16_t bf16_bits(float v) {
-  __nv_bfloat16 h = __float2bfloat16_rn(v);
-  return *reinterpret_cast<uint16_t*>(&h);
-}
-
-// Input normalisation (oracle normalize_input): x = clamp((g - mu_c)
-// / 127.5, -1, 1) in fp32, rounded to bf16; channels 3..7 and separators zero.
-__global__ void prep_sl_kernel(const uint8_t* __restrict__ small, int64_t pitch,
-                               const int32_t* __restrict__ idx, const int64_t* __restrict__ n_dev,
-                               int64_t n_max, int64_t chunk_base, int64_t chunk_len, float m0,
-                               float m1, float m2, uint4* __restrict__ out) {
-  const int64_t n = min(*n_dev, n_max);
-  const int64_t cnt = min(n - chunk_base, chunk_len);
-  if (cnt <= 0) return;
-  constexpr int W = 50, Wq = 51, P = 51 * 51, G = 52;
-  const int64_t total = G + cnt * P + Wq;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < total;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    uint4 v = make_uint4(0, 0, 0, 0);
-    const int64_t rel = r - G;
-    if (rel >= 0 && rel < cnt * P) {
-      const int64_t f = rel / P;
-      const int q = (int)(rel - f * P);
-      const int Y = q / Wq, x = q - Y * Wq;
-      if (Y >= 1 && x < W) {
-        const int64_t gf = chunk_base + f;
-        const int64_t fr = idx ? (int64_t)idx[gf] : gf;
-        const uint8_t* px = small + fr * pitch + ((Y - 1) * W + x) * 3;
-        const float a = fminf(fmaxf(((float)px[0] - m0) / 127.5f, -1.0f), 1.0f);
-        const float b = fminf(fmaxf(((float)px[1] - m1) / 127.5f, -1.0f), 1.0f);
-        const float c = fminf(fmaxf(((float)px[2] - m2) / 127.5f, -1.0f), 1.0f);
-        v.x = (uint32_t)bf16_bits(a) | ((uint32_t)bf16_bits(b) << 16);
-        v.y = bf16_bits(c);
-      }
-    }
-    out[r] = v;
-  }
-}
-
-noscope_status launch_prep_sl(const uint8_t* small, int64_t pitch, const int32_t* idx,
-                              const int64_t* n_dev, int64_t n_max, int64_t chunk_base,
-                              int64_t chunk_len, const float mean[3], uint8_t* out,
-                              cudaStream_t st) {
-  const int64_t rows = chunk_len * 51 * 51 + 52 + 51;
-  const int grid = (int)std::min<int64_t>((rows + 255) / 256, 8 * kNumSMs);
-  prep_sl_kernel<<<grid, 256, 0, st>>>(small, pitch, idx, n_dev, n_max, chunk_base, chunk_len,
-                                       mean[0], mean[1], mean[2], reinterpret_cast<uint4*>(out));
   NS_LAUNCH_CHECK();
   count_launch();
   return NOSCOPE_OK;
@@ -195,17 +142,17 @@ convg_kernel(ConvGArgs A) {
   if ((int64_t)blockIdx.x >= U) return;
   const int64_t my_units = (U - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ncg = g.cin_eff / 8;
+  const int ncgp = g.cin_eff / 16;                 // channel-group pairs
   const uint32_t plane = (uint32_t)g.rows_blk * 16;
-  const uint32_t ablk = (uint32_t)ncg * plane;
+  const uint32_t astage = 2 * plane;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + g.oBar);
-  uint64_t* act_full = bars;           // [2]
-  uint64_t* act_empty = bars + 2;      // [2]
-  uint64_t* b_full = bars + 4;         // [8]
-  uint64_t* b_empty = bars + 12;       // [8]
-  uint64_t* acc_full = bars + 20;      // [2]
-  uint64_t* acc_empty = bars + 22;     // [2]
+  uint64_t* a_full = bars;                   // [kMaxA]
+  uint64_t* a_empty = a_full + gm::kMaxA;     // [kMaxA]
+  uint64_t* b_full = a_empty + gm::kMaxA;     // [kMaxB]
+  uint64_t* b_empty = b_full + gm::kMaxB;     // [kMaxB]
+  uint64_t* acc_full = b_empty + gm::kMaxB;   // [2]
+  uint64_t* acc_empty = acc_full + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + gm::kNumBars);
   int* wcount = reinterpret_cast<int*>(tmem_slot + 1);
   float* bias = reinterpret_cast<float*>(smem + g.oBias);
@@ -213,12 +160,14 @@ convg_kernel(ConvGArgs A) {
 
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&act_full[i], 1);
-      mbar_init(&act_empty[i], 1);
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], gm::kEpi / 32);
     }
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < gm::kMaxA; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < gm::kMaxB; ++i) {
       mbar_init(&b_full[i], 1);
       mbar_init(&b_empty[i], 1);
     }
@@ -234,80 +183,83 @@ convg_kernel(ConvGArgs A) {
   if (warp == 10) {
     // ============================================== A producer
     if (lane == 0) {
+      uint32_t st = 0, ph = 0, fill = 0;
       for (int64_t it = 0; it < my_units; ++it) {
-        const int ab = (int)(it % g.nA);
-        if (it >= g.nA) mbar_wait(&act_empty[ab], (uint32_t)(((it / g.nA) - 1) & 1));
         const int64_t u = blockIdx.x + it * gridDim.x;
         const int64_t r0 = (int64_t)G + u * g.S - Wq - 1;
-        mbar_arrive_expect_tx(&act_full[ab], ablk);
-        for (int c = 0; c < ncg; ++c)
-          bulk_g2s(smem + (size_t)ab * ablk + (size_t)c * plane,
-                   A.in + ((int64_t)c * g.R + r0) * 16, plane, &act_full[ab]);
+        for (int p = 0; p < g.passes; ++p)
+          for (int cp = 0; cp < ncgp; ++cp) {
+            if (fill >= (uint32_t)g.nA) mbar_wait(&a_empty[st], ph ^ 1);
+            else ++fill;
+            mbar_arrive_expect_tx(&a_full[st], astage);
+            for (int h = 0; h < 2; ++h)
+              bulk_g2s(smem + (size_t)st * astage + (size_t)h * plane,
+                       A.in + ((int64_t)(2 * cp + h) * g.R + r0) * 16, plane, &a_full[st]);
+            if (++st == (uint32_t)g.nA) { st = 0; ph ^= 1; }
+          }
       }
     }
   } else if (warp == 0) {
     // ============================================== B producer
     if (lane == 0) {
       const uint32_t bbytes = (uint32_t)g.N * 32;
-      uint64_t seq = 0;
+      uint32_t st = 0, ph = 0, fill = 0;
       for (int64_t it = 0; it < my_units; ++it)
         for (int p = 0; p < g.passes; ++p)
-          for (int s = 0; s < g.steps; ++s, ++seq) {
-            const int st = (int)(seq % g.bstages);
-            if (seq >= (uint64_t)g.bstages)
-              mbar_wait(&b_empty[st], (uint32_t)(((seq / g.bstages) - 1) & 1));
+          for (int s = 0; s < g.steps; ++s) {
+            if (fill >= (uint32_t)g.bstages) mbar_wait(&b_empty[st], ph ^ 1);
+            else ++fill;
             mbar_arrive_expect_tx(&b_full[st], bbytes);
             bulk_g2s(smem + g.oB + (size_t)st * bbytes,
                      A.wpack + ((size_t)p * g.steps + s) * bbytes, bbytes, &b_full[st]);
+            if (++st == (uint32_t)g.bstages) { st = 0; ph ^= 1; }
           }
     }
   } else if (warp == 1) {
     // ============================================== MMA issuer
+    // The single issuing thread must stay far ahead of the tensor pipe: per
+    // step one ring wait, two descriptor adds and MT tcgen05.mma; the 9 tap
+    // offsets are loop constants, rings advance incrementally.
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16_f32(128, g.N);
-      const uint32_t sA = smem_u32(smem), sB = smem_u32(smem + g.oB);
-      const uint32_t bbytes = (uint32_t)g.N * 32;
-      uint64_t seq = 0, accseq = 0;
+      const uint32_t sB = smem_u32(smem + g.oB);
+      const uint32_t bstep = ((uint32_t)g.N * 32) >> 4;
+      const uint64_t bd0 = sdesc(sB, (uint32_t)g.N * 16, 128);
+      const uint64_t ad0 = sdesc(smem_u32(smem) + (uint32_t)(Wq + 1) * 16, plane, 128);
+      const uint32_t astep = astage >> 4;
+      uint64_t dtap[9];
+#pragma unroll
+      for (int t = 0; t < 9; ++t) dtap[t] = (uint64_t)(int64_t)((t / 3 - 1) * Wq + (t % 3 - 1));
+      const uint32_t acol = (uint32_t)g.N;
+      uint32_t ast = 0, aph = 0, bst = 0, bph = 0, accseq = 0;
+      const int lgacc = g.nacc == 2 ? 1 : 0;
       for (int64_t it = 0; it < my_units; ++it) {
-        const int ab = (int)(it % g.nA);
-        mbar_wait(&act_full[ab], (uint32_t)((it / g.nA) & 1));
-        tc_fence_after();
-        const uint32_t aBase = sA + (uint32_t)ab * ablk + (uint32_t)(Wq + 1) * 16;
         for (int p = 0; p < g.passes; ++p, ++accseq) {
-          const int b = (int)(accseq % g.nacc);
-          if (accseq >= (uint64_t)g.nacc)
-            mbar_wait(&acc_empty[b], (uint32_t)(((accseq / g.nacc) - 1) & 1));
+          const uint32_t b = accseq & (uint32_t)(g.nacc - 1);
+          if (accseq >= (uint32_t)g.nacc)
+            mbar_wait(&acc_empty[b], ((accseq >> lgacc) - 1) & 1u);
           tc_fence_after();
-          const uint32_t d = tmem + (uint32_t)(b * g.MT * g.N);
-          for (int s = 0; s < g.steps; ++s, ++seq) {
-            const int st = (int)(seq % g.bstages);
-            mbar_wait(&b_full[st], (uint32_t)((seq / g.bstages) & 1));
-            tc_fence_after();
-            int shift, lbo;
-            uint32_t coff;
-            if (g.cin_eff == 8) {   // two taps per K16 step
-              const int t0 = 2 * s, t1 = 2 * s + 1;
-              shift = (t0 / 3 - 1) * Wq + (t0 % 3 - 1);
-              const int shift1 = t1 < 9 ? (t1 / 3 - 1) * Wq + (t1 % 3 - 1) : shift + 1;
-              lbo = (shift1 - shift) * 16;
-              coff = 0;
-            } else {
-              const int cpt = g.cin_eff / 16;
-              const int tap = s / cpt;
-              shift = (tap / 3 - 1) * Wq + (tap % 3 - 1);
-              lbo = (int)plane;
-              coff = (uint32_t)((s % cpt) * 2) * plane;
+          const uint32_t d = tmem + b * (uint32_t)g.MT * acol;
+          for (int cp = 0; cp < ncgp; ++cp) {
+            mbar_wait(&a_full[ast], aph);
+            const uint64_t ac = ad0 + (uint64_t)(ast * astep);
+#pragma unroll
+            for (int t = 0; t < 9; ++t) {
+              mbar_wait(&b_full[bst], bph);
+              tc_fence_after();
+              const uint64_t ad = ac + dtap[t];
+              const uint64_t bd = bd0 + (uint64_t)(bst * bstep);
+              const uint32_t acc = (cp | t) ? 1u : 0u;
+              umma_bf16(d, ad, bd, idesc, acc);
+              umma_bf16(d + acol, ad + 128, bd, idesc, acc);   // +2048 B = next 128 rows
+              umma_commit(&b_empty[bst]);
+              if (++bst == (uint32_t)g.bstages) { bst = 0; bph ^= 1; }
             }
-            const uint64_t bd = sdesc(sB + (uint32_t)st * bbytes, (uint32_t)g.N * 16, 128);
-            const uint32_t a0 = aBase + coff + (uint32_t)(shift * 16);
-            for (int t = 0; t < g.MT; ++t)
-              umma_bf16(d + (uint32_t)(t * g.N), sdesc(a0 + (uint32_t)t * 2048, (uint32_t)lbo, 128),
-                        bd, idesc, s > 0 ? 1u : 0u);
-            umma_commit(&b_empty[st]);
+            umma_commit(&a_empty[ast]);
+            if (++ast == (uint32_t)g.nA) { ast = 0; aph ^= 1; }
           }
           umma_commit(&acc_full[b]);
         }
-        umma_commit(&act_empty[ab]);
       }
     }
   } else {
@@ -327,8 +279,8 @@ convg_kernel(ConvGArgs A) {
       }
     }
     uint8_t* stage = smem + g.oStage;
-    const uint32_t stage_bytes = (uint32_t)128 * g.MT * 32;
-    uint64_t accseq = 0, slab = 0;
+    const uint32_t stage_bytes = (uint32_t)128 * g.MT * 64;
+    uint32_t accseq = 0, slab = 0;
     for (int64_t it = 0; it < my_units; ++it) {
       const int64_t u = blockIdx.x + it * gridDim.x;
       const int64_t c0 = (int64_t)G + u * g.S;
@@ -337,37 +289,40 @@ convg_kernel(ConvGArgs A) {
       if (et == 0) *wcount = 0;
       nbar_sync(1, gm::kEpi);
       for (int j = et; j < g.S; j += gm::kEpi) {
-        const int64_t rel = c0 + j - G;
-        const int64_t f = rel / P;
+        const int rel = (int)(c0 + j - G);   // < chunk * P < 2^31
+        const int f = rel / P;
         if (f >= cnt) continue;
-        const int q = (int)(rel - f * P);
+        const int q = rel - f * P;
         const int Y = q / Wq, x = q - Y * Wq, y = Y - 1;
         if (Y < 1 || (y & 1) || (x & 1) || (y >> 1) >= Ho || (x >> 1) >= Wo) continue;
         const int k = atomicAdd(wcount, 1);
-        wins[k] = make_int2(j | ((y >> 1) << 16) | ((x >> 1) << 24), (int)f);
+        wins[k] = make_int2(j | ((y >> 1) << 16) | ((x >> 1) << 24), f);
       }
       nbar_sync(1, gm::kEpi);
       const int nwin = *wcount;
       for (int p = 0; p < g.passes; ++p, ++accseq) {
-        const int b = (int)(accseq % g.nacc);
-        mbar_wait(&acc_full[b], (uint32_t)((accseq / g.nacc) & 1));
+        const uint32_t b = accseq & (uint32_t)(g.nacc - 1);
+        mbar_wait(&acc_full[b], (accseq >> (g.nacc == 2 ? 1 : 0)) & 1u);
         tc_fence_after();
-        const int nsl = g.N / 16;
+        const int nsl = g.N / 32;
         for (int sl = 0; sl < nsl; ++sl, ++slab) {
           uint8_t* sbuf = stage + (slab & 1) * stage_bytes;
-          const int c = p * g.N + sl * 16;
+          const int c = p * g.N + sl * 32;
           for (int t = eg; t < g.MT; t += 2) {
-            uint32_t r[16];
-            tmem_ld16(tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)((b * g.MT + t) * g.N + sl * 16), r);
+            uint32_t r[32];
+            const uint32_t ta = tmem + ((uint32_t)(lq * 32) << 16) + (b * g.MT + t) * (uint32_t)g.N + sl * 32;
+            tmem_ld16(ta, *reinterpret_cast<uint32_t(*)[16]>(r));
+            tmem_ld16(ta + 16, *reinterpret_cast<uint32_t(*)[16]>(r + 16));
             tmem_ld_wait();
-            uint32_t pk[8];
+            uint32_t pk[16];
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
+            for (int j = 0; j < 16; ++j)
               pk[j] = relu_bf16x2(__uint_as_float(r[2 * j]) + bias[c + 2 * j],
                                   __uint_as_float(r[2 * j + 1]) + bias[c + 2 * j + 1]);
-            uint4* dst = reinterpret_cast<uint4*>(sbuf + (size_t)(t * 128 + lq * 32 + lane) * 32);
-            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            uint4* dst = reinterpret_cast<uint4*>(sbuf + (size_t)(t * 128 + lq * 32 + lane) * 64);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
           }
           if (sl == nsl - 1) {  // accumulators fully read: release them to the MMA
             tc_fence_before();
@@ -376,13 +331,13 @@ convg_kernel(ConvGArgs A) {
           }
           nbar_sync(1, gm::kEpi);
           // ---- 2x2 max pool of the owned windows (non-negative bf16: integer max)
-          for (int e = et; e < 2 * nwin; e += gm::kEpi) {
-            const int2 w = wins[e >> 1];
-            const int h = e & 1;
+          for (int e = et; e < 4 * nwin; e += gm::kEpi) {
+            const int2 w = wins[e >> 2];
+            const int h = e & 3;
             const int sr = w.x & 0xFFFF, yp = (w.x >> 16) & 0xFF, xp = (w.x >> 24) & 0xFF;
             const int64_t f = w.y;
-            const uint4* s0 = reinterpret_cast<const uint4*>(sbuf + (size_t)sr * 32) + h;
-            const uint4 a0 = s0[0], a1 = s0[2], a2 = s0[2 * Wq], a3 = s0[2 * Wq + 2];
+            const uint4* s0 = reinterpret_cast<const uint4*>(sbuf + (size_t)sr * 64) + h;
+            const uint4 a0 = s0[0], a1 = s0[4], a2 = s0[4 * Wq], a3 = s0[4 * Wq + 4];
             uint4 o;
             o.x = __vmaxu2(__vmaxu2(a0.x, a1.x), __vmaxu2(a2.x, a3.x));
             o.y = __vmaxu2(__vmaxu2(a0.y, a1.y), __vmaxu2(a2.y, a3.y));

@@ -113,17 +113,18 @@ noscope_status launch_labels(const noscope_dd_config& cfg, int64_t tau0, int64_t
 // Specialized CNN.
 // Fused conv1+conv2 (base_filters = 32), cnn_fused.cu.
 struct FusedArgs {
+  int C1;              // conv1 channels: 32 (conv2 fused) or 64 (conv1 only -> stacked map)
   const uint8_t* small;
   int64_t small_pitch;
   const int32_t* idx;
   const int64_t* n_dev;
   int64_t n_max, chunk_base, chunk_len;
-  const uint8_t* w1;   // packed [4][32][8]
+  const uint8_t* w1;   // packed [4][C1][8]
   const uint8_t* w2;   // packed [36][64][8]
   const float* b1;
   const float* b2;
   float mean[3];
-  int to_features;     // 1: FC feature tiles, 0: stacked 12x12x64 map (layer-3 input)
+  int to_features;     // 1: FC feature tiles, 0: stacked map (next layer's input)
   uint8_t* out;
   int K_feat;          // feature length (to_features)
   int64_t out_rows;    // rows per channel-group plane of the stacked map (!to_features)
@@ -138,9 +139,9 @@ size_t conv12_fused_smem();
 // right of each row are the 3x3 conv's zero padding on all four sides (the
 // column right of row y-1 is the left neighbour of row y).
 struct ConvGGeom {
-  int cin_real, cin_eff, cout, H, W;
+  int cin_real, cin_eff, cout, H, W;   // cin_eff = cin_real (multiple of 16)
   int N, passes, steps;      // MMA N (<= 256) per pass over Cout; K16 steps
-  int MT, nacc, nA, bstages; // M tiles per unit, accumulator sets, A buffers, B ring depth
+  int MT, nacc, nA, bstages; // M tiles per unit, accumulator sets, A / B ring depths
   int S, rows_blk;           // unit stride in rows; rows loaded per unit per plane
   int64_t R;                 // rows per plane of the layer input (chunk)
   uint32_t tmem_cols;
@@ -165,11 +166,7 @@ struct ConvGArgs {
 };
 noscope_status launch_convg(const ConvGArgs& a, cudaStream_t st);
 noscope_status pack_convg(const uint16_t* w, const ConvGGeom& g, uint8_t* out, cudaStream_t st);
-// u8 frames (gathered by idx) -> normalised bf16 stacked 50x50 map, 8 channels (3 real)
-noscope_status launch_prep_sl(const uint8_t* small, int64_t pitch, const int32_t* idx,
-                              const int64_t* n_dev, int64_t n_max, int64_t chunk_base,
-                              int64_t chunk_len, const float mean[3], uint8_t* out, cudaStream_t st);
-noscope_status pack_conv12_bias(const float* b1, uint8_t* w1_packed, cudaStream_t st);
+noscope_status pack_conv12_bias(const float* b1, int C, uint8_t* w1_packed, cudaStream_t st);
 noscope_status launch_conv12_fused(const FusedArgs& a, int grid, cudaStream_t st);
 size_t cnn_ws_bytes(const noscope_cnn_arch& a, int64_t n_max);
 noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& w,
