@@ -20,7 +20,7 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   return d;
 }
 
-template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0>
+template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0, int OFF = 0>
 __global__ void __launch_bounds__(512, 1) mma_loop(int iters, int ksteps, long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* A = smem;                      // 128 rows x 128 B per 4 K-steps (sw) / 4 KB per step
@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(512, 1) mma_loop(int iters, int ksteps, long l
             ad = sdesc_sw128(a0 + (k >> 2) * 16384 + (k & 3) * 32);
             bd = sdesc_sw128(b0 + (k >> 2) * (N * 128) + (k & 3) * 32);
           } else {
-            ad = sdesc(a0 + (k & 1) * 16 * (SBO / 16), 11680, SBO);
+            ad = sdesc(a0 + (k & 1) * 16 * (SBO / 16) + (OFF ? (k & 7) * OFF : 0), 11680, SBO);
             bd = sdesc(b0 + (k & 7) * N * 32, N * 16, 128);
           }
           umma_bf16(tmem + acc * N, ad, bd, idesc, (it | k) ? 1u : 0u);
@@ -83,21 +83,21 @@ __global__ void __launch_bounds__(512, 1) mma_loop(int iters, int ksteps, long l
   if (threadIdx.x < 32) tmem_dealloc<512>(tmem);
 }
 
-template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0>
+template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0, int OFF = 0>
 void run() {
   const int iters = 500, ksteps = 8;
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
-  size_t smem = 65536 + 16384 + 1024;
-  cudaFuncSetAttribute(mma_loop<N, NACC, SW, SBO, HAMMER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  mma_loop<N, NACC, SW, SBO, HAMMER><<<148, 512, smem>>>(iters, ksteps, d);
+  size_t smem = 32768 + 8 * 256 * 32 + 2048;
+  cudaFuncSetAttribute(mma_loop<N, NACC, SW, SBO, HAMMER, OFF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  mma_loop<N, NACC, SW, SBO, HAMMER, OFF><<<148, 512, smem>>>(iters, ksteps, d);
   cudaError_t err = cudaDeviceSynchronize();
   if (err != cudaSuccess) { printf("N=%d acc=%d sw=%d: %s\n", N, NACC, (int)SW, cudaGetErrorString(err)); fflush(stdout); return; }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  mma_loop<N, NACC, SW, SBO, HAMMER><<<148, 512, smem>>>(iters, ksteps, d);
+  mma_loop<N, NACC, SW, SBO, HAMMER, OFF><<<148, 512, smem>>>(iters, ksteps, d);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
@@ -106,7 +106,7 @@ void run() {
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double mmas = (double)iters * ksteps * NACC;
   double flops = mmas * 2.0 * 128 * N * 16 * 148;
-  printf("H=%d SBO=%3d N=%3d acc=%d %s: %6.2f cycles/MMA (floor %3d), %7.1f TFLOP/s  %s\n", HAMMER, SBO, N, NACC,
+  printf("H=%d OFF=%3d SBO=%3d N=%3d acc=%d %s: %6.2f cycles/MMA (floor %3d), %7.1f TFLOP/s  %s\n", HAMMER, OFF, SBO, N, NACC,
          SW ? "SW128" : "none ", (double)h[0] / mmas, 128 * N / 256, flops / (ms * 1e-3) / 1e12,
          cudaGetErrorString(cudaGetLastError()));
   fflush(stdout);
@@ -114,7 +114,9 @@ void run() {
 }
 
 int main() {
-  run<64, 4, false, 128, 0>(); run<64, 4, false, 128, 1>(); run<64, 4, false, 128, 2>();
-  run<128, 2, false, 128, 0>(); run<128, 2, false, 128, 1>(); run<128, 2, false, 128, 2>();
+  run<128, 2, false, 128, 0, 0>(); run<128, 2, false, 128, 0, 16>(); run<128, 2, false, 128, 0, 48>();
+  run<256, 2, false, 128, 0, 0>(); run<256, 2, false, 128, 0, 16>(); run<256, 1, false, 128, 0, 0>();
+  run<256, 2, false, 128, 1, 16>(); run<128, 2, false, 128, 1, 16>(); run<128, 2, false, 128, 2, 16>();
+  run<64, 4, false, 128, 0, 0>(); run<64, 4, false, 128, 0, 16>();
   return 0;
 }
