@@ -15,10 +15,11 @@
 //                         N = 32 per half); owns the TMEM allocation
 //   W2      conv2 MMA   — one thread issues the shifted-window conv2 tiles
 //                         (A and B from shared memory, K = 9 x 32, N = 64)
-//   W3-W6   builders    — normalisation through a 3x256 lookup table
-//                         of the exact fp32 formula into a zero-haloed bf16 image
-//                         (4 channel slots per pixel), then one im2col row per
-//                         thread stored into TMEM with tcgen05.st (no
+//   W3-W6   builders    — normalisation through a 3x256 table of the
+//                         exact fp32 formula into a
+//                         zero-haloed column-polyphase bf16 image, then per pool
+//                         window the 4 members' im2col rows from one 4x4 cell
+//                         neighbourhood, stored into TMEM with tcgen05.st (no
 //                         shared-memory traffic for A)
 //   W7-W14  epilogue 1  — two 4-warp groups on alternate (window group, half):
 //                         element-wise max of the window's 4 member accumulators
@@ -34,6 +35,10 @@
 // independent accumulators (4 TMEM buffers each).
 #include "common.cuh"
 #include "internal.h"
+
+#ifndef NS_EXP
+#define NS_EXP 0  // timing experiments only (tools/exp_fused.sh); 0 in the product
+#endif
 
 namespace ns {
 
@@ -136,7 +141,6 @@ conv12_fused_kernel(FusedArgs A) {
   uint64_t* w_full = t2_empty + kNB2;           // weights loaded
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
   float* bias1 = reinterpret_cast<float*>(smem + oBias);   // conv1 bias is folded into K
-  uint16_t* lut = reinterpret_cast<uint16_t*>(smem + oLut);
   uint2* X = reinterpret_cast<uint2*>(smem + oX);  // one 8-byte (4 x bf16) cell per pixel
 
   if (tid == 0) {
@@ -167,6 +171,7 @@ conv12_fused_kernel(FusedArgs A) {
   for (int e = tid; e < 2 * kActBytes / 16; e += blockDim.x)
     reinterpret_cast<uint4*>(smem + oAct)[e] = make_uint4(0, 0, 0, 0);
   for (int e = tid; e < 2 * kXPlane; e += blockDim.x) X[e] = make_uint2(0, 0);  // zero halo
+  uint16_t* lut = reinterpret_cast<uint16_t*>(smem + oLut);
   // normalisation LUT: x = bf16_RNE(clamp(((float)g - mu_c) / 127.5f, -1, 1)), exact fp32
   for (int e = tid; e < 3 * 256; e += blockDim.x) {
     const int c = e >> 8, g = e & 255;
@@ -294,7 +299,7 @@ conv12_fused_kernel(FusedArgs A) {
       mbar_wait(&in_full[s], (uint32_t)((it >> 1) & 1));
       nbar_sync(1, 128);  // previous frame's rows are all built: X may be overwritten
       const uint8_t* in = smem + oIn + s * kInBytes;
-      for (int p = bt; p < kIn * kIn; p += 128) {
+      for (int p = bt; p < ((NS_EXP & 2) ? 0 : kIn * kIn); p += 128) {
         const int y = p / kIn, x = p - kIn * y;
         const uint8_t* px = in + 3 * p;
         X[((x + 1) & 1) * kXPlane + (y + 1) * kXs + ((x + 1) >> 1)] =
@@ -303,45 +308,58 @@ conv12_fused_kernel(FusedArgs A) {
       }
       mbar_arrive(&in_empty[s]);
       nbar_sync(1, 128);  // X complete
-      for (int t = 0; t < kT1; ++t, ++u1) {
-        const int a = (int)(u1 % kA1Stages);
-        if (u1 >= kA1Stages) mbar_wait(&a1_empty[a], (uint32_t)(((u1 / kA1Stages) - 1) & 1));
-        // tile t = 4G + q: window w = 128G + row, window member q = (dy, dx)
-        const int w = (t >> 2) * 128 + bt, pq = t & 3;
-        uint32_t v[16];
-        if (w < kP1 * kP1) {
-          const int yp = w / kP1, xp = w - kP1 * yp;
-          const int y = 2 * yp + (pq >> 1), dx = pq & 1;
-          // padded column x + kx = 2*xp + dx + kx -> parity (dx+kx)&1, half (dx+kx)>>1
-          const uint2* even = X + ((dx & 1) ? kXPlane : 0) + y * kXs + xp;       // kx = 0, 2
-          const uint2* odd = X + ((dx & 1) ? 0 : kXPlane) + y * kXs + xp + dx;   // kx = 1
+      // One thread = one pool window of group G; its 4 members (dy, dx) are the
+      // 4 tiles 4G..4G+3 = A stages 0..3.  The 4x4 padded-pixel neighbourhood
+      // (16 cells) serves all 4 members' 3x3 patches.
+      for (int G = 0; G < kG1; ++G, u1 += 4) {
+        const int w = G * 128 + bt;
+        const bool valid = w < kP1 * kP1;
+        const int yp = valid ? w / kP1 : 0, xp = valid ? w - kP1 * yp : 0;
+        uint2 cell[4][4];  // [padded row 2yp + r][padded col 2xp + c]
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const uint2* ev = X + (2 * yp + r) * kXs + xp;             // even padded columns
+          const uint2* od = X + kXPlane + (2 * yp + r) * kXs + xp;   // odd padded columns
+          if (NS_EXP & 4) {
+            cell[r][0] = cell[r][1] = cell[r][2] = cell[r][3] = make_uint2(r, xp);
+            continue;
+          }
+          cell[r][0] = ev[0];
+          cell[r][1] = od[0];
+          cell[r][2] = ev[1];
+          cell[r][3] = od[1];
+        }
+#pragma unroll
+        for (int pq = 0; pq < 4; ++pq) {
+          const uint64_t u = u1 + pq;
+          const int a = (int)(u % kA1Stages);
+          if (u >= kA1Stages) mbar_wait(&a1_empty[a], (uint32_t)(((u / kA1Stages) - 1) & 1));
+          const int dy = pq >> 1, dx = pq & 1;
           uint32_t h[27];  // 27 bf16 in (tap, channel) order, one per 32-bit register
 #pragma unroll
           for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
             for (int kx = 0; kx < 3; ++kx) {
-              const uint2 c = kx == 1 ? odd[ky * kXs] : even[ky * kXs + (kx >> 1)];
+              const uint2 c = cell[dy + ky][dx + kx];
               const int k = (ky * 3 + kx) * 3;
               h[k] = c.x & 0xFFFFu;
               h[k + 1] = c.x >> 16;
               h[k + 2] = c.y & 0xFFFFu;
             }
+          uint32_t v[16];
 #pragma unroll
-          for (int j = 0; j < 13; ++j) v[j] = h[2 * j] | (h[2 * j + 1] << 16);
+          for (int j = 0; j < 13; ++j) v[j] = valid ? (h[2 * j] | (h[2 * j + 1] << 16)) : 0u;
           // K 27 and 28 = 1.0: the packed weights carry the bias there as a bf16
           // hi/lo pair, so the accumulator comes out as bias + sum (no epilogue add)
-          v[13] = h[26] | (0x3F80u << 16);
-          v[14] = 0x3F80u;
+          v[13] = valid ? (h[26] | (0x3F80u << 16)) : 0u;
+          v[14] = valid ? 0x3F80u : 0u;
           v[15] = 0;
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = 0;
+          tc_fence_after();
+          tmem_st16(tmem + ((uint32_t)lg << 16) + kColA1 + a * kA1Cols, v);
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&a1_full[a]);
         }
-        tc_fence_after();
-        tmem_st16(tmem + ((uint32_t)lg << 16) + kColA1 + a * kA1Cols, v);
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&a1_full[a]);
       }
     }
   } else if (warp < wEp2_0) {
@@ -401,6 +419,7 @@ conv12_fused_kernel(FusedArgs A) {
               const uint4 o0 = make_uint4(pk[0], pk[1], pk[2], pk[3]);
               const uint4 o1 = make_uint4(pk[4], pk[5], pk[6], pk[7]);
               if (kConv2) {
+                if (NS_EXP & 1) continue;
                 *reinterpret_cast<uint4*>(planes + (2 * cb) * kPlaneBytes + rho * 16) = o0;
                 *reinterpret_cast<uint4*>(planes + (2 * cb + 1) * kPlaneBytes + rho * 16) = o1;
               } else {

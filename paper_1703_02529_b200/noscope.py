@@ -15,7 +15,8 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libnoscope.so")
+# NOSCOPE_LIB: an alternative build of the same sources (tools/ experiments)
+LIB_PATH = os.environ.get("NOSCOPE_LIB") or os.path.join(_PKG, "libnoscope.so")
 
 c_i32, c_i64, c_f32, c_f64, c_p, c_sz = C.c_int32, C.c_int64, C.c_float, C.c_double, C.c_void_p, C.c_size_t
 

@@ -20,7 +20,7 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   return d;
 }
 
-template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0, int OFF = 0>
+template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0, int OFF = 0, int M = 128>
 __global__ void __launch_bounds__(512, 1) mma_loop(int iters, int ksteps, long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* A = smem;                      // 128 rows x 128 B per 4 K-steps (sw) / 4 KB per step
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(512, 1) mma_loop(int iters, int ksteps, long l
     if (acc.x == 12345) buf[0] = acc;
   }
   if (threadIdx.x == 0) {
-    const uint32_t idesc = idesc_bf16_f32(128, N);
+    const uint32_t idesc = idesc_bf16_f32(M, N);
     const uint32_t a0 = smem_u32(A), b0 = smem_u32(B);
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
@@ -83,21 +83,21 @@ __global__ void __launch_bounds__(512, 1) mma_loop(int iters, int ksteps, long l
   if (threadIdx.x < 32) tmem_dealloc<512>(tmem);
 }
 
-template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0, int OFF = 0>
+template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0, int OFF = 0, int M = 128>
 void run() {
   const int iters = 500, ksteps = 8;
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
   size_t smem = 32768 + 8 * 256 * 32 + 2048;
-  cudaFuncSetAttribute(mma_loop<N, NACC, SW, SBO, HAMMER, OFF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  mma_loop<N, NACC, SW, SBO, HAMMER, OFF><<<148, 512, smem>>>(iters, ksteps, d);
+  cudaFuncSetAttribute(mma_loop<N, NACC, SW, SBO, HAMMER, OFF, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  mma_loop<N, NACC, SW, SBO, HAMMER, OFF, M><<<148, 512, smem>>>(iters, ksteps, d);
   cudaError_t err = cudaDeviceSynchronize();
   if (err != cudaSuccess) { printf("N=%d acc=%d sw=%d: %s\n", N, NACC, (int)SW, cudaGetErrorString(err)); fflush(stdout); return; }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  mma_loop<N, NACC, SW, SBO, HAMMER, OFF><<<148, 512, smem>>>(iters, ksteps, d);
+  mma_loop<N, NACC, SW, SBO, HAMMER, OFF, M><<<148, 512, smem>>>(iters, ksteps, d);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
@@ -105,18 +105,16 @@ void run() {
   long long h[148];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double mmas = (double)iters * ksteps * NACC;
-  double flops = mmas * 2.0 * 128 * N * 16 * 148;
-  printf("H=%d OFF=%3d SBO=%3d N=%3d acc=%d %s: %6.2f cycles/MMA (floor %3d), %7.1f TFLOP/s  %s\n", HAMMER, OFF, SBO, N, NACC,
-         SW ? "SW128" : "none ", (double)h[0] / mmas, 128 * N / 256, flops / (ms * 1e-3) / 1e12,
+  double flops = mmas * 2.0 * M * N * 16 * 148;
+  printf("M=%3d H=%d OFF=%3d SBO=%3d N=%3d acc=%d %s: %6.2f cycles/MMA (floor %3d), %7.1f TFLOP/s  %s\n", M, HAMMER, OFF, SBO, N, NACC,
+         SW ? "SW128" : "none ", (double)h[0] / mmas, M * N / 256, flops / (ms * 1e-3) / 1e12,
          cudaGetErrorString(cudaGetLastError()));
   fflush(stdout);
   cudaFree(d);
 }
 
 int main() {
-  run<128, 2, false, 128, 0, 0>(); run<128, 2, false, 128, 0, 16>(); run<128, 2, false, 128, 0, 48>();
-  run<256, 2, false, 128, 0, 0>(); run<256, 2, false, 128, 0, 16>(); run<256, 1, false, 128, 0, 0>();
-  run<256, 2, false, 128, 1, 16>(); run<128, 2, false, 128, 1, 16>(); run<128, 2, false, 128, 2, 16>();
-  run<64, 4, false, 128, 0, 0>(); run<64, 4, false, 128, 0, 16>();
+  run<256, 2, false, 128, 0, 16, 64>(); run<256, 1, false, 128, 0, 16, 64>(); run<256, 2, false, 128, 1, 16, 64>();
+  run<128, 2, false, 128, 0, 16, 64>(); run<64, 4, false, 128, 1, 16, 128>(); run<64, 4, false, 128, 0, 16, 128>();
   return 0;
 }
