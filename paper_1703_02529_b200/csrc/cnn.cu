@@ -66,15 +66,24 @@ struct FcArgs {
   const int64_t* n_dev;
   int64_t n_max, chunk_base, chunk_len;
   uint32_t tmem_cols;
+  int ksplit;            // K split across CTAs (fixed per K: results do not depend on n)
+  float* part;           // [tiles][ksplit][128][D] fp32 partial sums (ksplit > 1)
+  unsigned* counters;    // [tiles] arrival counters, zero between uses
 };
 constexpr int kFcKChunk = 64;
 
+// FC1 (+ReLU, bf16) and FC2 for one 128-frame tile and one K slice.  One
+// CTA streams its features/weights through a kBStages bulk-copy ring; the K16
+// steps alternate between two TMEM accumulators (independent MMA chains).
+// With ksplit > 1 each CTA writes fp32 partials; the last CTA of a tile (arrival
+// counter) sums them in slice order (deterministic) and runs the epilogue.
 __global__ void __launch_bounds__(kCnnThreads)
 fc_kernel(FcArgs A) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int64_t n = min(*A.n_dev, A.n_max);
   const int64_t cnt = min(n - A.chunk_base, A.chunk_len);
-  const int64_t tile = blockIdx.x;
+  const int64_t tile = blockIdx.x / A.ksplit;
+  const int ks = blockIdx.x % A.ksplit;
   if (cnt <= 0 || tile * 128 >= cnt) return;
   const int tid = threadIdx.x, warp = tid >> 5;
   const uint32_t a_bytes = 128 * kFcKChunk * 2, b_bytes = (uint32_t)A.D * kFcKChunk * 2;
@@ -84,6 +93,7 @@ fc_kernel(FcArgs A) {
   uint64_t* empty = full + kBStages;
   uint64_t* bar_acc = empty + kBStages;
   uint32_t* tmem_s = reinterpret_cast<uint32_t*>(bar_acc + 1);
+  int* last = reinterpret_cast<int*>(tmem_s + 1);
   if (tid == 0) {
     for (int s = 0; s < kBStages; ++s) {
       mbar_init(&full[s], 1);
@@ -97,15 +107,18 @@ fc_kernel(FcArgs A) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_s;
-  const int nchunks = A.K / kFcKChunk;
-  const uint8_t* a_src = A.feat + tile * ((int64_t)A.K * 256);
+  const int nall = A.K / kFcKChunk;
+  const int c0 = (int)((int64_t)nall * ks / A.ksplit), c1 = (int)((int64_t)nall * (ks + 1) / A.ksplit);
+  const int nchunks = c1 - c0;
+  const uint8_t* a_src = A.feat + tile * ((int64_t)A.K * 256) + (size_t)c0 * a_bytes;
+  const uint8_t* b_src = A.wpack + (size_t)c0 * b_bytes;
   if (tid == 0) {
     auto issue = [&](int c) {
       const int s = c % kBStages;
       if (c >= kBStages) mbar_wait(&empty[s], (uint32_t)(((c / kBStages) - 1) & 1));
       mbar_arrive_expect_tx(&full[s], stage_bytes);
       bulk_g2s(stages + (size_t)s * stage_bytes, a_src + (size_t)c * a_bytes, a_bytes, &full[s]);
-      bulk_g2s(stages + (size_t)s * stage_bytes + a_bytes, A.wpack + (size_t)c * b_bytes, b_bytes,
+      bulk_g2s(stages + (size_t)s * stage_bytes + a_bytes, b_src + (size_t)c * b_bytes, b_bytes,
                &full[s]);
     };
     int issued = 0;
@@ -118,8 +131,8 @@ fc_kernel(FcArgs A) {
       const uint32_t as = smem_u32(stages + (size_t)s * stage_bytes), bs = as + a_bytes;
 #pragma unroll
       for (int kk = 0; kk < kFcKChunk / 16; ++kk)
-        umma_bf16(tmem, sdesc(as + kk * 2 * 2048, 2048, 128),
-                  sdesc(bs + kk * 2 * A.D * 16, A.D * 16, 128), idesc, (c > 0 || kk > 0) ? 1u : 0u);
+        umma_bf16(tmem + (kk & 1) * A.D, sdesc(as + kk * 2 * 2048, 2048, 128),
+                  sdesc(bs + kk * 2 * A.D * 16, A.D * 16, 128), idesc, (c > 0 || kk > 1) ? 1u : 0u);
       umma_commit(&empty[s]);
       if (issued < nchunks) issue(issued++);
     }
@@ -128,15 +141,65 @@ fc_kernel(FcArgs A) {
   __syncwarp();
   mbar_wait(bar_acc, 0);
   tc_fence_after();
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  float* mypart = A.part + (((size_t)tile * A.ksplit + ks) * 128 + tid) * A.D;
+  if (A.ksplit > 1) {
+    for (int cb = 0; cb < A.D / 16; ++cb) {
+      uint32_t r0[16], r1[16];
+      tmem_ld16(trow + cb * 16, r0);
+      tmem_ld16(trow + A.D + cb * 16, r1);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; j += 4)
+        *reinterpret_cast<float4*>(mypart + cb * 16 + j) =
+            make_float4(__uint_as_float(r0[j]) + __uint_as_float(r1[j]),
+                        __uint_as_float(r0[j + 1]) + __uint_as_float(r1[j + 1]),
+                        __uint_as_float(r0[j + 2]) + __uint_as_float(r1[j + 2]),
+                        __uint_as_float(r0[j + 3]) + __uint_as_float(r1[j + 3]));
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) *last = atomicAdd(&A.counters[tile], 1u) == (unsigned)(A.ksplit - 1);
+    __syncthreads();
+    if (!*last) {
+      tc_fence_before();
+      __syncthreads();
+      if (warp == 0) tmem_dealloc_rt(tmem, A.tmem_cols);
+      return;
+    }
+    __threadfence();
+    if (tid == 0) A.counters[tile] = 0u;  // ready for the next chunk / call
+  }
   float z = 0.0f;
   for (int cb = 0; cb < A.D / 16; ++cb) {
-    uint32_t r[16];
-    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + cb * 16, r);
-    tmem_ld_wait();
+    float acc[16];
+    if (A.ksplit > 1) {
+      const float* p0 = A.part + ((size_t)tile * A.ksplit * 128 + tid) * A.D + cb * 16;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = 0.0f;
+      for (int k = 0; k < A.ksplit; ++k) {   // slice order: deterministic
+        const float4* q = reinterpret_cast<const float4*>(p0 + (size_t)k * 128 * A.D);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 v = __ldcg(q + j);
+          acc[4 * j] += v.x;
+          acc[4 * j + 1] += v.y;
+          acc[4 * j + 2] += v.z;
+          acc[4 * j + 3] += v.w;
+        }
+      }
+    } else {
+      uint32_t r0[16], r1[16];
+      tmem_ld16(trow + cb * 16, r0);
+      tmem_ld16(trow + A.D + cb * 16, r1);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = __uint_as_float(r0[j]) + __uint_as_float(r1[j]);
+    }
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const int c = cb * 16 + j;
-      const float h = bf2f(f2bf(fmaxf(__uint_as_float(r[j]) + A.b1[c], 0.0f)));
+      const float h = bf2f(f2bf(fmaxf(acc[j] + A.b1[c], 0.0f)));
       z = fmaf(h, bf2f(A.w2[c]), z);
     }
   }
@@ -148,6 +211,7 @@ fc_kernel(FcArgs A) {
   if (warp == 0) tmem_dealloc_rt(tmem, A.tmem_cols);
 }
 
+static int fc_ksplit(int K) { return std::max(1, std::min(8, K / 1152)); }
 
 // =================================================================== host plan
 struct CnnPlan {
@@ -158,7 +222,7 @@ struct CnnPlan {
   ConvGGeom g[4];             // generic layers first_g .. L-1
   size_t gw_off[4];           // their packed weights
   size_t in_off[4];           // their stacked inputs
-  size_t fc_off, feat_off, total;
+  size_t fc_off, feat_off, part_off, cnt_off, total;
   int64_t chunk;
 };
 
@@ -200,6 +264,10 @@ static bool make_plan(const noscope_cnn_arch& a, int64_t n_max, CnnPlan* P) {
   }
   p.feat_off = off;
   off = align_up(off + (size_t)p.chunk * p.K * 2, 1024);
+  p.part_off = off;   // FC split-K partials
+  off = align_up(off + (size_t)(p.chunk / 128) * fc_ksplit(p.K) * 128 * p.D * 4, 1024);
+  p.cnt_off = off;
+  off = align_up(off + (size_t)(p.chunk / 128) * 4, 256);
   p.total = off;
   *P = p;
   return true;
@@ -273,6 +341,8 @@ noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& 
     cudaFuncSetAttribute(fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
+  if (fc_ksplit(P.K) > 1)   // FC split-K arrival counters start at zero (reset by their last CTA)
+    NS_CUDA_TRY(cudaMemsetAsync(ws + P.cnt_off, 0, (size_t)(P.chunk / 128) * 4, st));
   for (int64_t base = 0; base < n_max; base += P.chunk) {
     const int64_t len = std::min<int64_t>(P.chunk, n_max - base);
     FusedArgs fa{};
@@ -327,10 +397,13 @@ noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& 
     f.n_max = n_max;
     f.chunk_base = base;
     f.chunk_len = len;
-    f.tmem_cols = tmem_cols_host(P.D);
+    f.tmem_cols = tmem_cols_host(2 * P.D);
+    f.ksplit = fc_ksplit(P.K);
+    f.part = reinterpret_cast<float*>(ws + P.part_off);
+    f.counters = reinterpret_cast<unsigned*>(ws + P.cnt_off);
     const size_t fsm = (size_t)kBStages * (128 * kFcKChunk * 2 + P.D * kFcKChunk * 2) +
-                       (2 * kBStages + 1) * 8 + 16 + 1024;
-    fc_kernel<<<(int)((len + 127) / 128), kCnnThreads, fsm, st>>>(f);
+                       (2 * kBStages + 1) * 8 + 32 + 1024;
+    fc_kernel<<<(int)((len + 127) / 128) * f.ksplit, kCnnThreads, fsm, st>>>(f);
     NS_LAUNCH_CHECK();
     count_launch();
   }

@@ -25,7 +25,8 @@
 //                         element-wise max of the window's 4 member accumulators
 //                         -> ReLU -> bf16 -> conv2 operand planes (double-buffered
 //                         per frame) or the stacked map in HBM
-//   W15-W18 epilogue 2  — TMEM -> bias -> ReLU -> bf16 -> 2x2 max by shuffles ->
+//   W15-W18 epilogue 2  — TMEM (bias accumulated by an extra K step) -> ReLU -> bf16
+//                         -> 2x2 max by shuffles ->
 //                         FC feature tiles (L = 2) or the stacked layer-3 map (L = 4)
 // conv2 M tile = 16 conv rows x 8 conv columns: 16 core-matrix groups of 8
 // consecutive pixels at a stride of one image row (SBO = Wp*16 B), so a warp's
@@ -38,6 +39,8 @@
 
 #ifndef NS_EXP
 #define NS_EXP 0  // timing experiments only (tools/exp_fused.sh); 0 in the product
+// bits: 1 no conv2-plane stores, 2 no image build, 4 no im2col loads, 8 no conv1 MMAs,
+// 16 no conv2 MMAs, 32 no epilogue-2 work, 64 no epilogue-1 work, 128 no tcgen05.wait::st
 #endif
 
 namespace ns {
@@ -82,8 +85,11 @@ constexpr int oAct = oB2 + 9 * (C1 / 8) * C2 * 16;       // 2 x conv2 operand pl
 constexpr int oIn = oAct + 2 * kActBytes;                // 2 x u8 frames
 constexpr int oX = oIn + 2 * kInBytes;                   // bf16 image [52][52][4]
 constexpr int oLut = oX + 2 * kXPlane * 8;               // bf16 LUT [3][256]
-constexpr int oBias = oLut + 3 * 256 * 2;                // (64 + 64) x 4
-constexpr int oBar = oBias + (kC1Max + C2) * 4;
+// conv2 bias as one extra K16 step: A = "ones" tile (K columns 0, 1 = 1.0),
+// B = [bf16(b), bf16(b - bf16(b))] per output channel (~2^-17 relative)
+constexpr int oOnes = oLut + 3 * 256 * 2;                // [2][128][8] bf16
+constexpr int oB2b = oOnes + 2 * 128 * 16;               // [2][64][8] bf16
+constexpr int oBar = oB2b + 2 * C2 * 16;
 constexpr int kNumBars = 2 + 2 + 2 * kA1Stages + 2 * kNG1 + 2 + 2 + 2 * kNB2 + 1;
 constexpr int kSmem = oBar + kNumBars * 8 + 16;
 }  // namespace fz
@@ -140,7 +146,6 @@ conv12_fused_kernel(FusedArgs A) {
   uint64_t* t2_empty = t2_full + kNB2;          // [kNB2] 128 ep2 arrivals
   uint64_t* w_full = t2_empty + kNB2;           // weights loaded
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
-  float* bias1 = reinterpret_cast<float*>(smem + oBias);   // conv1 bias is folded into K
   uint2* X = reinterpret_cast<uint2*>(smem + oX);  // one 8-byte (4 x bf16) cell per pixel
 
   if (tid == 0) {
@@ -179,9 +184,23 @@ conv12_fused_kernel(FusedArgs A) {
     const float v = fminf(fmaxf(((float)g - mu) / 127.5f, -1.0f), 1.0f);
     lut[e] = f2bf_u(v);
   }
-  float* bias2 = bias1 + kC1Max;
-  if (kConv2)
-    for (int e = tid; e < C2; e += blockDim.x) bias2[e] = A.b2[e];
+  if (kConv2) {
+    uint32_t* ones = reinterpret_cast<uint32_t*>(smem + oOnes);
+    for (int e = tid; e < 2 * 128 * 4; e += blockDim.x)
+      ones[e] = (e < 128 * 4 && (e & 3) == 0) ? 0x3F803F80u : 0u;   // row r: K0 = K1 = 1.0
+    uint32_t* b2b = reinterpret_cast<uint32_t*>(smem + oB2b);
+    for (int e = tid; e < 2 * C2 * 4; e += blockDim.x) {
+      uint32_t v = 0;
+      if (e < C2 * 4 && (e & 3) == 0) {
+        const float b = A.b2[e >> 2];
+        const __nv_bfloat16 hi = __float2bfloat16_rn(b);
+        const __nv_bfloat16 lo = __float2bfloat16_rn(b - __bfloat162float(hi));
+        v = (uint32_t)*reinterpret_cast<const uint16_t*>(&hi) |
+            ((uint32_t)*reinterpret_cast<const uint16_t*>(&lo) << 16);
+      }
+      b2b[e] = v;
+    }
+  }
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -235,6 +254,7 @@ conv12_fused_kernel(FusedArgs A) {
             for (int kk = 0; kk < kK1 / 16; ++kk)
 #pragma unroll
               for (int q = 0; q < 2; ++q)
+                if (!(NS_EXP & 8))
                 umma_bf16_ts(tmem + kColD1 + (gb * 4 + (int)((u1 + q) & 3)) * C1,
                              tmem + kColA1 + a[q] * kA1Cols + kk * 8,
                              bd0 + (uint64_t)((kk * 2 * C1t * 16 + h * C1 * 16) >> 4), id1, kk);
@@ -250,6 +270,8 @@ conv12_fused_kernel(FusedArgs A) {
     if (kConv2 && lane == 0) {
       constexpr uint32_t id2 = idesc_bf16_f32(128, C2);
       const uint32_t sB2 = smem_u32(smem + oB2), sAct = smem_u32(smem + oAct);
+      const uint64_t dOnes = sdesc(smem_u32(smem + oOnes), 128 * 16, 128);
+      const uint64_t dBias = sdesc(smem_u32(smem + oB2b), C2 * 16, 128);
       mbar_wait(w_full, 0);
       uint64_t u2 = 0;
       for (int64_t it = 0; it < my_frames; ++it) {
@@ -281,9 +303,12 @@ conv12_fused_kernel(FusedArgs A) {
             const int shift = (tap / 3 - 1) * kWp + (tap % 3 - 1);
             const uint64_t aoff = (uint64_t)((cg * kPlaneBytes + shift * 16) >> 4);
             const uint64_t bd = bd0 + (uint64_t)(((tap * 4 + cg) * C2 * 16) >> 4);
+            if (NS_EXP & 16) continue;
             umma_bf16(d0, ad0 + aoff, bd, id2, ks > 0 ? 1u : 0u);
             umma_bf16(d1, ad1 + aoff, bd, id2, ks > 0 ? 1u : 0u);
           }
+          umma_bf16(d0, dOnes, dBias, id2, 1u);   // + bias (extra K16 step)
+          umma_bf16(d1, dOnes, dBias, id2, 1u);
           for (int q = 0; q < 2; ++q) umma_commit(&t2_full[b[q]]);
         }
         umma_commit(&act_empty[pb]);
@@ -356,7 +381,7 @@ conv12_fused_kernel(FusedArgs A) {
           v[15] = 0;
           tc_fence_after();
           tmem_st16(tmem + ((uint32_t)lg << 16) + kColA1 + a * kA1Cols, v);
-          tmem_st_wait();
+          if (!(NS_EXP & 128)) tmem_st_wait();
           tc_fence_before();
           mbar_arrive(&a1_full[a]);
         }
@@ -396,7 +421,7 @@ conv12_fused_kernel(FusedArgs A) {
           const int rho = (yp + 1) * kWp + (xp + 1) + 1;
           const uint32_t tb = tmem + ((uint32_t)lg << 16) + kColD1 + gb * 4 * C1;
 #pragma unroll
-          for (int cb = 0; cb < C1 / 16; ++cb) {
+          for (int cb = 0; cb < ((NS_EXP & 64) ? 0 : C1 / 16); ++cb) {
             // 2x2 max pool = element-wise max over the window's 4 accumulators
             // (bias already accumulated; max, ReLU and RNE commute: all monotone)
             uint32_t r0[16], r1[16], r2[16], r3[16];
@@ -477,15 +502,14 @@ conv12_fused_kernel(FusedArgs A) {
         const bool keep = pool_lane && yc < 24 && (yb == 0 || yc >= 16);
         const int yp = yc >> 1, xp = xc >> 1;
 #pragma unroll
-        for (int g = 0; g < C2 / 16; ++g) {
+        for (int g = 0; g < ((NS_EXP & 32) ? 0 : C2 / 16); ++g) {
           uint32_t r[16];
           tmem_ld16(tmem + ((uint32_t)lg << 16) + kColD2 + b * C2 + g * 16, r);
           tmem_ld_wait();
           uint32_t pk[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            uint32_t v = relu_bf16x2(__uint_as_float(r[2 * j]) + bias2[g * 16 + 2 * j],
-                                     __uint_as_float(r[2 * j + 1]) + bias2[g * 16 + 2 * j + 1]);
+          for (int j = 0; j < 8; ++j) {   // bias already accumulated (extra K step)
+            uint32_t v = relu_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
             v = __vmaxu2(v, __shfl_xor_sync(0xffffffffu, v, 1));   // x pair
             v = __vmaxu2(v, __shfl_xor_sync(0xffffffffu, v, 8));   // y pair
             pk[j] = v;
