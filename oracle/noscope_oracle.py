@@ -467,3 +467,86 @@ def sweep_greedy_paper(s, z, y, a, delta, u, timing, fp_limit, fn_limit):
     if not cands:
         return None
     return min(cands, key=lambda c: c[0])[1]
+
+
+# --------------------------------------------------------------------------
+# N1 DD fitting — P:557-558 "computes the reference image
+#    by averaging frames where the reference model returns no labels";
+#    P:577-581 / P:850-853 "trains a logistic regression (LR) classifier to weigh
+#    each block"; SPEC build_reference_image S:134-142, train_block_weights
+#    S:209-217.  Readings: R-21 rounding half up, on the 50x50 small
+#    frames the DD compares; R-22 LR = full-batch gradient descent on the mean log
+#    loss (+ l2/2 |w|^2) over z-scored features, folded back to raw features.
+# --------------------------------------------------------------------------
+def reference_image(small: np.ndarray, labels: np.ndarray) -> np.ndarray:
+    """small uint8 [n, h, w, 3], labels [n] (0 = no object).  Per-pixel mean over
+    the negative frames, rounded half up: floor((2*S + m) / (2*m)), m = #negatives.
+    Raises ValueError when there is no negative frame (caller falls back
+    to earlier-frame mode)."""
+    neg = np.asarray(labels) == 0
+    m = int(neg.sum())
+    if m == 0:
+        raise ValueError("no negative frame: use the earlier-frame difference detector")
+    S = small[neg].astype(np.int64).sum(axis=0)
+    return ((2 * S + m) // (2 * m)).astype(np.uint8)
+
+
+def block_features(small: np.ndarray, grid: int, mode: int, ref=None, k: int = 0) -> np.ndarray:
+    """float64 [n, grid*grid]: row i = blocked_mse(frame i, anchor) (O3), anchor =
+    the reference image (mode 0) or frame i - k of the same batch (mode 1; rows
+    i < k have no anchor and are NaN)."""
+    n = small.shape[0]
+    out = np.full((n, grid * grid), np.nan)
+    for i in range(n):
+        if mode == 0:
+            out[i] = blocked_mse(small[i], ref, grid)
+        elif i >= k:
+            out[i] = blocked_mse(small[i], small[i - k], grid)
+    return out
+
+
+def lr_fit(F: np.ndarray, t: np.ndarray, iters: int, lr: float = 0.0, l2: float = 0.0):
+    """Logistic regression by full-batch gradient descent (R-22), fp64.
+
+    X = (F - mu) / sd per feature (sd = population std; constant features sd := 1),
+    w = 0, b = 0; each iteration, in this order:
+        p = 1 / (1 + exp(-(X w + b)));  r = p - t
+        w <- w - lr * (X^T r / n + l2 * w);  b <- b - lr * mean(r)
+    lr <= 0 selects 4 / (d + 1) (the log loss Hessian is <= (d + 1) / 4 on
+    z-scored features, so the step is a guaranteed descent).  Returns raw-feature
+    parameters (w / sd, b - sum(w * mu / sd)) so that the scorer's logit
+    b + sum_k w_k m_k equals the fitted model's.  Errors: n < 2 or one class only
+    (S:212, "advising global metric")."""
+    F = np.asarray(F, dtype=np.float64)
+    t = np.asarray(t, dtype=np.float64)
+    n, d = F.shape
+    if n < 2 or t.min() == t.max():
+        raise ValueError("LR fit needs >= 2 examples of both classes; use the global metric")
+    mu = F.mean(axis=0)
+    sd = F.std(axis=0)
+    sd = np.where(sd > 0, sd, 1.0)
+    X = (F - mu) / sd
+    if lr <= 0:
+        lr = 4.0 / (d + 1)
+    w = np.zeros(d)
+    b = 0.0
+    for _ in range(iters):
+        p = 1.0 / (1.0 + np.exp(-(X @ w + b)))
+        r = p - t
+        gw = X.T @ r / n + l2 * w
+        gb = r.mean()
+        w = w - lr * gw
+        b = b - lr * gb
+    return w / sd, b - float(np.sum(w * mu / sd))
+
+
+def lr_loss(F, t, w_raw, b_raw, l2: float = 0.0) -> float:
+    """Mean log loss of raw-feature parameters (+ l2/2 |w_std|^2 in the z-scored
+    parameterisation), the objective lr_fit descends (used by its pins)."""
+    F = np.asarray(F, dtype=np.float64)
+    t = np.asarray(t, dtype=np.float64)
+    sd = F.std(axis=0)
+    sd = np.where(sd > 0, sd, 1.0)
+    z = F @ w_raw + b_raw
+    loss = np.mean(np.logaddexp(0.0, z) - t * z)
+    return float(loss + 0.5 * l2 * np.sum((w_raw * sd) ** 2))
