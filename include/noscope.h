@@ -318,6 +318,57 @@ noscope_status noscope_threshold_sweep(int32_t phase, const double* s, const flo
                                        noscope_sweep_best* best_host, void* ws, size_t ws_bytes,
                                        noscope_stream_t stream);
 
+/* ---- Difference-detector fitting -----------------
+ * The configuration steps that produce the DD's inputs: the reference image of
+ * mode 0 and the blocked-LR weights of metric 1.  Not on the per-frame path.
+ * All three are deterministic (fixed-order reductions).                     */
+
+/* Workspace for noscope_reference_image (small_bytes = out_w*out_h*3) and
+ * noscope_lr_fit (n examples x d features); take the max of the uses.        */
+size_t noscope_fit_workspace_bytes(int64_t n, int32_t d, int64_t small_bytes);
+
+/* Reference image ("computes the reference image by averaging frames
+ * where the reference model returns no labels"; SPEC build_reference_image
+ * S:134-142; reading R-21): ref[p] = floor((2*S_p + m) / (2*m)) over the m
+ * small frames with labels[i] == 0 (per-pixel mean rounded half up).
+ * small: device, n frames of out_h*out_w*3 u8 (HWC) at small_pitch (multiple of
+ * 16); labels: device u8 [n] (0 = no object); ref_out: device out_h*out_w*3 u8.
+ * Synchronous (reads back m).  No negative frame -> NOSCOPE_DATA, ref_out
+ * untouched (the caller falls back to the earlier-frame mode).
+ * Frame bytes must not exceed 2^32/255 per CTA slice: any n is accepted.     */
+noscope_status noscope_reference_image(const uint8_t* small, int64_t small_pitch, int32_t out_w,
+                                       int32_t out_h, const uint8_t* labels, int64_t n,
+                                       uint8_t* ref_out, void* ws, size_t ws_bytes,
+                                       noscope_stream_t stream);
+
+/* Per-frame block features (O3 blocked_mse on each frame): feats[i][k]
+ * = MSE of LR block k (row-major, remainder rows/columns in the last block)
+ * between small frame i and its anchor: dd->ref_image (dd->mode 0) or small
+ * frame i - dd->t_diff_frames of this batch (mode 1; rows i < t_diff_frames
+ * have no anchor and are NaN).  Uses dd->mode, out_w, out_h, grid (1..16),
+ * t_diff_frames, ref_image; feats: device fp64 [n][grid*grid].  Asynchronous. */
+noscope_status noscope_block_features(const noscope_dd_config* dd, const uint8_t* small,
+                                      int64_t small_pitch, int64_t n, double* feats,
+                                      noscope_stream_t stream);
+
+/* Blocked-LR fit ("trains a logistic regression (LR) classifier to
+ * weigh each block"; SPEC train_block_weights S:209-217; reading
+ * R-22): full-batch gradient descent in fp64 on the mean log loss
+ * (+ l2/2 |w|^2) over z-scored features (population mean/std per feature;
+ * constant features std := 1), w = b = 0, `iters` steps
+ *   r = sigmoid(X w + b) - t;  w -= lr (X^T r / n + l2 w);  b -= lr mean(r)
+ * (lr <= 0 selects 4/(d+1)); returned in raw-feature form: w_host[k] = w_k/sd_k,
+ * w_host[d] = b - sum_k w_k mu_k / sd_k, so the DD logit b + sum w_k m_k of
+ * noscope_dd_config (lr_weights = (float)w_host[0..d), lr_bias = (float)w_host[d])
+ * reproduces the fitted model.  feats: device fp64 [n][d] (finite); targets:
+ * device u8 [n] (nonzero = 1); w_host: host fp64 [d + 1].  Synchronous.
+ * NOSCOPE_DATA: n < 2, one class only, or a non-finite feature (use the
+ * global metric).  NOSCOPE_SHAPE if n / min(1024, ceil(n/256)) rows per CTA
+ * exceed shared memory (n > ~28 M).                                         */
+noscope_status noscope_lr_fit(const double* feats, const uint8_t* targets, int64_t n, int32_t d,
+                              int32_t iters, double lr, double l2, double* w_host, void* ws,
+                              size_t ws_bytes, noscope_stream_t stream);
+
 /* Reads and clears the device status word in a workspace (synchronises). */
 noscope_status noscope_check(void* ws, noscope_stream_t stream);
 

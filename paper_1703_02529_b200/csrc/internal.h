@@ -174,6 +174,16 @@ noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& 
                           const int64_t* n_dev, int64_t n_max, float* logits, void* ws,
                           uint32_t* status, cudaStream_t st);
 
+// DD fitting (fit.cu).
+size_t fit_ws_bytes(int64_t n, int32_t d, int64_t small_bytes);
+noscope_status launch_reference_image(const uint8_t* small, int64_t pitch, int bytes, const uint8_t* labels,
+                                      int64_t n, uint8_t* ref, void* ws, uint64_t* neg_count_host,
+                                      cudaStream_t st);
+noscope_status launch_block_features(const noscope_dd_config& c, const uint8_t* small, int64_t pitch,
+                                     int64_t n, double* feats, cudaStream_t st);
+noscope_status launch_lr_fit(const double* F, const uint8_t* t, int64_t n, int d, int iters, double lr,
+                             double l2, double* wb_host, void* ws, cudaStream_t st);
+
 // Threshold sweep.
 size_t sweep_ws_bytes(int32_t n_delta, int32_t m);
 noscope_status launch_sweep(int32_t phase, const double* s, const float* z, const uint8_t* y,

@@ -434,6 +434,62 @@ noscope_status noscope_threshold_sweep(int32_t phase, const double* s, const flo
   return infeasible ? NOSCOPE_INFEASIBLE : NOSCOPE_OK;
 }
 
+// ---- DD fitting (fit.cu)
+size_t noscope_fit_workspace_bytes(int64_t n, int32_t d, int64_t small_bytes) {
+  if (n < 0 || d < 1 || small_bytes < 0) return 0;
+  return fit_ws_bytes(n, d, small_bytes);
+}
+
+noscope_status noscope_reference_image(const uint8_t* small, int64_t small_pitch, int32_t out_w,
+                                       int32_t out_h, const uint8_t* labels, int64_t n,
+                                       uint8_t* ref_out, void* ws, size_t ws_bytes,
+                                       noscope_stream_t stream) {
+  if (!small || !labels || !ref_out || !ws || n < 0) return NOSCOPE_INVALID_ARGUMENT;
+  if (out_w < 1 || out_h < 1) return NOSCOPE_SHAPE;
+  const int64_t bytes = (int64_t)out_w * out_h * 3;
+  if (small_pitch % 16 || small_pitch < ((bytes + 15) & ~15ll) || !aligned16(small)) return NOSCOPE_SHAPE;
+  if (ws_bytes < fit_ws_bytes(1, 1, bytes)) return NOSCOPE_WORKSPACE_TOO_SMALL;
+  noscope_status s = check_device();
+  if (s != NOSCOPE_OK) return s;
+  if (n == 0) return NOSCOPE_DATA;
+  uint64_t m = 0;
+  s = launch_reference_image(small, small_pitch, (int)bytes, labels, n, ref_out, ws, &m,
+                             (cudaStream_t)stream);
+  if (s != NOSCOPE_OK) return s;
+  return m == 0 ? NOSCOPE_DATA : NOSCOPE_OK;
+}
+
+noscope_status noscope_block_features(const noscope_dd_config* dd, const uint8_t* small,
+                                      int64_t small_pitch, int64_t n, double* feats,
+                                      noscope_stream_t stream) {
+  if (!dd || !small || !feats || n < 0) return NOSCOPE_INVALID_ARGUMENT;
+  if (dd->mode != 0 && dd->mode != 1) return NOSCOPE_INVALID_ARGUMENT;
+  if (dd->mode == 0 && !dd->ref_image) return NOSCOPE_INVALID_ARGUMENT;
+  if (dd->mode == 1 && dd->t_diff_frames < 1) return NOSCOPE_INVALID_ARGUMENT;
+  if (dd->out_w < 1 || dd->out_h < 1) return NOSCOPE_SHAPE;
+  if (dd->grid < 1 || dd->grid > kMaxGrid || dd->grid > dd->out_w || dd->grid > dd->out_h)
+    return NOSCOPE_SHAPE;
+  const int64_t bytes = (int64_t)dd->out_w * dd->out_h * 3;
+  if (small_pitch % 16 || small_pitch < ((bytes + 15) & ~15ll)) return NOSCOPE_SHAPE;
+  noscope_status s = check_device();
+  if (s != NOSCOPE_OK) return s;
+  if (n == 0) return NOSCOPE_OK;
+  return launch_block_features(*dd, small, small_pitch, n, feats, (cudaStream_t)stream);
+}
+
+noscope_status noscope_lr_fit(const double* feats, const uint8_t* targets, int64_t n, int32_t d,
+                              int32_t iters, double lr, double l2, double* w_host, void* ws,
+                              size_t ws_bytes, noscope_stream_t stream) {
+  if (!feats || !targets || !w_host || !ws || d < 1 || iters < 0 || std::isnan(lr) || std::isnan(l2) ||
+      l2 < 0)
+    return NOSCOPE_INVALID_ARGUMENT;
+  if (n < 2) return NOSCOPE_DATA;
+  if (ws_bytes < fit_ws_bytes(n, d, 0)) return NOSCOPE_WORKSPACE_TOO_SMALL;
+  noscope_status s = check_device();
+  if (s != NOSCOPE_OK) return s;
+  return launch_lr_fit(feats, targets, n, d, iters, lr, l2, w_host, ws, (cudaStream_t)stream);
+}
+
 // Test/debug helper (not part of the four-call contract): internal CNN
 // activation offsets within the specialized_infer workspace, so tests can
 // check individual layers.  out[19]: per conv layer l = 0..3 {offset of its

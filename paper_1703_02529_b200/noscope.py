@@ -127,6 +127,15 @@ def lib():
                                           c_p, C.POINTER(Timing), C.c_uint64, C.c_uint64,
                                           C.POINTER(SweepTables), C.POINTER(SweepBest), c_p, c_sz,
                                           c_p]
+    L.noscope_fit_workspace_bytes.restype = c_sz
+    L.noscope_fit_workspace_bytes.argtypes = [c_i64, c_i32, c_i64]
+    L.noscope_reference_image.restype = c_i32
+    L.noscope_reference_image.argtypes = [c_p, c_i64, c_i32, c_i32, c_p, c_i64, c_p, c_p, c_sz, c_p]
+    L.noscope_block_features.restype = c_i32
+    L.noscope_block_features.argtypes = [C.POINTER(DDConfig), c_p, c_i64, c_i64, c_p, c_p]
+    L.noscope_lr_fit.restype = c_i32
+    L.noscope_lr_fit.argtypes = [c_p, c_p, c_i64, c_i32, c_i32, C.c_double, C.c_double,
+                                 C.POINTER(C.c_double), c_p, c_sz, c_p]
     L.noscope_debug_cnn_layout.restype = c_i32
     L.noscope_debug_cnn_layout.argtypes = [C.POINTER(CnnArchC), c_i64, C.POINTER(c_i64)]
     _lib = L
@@ -346,6 +355,47 @@ def noscope_threshold_sweep(phase, s, z, y, a, delta, u, hist, timing=(0, 0, 0),
     if not phase & 2:
         return None, code
     return {f: getattr(best, f) for f, _ in SweepBest._fields_}, code
+
+
+# ---------------------------------------------------------------- DD fitting
+def fit_workspace(n, d, small_bytes, device="cuda"):
+    nb = lib().noscope_fit_workspace_bytes(int(n), int(d), int(small_bytes))
+    return torch.empty(max(nb, 256), dtype=torch.uint8, device=device)
+
+
+def noscope_reference_image(small: torch.Tensor, labels: torch.Tensor, out_w=50, out_h=50, ref_out=None,
+                            ws=None, stream=None):
+    """small: device u8 [n, pitch]; labels: device u8 [n] -> device u8 [out_h*out_w*3]."""
+    n, pitch = small.shape
+    dev = small.device
+    ref_out = ref_out if ref_out is not None else torch.empty(out_w * out_h * 3, dtype=torch.uint8, device=dev)
+    ws = ws if ws is not None else fit_workspace(1, 1, out_w * out_h * 3, dev)
+    _check(lib().noscope_reference_image(_ptr(small), pitch, out_w, out_h, _ptr(labels), n, _ptr(ref_out),
+                                         _ptr(ws), ws.numel(), _stream(stream)), "noscope_reference_image")
+    return ref_out
+
+
+def noscope_block_features(dd: DD, small: torch.Tensor, n=None, feats=None, stream=None):
+    """Per-frame block MSEs vs the anchor -> device f64 [n, grid*grid] (mode 1: rows < k NaN)."""
+    n = small.shape[0] if n is None else n
+    g = dd.grid
+    feats = feats if feats is not None else torch.empty((n, g * g), dtype=torch.float64, device=small.device)
+    _check(lib().noscope_block_features(C.byref(dd.c()), _ptr(small), small.shape[1], n, _ptr(feats),
+                                        _stream(stream)), "noscope_block_features")
+    return feats
+
+
+def noscope_lr_fit(feats: torch.Tensor, targets: torch.Tensor, iters: int, lr=0.0, l2=0.0, ws=None,
+                   stream=None):
+    """feats: device f64 [n, d]; targets: device u8 [n] -> (w numpy f64 [d], b float), raw-feature form."""
+    n, d = feats.shape
+    ws = ws if ws is not None else fit_workspace(n, d, 0, feats.device)
+    out = (C.c_double * (d + 1))()
+    _check(lib().noscope_lr_fit(_ptr(feats), _ptr(targets), n, d, int(iters), float(lr), float(l2), out,
+                                _ptr(ws), ws.numel(), _stream(stream)), "noscope_lr_fit")
+    import numpy as np
+    v = np.array(out[:], dtype=np.float64)
+    return v[:d], float(v[d])
 
 
 def noscope_check(ws, stream=None):
