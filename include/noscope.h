@@ -369,6 +369,45 @@ noscope_status noscope_lr_fit(const double* feats, const uint8_t* targets, int64
                               int32_t iters, double lr, double l2, double* w_host, void* ws,
                               size_t ws_bytes, noscope_stream_t stream);
 
+/* ---- Full CBO search -------------------------------
+ * the CBO profiles every difference detector and every specialized
+ * NN on the evaluation set, sweeps (delta_diff, c_low, c_high) for each
+ * combination and keeps the cheapest cascade (cost model P:696) meeting FP* /
+ * FN*.  Reading R-23: every DD config and CNN runs unfiltered on all n frames
+ * (one unit, tau = 0..n-1, no prior state); per (DD, CNN) pair one
+ * noscope_threshold_sweep with records s = DD score, z = CNN logit, y =
+ * labels, a = the label emitted when not fired (skipped -> its period's
+ * checked frame's label; mode 0 -> 0; mode 1 -> label(t-k), 0 for t < k);
+ * timing (t_mse_ps, that CNN's t_snn_ps, t_full_ps).  Overall argmin key:
+ * (infeasible, violation, cost, U, dd index, cnn index).
+ * All DD configs must have out_w = out_h = 50 (the CNN input); frames as in
+ * noscope_diff_detect.  dds / cnns / result_host are host memory;
+ * delta_cand, logit_cand, labels are device.  Synchronous.  Returns
+ * NOSCOPE_INFEASIBLE (result = best-effort) when no pair meets the limits.   */
+typedef struct {
+  const noscope_dd_config* dd;   /* host pointer to the DD configuration      */
+  const double* delta_cand;      /* device, strictly ascending                */
+  int32_t n_delta;
+} noscope_cbo_dd;
+typedef struct {
+  const noscope_cnn_arch* arch;  /* host pointers                             */
+  const noscope_cnn_weights* weights;
+  uint64_t t_snn_ps;             /* measured per-frame cost of this CNN       */
+} noscope_cbo_cnn;
+typedef struct {
+  int32_t dd, cnn;               /* chosen indices                            */
+  noscope_sweep_best best;       /* that pair's sweep result                  */
+} noscope_cbo_result;
+
+size_t noscope_cbo_workspace_bytes(const noscope_cbo_cnn* cnns, int32_t n_cnn, int64_t n,
+                                   int32_t n_delta_max, int32_t m);
+noscope_status noscope_cbo_search(const noscope_cbo_dd* dds, int32_t n_dd, const noscope_cbo_cnn* cnns,
+                                  int32_t n_cnn, const uint8_t* frames, noscope_frames_desc desc,
+                                  int64_t n, const uint8_t* labels, const float* logit_cand, int32_t m,
+                                  uint64_t t_mse_ps, uint64_t t_full_ps, uint64_t fp_limit,
+                                  uint64_t fn_limit, noscope_cbo_result* result_host, void* ws,
+                                  size_t ws_bytes, noscope_stream_t stream);
+
 /* Reads and clears the device status word in a workspace (synchronises). */
 noscope_status noscope_check(void* ws, noscope_stream_t stream);
 

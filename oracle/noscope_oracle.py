@@ -550,3 +550,32 @@ def lr_loss(F, t, w_raw, b_raw, l2: float = 0.0) -> float:
     z = F @ w_raw + b_raw
     loss = np.mean(np.logaddexp(0.0, z) - t * z)
     return float(loss + 0.5 * l2 * np.sum((w_raw * sd) ** 2))
+
+
+# --------------------------------------------------------------------------
+# N2 Full CBO search — P:717-779 "NoScope's CBO ...
+#    profiles each filter ... on the evaluation set ... sweeps delta_diff ... the
+#    cost model selects the cheapest cascade meeting FP*/FN*" over the DD
+#    configurations x specialized-NN architectures.
+#    Reading R-23: every DD config and every CNN runs unfiltered on
+#    all evaluation frames; one sweep per (DD, CNN) pair with that CNN's own
+#    T_SNN; overall argmin of (infeasible, violation, cost, U, dd, cnn).
+# --------------------------------------------------------------------------
+def cbo_search(small: np.ndarray, y: np.ndarray, dd_cfgs, delta_grids, cnns, u, t_mse: int,
+               t_full: int, fp_limit: int, fn_limit: int):
+    """small uint8 [n, h, w, 3] (evaluation split, downsampled); dd_cfgs: list of
+    DDConfig; delta_grids: their candidate arrays; cnns: list of (arch, weights,
+    t_snn_ps).  Returns (dd index, cnn index, sweep_best dict of that pair)."""
+    logits = [cnn_logits(small, arch, w) for arch, w, _ in cnns]
+    best, best_key = None, None
+    for di, cfg in enumerate(dd_cfgs):
+        s, _ = diff_detect(small, cfg)
+        a = build_records(s, y, cfg.mode, cfg.t_diff_frames)
+        for ci, (_, _, t_snn) in enumerate(cnns):
+            _, b = sweep(s, logits[ci], y, a, delta_grids[di], u, (t_mse, t_snn, t_full),
+                         fp_limit, fn_limit)
+            viol = 0 if b["feasible"] else max(b["fp"] - fp_limit, b["fn"] - fn_limit, 0)
+            key = (0 if b["feasible"] else 1, viol, b["cost"], b["U"], di, ci)
+            if best_key is None or key < best_key:
+                best, best_key = (di, ci, b), key
+    return best

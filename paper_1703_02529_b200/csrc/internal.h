@@ -184,6 +184,10 @@ noscope_status launch_block_features(const noscope_dd_config& c, const uint8_t* 
 noscope_status launch_lr_fit(const double* F, const uint8_t* t, int64_t n, int d, int iters, double lr,
                              double l2, double* wb_host, void* ws, cudaStream_t st);
 
+// CBO search helper (cbo.cu).
+noscope_status launch_records_a(const double* score, const uint8_t* y, int64_t n, int mode, int k,
+                                int t_skip, uint8_t* a, cudaStream_t st);
+
 // Threshold sweep.
 size_t sweep_ws_bytes(int32_t n_delta, int32_t m);
 noscope_status launch_sweep(int32_t phase, const double* s, const float* z, const uint8_t* y,

@@ -490,6 +490,121 @@ noscope_status noscope_lr_fit(const double* feats, const uint8_t* targets, int64
   return launch_lr_fit(feats, targets, n, d, iters, lr, l2, w_host, ws, (cudaStream_t)stream);
 }
 
+// ---- Full CBO search (cbo.cu helper + the existing entry points)
+namespace {
+struct CboWs {
+  size_t small, score, disp, a, logits, hist, dd, cnn, sweep, total;
+  size_t cnn_bytes;
+};
+CboWs cbo_ws(const noscope_cbo_cnn* cnns, int32_t n_cnn, int64_t n, int32_t ndm, int32_t m) {
+  CboWs w{};
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    size_t r = off;
+    off = align256(off + b);
+    return r;
+  };
+  w.small = take((size_t)n * 7504);
+  w.score = take((size_t)n * 8);
+  w.disp = take((size_t)n);
+  w.a = take((size_t)n);
+  w.logits = take((size_t)n_cnn * n * 4);
+  w.hist = take(noscope_sweep_hist_words(ndm, m) * 8);
+  w.dd = take(dd_ws(n).total);
+  size_t cb = 0;
+  for (int c = 0; c < n_cnn; ++c)
+    cb = std::max(cb, noscope_workspace_bytes(NOSCOPE_OP_SPECIALIZED_INFER, nullptr, cnns[c].arch, n, 0, 0));
+  w.cnn_bytes = cb;
+  w.cnn = take(cb);
+  w.sweep = take(sweep_ws_bytes(ndm, m));
+  w.total = off;
+  return w;
+}
+}  // namespace
+
+size_t noscope_cbo_workspace_bytes(const noscope_cbo_cnn* cnns, int32_t n_cnn, int64_t n,
+                                   int32_t n_delta_max, int32_t m) {
+  if (!cnns || n_cnn < 1 || n < 0 || n_delta_max < 1 || m < 1) return 0;
+  for (int c = 0; c < n_cnn; ++c)
+    if (!cnns[c].arch || !cnn_arch_supported(*cnns[c].arch)) return 0;
+  return cbo_ws(cnns, n_cnn, n, n_delta_max, m).total;
+}
+
+noscope_status noscope_cbo_search(const noscope_cbo_dd* dds, int32_t n_dd, const noscope_cbo_cnn* cnns,
+                                  int32_t n_cnn, const uint8_t* frames, noscope_frames_desc desc,
+                                  int64_t n, const uint8_t* labels, const float* logit_cand, int32_t m,
+                                  uint64_t t_mse_ps, uint64_t t_full_ps, uint64_t fp_limit,
+                                  uint64_t fn_limit, noscope_cbo_result* result_host, void* ws,
+                                  size_t ws_bytes, noscope_stream_t stream) {
+  if (!dds || n_dd < 1 || !cnns || n_cnn < 1 || !frames || !labels || !logit_cand || m < 1 ||
+      !result_host || !ws || n < 1)
+    return NOSCOPE_INVALID_ARGUMENT;
+  int32_t ndm = 0;
+  for (int d = 0; d < n_dd; ++d) {
+    if (!dds[d].dd || !dds[d].delta_cand || dds[d].n_delta < 1) return NOSCOPE_INVALID_ARGUMENT;
+    if (dds[d].dd->out_w != 50 || dds[d].dd->out_h != 50) return NOSCOPE_SHAPE;
+    noscope_status s = validate_dd(dds[d].dd);
+    if (s != NOSCOPE_OK) return s;
+    ndm = std::max(ndm, dds[d].n_delta);
+  }
+  const size_t need = noscope_cbo_workspace_bytes(cnns, n_cnn, n, ndm, m);
+  if (need == 0) return NOSCOPE_SHAPE;
+  if (ws_bytes < need) return NOSCOPE_WORKSPACE_TOO_SMALL;
+  CboWs w = cbo_ws(cnns, n_cnn, n, ndm, m);
+  uint8_t* b = reinterpret_cast<uint8_t*>(ws);
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* small = b + w.small;
+  double* score = reinterpret_cast<double*>(b + w.score);
+  uint8_t* a = b + w.a;
+  uint64_t* hist = reinterpret_cast<uint64_t*>(b + w.hist);
+  bool have = false;
+  noscope_cbo_result best{};
+  uint64_t bk[4] = {0, 0, 0, 0};
+  for (int d = 0; d < n_dd; ++d) {
+    const noscope_dd_config& dd = *dds[d].dd;
+    noscope_status s = noscope_diff_detect(&dd, frames, desc, n, 0, nullptr, small, 7504, score,
+                                           b + w.disp, nullptr, nullptr, b + w.dd, dd_ws(n).total, stream);
+    if (s != NOSCOPE_OK) return s;
+    if (d == 0)   // the CNN sees the same 50x50 small frames under every DD config
+      for (int c = 0; c < n_cnn; ++c) {
+        s = noscope_specialized_infer(cnns[c].arch, cnns[c].weights, small, 7504, nullptr, nullptr, n,
+                                      reinterpret_cast<float*>(b + w.logits) + (size_t)c * n, b + w.cnn,
+                                      w.cnn_bytes, stream);
+        if (s != NOSCOPE_OK) return s;
+      }
+    s = launch_records_a(score, labels, n, dd.mode, dd.t_diff_frames, dd.t_skip_frames, a, st);
+    if (s != NOSCOPE_OK) return s;
+    for (int c = 0; c < n_cnn; ++c) {
+      NS_CUDA_TRY(cudaMemsetAsync(hist, 0, noscope_sweep_hist_words(dds[d].n_delta, m) * 8, st));
+      const noscope_timing tm{t_mse_ps, cnns[c].t_snn_ps, t_full_ps};
+      noscope_sweep_best r{};
+      s = noscope_threshold_sweep(3, score, reinterpret_cast<const float*>(b + w.logits) + (size_t)c * n,
+                                  labels, a, n, dds[d].delta_cand, dds[d].n_delta, logit_cand, m, hist,
+                                  &tm, fp_limit, fn_limit, nullptr, &r, b + w.sweep,
+                                  sweep_ws_bytes(ndm, m), stream);
+      if (s != NOSCOPE_OK && s != NOSCOPE_INFEASIBLE) return s;
+      const uint64_t viol =
+          r.feasible ? 0
+                     : std::max<uint64_t>(r.fp > fp_limit ? r.fp - fp_limit : 0, r.fn > fn_limit ? r.fn - fn_limit : 0);
+      const uint64_t key[4] = {r.feasible ? 0u : 1u, viol, r.cost_ps, r.uncertain};
+      bool better = !have;
+      for (int q = 0; q < 4 && !better; ++q) {
+        if (key[q] < bk[q]) better = true;
+        if (key[q] != bk[q]) break;
+      }
+      if (better) {   // ties keep the earlier (dd, cnn): iteration order is the key's tail
+        have = true;
+        std::memcpy(bk, key, sizeof(bk));
+        best.dd = d;
+        best.cnn = c;
+        best.best = r;
+      }
+    }
+  }
+  *result_host = best;
+  return best.best.feasible ? NOSCOPE_OK : NOSCOPE_INFEASIBLE;
+}
+
 // Test/debug helper (not part of the four-call contract): internal CNN
 // activation offsets within the specialized_infer workspace, so tests can
 // check individual layers.  out[19]: per conv layer l = 0..3 {offset of its

@@ -74,6 +74,18 @@ class SweepBest(C.Structure):
                 ("total", C.c_uint64), ("delta", c_f64), ("lo_logit", c_f32), ("hi_logit", c_f32)]
 
 
+class CboDD(C.Structure):
+    _fields_ = [("dd", C.POINTER(DDConfig)), ("delta_cand", c_p), ("n_delta", c_i32)]
+
+
+class CboCNN(C.Structure):
+    _fields_ = [("arch", C.POINTER(CnnArchC)), ("weights", C.POINTER(CnnWeightsC)), ("t_snn_ps", C.c_uint64)]
+
+
+class CboResult(C.Structure):
+    _fields_ = [("dd", c_i32), ("cnn", c_i32), ("best", SweepBest)]
+
+
 class SweepTables(C.Structure):
     _fields_ = [(n, c_p) for n in ("F", "FPnf", "FNnf", "FPf", "FNf", "GE", "GT")]
 
@@ -136,6 +148,12 @@ def lib():
     L.noscope_lr_fit.restype = c_i32
     L.noscope_lr_fit.argtypes = [c_p, c_p, c_i64, c_i32, c_i32, C.c_double, C.c_double,
                                  C.POINTER(C.c_double), c_p, c_sz, c_p]
+    L.noscope_cbo_workspace_bytes.restype = c_sz
+    L.noscope_cbo_workspace_bytes.argtypes = [C.POINTER(CboCNN), c_i32, c_i64, c_i32, c_i32]
+    L.noscope_cbo_search.restype = c_i32
+    L.noscope_cbo_search.argtypes = [C.POINTER(CboDD), c_i32, C.POINTER(CboCNN), c_i32, c_p, FramesDesc,
+                                     c_i64, c_p, c_p, c_i32, C.c_uint64, C.c_uint64, C.c_uint64,
+                                     C.c_uint64, C.POINTER(CboResult), c_p, c_sz, c_p]
     L.noscope_debug_cnn_layout.restype = c_i32
     L.noscope_debug_cnn_layout.argtypes = [C.POINTER(CnnArchC), c_i64, C.POINTER(c_i64)]
     _lib = L
@@ -396,6 +414,36 @@ def noscope_lr_fit(feats: torch.Tensor, targets: torch.Tensor, iters: int, lr=0.
     import numpy as np
     v = np.array(out[:], dtype=np.float64)
     return v[:d], float(v[d])
+
+
+def noscope_cbo_search(dds, cnns, frames: torch.Tensor, width: int, height: int, labels: torch.Tensor,
+                       logit_cand: torch.Tensor, t_mse_ps: int, t_full_ps: int, fp_limit: int, fn_limit: int,
+                       stream=None):
+    """dds: list of (DD, delta_cand device f64); cnns: list of (Arch, Weights, t_snn_ps).
+    Returns (dd index, cnn index, best dict, status code 0 or 7)."""
+    n, pitch = frames.shape
+    keep = []                                  # keep the ctypes structs alive
+    dd_arr = (CboDD * len(dds))()
+    for i, (dd, dc) in enumerate(dds):
+        c = dd.c()
+        keep.append(c)
+        dd_arr[i] = CboDD(C.pointer(c), dc.data_ptr(), dc.numel())
+    cnn_arr = (CboCNN * len(cnns))()
+    for i, (arch, w, t) in enumerate(cnns):
+        ac, wc = arch.c(), w.c()
+        keep += [ac, wc]
+        cnn_arr[i] = CboCNN(C.pointer(ac), C.pointer(wc), int(t))
+    ndm = max(dc.numel() for _, dc in dds)
+    nb = lib().noscope_cbo_workspace_bytes(cnn_arr, len(cnns), n, ndm, logit_cand.numel())
+    ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=frames.device)
+    res = CboResult()
+    code = lib().noscope_cbo_search(dd_arr, len(dds), cnn_arr, len(cnns), _ptr(frames),
+                                    FramesDesc(width, height, pitch), n, _ptr(labels), _ptr(logit_cand),
+                                    logit_cand.numel(), int(t_mse_ps), int(t_full_ps), int(fp_limit),
+                                    int(fn_limit), C.byref(res), _ptr(ws), ws.numel(), _stream(stream))
+    if code not in (0, 7):
+        raise NoScopeError(code, "noscope_cbo_search")
+    return res.dd, res.cnn, {f: getattr(res.best, f) for f, _ in SweepBest._fields_}, code
 
 
 def noscope_check(ws, stream=None):
