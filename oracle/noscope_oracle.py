@@ -579,3 +579,83 @@ def cbo_search(small: np.ndarray, y: np.ndarray, dd_cfgs, delta_grids, cnns, u, 
             if best_key is None or key < best_key:
                 best, best_key = (di, ci, b), key
     return best
+
+
+# --------------------------------------------------------------------------
+# N3 Evaluation harness — P:1027-1032 "comparing frames
+#    labeled by the reference model and NoScope in 30 frame windows ... agree on
+#    the presence of the target object in 28 of the 30 frames"
+#    factor analysis / lesion study.  Reading R-24:
+#    the modeled cost charges T_MSE per checked frame only when the difference
+#    detector is in the cascade, T_SNN per fired frame only when the specialized
+#    NN is, and T_full per frame that reaches the reference NN.
+# --------------------------------------------------------------------------
+def windowed_accuracy(pred, ref, window: int = 30, agree_min: int = 28) -> float:
+    """Consecutive non-overlapping windows (final partial window dropped); a
+    window is correct iff >= agree_min frames agree."""
+    pred, ref = np.asarray(pred), np.asarray(ref)
+    if pred.shape != ref.shape:
+        raise ValueError("length mismatch")
+    nw = len(pred) // window
+    if nw == 0:
+        raise ValueError("shorter than one window")
+    agree = (pred[:nw * window] != 0) == (ref[:nw * window] != 0)
+    per = agree.reshape(nw, window).sum(axis=1)
+    return float((per >= agree_min).sum()) / nw
+
+
+def fp_fn(pred, ref):
+    """(fp, fn, tp, tn) frame counts."""
+    p, r = np.asarray(pred) != 0, np.asarray(ref) != 0
+    if p.shape != r.shape:
+        raise ValueError("length mismatch")
+    return int((p & ~r).sum()), int((~p & r).sum()), int((p & r).sum()), int((~p & ~r).sum())
+
+
+def cascade_counts(res) -> dict:
+    """Per-stage frame counts of one oracle cascade result."""
+    disp, route_pf = res["disp"], res["route"]
+    return dict(n=len(disp), checked=int((disp != SKIPPED).sum()), fired=int((disp == FIRED).sum()),
+                uncertain=int((route_pf == R_UNC).sum()))
+
+
+def modeled_speedup(c: dict, stages, t_mse: int, t_snn: int, t_full: int) -> float:
+    """N*T_full / modeled cascade time (R-24).  stages: subset of
+    {"skip", "dd", "cnn"}; frames reaching the reference NN = uncertain frames
+    with the CNN, fired frames without it."""
+    oracle_frames = c["uncertain"] if "cnn" in stages else c["fired"]
+    t = (c["checked"] * t_mse if "dd" in stages else 0) + (c["fired"] * t_snn if "cnn" in stages else 0) \
+        + oracle_frames * t_full
+    if t == 0:
+        raise ValueError("zero modeled time")
+    return c["n"] * t_full / t
+
+
+FACTOR_ROWS = [("oracle only", ()), ("+skipping", ("skip",)), ("+difference detection", ("skip", "dd")),
+               ("+specialized model", ("skip", "dd", "cnn"))]
+LESION_ROWS = [("full", ("skip", "dd", "cnn")), ("-skipping", ("dd", "cnn")),
+               ("-difference detection", ("skip", "cnn")), ("-specialized model", ("skip", "dd"))]
+
+
+def stage_config(cfg: DDConfig, lo: float, hi: float, stages):
+    """The cascade with only `stages` active: no skipping -> t_skip 1; no DD ->
+    delta = -inf (every checked frame fires); no CNN -> (lo, hi) = (-inf, +inf)
+    (every fired frame is uncertain and goes to the reference NN)."""
+    c = dataclasses.replace(cfg, t_skip_frames=cfg.t_skip_frames if "skip" in stages else 1,
+                            delta_diff=cfg.delta_diff if "dd" in stages else -math.inf)
+    return c, (lo if "cnn" in stages else -math.inf), (hi if "cnn" in stages else math.inf)
+
+
+def factor_analysis(frames_hw3, cfg: DDConfig, arch, weights, lo, hi, truth, timing, rows=FACTOR_ROWS):
+    """Rows of (name, windowed accuracy vs the reference labels, fp, fn, counts,
+    modeled speedup) for nested (FACTOR_ROWS) or leave-one-out (LESION_ROWS)
+    stage sets."""
+    out = []
+    for name, stages in rows:
+        c, l, h = stage_config(cfg, lo, hi, stages)
+        res = cascade(frames_hw3, c, arch, weights, l, h, truth)
+        cnt = cascade_counts(res)
+        fp, fn, _, _ = fp_fn(res["labels"], truth)
+        out.append(dict(name=name, accuracy=windowed_accuracy(res["labels"], truth), fp=fp, fn=fn,
+                        speedup=modeled_speedup(cnt, stages, *timing), **cnt))
+    return out
