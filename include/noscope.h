@@ -408,6 +408,21 @@ noscope_status noscope_cbo_search(const noscope_cbo_dd* dds, int32_t n_dd, const
                                   uint64_t fn_limit, noscope_cbo_result* result_host, void* ws,
                                   size_t ws_bytes, noscope_stream_t stream);
 
+/* ---- Evaluation -----------------------------------
+ * "comparing frames labeled by the reference model and NoScope in
+ * 30 frame windows ... agree on the presence of the target object in 28 of the
+ * 30 frames"; SPEC windowed_accuracy / fp_fn_rates S:523-540.  Consecutive
+ * non-overlapping windows of `window` frames (final partial window dropped);
+ * a window is correct iff >= agree_min frames agree (label != 0 on both sides
+ * or on neither).  Confusion counts cover all n frames.  pred, ref: device u8
+ * [n]; counts_host: host.  ws: >= 256 bytes of device scratch.  Synchronous. */
+typedef struct {
+  int64_t windows, correct_windows, tp, tn, fp, fn;
+} noscope_eval_counts;
+noscope_status noscope_eval_labels(const uint8_t* pred, const uint8_t* ref, int64_t n, int32_t window,
+                                   int32_t agree_min, noscope_eval_counts* counts_host, void* ws,
+                                   size_t ws_bytes, noscope_stream_t stream);
+
 /* Reads and clears the device status word in a workspace (synchronises). */
 noscope_status noscope_check(void* ws, noscope_stream_t stream);
 

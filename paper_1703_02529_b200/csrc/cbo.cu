@@ -32,3 +32,50 @@ noscope_status launch_records_a(const double* score, const uint8_t* y, int64_t n
 }
 
 }  // namespace ns
+
+namespace ns {
+// ---------------------------------------------------------------- evaluation
+// Windowed accuracy (30-frame windows, correct iff >= 28 agree) and
+// frame confusion counts in one pass; counters[0..5] = windows, correct windows,
+// tp, tn, fp, fn (u64, zeroed by the caller).
+__global__ void eval_labels_kernel(const uint8_t* __restrict__ pred, const uint8_t* __restrict__ ref,
+                                   int64_t n, int window, int agree_min,
+                                   unsigned long long* __restrict__ counters) {
+  unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
+  const int64_t nw = n / window;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += stride) {
+    int agree = 0;
+    for (int j = 0; j < window; ++j) agree += ((pred[w * window + j] != 0) == (ref[w * window + j] != 0));
+    c[0] += 1;
+    c[1] += agree >= agree_min;
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const bool p = pred[i] != 0, r = ref[i] != 0;
+    c[2] += p && r;
+    c[3] += !p && !r;
+    c[4] += p && !r;
+    c[5] += !p && r;
+  }
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const unsigned long long v = warp_sum(c[q]);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&counters[q], v);
+  }
+}
+
+noscope_status launch_eval_labels(const uint8_t* pred, const uint8_t* ref, int64_t n, int window,
+                                  int agree_min, unsigned long long* counters, int64_t* out_host,
+                                  cudaStream_t st) {
+  NS_CUDA_TRY(cudaMemsetAsync(counters, 0, 6 * 8, st));
+  if (n > 0) {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4 * kNumSMs));
+    eval_labels_kernel<<<grid, 256, 0, st>>>(pred, ref, n, window, agree_min, counters);
+    NS_LAUNCH_CHECK();
+    count_launch();
+  }
+  NS_CUDA_TRY(cudaMemcpyAsync(out_host, counters, 6 * 8, cudaMemcpyDeviceToHost, st));
+  NS_CUDA_TRY(cudaStreamSynchronize(st));
+  return NOSCOPE_OK;
+}
+}  // namespace ns

@@ -188,6 +188,10 @@ noscope_status launch_lr_fit(const double* F, const uint8_t* t, int64_t n, int d
 noscope_status launch_records_a(const double* score, const uint8_t* y, int64_t n, int mode, int k,
                                 int t_skip, uint8_t* a, cudaStream_t st);
 
+noscope_status launch_eval_labels(const uint8_t* pred, const uint8_t* ref, int64_t n, int window,
+                                  int agree_min, unsigned long long* counters, int64_t* out_host,
+                                  cudaStream_t st);
+
 // Threshold sweep.
 size_t sweep_ws_bytes(int32_t n_delta, int32_t m);
 noscope_status launch_sweep(int32_t phase, const double* s, const float* z, const uint8_t* y,

@@ -605,6 +605,22 @@ noscope_status noscope_cbo_search(const noscope_cbo_dd* dds, int32_t n_dd, const
   return best.best.feasible ? NOSCOPE_OK : NOSCOPE_INFEASIBLE;
 }
 
+noscope_status noscope_eval_labels(const uint8_t* pred, const uint8_t* ref, int64_t n, int32_t window,
+                                   int32_t agree_min, noscope_eval_counts* counts_host, void* ws,
+                                   size_t ws_bytes, noscope_stream_t stream) {
+  if (!pred || !ref || !counts_host || !ws || n < 0 || window < 1 || agree_min < 0 || agree_min > window)
+    return NOSCOPE_INVALID_ARGUMENT;
+  if (ws_bytes < 256) return NOSCOPE_WORKSPACE_TOO_SMALL;
+  noscope_status s = check_device();
+  if (s != NOSCOPE_OK) return s;
+  int64_t out[6];
+  s = launch_eval_labels(pred, ref, n, window, agree_min, reinterpret_cast<unsigned long long*>(ws), out,
+                         (cudaStream_t)stream);
+  if (s != NOSCOPE_OK) return s;
+  *counts_host = noscope_eval_counts{out[0], out[1], out[2], out[3], out[4], out[5]};
+  return NOSCOPE_OK;
+}
+
 // Test/debug helper (not part of the four-call contract): internal CNN
 // activation offsets within the specialized_infer workspace, so tests can
 // check individual layers.  out[19]: per conv layer l = 0..3 {offset of its

@@ -86,6 +86,10 @@ class CboResult(C.Structure):
     _fields_ = [("dd", c_i32), ("cnn", c_i32), ("best", SweepBest)]
 
 
+class EvalCounts(C.Structure):
+    _fields_ = [(f, c_i64) for f in ("windows", "correct_windows", "tp", "tn", "fp", "fn")]
+
+
 class SweepTables(C.Structure):
     _fields_ = [(n, c_p) for n in ("F", "FPnf", "FNnf", "FPf", "FNf", "GE", "GT")]
 
@@ -154,6 +158,8 @@ def lib():
     L.noscope_cbo_search.argtypes = [C.POINTER(CboDD), c_i32, C.POINTER(CboCNN), c_i32, c_p, FramesDesc,
                                      c_i64, c_p, c_p, c_i32, C.c_uint64, C.c_uint64, C.c_uint64,
                                      C.c_uint64, C.POINTER(CboResult), c_p, c_sz, c_p]
+    L.noscope_eval_labels.restype = c_i32
+    L.noscope_eval_labels.argtypes = [c_p, c_p, c_i64, c_i32, c_i32, C.POINTER(EvalCounts), c_p, c_sz, c_p]
     L.noscope_debug_cnn_layout.restype = c_i32
     L.noscope_debug_cnn_layout.argtypes = [C.POINTER(CnnArchC), c_i64, C.POINTER(c_i64)]
     _lib = L
@@ -444,6 +450,15 @@ def noscope_cbo_search(dds, cnns, frames: torch.Tensor, width: int, height: int,
     if code not in (0, 7):
         raise NoScopeError(code, "noscope_cbo_search")
     return res.dd, res.cnn, {f: getattr(res.best, f) for f, _ in SweepBest._fields_}, code
+
+
+def noscope_eval_labels(pred: torch.Tensor, ref: torch.Tensor, window=30, agree_min=28, stream=None):
+    """Windowed accuracy + confusion counts of device u8 label tracks -> dict."""
+    ws = torch.empty(256, dtype=torch.uint8, device=pred.device)
+    out = EvalCounts()
+    _check(lib().noscope_eval_labels(_ptr(pred), _ptr(ref), pred.numel(), window, agree_min, C.byref(out),
+                                     _ptr(ws), ws.numel(), _stream(stream)), "noscope_eval_labels")
+    return {f: getattr(out, f) for f, _ in EvalCounts._fields_}
 
 
 def noscope_check(ws, stream=None):
