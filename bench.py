@@ -396,6 +396,7 @@ def run_extras(device):
                         "tflops": round(fl / ms / 1e9, 1), "frac_of_bf16_peak": round(fl / ms / 1e9 / bf16, 4)}
         del ws
     out["cnn_grid_65536"] = grid
+    out["next_rows"] = next_rows_extras(device, sc, gs, small, nG)
     # configs[3]: sweep over 1M labelled records, 100 x 100 candidates
     rng = np.random.default_rng(4)
     M = 1_000_000
@@ -460,6 +461,76 @@ def run_extras(device):
                              "smem_atomics_per_record": round((M9 + n_h1) / M9, 3),
                              "atomic_floor_ms": round(floor_ms, 3), "frac_of_atomic_floor": round(floor_ms / ms9, 3)}
     del s9, z9, y9, a9
+    return out
+
+
+def _time_ms(fn, reps=3):
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def next_rows_extras(device, sc, gs, small, n):
+    """SURVEY 8(f) NEXT #1-#3 measured on the CNN-grid frames (50x50, 65,536):
+    bytes are algorithmic (what the step must read)."""
+    import torch
+    import synthgen as sg
+    from paper_1703_02529_b200 import noscope as N
+    hbm = measured_peaks()[0]
+    out = {}
+    y = gs.truth[:n].contiguous()
+    neg = int((y == 0).sum())
+    ws = N.fit_workspace(1, 1, 7500, device)
+    ref = torch.empty(7500, dtype=torch.uint8, device=device)
+    ms = _time_ms(lambda: N.noscope_reference_image(small, y, ref_out=ref, ws=ws))
+    gb = neg * 7500 / ms / 1e6
+    out["reference_image"] = {"frames": n, "ms_incl_sync": round(ms, 4), "GBps": round(gb, 1),
+                              "frac_of_hbm": round(gb / hbm, 4)}
+    k, g = 30, 10
+    dd = N.DD(mode=1, metric=1, grid=g, t_diff_frames=k, lr_weights=torch.ones(g * g, device=device))
+    feats = torch.empty((n, g * g), dtype=torch.float64, device=device)
+    ms = _time_ms(lambda: N.noscope_block_features(dd, small, feats=feats))
+    gb = (n * 7500 * 2 + n * g * g * 8) / ms / 1e6
+    out["block_features"] = {"frames": n, "ms": round(ms, 4), "GBps": round(gb, 1), "frac_of_hbm": round(gb / hbm, 4)}
+    F = feats[k:].contiguous()
+    t = (y[k:] != y[:-k]).to(torch.uint8).contiguous()
+    wsl = N.fit_workspace(F.shape[0], g * g, 0, device)
+    iters = 100
+    ms = _time_ms(lambda: N.noscope_lr_fit(F, t, iters, l2=1e-3, ws=wsl), reps=2)
+    gb = iters * 2 * F.numel() * 8 / ms / 1e6
+    out["lr_fit"] = {"examples": F.shape[0], "features": g * g, "iters": iters, "ms": round(ms, 3),
+                     "ms_per_iter": round(ms / iters, 4), "GBps_per_iter_stream": round(gb, 1)}
+    big = torch.randint(0, 2, (256 * 1024 * 1024,), dtype=torch.uint8, device=device)
+    ref2 = big.roll(7)
+    ms = _time_ms(lambda: N.noscope_eval_labels(big, ref2))
+    gb = 2 * big.numel() / ms / 1e6
+    out["eval_labels"] = {"frames": big.numel(), "ms_incl_sync": round(ms, 3), "GBps": round(gb, 1),
+                          "frac_of_hbm": round(gb / hbm, 4)}
+    del big, ref2
+    # full CBO search: 2 DD configs x 2 CNNs on 16,384 evaluation frames
+    m = 16384
+    fr = small[:m]
+    ym = y[:m]
+    bg = torch.from_numpy(sg.background(sc.spec)).to(device)
+    u = torch.linspace(-3, 3, 100, device=device, dtype=torch.float32)
+    d0 = N.DD(mode=0, metric=0, ref_image=bg)
+    d1 = N.DD(mode=1, metric=1, grid=10, t_diff_frames=30, lr_weights=torch.full((100,), 0.02, device=device),
+              lr_bias=-1.0)
+    dg = torch.logspace(-1, 4, 100, dtype=torch.float64, device=device)
+    cnns = []
+    for a in (sg.CnnArch(2, 32, 32), sg.CnnArch(4, 32, 32)):
+        cnns.append((N.Arch(a.n_conv, a.base_filters, a.dense), N.Weights(sg.he_normal_weights(a, 3), device=device),
+                     40 if a.n_conv == 2 else 100))
+    ms = _time_ms(lambda: N.noscope_cbo_search([(d0, dg), (d1, dg)], cnns, fr, 50, 50, ym, u, 5, 12_500_000,
+                                               m // 100, m // 100), reps=2)
+    out["cbo_search"] = {"eval_frames": m, "dd_configs": 2, "cnns": 2, "ms_incl_sync": round(ms, 2)}
     return out
 
 

@@ -319,10 +319,14 @@ convg_kernel(ConvGArgs A) {
             for (int j = 0; j < 16; ++j)
               pk[j] = relu_bf16x2(__uint_as_float(r[2 * j]) + bias[c + 2 * j],
                                   __uint_as_float(r[2 * j + 1]) + bias[c + 2 * j + 1]);
-            uint4* dst = reinterpret_cast<uint4*>(sbuf + (size_t)(t * 128 + lq * 32 + lane) * 64);
+            // 16-B chunk q of row r lives at chunk q ^ ((r >> 1) & 3): the 8 rows of a
+            // 128-B wavefront then hit 8 distinct bank groups (no 4-way conflicts)
+            const int row = t * 128 + lq * 32 + lane;
+            uint4* dst = reinterpret_cast<uint4*>(sbuf + (size_t)row * 64);
+            const int sw = (row >> 1) & 3;
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+              dst[q ^ sw] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
           }
           if (sl == nsl - 1) {  // accumulators fully read: release them to the MMA
             tc_fence_before();
@@ -336,8 +340,9 @@ convg_kernel(ConvGArgs A) {
             const int h = e & 3;
             const int sr = w.x & 0xFFFF, yp = (w.x >> 16) & 0xFF, xp = (w.x >> 24) & 0xFF;
             const int64_t f = w.y;
-            const uint4* s0 = reinterpret_cast<const uint4*>(sbuf + (size_t)sr * 64) + h;
-            const uint4 a0 = s0[0], a1 = s0[4], a2 = s0[4 * Wq], a3 = s0[4 * Wq + 4];
+            const uint4* sb4 = reinterpret_cast<const uint4*>(sbuf);
+            auto at = [&](int r) { return sb4[r * 4 + (h ^ ((r >> 1) & 3))]; };   // swizzled chunk
+            const uint4 a0 = at(sr), a1 = at(sr + 1), a2 = at(sr + Wq), a3 = at(sr + Wq + 1);
             uint4 o;
             o.x = __vmaxu2(__vmaxu2(a0.x, a1.x), __vmaxu2(a2.x, a3.x));
             o.y = __vmaxu2(__vmaxu2(a0.y, a1.y), __vmaxu2(a2.y, a3.y));
