@@ -501,22 +501,35 @@ conv12_fused_kernel(FusedArgs A) {
         // the second y block re-computes conv rows 8..15: only rows >= 16 are new
         const bool keep = pool_lane && yc < 24 && (yb == 0 || yc >= 16);
         const int yp = yc >> 1, xp = xc >> 1;
+        // All 64 accumulator columns -> packed bf16x2 registers first (two 32-column
+        // loads, one wait each), then release the TMEM buffer to the conv2 issuer
+        // before the shuffles and global stores.
+        uint32_t pk[32];
+#pragma unroll
+        for (int hg = 0; hg < ((NS_EXP & 32) ? 0 : 2); ++hg) {
+          uint32_t r[32];
+          tmem_ld16(tmem + ((uint32_t)lg << 16) + kColD2 + b * C2 + hg * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
+          tmem_ld16(tmem + ((uint32_t)lg << 16) + kColD2 + b * C2 + hg * 32 + 16,
+                    *reinterpret_cast<uint32_t(*)[16]>(r + 16));
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j)   // bias already accumulated (extra K step)
+            pk[hg * 16 + j] = relu_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+        }
+        tc_fence_before();
+        mbar_arrive(&t2_empty[b]);
 #pragma unroll
         for (int g = 0; g < ((NS_EXP & 32) ? 0 : C2 / 16); ++g) {
-          uint32_t r[16];
-          tmem_ld16(tmem + ((uint32_t)lg << 16) + kColD2 + b * C2 + g * 16, r);
-          tmem_ld_wait();
-          uint32_t pk[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {   // bias already accumulated (extra K step)
-            uint32_t v = relu_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+          for (int j = 0; j < 8; ++j) {
+            uint32_t v = pk[g * 8 + j];
             v = __vmaxu2(v, __shfl_xor_sync(0xffffffffu, v, 1));   // x pair
             v = __vmaxu2(v, __shfl_xor_sync(0xffffffffu, v, 8));   // y pair
-            pk[j] = v;
+            pk[g * 8 + j] = v;
           }
           if (keep) {
-            const uint4 o0 = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            const uint4 o1 = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            const uint4 o0 = make_uint4(pk[g * 8 + 0], pk[g * 8 + 1], pk[g * 8 + 2], pk[g * 8 + 3]);
+            const uint4 o1 = make_uint4(pk[g * 8 + 4], pk[g * 8 + 5], pk[g * 8 + 6], pk[g * 8 + 7]);
             const int cgo = g * 2;
             if (A.to_features) {
               const int64_t kc = ((int64_t)(yp * kHpool + xp) * C2) / 8 + cgo;
@@ -539,8 +552,6 @@ conv12_fused_kernel(FusedArgs A) {
             }
           }
         }
-        tc_fence_before();
-        mbar_arrive(&t2_empty[b]);
       }
     }
   }
