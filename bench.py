@@ -531,6 +531,34 @@ def next_rows_extras(device, sc, gs, small, n):
     ms = _time_ms(lambda: N.noscope_cbo_search([(d0, dg), (d1, dg)], cnns, fr, 50, 50, ym, u, 5, 12_500_000,
                                                m // 100, m // 100), reps=2)
     out["cbo_search"] = {"eval_frames": m, "dd_configs": 2, "cnns": 2, "ms_incl_sync": round(ms, 2)}
+    # live-stream latency: one 30-frame chunk (1 s of 30 fps video) per call, direct
+    # vs replayed from a CUDA graph captured once (the chunk pipeline has no host sync)
+    from synthgen.gpu import truth_labeller_address
+    c = 30
+    fr30 = small[:c].contiguous()
+    y30 = y[:c].contiguous()
+    arch = sg.CnnArch(2, 32, 32)
+    A, Wt = N.Arch(2, 32, 32), N.Weights(sg.he_normal_weights(arch, 3), device=device)
+    st = N.noscope_stream_state_init(d0)
+    wsc = N.workspace(N.OP_CASCADE_RUN, d0, A, c, device=device)
+    bufs = dict(labels=torch.zeros(c, dtype=torch.uint8, device=device),
+                route_out=torch.zeros(c, dtype=torch.uint8, device=device))
+    cur = torch.cuda.current_stream()
+    call = lambda: N.noscope_cascade_run(d0, A, Wt, -0.05, 0.05, fr30, 50, 50, st, truth_labeller_address(), y30,
+                                         ws=wsc, stream=cur, **bufs)
+    side = torch.cuda.Stream()
+    side.wait_stream(cur)
+    with torch.cuda.stream(side):
+        call()
+    cur.wait_stream(side)
+    ms_direct = _time_ms(call, reps=50)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        N.noscope_cascade_run(d0, A, Wt, -0.05, 0.05, fr30, 50, 50, st, truth_labeller_address(), y30, ws=wsc,
+                              stream=torch.cuda.current_stream(), **bufs)
+    ms_graph = _time_ms(graph.replay, reps=50)
+    out["live_chunk_30"] = {"frames": c, "source": "50x50", "us_direct": round(ms_direct * 1e3, 1),
+                            "us_graph_replay": round(ms_graph * 1e3, 1)}
     return out
 
 
