@@ -23,7 +23,7 @@ constexpr int kFitThreads = 256;
 // Per-position sums over the negative frames.  Thread = one 16-byte vector of
 // the small frame; a CTA takes a contiguous frame range, accumulates u32 sums in
 // registers (<= 2^32 / 255 frames per CTA) and adds them to the u64 totals.
-__global__ void __launch_bounds__(kFitThreads)
+__global__ void __launch_bounds__(512)
 ref_sum_kernel(const uint8_t* __restrict__ small, int64_t pitch, int nvec, const uint8_t* __restrict__ labels,
                int64_t n, unsigned long long* __restrict__ sums, unsigned long long* __restrict__ count) {
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
@@ -34,12 +34,22 @@ ref_sum_kernel(const uint8_t* __restrict__ small, int64_t pitch, int nvec, const
     uint32_t acc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = 0;
-    for (int64_t f = f0; f < f1; ++f) {
-      if (labels[f] != 0) continue;
-      if (v0 == 0 && threadIdx.x == 0) ++cnt;
-      if (v < nvec) {
-        const uint4 q = __ldg(reinterpret_cast<const uint4*>(small + f * pitch) + v);
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    // 8 frames per step: their labels and (negative frames') vectors are loaded
+    // before any is used, so each thread keeps 8 independent loads in flight
+    for (int64_t fb = f0; fb < f1; fb += 8) {
+      uint4 q[8];
+      bool use[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t f = fb + u;
+        use[u] = f < f1 && __ldg(labels + f) == 0;
+        q[u] = (use[u] && v < nvec) ? __ldg(reinterpret_cast<const uint4*>(small + f * pitch) + v)
+                                    : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (v0 == 0 && threadIdx.x == 0 && use[u]) ++cnt;
+        const uint32_t w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j] += (w[j >> 2] >> (8 * (j & 3))) & 0xFFu;
       }
@@ -63,13 +73,16 @@ __global__ void ref_finish_kernel(const unsigned long long* __restrict__ sums,
 }
 
 // ------------------------------------------------------------ block features
-// One CTA per frame (grid-stride): integer SSD per LR block accumulated in
-// shared memory, then MSE = SSD / (block pixels * 3) in fp64 (O3 blocked_mse).
+// One CTA per frame (grid-stride).  A thread sums the integer SSD of one
+// (image row, block column) segment — consecutive pixels of one LR block — and
+// adds it with one 32-bit shared atomic (a block's SSD < 2^32 for 8-bit frames
+// up to 2^32 / (3 * 255^2) pixels); MSE = SSD / (block pixels * 3) in fp64.
 __global__ void __launch_bounds__(kFitThreads)
 block_feat_kernel(const uint8_t* __restrict__ small, int64_t pitch, int out_w, int out_h, int grid,
                   int mode, const uint8_t* __restrict__ ref, int k, int64_t n, double* __restrict__ feats) {
-  __shared__ unsigned long long ssd[kMaxGrid * kMaxGrid];
+  __shared__ unsigned ssd[kMaxGrid * kMaxGrid];
   const int sy = out_h / grid, sx = out_w / grid, nb = grid * grid;
+  const int nseg = out_h * grid;
   for (int64_t f = blockIdx.x; f < n; f += gridDim.x) {
     double* row = feats + f * nb;
     if (mode == 1 && f < k) {
@@ -80,16 +93,17 @@ block_feat_kernel(const uint8_t* __restrict__ small, int64_t pitch, int out_w, i
     const uint8_t* r = mode == 0 ? ref : small + (f - k) * pitch;
     for (int b = threadIdx.x; b < nb; b += blockDim.x) ssd[b] = 0;
     __syncthreads();
-    for (int px = threadIdx.x; px < out_w * out_h; px += blockDim.x) {
-      const int y = px / out_w, x = px - y * out_w;
-      const int by = min(y / sy, grid - 1), bx = min(x / sx, grid - 1);
+    for (int sgi = threadIdx.x; sgi < nseg; sgi += blockDim.x) {
+      const int y = sgi / grid, bx = sgi - y * grid;
+      const int x0 = bx * sx, x1 = (bx == grid - 1) ? out_w : x0 + sx;
+      const uint8_t* pa = a + (y * out_w + x0) * 3;
+      const uint8_t* pr = r + (y * out_w + x0) * 3;
       unsigned s = 0;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int d = (int)a[px * 3 + c] - (int)r[px * 3 + c];
+      for (int e = 0; e < (x1 - x0) * 3; ++e) {
+        const int d = (int)pa[e] - (int)pr[e];
         s += (unsigned)(d * d);
       }
-      atomicAdd(&ssd[by * grid + bx], (unsigned long long)s);
+      atomicAdd(&ssd[min(y / sy, grid - 1) * grid + bx], s);
     }
     __syncthreads();
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
@@ -186,14 +200,30 @@ lr_step_kernel(const uint8_t* __restrict__ t, int64_t n, int d, int64_t per, dou
     r[i - r0] = 1.0 / (1.0 + exp(-z)) - (double)(t[i] != 0);
   }
   __syncthreads();
+  // partial X^T r over this CTA's rows: P = blockDim / (d + 1) threads per feature
+  // take interleaved rows (4 independent accumulators each); the P sums are then
+  // combined in p order — a fixed order, so the result is reproducible.
+  double* red = r + per;   // [P][d + 1]
+  const int P = max(1, (int)blockDim.x / (d + 1));
+  for (int e = threadIdx.x; e < P * (d + 1); e += blockDim.x) {
+    const int k = e % (d + 1), p = e / (d + 1);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const double* xk = k < d ? W.X + (size_t)k * n : nullptr;
+    int64_t i = r0 + p;
+    for (; i + 3 * P < r1; i += 4 * P) {
+      const double g0 = r[i - r0], g1 = r[i + P - r0], g2 = r[i + 2 * P - r0], g3 = r[i + 3 * P - r0];
+      a0 += xk ? xk[i] * g0 : g0;
+      a1 += xk ? xk[i + P] * g1 : g1;
+      a2 += xk ? xk[i + 2 * P] * g2 : g2;
+      a3 += xk ? xk[i + 3 * P] * g3 : g3;
+    }
+    for (; i < r1; i += P) a0 += xk ? xk[i] * r[i - r0] : r[i - r0];
+    red[p * (d + 1) + k] = (a0 + a1) + (a2 + a3);
+  }
+  __syncthreads();
   for (int k = threadIdx.x; k <= d; k += blockDim.x) {
     double s = 0.0;
-    if (k < d) {
-      const double* xk = W.X + (size_t)k * n;
-      for (int64_t i = r0; i < r1; ++i) s += xk[i] * r[i - r0];
-    } else {
-      for (int64_t i = r0; i < r1; ++i) s += r[i - r0];
-    }
+    for (int p = 0; p < P; ++p) s += red[p * (d + 1) + k];
     W.part[(size_t)blockIdx.x * (d + 1) + k] = s;
   }
   __threadfence();
@@ -263,7 +293,8 @@ noscope_status launch_reference_image(const uint8_t* small, int64_t pitch, int b
   // <= 2^32 / 255 frames per CTA keeps the u32 register sums exact
   const int64_t min_blocks = (n + 16000000 - 1) / 16000000;
   const int grid = (int)std::max<int64_t>(min_blocks, std::min<int64_t>(2 * kNumSMs, (n + 63) / 64));
-  ref_sum_kernel<<<std::max(grid, 1), kFitThreads, 0, st>>>(small, pitch, nvec, labels, n, sums, count);
+  const int threads = nvec <= 512 ? ((nvec + 31) / 32) * 32 : 512;   // one pass when a frame fits
+  ref_sum_kernel<<<std::max(grid, 1), threads, 0, st>>>(small, pitch, nvec, labels, n, sums, count);
   NS_LAUNCH_CHECK();
   ref_finish_kernel<<<(bytes + 255) / 256, 256, 0, st>>>(sums, count, bytes, ref);
   NS_LAUNCH_CHECK();
@@ -308,7 +339,8 @@ noscope_status launch_lr_fit(const double* F, const uint8_t* t, int64_t n, int d
   count_launch();
   if (lr <= 0.0) lr = 4.0 / (d + 1);
   const int64_t per = (n + nblk - 1) / nblk;
-  const size_t smem = (size_t)(d + 1 + per) * 8;
+  const int P = std::max(1, kFitThreads / (d + 1));
+  const size_t smem = (size_t)(d + 1 + per + (size_t)P * (d + 1)) * 8;
   constexpr size_t kMaxDyn = 220 * 1024;   // + the kernel's static shared flag
   static bool attr = false;
   if (!attr) {

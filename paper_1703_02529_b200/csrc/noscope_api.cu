@@ -471,6 +471,7 @@ noscope_status noscope_block_features(const noscope_dd_config* dd, const uint8_t
     return NOSCOPE_SHAPE;
   const int64_t bytes = (int64_t)dd->out_w * dd->out_h * 3;
   if (small_pitch % 16 || small_pitch < ((bytes + 15) & ~15ll)) return NOSCOPE_SHAPE;
+  if (bytes * 65025 >= (int64_t)1 << 32) return NOSCOPE_SHAPE;   // u32 block SSD
   noscope_status s = check_device();
   if (s != NOSCOPE_OK) return s;
   if (n == 0) return NOSCOPE_OK;
