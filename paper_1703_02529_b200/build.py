@@ -21,7 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 
-LIB_SOURCES = ["noscope_api.cu", "dd.cu", "scan.cu", "sweep.cu", "cnn.cu", "cnn_fused.cu", "cnn_gemm.cu", "fit.cu", "cbo.cu"]
+LIB_SOURCES = ["noscope_api.cu", "dd.cu", "scan.cu", "sweep.cu", "cnn.cu", "cnn_fused.cu", "cnn_gemm.cu", "cnn_tile.cu", "fit.cu", "cbo.cu"]
 LIB_HEADERS = ["common.cuh", "internal.h"]
 
 

@@ -247,7 +247,9 @@ static bool make_plan(const noscope_cnn_arch& a, int64_t n_max, CnnPlan* P) {
   for (int l = 0; l < p.L; ++l) {
     const int cout = p.C << l;
     if (l >= p.first_g) {
-      if (!make_convg_geom(cin, cout, h, p.chunk, &p.g[l])) return false;
+      if (!make_convt_geom(cin, cout, h, p.chunk, &p.g[l]) &&
+          !make_convg_geom(cin, cout, h, p.chunk, &p.g[l]))
+        return false;
       p.gw_off[l] = off;
       off = align_up(off + (size_t)cout * p.g[l].steps * 32, 256);
     }
@@ -381,7 +383,7 @@ noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& 
       c.n_max = n_max;
       c.chunk_base = base;
       c.chunk_len = len;
-      noscope_status s = launch_convg(c, st);
+      noscope_status s = c.g.tiled ? launch_convt(c, st) : launch_convg(c, st);
       if (s != NOSCOPE_OK) return s;
     }
     FcArgs f{};

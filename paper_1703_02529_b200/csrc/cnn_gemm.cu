@@ -77,7 +77,10 @@ bool make_convg_geom(int cin_real, int cout, int H, int64_t chunk, ConvGGeom* ou
   while ((int)tc < g.nacc * g.MT * g.N) tc <<= 1;
   g.tmem_cols = tc;
   const size_t astage = (size_t)2 * g.rows_blk * 16;   // two channel-group planes
-  const size_t bstage = (size_t)g.N * 32;
+  // B stage = 3 K16 steps (taps (ky, 0..2) of one channel-group pair): one ring
+  // wait + commit per 3 steps keeps the single issuing thread ahead of the pipe
+  g.kb = 3;
+  const size_t bstage = (size_t)g.kb * g.N * 32;
   auto layout = [&](int na, int nb) {
     size_t o = al((size_t)na * astage, 1024);
     g.oB = o;
@@ -94,7 +97,7 @@ bool make_convg_geom(int cin_real, int cout, int H, int64_t chunk, ConvGGeom* ou
   };
   const size_t kMax = 227 * 1024;
   g.nA = 4;
-  g.bstages = gm::kMaxB;
+  g.bstages = 12;
   while (layout(g.nA, g.bstages) > kMax && g.bstages > 4) --g.bstages;
   g.smem = layout(g.nA, g.bstages);
   if (g.smem > kMax) return false;
@@ -202,16 +205,16 @@ convg_kernel(ConvGArgs A) {
   } else if (warp == 0) {
     // ============================================== B producer
     if (lane == 0) {
-      const uint32_t bbytes = (uint32_t)g.N * 32;
+      const uint32_t bbytes = (uint32_t)g.kb * (uint32_t)g.N * 32;
       uint32_t st = 0, ph = 0, fill = 0;
       for (int64_t it = 0; it < my_units; ++it)
         for (int p = 0; p < g.passes; ++p)
-          for (int s = 0; s < g.steps; ++s) {
+          for (int s = 0; s < g.steps; s += g.kb) {
             if (fill >= (uint32_t)g.bstages) mbar_wait(&b_empty[st], ph ^ 1);
             else ++fill;
             mbar_arrive_expect_tx(&b_full[st], bbytes);
             bulk_g2s(smem + g.oB + (size_t)st * bbytes,
-                     A.wpack + ((size_t)p * g.steps + s) * bbytes, bbytes, &b_full[st]);
+                     A.wpack + ((size_t)p * g.steps + s) * (bbytes / g.kb), bbytes, &b_full[st]);
             if (++st == (uint32_t)g.bstages) { st = 0; ph ^= 1; }
           }
     }
@@ -223,7 +226,8 @@ convg_kernel(ConvGArgs A) {
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16_f32(128, g.N);
       const uint32_t sB = smem_u32(smem + g.oB);
-      const uint32_t bstep = ((uint32_t)g.N * 32) >> 4;
+      const uint32_t bstep = ((uint32_t)g.N * 32) >> 4;   // one K16 step of B
+      const uint32_t bstage = (uint32_t)g.kb * bstep;
       const uint64_t bd0 = sdesc(sB, (uint32_t)g.N * 16, 128);
       const uint64_t ad0 = sdesc(smem_u32(smem) + (uint32_t)(Wq + 1) * 16, plane, 128);
       const uint32_t astep = astage >> 4;
@@ -244,14 +248,19 @@ convg_kernel(ConvGArgs A) {
             mbar_wait(&a_full[ast], aph);
             const uint64_t ac = ad0 + (uint64_t)(ast * astep);
 #pragma unroll
-            for (int t = 0; t < 9; ++t) {
+            for (int ky = 0; ky < 3; ++ky) {        // B stage = taps (ky, 0..2)
               mbar_wait(&b_full[bst], bph);
               tc_fence_after();
-              const uint64_t ad = ac + dtap[t];
-              const uint64_t bd = bd0 + (uint64_t)(bst * bstep);
-              const uint32_t acc = (cp | t) ? 1u : 0u;
-              umma_bf16(d, ad, bd, idesc, acc);
-              umma_bf16(d + acol, ad + 128, bd, idesc, acc);   // +2048 B = next 128 rows
+              const uint64_t bs = bd0 + (uint64_t)(bst * bstage);
+#pragma unroll
+              for (int kx = 0; kx < 3; ++kx) {
+                const int t = ky * 3 + kx;
+                const uint64_t ad = ac + dtap[t];
+                const uint64_t bd = bs + (uint64_t)(kx * bstep);
+                const uint32_t acc = (cp | t) ? 1u : 0u;
+                umma_bf16(d, ad, bd, idesc, acc);
+                umma_bf16(d + acol, ad + 128, bd, idesc, acc);   // +2048 B = next 128 rows
+              }
               umma_commit(&b_empty[bst]);
               if (++bst == (uint32_t)g.bstages) { bst = 0; bph ^= 1; }
             }

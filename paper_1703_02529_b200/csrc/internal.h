@@ -139,9 +139,11 @@ size_t conv12_fused_smem();
 // right of each row are the 3x3 conv's zero padding on all four sides (the
 // column right of row y-1 is the left neighbour of row y).
 struct ConvGGeom {
+  int tiled;                 // 1: 2-D tile variant (cnn_tile.cu), even row period H + 1
   int cin_real, cin_eff, cout, H, W;   // cin_eff = cin_real (multiple of 16)
   int N, passes, steps;      // MMA N (<= 256) per pass over Cout; K16 steps
   int MT, nacc, nA, bstages; // M tiles per unit, accumulator sets, A / B ring depths
+  int kb;                    // K16 steps per B ring stage
   int S, rows_blk;           // unit stride in rows; rows loaded per unit per plane
   int64_t R;                 // rows per plane of the layer input (chunk)
   uint32_t tmem_cols;
@@ -165,6 +167,8 @@ struct ConvGArgs {
   int64_t n_max, chunk_base, chunk_len;
 };
 noscope_status launch_convg(const ConvGArgs& a, cudaStream_t st);
+bool make_convt_geom(int cin, int cout, int H, int64_t chunk, ConvGGeom* g);
+noscope_status launch_convt(const ConvGArgs& a, cudaStream_t st);
 noscope_status pack_convg(const uint16_t* w, const ConvGGeom& g, uint8_t* out, cudaStream_t st);
 noscope_status pack_conv12_bias(const float* b1, int C, uint8_t* w1_packed, cudaStream_t st);
 noscope_status launch_conv12_fused(const FusedArgs& a, int grid, cudaStream_t st);

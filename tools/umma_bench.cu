@@ -20,16 +20,16 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   return d;
 }
 
-template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0, int OFF = 0, int M = 128>
+template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0, int OFF = 0, int M = 128, int CE = 0>
 __global__ void __launch_bounds__(512, 1) mma_loop(int iters, int ksteps, long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* A = smem;                      // 128 rows x 128 B per 4 K-steps (sw) / 4 KB per step
   uint8_t* B = smem + 32768;
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2;
   __shared__ uint32_t tslot;
   for (int i = threadIdx.x; i < (32768 + 32768) / 4; i += blockDim.x)
     reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
-  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&bar2, 1); fence_mbar_init(); }
   if (threadIdx.x < 32) tmem_alloc<512>(&tslot);
   fence_proxy_async_smem();
   tc_fence_before();
@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(512, 1) mma_loop(int iters, int ksteps, long l
           }
           umma_bf16(tmem + acc * N, ad, bd, idesc, (it | k) ? 1u : 0u);
         }
+        if (CE && (k % CE) == CE - 1) umma_commit(&bar2);   // per-step completion tracking
       }
     }
     umma_commit(&bar);
@@ -83,21 +84,21 @@ __global__ void __launch_bounds__(512, 1) mma_loop(int iters, int ksteps, long l
   if (threadIdx.x < 32) tmem_dealloc<512>(tmem);
 }
 
-template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0, int OFF = 0, int M = 128>
+template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0, int OFF = 0, int M = 128, int CE = 0>
 void run() {
   const int iters = 500, ksteps = 8;
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
   size_t smem = 32768 + 8 * 256 * 32 + 2048;
-  cudaFuncSetAttribute(mma_loop<N, NACC, SW, SBO, HAMMER, OFF, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  mma_loop<N, NACC, SW, SBO, HAMMER, OFF, M><<<148, 512, smem>>>(iters, ksteps, d);
+  cudaFuncSetAttribute(mma_loop<N, NACC, SW, SBO, HAMMER, OFF, M, CE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  mma_loop<N, NACC, SW, SBO, HAMMER, OFF, M, CE><<<148, 512, smem>>>(iters, ksteps, d);
   cudaError_t err = cudaDeviceSynchronize();
   if (err != cudaSuccess) { printf("N=%d acc=%d sw=%d: %s\n", N, NACC, (int)SW, cudaGetErrorString(err)); fflush(stdout); return; }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  mma_loop<N, NACC, SW, SBO, HAMMER, OFF, M><<<148, 512, smem>>>(iters, ksteps, d);
+  mma_loop<N, NACC, SW, SBO, HAMMER, OFF, M, CE><<<148, 512, smem>>>(iters, ksteps, d);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
@@ -106,7 +107,7 @@ void run() {
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double mmas = (double)iters * ksteps * NACC;
   double flops = mmas * 2.0 * M * N * 16 * 148;
-  printf("M=%3d H=%d OFF=%3d SBO=%3d N=%3d acc=%d %s: %6.2f cycles/MMA (floor %3d), %7.1f TFLOP/s  %s\n", M, HAMMER, OFF, SBO, N, NACC,
+  printf("CE=%d M=%3d H=%d OFF=%3d SBO=%3d N=%3d acc=%d %s: %6.2f cycles/MMA (floor %3d), %7.1f TFLOP/s  %s\n", CE, M, HAMMER, OFF, SBO, N, NACC,
          SW ? "SW128" : "none ", (double)h[0] / mmas, M * N / 256, flops / (ms * 1e-3) / 1e12,
          cudaGetErrorString(cudaGetLastError()));
   fflush(stdout);
@@ -114,7 +115,8 @@ void run() {
 }
 
 int main() {
-  run<256, 2, false, 128, 0, 16, 64>(); run<256, 1, false, 128, 0, 16, 64>(); run<256, 2, false, 128, 1, 16, 64>();
-  run<128, 2, false, 128, 0, 16, 64>(); run<64, 4, false, 128, 1, 16, 128>(); run<64, 4, false, 128, 0, 16, 128>();
+  run<128, 3, false, 416, 0, 16, 128, 0>(); run<128, 3, false, 416, 0, 16, 128, 1>();
+  run<128, 3, false, 416, 0, 16, 128, 3>(); run<128, 2, false, 128, 0, 16, 128, 1>();
+  run<256, 2, false, 128, 0, 16, 128, 1>(); run<64, 2, false, 432, 0, 16, 128, 1>();
   return 0;
 }
