@@ -73,6 +73,7 @@ constexpr int kColD2 = kColD1 + kNG1 * 4 * C1;            // 320
 constexpr int kTmemCols = 512;                            // 320 + 192 = 512
 constexpr int kWp = 27, kHp = 27;       // conv2 input map with halo
 constexpr int kT2 = 6;                  // conv2 tiles: y blocks {0, 8} x x blocks {0, 8, 16}
+static_assert(kT2 == 2 * kNB2, "buffer/phase closed forms assume kT2 = 2 * kNB2");
 constexpr int kK2 = 9 * C1 / 16;        // 18 K16 steps for conv2
 constexpr int kPlaneRows = kHp * kWp + 1;  // rho = q + 1, q in [-1, 729)
 constexpr int kPlaneBytes = kPlaneRows * 16;  // 11,680
@@ -273,18 +274,19 @@ conv12_fused_kernel(FusedArgs A) {
       const uint64_t dOnes = sdesc(smem_u32(smem + oOnes), 128 * 16, 128);
       const uint64_t dBias = sdesc(smem_u32(smem + oB2b), C2 * 16, 128);
       mbar_wait(w_full, 0);
-      uint64_t u2 = 0;
       for (int64_t it = 0; it < my_frames; ++it) {
         const int pb = (int)(it & 1);
         mbar_wait(&act_full[pb], (uint32_t)((it >> 1) & 1));
-        for (int t = 0; t < kT2; t += 2, u2 += 2) {
+        for (int t = 0; t < kT2; t += 2) {
           int b[2], q0[2];
+          // kT2 = 2 * kNB2: tile t of any frame uses buffer t % 3 with phase
+          // (t / 3) & 1 (no 64-bit division by 3 in the issue loop)
           for (int q = 0; q < 2; ++q) {
-            const uint64_t u = u2 + q;
-            b[q] = (int)(u % kNB2);
-            const int yb = ((t + q) / 3) * 8, xb = ((t + q) % 3) * 8;
+            const int tq = t + q;
+            b[q] = tq % kNB2;
+            const int yb = (tq / 3) * 8, xb = (tq % 3) * 8;
             q0[q] = (yb + 1) * kWp + (xb + 1);
-            if (u >= kNB2) mbar_wait(&t2_empty[b[q]], (uint32_t)(((u / kNB2) - 1) & 1));
+            if (it > 0 || tq >= kNB2) mbar_wait(&t2_empty[b[q]], (uint32_t)(((tq / kNB2) + 1) & 1));
           }
           tc_fence_after();
           // Descriptors = base + (byte offset >> 4) in the start-address field; all
@@ -479,7 +481,6 @@ conv12_fused_kernel(FusedArgs A) {
     // lane -> conv position inside the tile: 4 conv rows x 8 conv columns per warp
     const int rl = (warp & 3) * 4 + (lane >> 3), cl = lane & 7;
     const bool pool_lane = ((lane & 1) == 0) && (((lane >> 3) & 1) == 0);
-    uint64_t ut2 = 0;
     // pooled 12x12; layer-3 input in the stacked layout (internal.h): row pitch
     // 13, 169 rows per frame, 14 leading guard rows
     constexpr int kHpool = 12, kWqo = 13, kPo = 13 * 13, kGo = 14;
@@ -492,9 +493,9 @@ conv12_fused_kernel(FusedArgs A) {
     }
     for (int64_t it = 0; it < my_frames; ++it) {
       const int64_t i = blockIdx.x + it * gridDim.x;  // chunk-relative frame
-      for (int t = 0; t < kT2; ++t, ++ut2) {
-        const int b = (int)(ut2 % kNB2);
-        mbar_wait(&t2_full[b], (uint32_t)((ut2 / kNB2) & 1));
+      for (int t = 0; t < kT2; ++t) {
+        const int b = t % kNB2;                          // kT2 = 2 * kNB2
+        mbar_wait(&t2_full[b], (uint32_t)((t / kNB2) & 1));
         tc_fence_after();
         const int yb = (t / 3) * 8, xb = (t % 3) * 8;
         const int yc = yb + rl, xc = xb + cl;                 // conv output position
