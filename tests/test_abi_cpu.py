@@ -82,3 +82,33 @@ def test_oracle_and_product_share_no_code():
                     for f in forbidden:
                         assert not re.search(rf"^\s*(from|import)\s+{f}\b", txt, re.M), (fn, f)
                         assert f"#include \"../../{f}" not in txt
+
+
+def test_next_row_entry_points_validate_before_device_use(lib):
+    """NEXT #1-#3 calls reject bad arguments on the host (no GPU needed)."""
+    from paper_1703_02529_b200 import noscope as N
+    v = ctypes.c_void_p(16)
+    # fit workspace sizing: LR needs n*d doubles of z-scored features
+    assert lib.noscope_fit_workspace_bytes(1000, 100, 7500) >= 1000 * 100 * 8
+    assert lib.noscope_fit_workspace_bytes(-1, 100, 7500) == 0
+    # reference image: null pointers / pitch not /16 / too-small workspace
+    assert lib.noscope_reference_image(None, 7504, 50, 50, v, 10, v, v, 1 << 20, None) == 1
+    assert lib.noscope_reference_image(v, 7501, 50, 50, v, 10, v, v, 1 << 20, None) == 2
+    assert lib.noscope_reference_image(v, 7504, 50, 50, v, 10, v, v, 16, None) == 3
+    # block features: grid above the 16x16 limit, mode 0 without a reference image
+    dd = N.DD(mode=1, metric=1, grid=17, t_diff_frames=3).c()
+    assert lib.noscope_block_features(ctypes.byref(dd), v, 7504, 4, v, None) == 2
+    dd = N.DD(mode=0, metric=1, grid=10).c()
+    assert lib.noscope_block_features(ctypes.byref(dd), v, 7504, 4, v, None) == 1
+    # LR fit: n < 2 is a data error, negative l2 an argument error
+    out = (ctypes.c_double * 3)()
+    assert lib.noscope_lr_fit(v, v, 1, 2, 10, 0.0, 0.0, out, v, 1 << 20, None) == 6
+    assert lib.noscope_lr_fit(v, v, 10, 2, 10, 0.0, -1.0, out, v, 1 << 20, None) == 1
+    # eval: window / agree_min consistency
+    cnt = N.EvalCounts()
+    assert lib.noscope_eval_labels(v, v, 90, 30, 31, ctypes.byref(cnt), v, 256, None) == 1
+    assert lib.noscope_eval_labels(v, v, 90, 0, 0, ctypes.byref(cnt), v, 256, None) == 1
+    # CBO search: empty lists
+    res = N.CboResult()
+    assert lib.noscope_cbo_search(None, 0, None, 0, v, N.FramesDesc(50, 50, 7504), 10, v, v, 3, 1, 1, 0, 0,
+                                  ctypes.byref(res), v, 1 << 20, None) == 1
