@@ -279,7 +279,12 @@ def run_ours(args):
     del S["frames"]
     torch.cuda.empty_cache()
     if not args.no_extras and rank == 0:
-        line["extras"] = run_extras(device)
+        # measured per-frame costs (ps) for the CBO cost model: T_MSE from the DD
+        # kernel, T_SNN from the cascade's CNN stage; T_full = the paper's YOLOv2
+        # (80 fps on a P100, P:162-164 — the reference NN is not run here)
+        t_mse = int(stage[0] * 1e9 / n) if stage[0] > 0 else 1000
+        t_snn = int(stage[3] * 1e9 / max(nf, 1)) if stage[3] > 0 else 20000
+        line["extras"] = run_extras(device, (t_mse, t_snn, 12_500_000_000))
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args, S)
     if rank == 0:
@@ -361,7 +366,7 @@ def run_e2e(args, S, device, world):
             "frames_per_step": n, "chunk": chunk, "ms_per_step": round(ms, 3)}
 
 
-def run_extras(device):
+def run_extras(device, timing=(1000, 20000, 12_500_000_000)):
     """Secondary measurements of the other BASELINE configs (not the headline)."""
     import torch
     import synthgen as sg
@@ -396,6 +401,7 @@ def run_extras(device):
                         "tflops": round(fl / ms / 1e9, 1), "frac_of_bf16_peak": round(fl / ms / 1e9 / bf16, 4)}
         del ws
     out["cnn_grid_65536"] = grid
+    out["tiny_T"] = tiny_config(device)
     out["next_rows"] = next_rows_extras(device, sc, gs, small, nG)
     # configs[3]: sweep over 1M labelled records, 100 x 100 candidates
     rng = np.random.default_rng(4)
@@ -409,7 +415,7 @@ def run_extras(device):
     dl, ul = T(sg.delta_grid(s, 100), np.float64), T(sg.logit_grid(100), np.float32)
     hist = torch.zeros(N.sweep_hist_words(100, 100), dtype=torch.int64, device=device)
     ws = N.workspace(N.OP_THRESHOLD_SWEEP, None, None, 0, 100, 100, device=device)
-    timing = (1000, 20000, 12_500_000)
+    # (timing: B200-measured T_MSE / T_SNN in ps, see the caller)
     for _ in range(2):
         hist.zero_()
         N.noscope_threshold_sweep(3, sd, zd, yd, ad, dl, ul, hist, timing, M // 100, M // 100, ws=ws)
@@ -428,7 +434,8 @@ def run_extras(device):
     e1.record()
     torch.cuda.synchronize()
     h_ms = e0.elapsed_time(e1) / reps
-    out["sweep_1M"] = {"wall_ms_incl_readback": round(wall * 1e3, 3), "hist_ms": round(h_ms, 4),
+    out["sweep_1M"] = {"timing_ps_mse_snn_full": list(timing),
+                       "wall_ms_incl_readback": round(wall * 1e3, 3), "hist_ms": round(h_ms, 4),
                        "records_per_s": round(M / wall, 1), "hist_GBps": round(M * 14 / h_ms / 1e6, 1),
                        "best": {k: best[k] for k in ("j", "l", "h", "feasible", "cost_ps", "uncertain")}}
     # Scale point: 1e9 records generated on device, histogram
@@ -475,6 +482,56 @@ def _time_ms(fn, reps=3):
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps
+
+
+def tiny_config(device):
+    """BASELINE configs[0]: 1,000 50x50 frames, global MSE vs the
+    reference image, t_skip 1, L2C32D32, thresholds -2/+2 logits; launch-latency
+    bound: median of 100 calls after 10 warm-ups, direct and CUDA-graph replay."""
+    import torch
+    import synthgen as sg
+    from paper_1703_02529_b200 import noscope as N
+    from synthgen.gpu import GpuScene, truth_labeller_address
+    n = 1000
+    sc = sg.make_scene(sg.SceneSpec(50, 50, n, seed=1, prevalence=0.15))
+    gs = GpuScene(sc, device=device)
+    fr = torch.empty((n, 7504), dtype=torch.uint8, device=device)
+    gs.render(fr, 0, n)
+    dd = N.DD(mode=0, metric=0, delta_diff=20.0, ref_image=torch.from_numpy(sg.background(sc.spec)).to(device))
+    arch = sg.CnnArch(2, 32, 32)
+    A, W = N.Arch(2, 32, 32), N.Weights(sg.he_normal_weights(arch, 1), device=device)
+    st = N.noscope_stream_state_init(dd)
+    ws = N.workspace(N.OP_CASCADE_RUN, dd, A, n, device=device)
+    bufs = dict(labels=torch.zeros(n, dtype=torch.uint8, device=device))
+    cur = torch.cuda.current_stream()
+
+    def call(stream):
+        N.noscope_cascade_run(dd, A, W, -2.0, 2.0, fr, 50, 50, st, truth_labeller_address(), gs.truth, ws=ws,
+                              stream=stream, **bufs)
+
+    def median_us(fn):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(100)]
+        for _ in range(10):
+            fn()
+        for a, b in ev:
+            a.record()
+            fn()
+            b.record()
+        torch.cuda.synchronize()
+        return float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3
+
+    side = torch.cuda.Stream()
+    side.wait_stream(cur)
+    with torch.cuda.stream(side):
+        call(side)
+    cur.wait_stream(side)
+    us = median_us(lambda: call(cur))
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        call(torch.cuda.current_stream())
+    us_g = median_us(g.replay)
+    return {"frames": n, "us_direct_median": round(us, 1), "fps_direct": round(n / us * 1e6, 1),
+            "us_graph_median": round(us_g, 1), "fps_graph": round(n / us_g * 1e6, 1)}
 
 
 def next_rows_extras(device, sc, gs, small, n):
