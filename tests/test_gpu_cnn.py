@@ -142,3 +142,24 @@ def test_cnn_zero_and_bias_weights():
     z = nsm.noscope_specialized_infer(nsm.Arch(4, 64, 128), nsm.Weights(w), torch.from_numpy(small).cuda())
     torch.cuda.synchronize()
     assert np.allclose(1 / (1 + np.exp(-z.cpu().numpy())), 0.75, atol=1e-6)
+
+
+@pytest.mark.parametrize("L,C", [(2, 64), (4, 64), (4, 32)])
+def test_cnn_multi_chunk_sampled(L, C):
+    """More frames than one internal chunk (8,192): the generic layer kernels see
+    chunk_base > 0 and a ragged last chunk.  Sampled frames from both chunks,
+    including the chunk boundary, against the oracle."""
+    nsm = ns()
+    n = 8192 + 301
+    sc, fr = scene_frames(50, 50, n, seed=19, prevalence=0.4)
+    small = np.zeros((n, 7504), np.uint8)
+    small[:, :7500] = fr[:, :7500]
+    arch = sg.CnnArch(L, C, 32)
+    w = sg.he_normal_weights(arch, 8)
+    z = nsm.noscope_specialized_infer(nsm.Arch(L, C, 32), nsm.Weights(w), torch.from_numpy(small).cuda())
+    torch.cuda.synchronize()
+    z = z.cpu().numpy()
+    pick = np.array([0, 1, 4095, 8190, 8191, 8192, 8193, 8300, n - 2, n - 1])
+    z_o = O.cnn_logits(hw3(fr[pick], 50, 50), arch, w)
+    assert np.abs(z[pick] - z_o).max() <= TOL
+    assert np.isfinite(z).all()
