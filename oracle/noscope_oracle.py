@@ -659,3 +659,143 @@ def factor_analysis(frames_hw3, cfg: DDConfig, arch, weights, lo, hi, truth, tim
         out.append(dict(name=name, accuracy=windowed_accuracy(res["labels"], truth), fp=fp, fn=fn,
                         speedup=modeled_speedup(cnt, stages, *timing), **cnt))
     return out
+
+
+# --------------------------------------------------------------------------
+# N4 Specialized-CNN training — P:472-477 "We train our
+#    specialized NNs ... RMSprop ... between one and five epochs ... early
+#    stopping", P:855-860 (cross-validation set).  Reading R-25:
+#    fp64 here / fp32 on the GPU, no bf16 rounding inside training (the input is
+#    the inference normalisation O6); mean binary cross-entropy on the logit;
+#    RMSprop v <- rho v + (1 - rho) g^2, w <- w - lr g / (sqrt(v) + eps); the
+#    mini-batch order is an input (a permutation per epoch); max-pool gradients go
+#    to the first maximum of each window in (dy, dx) row-major order.
+# --------------------------------------------------------------------------
+def cnn_params_from_weights(weights: dict) -> dict:
+    """bf16-bit weight dict (synthgen layout) -> fp64 parameter dict."""
+    return {"conv_w": [bf16_bits_to_f64(w) for w in weights["conv_w"]],
+            "conv_b": [np.asarray(b, np.float64) for b in weights["conv_b"]],
+            "fc1_w": bf16_bits_to_f64(weights["fc1_w"]), "fc1_b": np.asarray(weights["fc1_b"], np.float64),
+            "fc2_w": bf16_bits_to_f64(weights["fc2_w"]), "fc2_b": np.asarray(weights["fc2_b"], np.float64)}
+
+
+def _pool_argmax(a: np.ndarray):
+    """2x2 floor max pool returning (pooled, index 0..3 of the first maximum)."""
+    n, H, W, C = a.shape
+    Ho, Wo = H // 2, W // 2
+    v = a[:, :2 * Ho, :2 * Wo, :].reshape(n, Ho, 2, Wo, 2, C).transpose(0, 1, 3, 2, 4, 5)
+    v = v.reshape(n, Ho, Wo, 4, C)                     # window member q = 2*dy + dx
+    return v.max(axis=3), v.argmax(axis=3)             # argmax: first maximum
+
+
+def cnn_forward_train(small: np.ndarray, arch, P: dict):
+    """Forward pass keeping what the backward pass needs (fp64, no bf16)."""
+    x = normalize_input(small, arch.chan_mean)
+    cache = []
+    for l in range(arch.n_conv):
+        pre = conv3x3_same(x, P["conv_w"][l], P["conv_b"][l])
+        a = np.maximum(pre, 0.0)
+        p, arg = _pool_argmax(a)
+        cache.append((x, a, arg))
+        x = p
+    f = x.reshape(x.shape[0], -1)
+    h1 = np.maximum(f @ P["fc1_w"].T + P["fc1_b"], 0.0)
+    z = h1 @ P["fc2_w"] + P["fc2_b"][0]
+    return z, (cache, x.shape, f, h1)
+
+
+def bce_with_logits(z, t) -> float:
+    """mean(softplus(z) - t z)."""
+    return float(np.mean(np.logaddexp(0.0, z) - np.asarray(t, np.float64) * z))
+
+
+def cnn_backward(z, t, st, P: dict) -> dict:
+    """Gradients of the mean BCE w.r.t. every parameter (same keys as P)."""
+    cache, xs, f, h1 = st
+    B = len(z)
+    dz = (1.0 / (1.0 + np.exp(-z)) - np.asarray(t, np.float64)) / B
+    g = {"fc2_w": h1.T @ dz, "fc2_b": np.array([dz.sum()])}
+    dh1 = np.outer(dz, P["fc2_w"]) * (h1 > 0)
+    g["fc1_w"] = dh1.T @ f
+    g["fc1_b"] = dh1.sum(axis=0)
+    dx = (dh1 @ P["fc1_w"]).reshape(xs)
+    g["conv_w"] = [None] * len(cache)
+    g["conv_b"] = [None] * len(cache)
+    for l in range(len(cache) - 1, -1, -1):
+        x, a, arg = cache[l]
+        n, H, W, C = a.shape
+        Ho, Wo = H // 2, W // 2
+        da = np.zeros_like(a)
+        onehot = np.eye(4)[arg]                                        # [n, Ho, Wo, C, 4]
+        d4 = (onehot * dx[..., None]).transpose(0, 1, 2, 4, 3).reshape(n, Ho, Wo, 2, 2, C)
+        da[:, :2 * Ho, :2 * Wo, :] = d4.transpose(0, 1, 3, 2, 4, 5).reshape(n, 2 * Ho, 2 * Wo, C)
+        da *= (a > 0)
+        cin = x.shape[3]
+        xp = np.zeros((n, H + 2, W + 2, cin))
+        xp[:, 1:H + 1, 1:W + 1, :] = x
+        gw = np.empty((C, 3, 3, cin))
+        for ky in range(3):
+            for kx in range(3):
+                gw[:, ky, kx, :] = da.reshape(-1, C).T @ xp[:, ky:ky + H, kx:kx + W, :].reshape(-1, cin)
+        g["conv_w"][l] = gw
+        g["conv_b"][l] = da.sum(axis=(0, 1, 2))
+        if l > 0:
+            dap = np.zeros((n, H + 2, W + 2, C))
+            dap[:, 1:H + 1, 1:W + 1, :] = da
+            dxl = np.zeros((n, H, W, cin))
+            w = P["conv_w"][l]
+            for ky in range(3):
+                for kx in range(3):   # x[y+ky-1] fed out[y] => dx[y'] += da[y'-ky+1] w[ky]
+                    dxl += dap[:, 2 - ky:2 - ky + H, 2 - kx:2 - kx + W, :] @ w[:, ky, kx, :]
+            dx = dxl
+    return g
+
+
+def rmsprop_step(P: dict, G: dict, V: dict, lr: float, rho: float, eps: float):
+    """v <- rho v + (1 - rho) g^2; p <- p - lr g / (sqrt(v) + eps), every tensor."""
+    def upd(p, g, v):
+        v[...] = rho * v + (1.0 - rho) * g * g
+        p[...] = p - lr * g / (np.sqrt(v) + eps)
+    for k in ("conv_w", "conv_b"):
+        for l in range(len(P[k])):
+            upd(P[k][l], G[k][l], V[k][l])
+    for k in ("fc1_w", "fc1_b", "fc2_w", "fc2_b"):
+        upd(P[k], G[k], V[k])
+
+
+def _zeros_like_params(P):
+    return {k: ([np.zeros_like(x) for x in v] if isinstance(v, list) else np.zeros_like(v)) for k, v in P.items()}
+
+
+def _copy_params(P):
+    return {k: ([x.copy() for x in v] if isinstance(v, list) else v.copy()) for k, v in P.items()}
+
+
+def cnn_train(small_tr, y_tr, small_va, y_va, arch, P0: dict, perms, batch: int, lr=1e-3, rho=0.9,
+              eps=1e-7, patience=1):
+    """RMSprop over epochs (len(perms)); each epoch visits perms[e] in mini-batches
+    of `batch` (last one partial); after each epoch the cross-validation loss
+    decides early stopping: stop after `patience` epochs without improvement,
+    return the best epoch's parameters.  Returns (params, history) with history
+    = list of (train_loss, val_loss) per epoch run (train loss = mean over the
+    epoch's samples of the loss of their batch before its update)."""
+    P = _copy_params(P0)
+    V = _zeros_like_params(P)
+    best, best_val, since, hist = _copy_params(P), math.inf, 0, []
+    for perm in perms:
+        tot = 0.0
+        for s in range(0, len(perm), batch):
+            idx = np.asarray(perm[s:s + batch])
+            z, st = cnn_forward_train(small_tr[idx], arch, P)
+            tot += bce_with_logits(z, y_tr[idx]) * len(idx)
+            rmsprop_step(P, cnn_backward(z, y_tr[idx], st, P), V, lr, rho, eps)
+        zv, _ = cnn_forward_train(small_va, arch, P)
+        val = bce_with_logits(zv, y_va)
+        hist.append((tot / len(perm), val))
+        if val < best_val:
+            best, best_val, since = _copy_params(P), val, 0
+        else:
+            since += 1
+            if since >= patience:
+                break
+    return best, hist
