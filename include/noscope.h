@@ -423,6 +423,41 @@ noscope_status noscope_eval_labels(const uint8_t* pred, const uint8_t* ref, int6
                                    int32_t agree_min, noscope_eval_counts* counts_host, void* ws,
                                    size_t ws_bytes, noscope_stream_t stream);
 
+/* ---- Specialized-CNN training ----------------------
+ * P:472-477 "RMSprop ... between one and five epochs ... early stopping";
+ * P:855-860 cross-validation.  Reading R-25: fp32 forward/backward (input =
+ * the inference normalisation, no bf16 rounding inside), loss = mean binary
+ * cross-entropy of the logit against labels[i] != 0, RMSprop
+ *   v <- rho v + (1-rho) g^2;  p <- p - lr g / (sqrt(v) + eps)
+ * on every parameter, one step per mini-batch of `batch` frames (last partial).
+ * Epoch e visits perms[e][0..n_train) (device int32 frame indices into small,
+ * the shuffled order is the caller's); after each epoch the mean loss over
+ * val_idx decides early stopping: stop after `patience` epochs without a new
+ * best, and leave the best epoch's parameters in `params`.
+ * params: device fp32 [noscope_cnn_param_count] in this order, each row-major:
+ *   for each conv layer l: w [Cout][3][3][Cin], b [Cout]; then fc1 w [D][K]
+ *   ((h, w, c) feature order), fc1 b [D], fc2 w [D], fc2 b [1].
+ * history_host: host double [2 * epochs] (train loss, val loss per epoch run);
+ * epochs_run_host: host.  Convolutions and dense layers run as cuBLAS SGEMMs on
+ * explicit im2col rows (plain library GEMMs); everything else in this
+ * library's kernels.  Synchronous (one host sync per epoch).                 */
+typedef struct {
+  int32_t batch, epochs, patience;
+  float lr, rho, eps;
+} noscope_train_config;
+int64_t noscope_cnn_param_count(const noscope_cnn_arch* arch);
+size_t noscope_cnn_train_workspace_bytes(const noscope_cnn_arch* arch, int32_t batch);
+noscope_status noscope_cnn_train(const noscope_cnn_arch* arch, const noscope_train_config* cfg, float* params,
+                                 const uint8_t* small, int64_t small_pitch, const uint8_t* labels,
+                                 const int32_t* perms, int64_t n_train, const int32_t* val_idx, int64_t n_val,
+                                 double* history_host, int32_t* epochs_run_host, void* ws, size_t ws_bytes,
+                                 noscope_stream_t stream);
+/* Trained fp32 parameters -> the inference weight buffers of `weights_out`
+ * (conv / FC weights rounded to bf16 RNE, biases fp32; the caller owns and
+ * sizes the buffers as for noscope_specialized_infer).  Asynchronous.         */
+noscope_status noscope_cnn_params_to_weights(const noscope_cnn_arch* arch, const float* params,
+                                             const noscope_cnn_weights* weights_out, noscope_stream_t stream);
+
 /* Reads and clears the device status word in a workspace (synchronises). */
 noscope_status noscope_check(void* ws, noscope_stream_t stream);
 

@@ -196,6 +196,16 @@ noscope_status launch_eval_labels(const uint8_t* pred, const uint8_t* ref, int64
                                   int agree_min, unsigned long long* counters, int64_t* out_host,
                                   cudaStream_t st);
 
+// Specialized-CNN training (train.cu).
+int64_t train_param_count(const noscope_cnn_arch& a);
+size_t train_ws_bytes(const noscope_cnn_arch& a, int batch);
+noscope_status launch_cnn_train(const noscope_cnn_arch& a, const noscope_train_config& cfg, float* P,
+                                const uint8_t* small, int64_t pitch, const uint8_t* labels, const int32_t* perms,
+                                int64_t n_train, const int32_t* val_idx, int64_t n_val, double* hist,
+                                int32_t* epochs_run, void* ws, cudaStream_t st);
+noscope_status launch_params_to_weights(const noscope_cnn_arch& a, const float* P, const noscope_cnn_weights& wt,
+                                        cudaStream_t st);
+
 // Threshold sweep.
 size_t sweep_ws_bytes(int32_t n_delta, int32_t m);
 noscope_status launch_sweep(int32_t phase, const double* s, const float* z, const uint8_t* y,

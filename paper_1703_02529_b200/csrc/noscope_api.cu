@@ -622,6 +622,49 @@ noscope_status noscope_eval_labels(const uint8_t* pred, const uint8_t* ref, int6
   return NOSCOPE_OK;
 }
 
+// ---- specialized-CNN training (train.cu)
+int64_t noscope_cnn_param_count(const noscope_cnn_arch* arch) {
+  if (!arch || !cnn_arch_supported(*arch)) return 0;
+  return train_param_count(*arch);
+}
+
+size_t noscope_cnn_train_workspace_bytes(const noscope_cnn_arch* arch, int32_t batch) {
+  if (!arch || !cnn_arch_supported(*arch) || batch < 1 || batch > 1024) return 0;
+  return train_ws_bytes(*arch, batch);
+}
+
+noscope_status noscope_cnn_train(const noscope_cnn_arch* arch, const noscope_train_config* cfg, float* params,
+                                 const uint8_t* small, int64_t small_pitch, const uint8_t* labels,
+                                 const int32_t* perms, int64_t n_train, const int32_t* val_idx, int64_t n_val,
+                                 double* history_host, int32_t* epochs_run_host, void* ws, size_t ws_bytes,
+                                 noscope_stream_t stream) {
+  if (!arch || !cfg || !params || !small || !labels || !perms || !history_host || !epochs_run_host || !ws)
+    return NOSCOPE_INVALID_ARGUMENT;
+  if (!cnn_arch_supported(*arch)) return NOSCOPE_SHAPE;
+  if (cfg->batch < 1 || cfg->batch > 1024 || cfg->epochs < 1 || cfg->patience < 1 || !(cfg->lr > 0) ||
+      !(cfg->rho >= 0 && cfg->rho < 1) || !(cfg->eps > 0) || n_train < 1 || n_val < 0 || (n_val > 0 && !val_idx))
+    return NOSCOPE_INVALID_ARGUMENT;
+  if (small_pitch % 16 || small_pitch < 7504) return NOSCOPE_SHAPE;
+  if (ws_bytes < train_ws_bytes(*arch, cfg->batch)) return NOSCOPE_WORKSPACE_TOO_SMALL;
+  noscope_status s = check_device();
+  if (s != NOSCOPE_OK) return s;
+  return launch_cnn_train(*arch, *cfg, params, small, small_pitch, labels, perms, n_train, val_idx, n_val,
+                          history_host, epochs_run_host, ws, (cudaStream_t)stream);
+}
+
+noscope_status noscope_cnn_params_to_weights(const noscope_cnn_arch* arch, const float* params,
+                                             const noscope_cnn_weights* weights_out, noscope_stream_t stream) {
+  if (!arch || !params || !weights_out) return NOSCOPE_INVALID_ARGUMENT;
+  if (!cnn_arch_supported(*arch)) return NOSCOPE_SHAPE;
+  for (int l = 0; l < arch->n_conv; ++l)
+    if (!weights_out->conv_w[l] || !weights_out->conv_b[l]) return NOSCOPE_INVALID_ARGUMENT;
+  if (!weights_out->fc1_w || !weights_out->fc1_b || !weights_out->fc2_w || !weights_out->fc2_b)
+    return NOSCOPE_INVALID_ARGUMENT;
+  noscope_status s = check_device();
+  if (s != NOSCOPE_OK) return s;
+  return launch_params_to_weights(*arch, params, *weights_out, (cudaStream_t)stream);
+}
+
 // Test/debug helper (not part of the four-call contract): internal CNN
 // activation offsets within the specialized_infer workspace, so tests can
 // check individual layers.  out[19]: per conv layer l = 0..3 {offset of its

@@ -1,0 +1,444 @@
+// train.cu — specialized-CNN training on the GPU (P:472-477
+// "RMSprop ... between one and five epochs ... early stopping"
+// cross-validation).  Reading R-25: fp32 forward/backward without
+// bf16 rounding (input = the inference normalisation), mean binary cross-entropy
+// on the logit, RMSprop, max-pool gradient to the first maximum of each window.
+//
+// Every convolution and dense layer is a plain GEMM on explicit im2col rows
+// (cuBLAS SGEMM: forward Y = cols W^T, weight gradient dW = dY^T cols, input
+// gradient dcols = dY W); the custom kernels here do the rest: normalisation +
+// gather, im2col / col2im (gather form, no atomics), bias + ReLU + 2x2 max pool
+// with argmax, the unpool/ReLU mask, the dense-head elementwise steps, the loss
+// and RMSprop.  All reductions are fixed-order, so a run is reproducible.
+#include <cublas_v2.h>
+
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace ns {
+
+namespace {
+constexpr int kT = 256;
+
+inline int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + kT - 1) / kT, 16 * kNumSMs)); }
+
+// x = bf16_RNE(clamp(((float)g - mu) / 127.5f, -1, 1)) (the inference input), NHWC fp32
+__global__ void norm_gather_kernel(const uint8_t* __restrict__ small, int64_t pitch, const int32_t* __restrict__ idx,
+                                   int B, float m0, float m1, float m2, float* __restrict__ x) {
+  const int64_t total = (int64_t)B * 7500;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(e / 7500), r = (int)(e % 7500), c = r % 3;
+    const float g = (float)small[(int64_t)idx[b] * pitch + r];
+    const float mu = c == 0 ? m0 : (c == 1 ? m1 : m2);
+    const float v = fminf(fmaxf((g - mu) / 127.5f, -1.0f), 1.0f);
+    x[e] = __bfloat162float(__float2bfloat16_rn(v));
+  }
+}
+
+// cols[(b*H + y)*W + x][(ky*3 + kx)*C + c] = x[b][y+ky-1][x+kx-1][c] (0 outside)
+__global__ void im2col_kernel(const float* __restrict__ x, int B, int H, int W, int C, float* __restrict__ cols) {
+  const int K = 9 * C;
+  const int64_t total = (int64_t)B * H * W * K;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(e % K);
+    const int64_t p = e / K;
+    const int xx = (int)(p % W), yy = (int)((p / W) % H);
+    const int64_t b = p / ((int64_t)W * H);
+    const int tap = k / C, c = k - tap * C;
+    const int sy = yy + tap / 3 - 1, sx = xx + tap % 3 - 1;
+    cols[e] = (sy >= 0 && sy < H && sx >= 0 && sx < W) ? x[((b * H + sy) * W + sx) * C + c] : 0.0f;
+  }
+}
+
+// a = relu(pre + bias) for the pooled region (in place), pooled = 2x2 max,
+// arg = first maximum in (dy, dx) order.  Rows/columns outside the floor pool
+// region are set to 0 (they never receive a gradient).
+__global__ void bias_relu_pool_kernel(float* __restrict__ a, const float* __restrict__ bias, int B, int H, int W,
+                                      int C, float* __restrict__ pooled, uint8_t* __restrict__ arg) {
+  const int Ho = H / 2, Wo = W / 2;
+  const int64_t total = (int64_t)B * Ho * Wo * C;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % C);
+    const int64_t q = e / C;
+    const int xo = (int)(q % Wo), yo = (int)((q / Wo) % Ho);
+    const int64_t b = q / ((int64_t)Wo * Ho);
+    float best = 0.0f;
+    int bi = 0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int64_t off = ((b * H + 2 * yo + (m >> 1)) * W + 2 * xo + (m & 1)) * C + c;
+      const float v = fmaxf(a[off] + bias[c], 0.0f);
+      a[off] = v;
+      if (m == 0 || v > best) { best = v; bi = m; }
+    }
+    pooled[e] = best;
+    arg[e] = (uint8_t)bi;
+  }
+  // the row / column dropped by the floor pool (odd H, W)
+  if ((H & 1) || (W & 1)) {
+    const int64_t edge = (int64_t)B * (H * W - 4 * Ho * Wo) * C;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < edge; e += (int64_t)gridDim.x * blockDim.x) {
+      const int c = (int)(e % C);
+      const int64_t q = e / C;
+      const int per = H * W - 4 * Ho * Wo;
+      const int64_t b = q / per;
+      const int r = (int)(q % per);
+      int y, x;
+      if (r < W * (H - 2 * Ho)) { y = 2 * Ho + r / W; x = r % W; }
+      else { const int s = r - W * (H - 2 * Ho); y = s / (W - 2 * Wo); x = 2 * Wo + s % (W - 2 * Wo); }
+      a[((b * H + y) * W + x) * C + c] = 0.0f;
+    }
+  }
+}
+
+// da (in place over a): the pooled gradient goes to the window's argmax if its
+// activation is positive (ReLU'), every other position gets 0
+__global__ void unpool_relu_kernel(float* __restrict__ a, const float* __restrict__ dpooled,
+                                   const uint8_t* __restrict__ arg, int B, int H, int W, int C) {
+  const int Ho = H / 2, Wo = W / 2;
+  const int64_t total = (int64_t)B * Ho * Wo * C;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % C);
+    const int64_t q = e / C;
+    const int xo = (int)(q % Wo), yo = (int)((q / Wo) % Ho);
+    const int64_t b = q / ((int64_t)Wo * Ho);
+    const int am = arg[e];
+    const float g = dpooled[e];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int64_t off = ((b * H + 2 * yo + (m >> 1)) * W + 2 * xo + (m & 1)) * C + c;
+      a[off] = (m == am && a[off] > 0.0f) ? g : 0.0f;
+    }
+  }
+}
+
+// dx[b][y][x][c] = sum_{ky,kx} dcols[(b, y-ky+1, x-kx+1)][(ky*3+kx)*C + c] (gather)
+__global__ void col2im_kernel(const float* __restrict__ dcols, int B, int H, int W, int C, float* __restrict__ dx) {
+  const int K = 9 * C;
+  const int64_t total = (int64_t)B * H * W * C;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % C);
+    const int64_t p = e / C;
+    const int xx = (int)(p % W), yy = (int)((p / W) % H);
+    const int64_t b = p / ((int64_t)W * H);
+    float s = 0.0f;
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) {
+        const int oy = yy - ky + 1, ox = xx - kx + 1;
+        if (oy >= 0 && oy < H && ox >= 0 && ox < W)
+          s += dcols[((b * H + oy) * W + ox) * K + (ky * 3 + kx) * C + c];
+      }
+    dx[e] = s;
+  }
+}
+
+__global__ void bias_relu_kernel(float* __restrict__ h, const float* __restrict__ bias, int B, int D) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < B * D; e += gridDim.x * blockDim.x)
+    h[e] = fmaxf(h[e] + bias[e % D], 0.0f);
+}
+
+// z = h1 . w2 + b2; loss partial (fixed order, one block); dz = (sigmoid(z) - t) / B
+__global__ void head_kernel(const float* __restrict__ h1, const float* __restrict__ w2, const float* __restrict__ b2,
+                            const uint8_t* __restrict__ labels, const int32_t* __restrict__ idx, int B, int D,
+                            float* __restrict__ dz, double* __restrict__ loss_acc, int want_grad) {
+  __shared__ double red[kT];
+  double l = 0.0;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    float z = b2[0];
+    for (int d = 0; d < D; ++d) z = fmaf(h1[b * D + d], w2[d], z);
+    const float t = labels[idx[b]] ? 1.0f : 0.0f;
+    // softplus(z) - t z, stable: max(z, 0) + log1p(exp(-|z|)) - t z
+    l += (double)(fmaxf(z, 0.0f) + log1pf(expf(-fabsf(z))) - t * z);
+    if (want_grad) dz[b] = (1.0f / (1.0f + expf(-z)) - t) / (float)B;
+  }
+  red[threadIdx.x] = l;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < blockDim.x; ++i) s += red[i];
+    *loss_acc += s;
+  }
+}
+
+// g_w2[d] = sum_b h1[b][d] dz[b]; g_b2 = sum_b dz[b]; dh1 = dz w2 (h1 > 0)
+__global__ void head_grad_kernel(const float* __restrict__ h1, const float* __restrict__ w2, const float* __restrict__ dz,
+                                 int B, int D, float* __restrict__ g_w2, float* __restrict__ g_b2,
+                                 float* __restrict__ dh1) {
+  for (int d = threadIdx.x; d <= D; d += blockDim.x) {
+    float s = 0.0f;
+    for (int b = 0; b < B; ++b) s += d < D ? h1[b * D + d] * dz[b] : dz[b];
+    if (d < D) g_w2[d] = s;
+    else g_b2[0] = s;
+  }
+  for (int e = threadIdx.x; e < B * D; e += blockDim.x)
+    dh1[e] = h1[e] > 0.0f ? dz[e / D] * w2[e % D] : 0.0f;
+}
+
+// column sums of a row-major [rows][C] matrix: fixed-order two-level reduction
+__global__ void colsum_partial_kernel(const float* __restrict__ m, int64_t rows, int C, int64_t per,
+                                      float* __restrict__ part) {
+  const int64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float s = 0.0f;
+    for (int64_t r = r0; r < r1; ++r) s += m[r * C + c];
+    part[(int64_t)blockIdx.x * C + c] = s;
+  }
+}
+__global__ void colsum_final_kernel(const float* __restrict__ part, int nblk, int C, float* __restrict__ out) {
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float s = 0.0f;
+    for (int b = 0; b < nblk; ++b) s += part[(int64_t)b * C + c];
+    out[c] = s;
+  }
+}
+
+__global__ void rmsprop_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ v, int64_t n,
+                               float lr, float rho, float eps) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const float gg = g[e];
+    const float vv = rho * v[e] + (1.0f - rho) * gg * gg;
+    v[e] = vv;
+    p[e] -= lr * gg / (sqrtf(vv) + eps);
+  }
+}
+
+// fp32 parameters -> inference weights (bf16 RNE conv / FC weights, fp32 biases)
+__global__ void to_bf16_kernel(const float* __restrict__ s, uint16_t* __restrict__ d, int64_t n) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const __nv_bfloat16 h = __float2bfloat16_rn(s[e]);
+    d[e] = *reinterpret_cast<const uint16_t*>(&h);
+  }
+}
+
+// ---------------------------------------------------------------- host plan
+struct TLayer { int H, W, cin, cout; int64_t w_off, b_off; };
+struct TPlan {
+  int L, D, K;
+  TLayer lay[4];
+  int64_t fc1_w, fc1_b, fc2_w, fc2_b, nparams;
+};
+
+TPlan make_tplan(const noscope_cnn_arch& a) {
+  TPlan p{};
+  p.L = a.n_conv;
+  p.D = a.dense;
+  int h = a.in_h, cin = 3;
+  int64_t off = 0;
+  for (int l = 0; l < p.L; ++l) {
+    const int cout = a.base_filters << l;
+    p.lay[l] = TLayer{h, h, cin, cout, off, off + (int64_t)cout * 9 * cin};
+    off += (int64_t)cout * 9 * cin + cout;
+    cin = cout;
+    h /= 2;
+  }
+  p.K = h * h * cin;
+  p.fc1_w = off;
+  p.fc1_b = off + (int64_t)p.D * p.K;
+  p.fc2_w = p.fc1_b + p.D;
+  p.fc2_b = p.fc2_w + p.D;
+  p.nparams = p.fc2_b + 1;
+  return p;
+}
+
+// Row-major GEMM on cuBLAS (column-major): C[M][N] = op(A) op(B), op(A) M x K.
+bool g_gemm_ok = true;   // sticky per call of launch_cnn_train (host-side, single thread)
+void sgemm_rm(cublasHandle_t h, bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B,
+              int ldb, float* C, int ldc, float beta = 0.0f) {
+  const float one = 1.0f;
+  if (cublasSgemm(h, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, N, M, K, &one, B, ldb, A,
+                  lda, &beta, C, ldc) != CUBLAS_STATUS_SUCCESS)
+    g_gemm_ok = false;
+}
+
+struct TWs {
+  float *G, *V, *best, *x[5], *a[4], *cols, *dcols, *dx, *dxb, *h1, *dz, *dh1, *part;
+  uint8_t* arg[4];
+  int32_t* idx_tmp;
+  double* loss;
+  size_t total;
+};
+
+TWs carve_t(const TPlan& p, int B, void* base) {
+  uint8_t* c = reinterpret_cast<uint8_t*>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    uint8_t* r = c ? c + off : nullptr;
+    off = (off + bytes + 255) & ~size_t(255);
+    return r;
+  };
+  TWs w{};
+  w.G = (float*)take(p.nparams * 4);
+  w.V = (float*)take(p.nparams * 4);
+  w.best = (float*)take(p.nparams * 4);
+  size_t cols = 0, xmax = 0;
+  for (int l = 0; l < p.L; ++l) {
+    const TLayer& t = p.lay[l];
+    w.x[l] = (float*)take((size_t)B * t.H * t.W * t.cin * 4);
+    w.a[l] = (float*)take((size_t)B * t.H * t.W * t.cout * 4);
+    w.arg[l] = take((size_t)B * (t.H / 2) * (t.W / 2) * t.cout);
+    cols = std::max(cols, (size_t)B * t.H * t.W * 9 * t.cin);
+    xmax = std::max(xmax, (size_t)B * t.H * t.W * t.cin);
+    xmax = std::max(xmax, (size_t)B * (t.H / 2) * (t.W / 2) * t.cout);
+  }
+  w.x[p.L] = (float*)take((size_t)B * p.K * 4);
+  w.cols = (float*)take(cols * 4);
+  w.dcols = (float*)take(cols * 4);
+  w.dx = (float*)take(xmax * 4);
+  w.dxb = (float*)take(xmax * 4);
+  w.h1 = (float*)take((size_t)B * p.D * 4);
+  w.dz = (float*)take((size_t)B * 4);
+  w.dh1 = (float*)take((size_t)B * p.D * 4);
+  w.part = (float*)take((size_t)1024 * 512 * 4);
+  w.loss = (double*)take(8);
+  w.total = off;
+  return w;
+}
+
+void colsum(const float* m, int64_t rows, int C, float* out, float* part, cudaStream_t st) {
+  const int nblk = (int)std::min<int64_t>(1024, std::max<int64_t>(1, rows / 256));
+  const int64_t per = (rows + nblk - 1) / nblk;
+  colsum_partial_kernel<<<nblk, std::min(C, 512), 0, st>>>(m, rows, C, per, part);
+  colsum_final_kernel<<<1, std::min(C, 512), 0, st>>>(part, nblk, C, out);
+}
+
+// Forward on B frames (idx on device); leaves activations for the backward pass,
+// adds the batch's summed loss to *w.loss; dz if want_grad.
+noscope_status forward(cublasHandle_t h, const TPlan& p, const noscope_cnn_arch& a, const float* P, TWs& w,
+                       const uint8_t* small, int64_t pitch, const uint8_t* labels, const int32_t* idx, int B,
+                       int want_grad, cudaStream_t st) {
+  norm_gather_kernel<<<grid_for((int64_t)B * 7500), kT, 0, st>>>(small, pitch, idx, B, a.chan_mean[0],
+                                                                  a.chan_mean[1], a.chan_mean[2], w.x[0]);
+  for (int l = 0; l < p.L; ++l) {
+    const TLayer& t = p.lay[l];
+    const int64_t rows = (int64_t)B * t.H * t.W;
+    im2col_kernel<<<grid_for(rows * 9 * t.cin), kT, 0, st>>>(w.x[l], B, t.H, t.W, t.cin, w.cols);
+    sgemm_rm(h, false, true, (int)rows, t.cout, 9 * t.cin, w.cols, 9 * t.cin, P + t.w_off, 9 * t.cin, w.a[l],
+             t.cout);
+    bias_relu_pool_kernel<<<grid_for((int64_t)B * (t.H / 2) * (t.W / 2) * t.cout), kT, 0, st>>>(
+        w.a[l], P + t.b_off, B, t.H, t.W, t.cout, w.x[l + 1], w.arg[l]);
+  }
+  sgemm_rm(h, false, true, B, p.D, p.K, w.x[p.L], p.K, P + p.fc1_w, p.K, w.h1, p.D);
+  bias_relu_kernel<<<grid_for((int64_t)B * p.D), kT, 0, st>>>(w.h1, P + p.fc1_b, B, p.D);
+  head_kernel<<<1, kT, 0, st>>>(w.h1, P + p.fc2_w, P + p.fc2_b, labels, idx, B, p.D, w.dz, w.loss, want_grad);
+  NS_LAUNCH_CHECK();
+  return g_gemm_ok ? NOSCOPE_OK : NOSCOPE_CUDA;
+}
+
+noscope_status backward(cublasHandle_t h, const TPlan& p, const float* P, TWs& w, int B, cudaStream_t st) {
+  float* G = w.G;
+  head_grad_kernel<<<1, kT, 0, st>>>(w.h1, P + p.fc2_w, w.dz, B, p.D, G + p.fc2_w, G + p.fc2_b, w.dh1);
+  sgemm_rm(h, true, false, p.D, p.K, B, w.dh1, p.D, w.x[p.L], p.K, G + p.fc1_w, p.K);
+  colsum(w.dh1, B, p.D, G + p.fc1_b, w.part, st);
+  float* dpool = w.dx;   // gradient w.r.t. the current pooled map
+  sgemm_rm(h, false, false, B, p.K, p.D, w.dh1, p.D, P + p.fc1_w, p.K, dpool, p.K);
+  for (int l = p.L - 1; l >= 0; --l) {
+    const TLayer& t = p.lay[l];
+    const int64_t rows = (int64_t)B * t.H * t.W;
+    unpool_relu_kernel<<<grid_for((int64_t)B * (t.H / 2) * (t.W / 2) * t.cout), kT, 0, st>>>(
+        w.a[l], dpool, w.arg[l], B, t.H, t.W, t.cout);
+    // the forward im2col of this layer was overwritten by later layers: rebuild it
+    im2col_kernel<<<grid_for(rows * 9 * t.cin), kT, 0, st>>>(w.x[l], B, t.H, t.W, t.cin, w.cols);
+    sgemm_rm(h, true, false, t.cout, 9 * t.cin, (int)rows, w.a[l], t.cout, w.cols, 9 * t.cin, G + t.w_off,
+             9 * t.cin);
+    colsum(w.a[l], rows, t.cout, G + t.b_off, w.part, st);
+    if (l > 0) {
+      sgemm_rm(h, false, false, (int)rows, 9 * t.cin, t.cout, w.a[l], t.cout, P + t.w_off, 9 * t.cin, w.dcols,
+               9 * t.cin);
+      float* out = (dpool == w.dx) ? w.dxb : w.dx;
+      col2im_kernel<<<grid_for(rows * t.cin), kT, 0, st>>>(w.dcols, B, t.H, t.W, t.cin, out);
+      dpool = out;
+    }
+  }
+  NS_LAUNCH_CHECK();
+  return g_gemm_ok ? NOSCOPE_OK : NOSCOPE_CUDA;
+}
+}  // namespace
+
+int64_t train_param_count(const noscope_cnn_arch& a) { return make_tplan(a).nparams; }
+
+size_t train_ws_bytes(const noscope_cnn_arch& a, int batch) {
+  TPlan p = make_tplan(a);
+  return carve_t(p, batch, nullptr).total + 256;
+}
+
+noscope_status launch_cnn_train(const noscope_cnn_arch& a, const noscope_train_config& cfg, float* P,
+                                const uint8_t* small, int64_t pitch, const uint8_t* labels, const int32_t* perms,
+                                int64_t n_train, const int32_t* val_idx, int64_t n_val, double* hist,
+                                int32_t* epochs_run, void* ws, cudaStream_t st) {
+  const TPlan p = make_tplan(a);
+  TWs w = carve_t(p, cfg.batch, ws);
+  cublasHandle_t h;
+  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return NOSCOPE_CUDA;
+  g_gemm_ok = true;
+  cublasSetStream(h, st);
+  cublasSetMathMode(h, CUBLAS_PEDANTIC_MATH);   // fp32 throughout (no TF32)
+  noscope_status s = NOSCOPE_OK;
+  auto fail = [&](noscope_status e) { cublasDestroy(h); return e; };
+  NS_CUDA_TRY(cudaMemsetAsync(w.V, 0, p.nparams * 4, st));
+  NS_CUDA_TRY(cudaMemcpyAsync(w.best, P, p.nparams * 4, cudaMemcpyDeviceToDevice, st));
+  double best_val = INFINITY;
+  int since = 0, run = 0;
+  for (int e = 0; e < cfg.epochs; ++e) {
+    NS_CUDA_TRY(cudaMemsetAsync(w.loss, 0, 8, st));
+    for (int64_t s0 = 0; s0 < n_train; s0 += cfg.batch) {
+      const int B = (int)std::min<int64_t>(cfg.batch, n_train - s0);
+      const int32_t* idx = perms + (int64_t)e * n_train + s0;
+      if ((s = forward(h, p, a, P, w, small, pitch, labels, idx, B, 1, st)) != NOSCOPE_OK) return fail(s);
+      if ((s = backward(h, p, P, w, B, st)) != NOSCOPE_OK) return fail(s);
+      rmsprop_kernel<<<grid_for(p.nparams), kT, 0, st>>>(P, w.G, w.V, p.nparams, cfg.lr, cfg.rho, cfg.eps);
+    }
+    double tr = 0.0, va = 0.0;
+    NS_CUDA_TRY(cudaMemcpyAsync(&tr, w.loss, 8, cudaMemcpyDeviceToHost, st));
+    NS_CUDA_TRY(cudaStreamSynchronize(st));
+    NS_CUDA_TRY(cudaMemsetAsync(w.loss, 0, 8, st));
+    for (int64_t s0 = 0; s0 < n_val; s0 += cfg.batch) {
+      const int B = (int)std::min<int64_t>(cfg.batch, n_val - s0);
+      if ((s = forward(h, p, a, P, w, small, pitch, labels, val_idx + s0, B, 0, st)) != NOSCOPE_OK) return fail(s);
+    }
+    NS_CUDA_TRY(cudaMemcpyAsync(&va, w.loss, 8, cudaMemcpyDeviceToHost, st));
+    NS_CUDA_TRY(cudaStreamSynchronize(st));
+    tr /= (double)n_train;
+    va /= (double)std::max<int64_t>(n_val, 1);
+    hist[2 * e] = tr;
+    hist[2 * e + 1] = va;
+    run = e + 1;
+    if (va < best_val) {
+      best_val = va;
+      since = 0;
+      NS_CUDA_TRY(cudaMemcpyAsync(w.best, P, p.nparams * 4, cudaMemcpyDeviceToDevice, st));
+    } else if (++since >= cfg.patience) {
+      break;
+    }
+  }
+  NS_CUDA_TRY(cudaMemcpyAsync(P, w.best, p.nparams * 4, cudaMemcpyDeviceToDevice, st));
+  NS_CUDA_TRY(cudaStreamSynchronize(st));
+  *epochs_run = run;
+  cublasDestroy(h);
+  return NOSCOPE_OK;
+}
+
+noscope_status launch_params_to_weights(const noscope_cnn_arch& a, const float* P, const noscope_cnn_weights& wt,
+                                        cudaStream_t st) {
+  const TPlan p = make_tplan(a);
+  for (int l = 0; l < p.L; ++l) {
+    const TLayer& t = p.lay[l];
+    const int64_t nw = (int64_t)t.cout * 9 * t.cin;
+    to_bf16_kernel<<<grid_for(nw), kT, 0, st>>>(P + t.w_off, const_cast<uint16_t*>(wt.conv_w[l]), nw);
+    NS_CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(wt.conv_b[l]), P + t.b_off, t.cout * 4,
+                                cudaMemcpyDeviceToDevice, st));
+  }
+  to_bf16_kernel<<<grid_for((int64_t)p.D * p.K), kT, 0, st>>>(P + p.fc1_w, const_cast<uint16_t*>(wt.fc1_w),
+                                                              (int64_t)p.D * p.K);
+  NS_CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(wt.fc1_b), P + p.fc1_b, p.D * 4, cudaMemcpyDeviceToDevice, st));
+  to_bf16_kernel<<<grid_for(p.D), kT, 0, st>>>(P + p.fc2_w, const_cast<uint16_t*>(wt.fc2_w), p.D);
+  NS_CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(wt.fc2_b), P + p.fc2_b, 4, cudaMemcpyDeviceToDevice, st));
+  NS_LAUNCH_CHECK();
+  return NOSCOPE_OK;
+}
+
+}  // namespace ns

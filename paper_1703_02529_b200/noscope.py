@@ -90,6 +90,11 @@ class EvalCounts(C.Structure):
     _fields_ = [(f, c_i64) for f in ("windows", "correct_windows", "tp", "tn", "fp", "fn")]
 
 
+class TrainConfig(C.Structure):
+    _fields_ = [("batch", c_i32), ("epochs", c_i32), ("patience", c_i32), ("lr", c_f32), ("rho", c_f32),
+                ("eps", c_f32)]
+
+
 class SweepTables(C.Structure):
     _fields_ = [(n, c_p) for n in ("F", "FPnf", "FNnf", "FPf", "FNf", "GE", "GT")]
 
@@ -160,6 +165,15 @@ def lib():
                                      C.c_uint64, C.POINTER(CboResult), c_p, c_sz, c_p]
     L.noscope_eval_labels.restype = c_i32
     L.noscope_eval_labels.argtypes = [c_p, c_p, c_i64, c_i32, c_i32, C.POINTER(EvalCounts), c_p, c_sz, c_p]
+    L.noscope_cnn_param_count.restype = c_i64
+    L.noscope_cnn_param_count.argtypes = [C.POINTER(CnnArchC)]
+    L.noscope_cnn_train_workspace_bytes.restype = c_sz
+    L.noscope_cnn_train_workspace_bytes.argtypes = [C.POINTER(CnnArchC), c_i32]
+    L.noscope_cnn_train.restype = c_i32
+    L.noscope_cnn_train.argtypes = [C.POINTER(CnnArchC), C.POINTER(TrainConfig), c_p, c_p, c_i64, c_p, c_p, c_i64,
+                                    c_p, c_i64, C.POINTER(C.c_double), C.POINTER(c_i32), c_p, c_sz, c_p]
+    L.noscope_cnn_params_to_weights.restype = c_i32
+    L.noscope_cnn_params_to_weights.argtypes = [C.POINTER(CnnArchC), c_p, C.POINTER(CnnWeightsC), c_p]
     L.noscope_debug_cnn_layout.restype = c_i32
     L.noscope_debug_cnn_layout.argtypes = [C.POINTER(CnnArchC), c_i64, C.POINTER(c_i64)]
     _lib = L
@@ -459,6 +473,46 @@ def noscope_eval_labels(pred: torch.Tensor, ref: torch.Tensor, window=30, agree_
     _check(lib().noscope_eval_labels(_ptr(pred), _ptr(ref), pred.numel(), window, agree_min, C.byref(out),
                                      _ptr(ws), ws.numel(), _stream(stream)), "noscope_eval_labels")
     return {f: getattr(out, f) for f, _ in EvalCounts._fields_}
+
+
+# ---------------------------------------------------------------- CNN training
+def params_from_weight_dict(arch: Arch, w: dict, device="cuda"):
+    """Host marshalling of a synthgen-layout weight dict (bf16 bits) into the
+    flat fp32 parameter vector of noscope_cnn_train (header order)."""
+    import numpy as np
+    f32 = lambda bits: (np.asarray(bits, np.uint16).astype(np.uint32) << 16).view(np.float32).ravel()
+    parts = []
+    for l in range(arch.n_conv):
+        parts += [f32(w["conv_w"][l]), np.asarray(w["conv_b"][l], np.float32).ravel()]
+    parts += [f32(w["fc1_w"]), np.asarray(w["fc1_b"], np.float32).ravel(), f32(w["fc2_w"]),
+              np.asarray(w["fc2_b"], np.float32).ravel()]
+    v = np.concatenate(parts)
+    assert v.size == lib().noscope_cnn_param_count(C.byref(arch.c()))
+    return torch.from_numpy(v).to(device)
+
+
+def noscope_cnn_train(arch: Arch, params: torch.Tensor, small: torch.Tensor, labels: torch.Tensor,
+                      perms: torch.Tensor, val_idx: torch.Tensor, batch=32, lr=1e-3, rho=0.9, eps=1e-7,
+                      patience=1, stream=None):
+    """params: device fp32 (updated in place to the best epoch's); perms: device int32
+    [epochs, n_train]; val_idx: device int32 [n_val].  Returns (history, epochs_run)."""
+    epochs, n_train = perms.shape
+    ac = arch.c()
+    nb = lib().noscope_cnn_train_workspace_bytes(C.byref(ac), batch)
+    ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=params.device)
+    cfg = TrainConfig(batch, epochs, patience, lr, rho, eps)
+    hist = (C.c_double * (2 * epochs))()
+    run = c_i32(0)
+    _check(lib().noscope_cnn_train(C.byref(ac), C.byref(cfg), _ptr(params), _ptr(small), small.shape[1],
+                                   _ptr(labels), _ptr(perms), n_train, _ptr(val_idx), val_idx.numel(), hist,
+                                   C.byref(run), _ptr(ws), ws.numel(), _stream(stream)), "noscope_cnn_train")
+    return [(hist[2 * e], hist[2 * e + 1]) for e in range(run.value)], run.value
+
+
+def noscope_cnn_params_to_weights(arch: Arch, params: torch.Tensor, weights: "Weights", stream=None):
+    _check(lib().noscope_cnn_params_to_weights(C.byref(arch.c()), _ptr(params), C.byref(weights.c()),
+                                               _stream(stream)), "noscope_cnn_params_to_weights")
+    return weights
 
 
 def noscope_check(ws, stream=None):

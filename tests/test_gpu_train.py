@@ -1,0 +1,93 @@
+"""GPU parity of specialized-CNN training (reading R-25)
+against the oracle's fp64 cnn_train: gradients through one RMSprop step in its
+linear regime, loss histories and early stopping over epochs, and the export to
+inference weights."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synthgen as sg
+from gpu_util import hw3, ns, requires_gpu, scene_frames
+
+pytestmark = [pytest.mark.gpu, requires_gpu]
+
+
+def _data(n, seed, prevalence=0.5):
+    sc, fr = scene_frames(50, 50, n, seed=seed, prevalence=prevalence)
+    small = np.zeros((n, 7504), np.uint8)
+    small[:, :7500] = fr[:, :7500]
+    return small, hw3(fr, 50, 50), sc.truth[:n].astype(np.uint8)
+
+
+def _flat(P):
+    parts = []
+    for l in range(len(P["conv_w"])):
+        parts += [P["conv_w"][l].ravel(), P["conv_b"][l].ravel()]
+    parts += [P["fc1_w"].ravel(), P["fc1_b"].ravel(), P["fc2_w"].ravel(), P["fc2_b"].ravel()]
+    return np.concatenate(parts)
+
+
+@pytest.mark.parametrize("L,C", [(2, 32), (4, 32)])
+def test_one_step_gradients(L, C):
+    """eps = 1 >> sqrt(v): the step is -lr * g / (sqrt(0.1 g^2) + 1), a smooth function
+    of the gradient, so parameter deltas compare the fp32 backward pass with the
+    oracle's fp64 one."""
+    nsm = ns()
+    small, g, y = _data(24, 5)
+    arch = sg.CnnArch(L, C, 32)
+    w = sg.he_normal_weights(arch, 6)
+    A = nsm.Arch(L, C, 32)
+    p0 = nsm.params_from_weight_dict(A, w)
+    p = p0.clone()
+    perm = torch.arange(24, dtype=torch.int32, device="cuda").reshape(1, 24)
+    val = torch.arange(4, dtype=torch.int32, device="cuda")
+    hist, run = nsm.noscope_cnn_train(A, p, torch.from_numpy(small).cuda(), torch.from_numpy(y).cuda(), perm, val,
+                                      batch=24, lr=1.0, rho=0.9, eps=1.0)
+    P0 = O.cnn_params_from_weights(w)
+    P1, hist_o = O.cnn_train(g, y, g[:4], y[:4], arch, P0, [np.arange(24)], 24, lr=1.0, rho=0.9, eps=1.0)
+    d_gpu = (p - p0).cpu().numpy().astype(np.float64)
+    d_o = _flat(P1) - _flat(P0)
+    scale = np.abs(d_o).max()
+    assert np.abs(d_gpu - d_o).max() <= 1e-3 * scale, (np.abs(d_gpu - d_o).max(), scale)
+    assert abs(hist[0][0] - hist_o[0][0]) <= 1e-5 * abs(hist_o[0][0])     # loss before the step
+
+
+def test_training_epochs_and_early_stopping():
+    nsm = ns()
+    n_tr, n_va = 96, 32
+    small, g, y = _data(n_tr + n_va, 7)
+    arch = sg.CnnArch(2, 32, 32)
+    w = sg.he_normal_weights(arch, 8)
+    A = nsm.Arch(2, 32, 32)
+    rng = np.random.default_rng(3)
+    perms = np.stack([rng.permutation(n_tr) for _ in range(4)]).astype(np.int32)
+    p = nsm.params_from_weight_dict(A, w)
+    hist, run = nsm.noscope_cnn_train(A, p, torch.from_numpy(small).cuda(), torch.from_numpy(y).cuda(),
+                                      torch.from_numpy(perms).cuda(),
+                                      torch.arange(n_tr, n_tr + n_va, dtype=torch.int32, device="cuda"),
+                                      batch=16, lr=1e-3, patience=1)
+    P, hist_o = O.cnn_train(g[:n_tr], y[:n_tr], g[n_tr:], y[n_tr:], arch, O.cnn_params_from_weights(w),
+                            list(perms), 16, lr=1e-3, patience=1)
+    assert run == len(hist_o)
+    for (a, b), (c, d) in zip(hist, hist_o):
+        assert abs(a - c) <= 2e-3 * abs(c) and abs(b - d) <= 2e-3 * abs(d), (hist, hist_o)
+    # the returned parameters are the best epoch's: their val loss is the minimum
+    best = min(h[1] for h in hist)
+    Wt = nsm.noscope_cnn_params_to_weights(A, p, nsm.Weights(w))
+    z = nsm.noscope_specialized_infer(A, Wt, torch.from_numpy(small[n_tr:]).cuda()).cpu().numpy()
+    bce = float(np.mean(np.logaddexp(0, z) - y[n_tr:] * z))
+    assert abs(bce - best) < 0.05 * abs(best) + 0.02      # bf16 inference of the trained fp32 model
+
+
+def test_params_to_weights_rounding():
+    nsm = ns()
+    arch = sg.CnnArch(2, 32, 32)
+    w = sg.he_normal_weights(arch, 9)
+    A = nsm.Arch(2, 32, 32)
+    p = nsm.params_from_weight_dict(A, w) * 1.001                        # off the bf16 grid
+    out = nsm.noscope_cnn_params_to_weights(A, p, nsm.Weights(sg.zero_weights(arch)))
+    n0 = w["conv_w"][0].size
+    exp = p[:n0].to(torch.bfloat16).view(torch.int16)
+    assert torch.equal(out.conv_w[0].view(-1), exp)
+    assert torch.equal(out.conv_b[0], p[n0:n0 + 32])
