@@ -588,6 +588,26 @@ def next_rows_extras(device, sc, gs, small, n):
     ms = _time_ms(lambda: N.noscope_cbo_search([(d0, dg), (d1, dg)], cnns, fr, 50, 50, ym, u, 5, 12_500_000,
                                                m // 100, m // 100), reps=2)
     out["cbo_search"] = {"eval_frames": m, "dd_configs": 2, "cnns": 2, "ms_incl_sync": round(ms, 2)}
+    # NEXT #4: specialized-CNN training, L2C32D32, 8,192 frames x 2 epochs, batch 64;
+    # GEMMs are fp32 SGEMM on CUDA cores: peak = 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz
+    arch = sg.CnnArch(2, 32, 32)
+    A = N.Arch(2, 32, 32)
+    nt, ep = 8192, 2
+    p = N.params_from_weight_dict(A, sg.he_normal_weights(arch, 3), device)
+    perms = torch.stack([torch.randperm(nt, device=device) for _ in range(ep)]).to(torch.int32)
+    val = torch.arange(nt, nt + 1024, dtype=torch.int32, device=device)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    hist, run = N.noscope_cnn_train(A, p, small, y, perms, val, batch=64, patience=ep)
+    dt = time.perf_counter() - t0
+    fwd = cnn_flops_per_frame((2, 32, 32))
+    conv1 = 2 * 2500 * 27 * 32
+    train_flops = (3 * fwd - conv1) * nt * run + fwd * 1024 * run     # fwd + dW + dX (no dX for conv1), + val
+    peak32 = 148 * 128 * 2 * 1.965e3   # GFLOP/s
+    out["cnn_train"] = {"arch": "L2C32D32", "frames": nt, "epochs": run, "batch": 64, "s": round(dt, 3),
+                        "frames_per_s": round(nt * run / dt, 1), "tflops": round(train_flops / dt / 1e12, 2),
+                        "frac_of_fp32_alu_peak": round(train_flops / dt / 1e9 / peak32, 4),
+                        "history": [[round(a, 5), round(b, 5)] for a, b in hist]}
     # live-stream latency: one 30-frame chunk (1 s of 30 fps video) per call, direct
     # vs replayed from a CUDA graph captured once (the chunk pipeline has no host sync)
     from synthgen.gpu import truth_labeller_address
