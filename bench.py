@@ -603,7 +603,7 @@ def next_rows_extras(device, sc, gs, small, n):
     fwd = cnn_flops_per_frame((2, 32, 32))
     conv1 = 2 * 2500 * 27 * 32
     train_flops = (3 * fwd - conv1) * nt * run + fwd * 1024 * run     # fwd + dW + dX (no dX for conv1), + val
-    peak32 = 148 * 128 * 2 * 1.965e3   # GFLOP/s
+    peak32 = 148 * 128 * 2 * 1.965   # GFLOP/s
     out["cnn_train"] = {"arch": "L2C32D32", "frames": nt, "epochs": run, "batch": 64, "s": round(dt, 3),
                         "frames_per_s": round(nt * run / dt, 1), "tflops": round(train_flops / dt / 1e12, 2),
                         "frac_of_fp32_alu_peak": round(train_flops / dt / 1e9 / peak32, 4),

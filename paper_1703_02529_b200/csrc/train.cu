@@ -9,7 +9,8 @@
 // gradient dcols = dY W); the custom kernels here do the rest: normalisation +
 // gather, im2col / col2im (gather form, no atomics), bias + ReLU + 2x2 max pool
 // with argmax, the unpool/ReLU mask, the dense-head elementwise steps, the loss
-// and RMSprop.  All reductions are fixed-order, so a run is reproducible.
+// and RMSprop; bias gradients are cuBLAS GEMVs against a ones vector.  No
+// atomics anywhere, so a run is reproducible.
 #include <cublas_v2.h>
 
 #include <cmath>
@@ -38,18 +39,30 @@ __global__ void norm_gather_kernel(const uint8_t* __restrict__ small, int64_t pi
   }
 }
 
-// cols[(b*H + y)*W + x][(ky*3 + kx)*C + c] = x[b][y+ky-1][x+kx-1][c] (0 outside)
+// cols[(b*H + y)*W + x][(ky*3 + kx)*C + c] = x[b][y+ky-1][x+kx-1][c] (0 outside).
+// One thread per (pixel, tap, 4-channel group) when C % 4 == 0 (float4 copies),
+// else per (pixel, tap) copying C scalars: the index arithmetic is paid once.
 __global__ void im2col_kernel(const float* __restrict__ x, int B, int H, int W, int C, float* __restrict__ cols) {
   const int K = 9 * C;
-  const int64_t total = (int64_t)B * H * W * K;
+  const int vec = (C % 4 == 0) ? C / 4 : 1;
+  const int64_t total = (int64_t)B * H * W * 9 * vec;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int k = (int)(e % K);
-    const int64_t p = e / K;
-    const int xx = (int)(p % W), yy = (int)((p / W) % H);
-    const int64_t b = p / ((int64_t)W * H);
-    const int tap = k / C, c = k - tap * C;
+    const int v = (int)(e % vec);
+    const int64_t pt = e / vec;
+    const int tap = (int)(pt % 9);
+    const int64_t p = pt / 9;
+    const int xx = (int)(p % W);
+    const int64_t by = p / W;
+    const int yy = (int)(by % H);
     const int sy = yy + tap / 3 - 1, sx = xx + tap % 3 - 1;
-    cols[e] = (sy >= 0 && sy < H && sx >= 0 && sx < W) ? x[((b * H + sy) * W + sx) * C + c] : 0.0f;
+    const bool in = sy >= 0 && sy < H && sx >= 0 && sx < W;
+    float* dst = cols + p * K + tap * C;
+    const float* src = x + (p + (int64_t)(sy - yy) * W + (sx - xx)) * C;
+    if (C % 4 == 0) {
+      reinterpret_cast<float4*>(dst)[v] = in ? reinterpret_cast<const float4*>(src)[v] : make_float4(0, 0, 0, 0);
+    } else {
+      for (int c = 0; c < C; ++c) dst[c] = in ? src[c] : 0.0f;
+    }
   }
 }
 
@@ -179,22 +192,8 @@ __global__ void head_grad_kernel(const float* __restrict__ h1, const float* __re
     dh1[e] = h1[e] > 0.0f ? dz[e / D] * w2[e % D] : 0.0f;
 }
 
-// column sums of a row-major [rows][C] matrix: fixed-order two-level reduction
-__global__ void colsum_partial_kernel(const float* __restrict__ m, int64_t rows, int C, int64_t per,
-                                      float* __restrict__ part) {
-  const int64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    float s = 0.0f;
-    for (int64_t r = r0; r < r1; ++r) s += m[r * C + c];
-    part[(int64_t)blockIdx.x * C + c] = s;
-  }
-}
-__global__ void colsum_final_kernel(const float* __restrict__ part, int nblk, int C, float* __restrict__ out) {
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    float s = 0.0f;
-    for (int b = 0; b < nblk; ++b) s += part[(int64_t)b * C + c];
-    out[c] = s;
-  }
+__global__ void fill_kernel(float* __restrict__ d, int64_t n, float v) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) d[e] = v;
 }
 
 __global__ void rmsprop_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ v, int64_t n,
@@ -256,7 +255,7 @@ void sgemm_rm(cublasHandle_t h, bool ta, bool tb, int M, int N, int K, const flo
 }
 
 struct TWs {
-  float *G, *V, *best, *x[5], *a[4], *cols, *dcols, *dx, *dxb, *h1, *dz, *dh1, *part;
+  float *G, *V, *best, *x[5], *a[4], *cols, *dcols, *dx, *dxb, *h1, *dz, *dh1, *ones;
   uint8_t* arg[4];
   int32_t* idx_tmp;
   double* loss;
@@ -293,17 +292,17 @@ TWs carve_t(const TPlan& p, int B, void* base) {
   w.h1 = (float*)take((size_t)B * p.D * 4);
   w.dz = (float*)take((size_t)B * 4);
   w.dh1 = (float*)take((size_t)B * p.D * 4);
-  w.part = (float*)take((size_t)1024 * 512 * 4);
+  w.ones = (float*)take((size_t)B * p.lay[0].H * p.lay[0].W * 4);
   w.loss = (double*)take(8);
   w.total = off;
   return w;
 }
 
-void colsum(const float* m, int64_t rows, int C, float* out, float* part, cudaStream_t st) {
-  const int nblk = (int)std::min<int64_t>(1024, std::max<int64_t>(1, rows / 256));
-  const int64_t per = (rows + nblk - 1) / nblk;
-  colsum_partial_kernel<<<nblk, std::min(C, 512), 0, st>>>(m, rows, C, per, part);
-  colsum_final_kernel<<<1, std::min(C, 512), 0, st>>>(part, nblk, C, out);
+// column sums of a row-major [rows][C] matrix = (column-major C x rows) * ones
+void colsum(cublasHandle_t h, const float* m, int64_t rows, int C, float* out, const float* ones) {
+  const float one = 1.0f, zero = 0.0f;
+  if (cublasSgemv(h, CUBLAS_OP_N, C, (int)rows, &one, m, C, ones, 1, &zero, out, 1) != CUBLAS_STATUS_SUCCESS)
+    g_gemm_ok = false;
 }
 
 // Forward on B frames (idx on device); leaves activations for the backward pass,
@@ -316,7 +315,8 @@ noscope_status forward(cublasHandle_t h, const TPlan& p, const noscope_cnn_arch&
   for (int l = 0; l < p.L; ++l) {
     const TLayer& t = p.lay[l];
     const int64_t rows = (int64_t)B * t.H * t.W;
-    im2col_kernel<<<grid_for(rows * 9 * t.cin), kT, 0, st>>>(w.x[l], B, t.H, t.W, t.cin, w.cols);
+    im2col_kernel<<<grid_for(rows * 9 * (t.cin % 4 ? 1 : t.cin / 4)), kT, 0, st>>>(w.x[l], B, t.H, t.W, t.cin,
+                                                                                 w.cols);
     sgemm_rm(h, false, true, (int)rows, t.cout, 9 * t.cin, w.cols, 9 * t.cin, P + t.w_off, 9 * t.cin, w.a[l],
              t.cout);
     bias_relu_pool_kernel<<<grid_for((int64_t)B * (t.H / 2) * (t.W / 2) * t.cout), kT, 0, st>>>(
@@ -333,7 +333,7 @@ noscope_status backward(cublasHandle_t h, const TPlan& p, const float* P, TWs& w
   float* G = w.G;
   head_grad_kernel<<<1, kT, 0, st>>>(w.h1, P + p.fc2_w, w.dz, B, p.D, G + p.fc2_w, G + p.fc2_b, w.dh1);
   sgemm_rm(h, true, false, p.D, p.K, B, w.dh1, p.D, w.x[p.L], p.K, G + p.fc1_w, p.K);
-  colsum(w.dh1, B, p.D, G + p.fc1_b, w.part, st);
+  colsum(h, w.dh1, B, p.D, G + p.fc1_b, w.ones);
   float* dpool = w.dx;   // gradient w.r.t. the current pooled map
   sgemm_rm(h, false, false, B, p.K, p.D, w.dh1, p.D, P + p.fc1_w, p.K, dpool, p.K);
   for (int l = p.L - 1; l >= 0; --l) {
@@ -342,10 +342,11 @@ noscope_status backward(cublasHandle_t h, const TPlan& p, const float* P, TWs& w
     unpool_relu_kernel<<<grid_for((int64_t)B * (t.H / 2) * (t.W / 2) * t.cout), kT, 0, st>>>(
         w.a[l], dpool, w.arg[l], B, t.H, t.W, t.cout);
     // the forward im2col of this layer was overwritten by later layers: rebuild it
-    im2col_kernel<<<grid_for(rows * 9 * t.cin), kT, 0, st>>>(w.x[l], B, t.H, t.W, t.cin, w.cols);
+    im2col_kernel<<<grid_for(rows * 9 * (t.cin % 4 ? 1 : t.cin / 4)), kT, 0, st>>>(w.x[l], B, t.H, t.W, t.cin,
+                                                                                 w.cols);
     sgemm_rm(h, true, false, t.cout, 9 * t.cin, (int)rows, w.a[l], t.cout, w.cols, 9 * t.cin, G + t.w_off,
              9 * t.cin);
-    colsum(w.a[l], rows, t.cout, G + t.b_off, w.part, st);
+    colsum(h, w.a[l], rows, t.cout, G + t.b_off, w.ones);
     if (l > 0) {
       sgemm_rm(h, false, false, (int)rows, 9 * t.cin, t.cout, w.a[l], t.cout, P + t.w_off, 9 * t.cin, w.dcols,
                9 * t.cin);
@@ -380,6 +381,10 @@ noscope_status launch_cnn_train(const noscope_cnn_arch& a, const noscope_train_c
   noscope_status s = NOSCOPE_OK;
   auto fail = [&](noscope_status e) { cublasDestroy(h); return e; };
   NS_CUDA_TRY(cudaMemsetAsync(w.V, 0, p.nparams * 4, st));
+  {
+    const int64_t nr = (int64_t)cfg.batch * p.lay[0].H * p.lay[0].W;
+    fill_kernel<<<grid_for(nr), kT, 0, st>>>(w.ones, nr, 1.0f);
+  }
   NS_CUDA_TRY(cudaMemcpyAsync(w.best, P, p.nparams * 4, cudaMemcpyDeviceToDevice, st));
   double best_val = INFINITY;
   int since = 0, run = 0;
