@@ -596,6 +596,7 @@ def next_rows_extras(device, sc, gs, small, n):
     p = N.params_from_weight_dict(A, sg.he_normal_weights(arch, 3), device)
     perms = torch.stack([torch.randperm(nt, device=device) for _ in range(ep)]).to(torch.int32)
     val = torch.arange(nt, nt + 1024, dtype=torch.int32, device=device)
+    N.noscope_cnn_train(A, p.clone(), small, y, perms[:1, :128].contiguous(), val[:64], batch=64)   # warm-up
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     hist, run = N.noscope_cnn_train(A, p, small, y, perms, val, batch=64, patience=ep)

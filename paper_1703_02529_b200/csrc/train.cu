@@ -373,13 +373,15 @@ noscope_status launch_cnn_train(const noscope_cnn_arch& a, const noscope_train_c
                                 int32_t* epochs_run, void* ws, cudaStream_t st) {
   const TPlan p = make_tplan(a);
   TWs w = carve_t(p, cfg.batch, ws);
-  cublasHandle_t h;
-  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return NOSCOPE_CUDA;
+  // one cuBLAS handle per host thread, created on first use and kept (creation
+  // and cuBLAS's lazy kernel loading cost far more than a training epoch)
+  static thread_local cublasHandle_t h = nullptr;
+  if (!h && cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) { h = nullptr; return NOSCOPE_CUDA; }
   g_gemm_ok = true;
   cublasSetStream(h, st);
   cublasSetMathMode(h, CUBLAS_PEDANTIC_MATH);   // fp32 throughout (no TF32)
   noscope_status s = NOSCOPE_OK;
-  auto fail = [&](noscope_status e) { cublasDestroy(h); return e; };
+  auto fail = [&](noscope_status e) { return e; };
   NS_CUDA_TRY(cudaMemsetAsync(w.V, 0, p.nparams * 4, st));
   {
     const int64_t nr = (int64_t)cfg.batch * p.lay[0].H * p.lay[0].W;
@@ -423,7 +425,6 @@ noscope_status launch_cnn_train(const noscope_cnn_arch& a, const noscope_train_c
   NS_CUDA_TRY(cudaMemcpyAsync(P, w.best, p.nparams * 4, cudaMemcpyDeviceToDevice, st));
   NS_CUDA_TRY(cudaStreamSynchronize(st));
   *epochs_run = run;
-  cublasDestroy(h);
   return NOSCOPE_OK;
 }
 
