@@ -236,12 +236,11 @@ conv12_fused_kernel(FusedArgs A) {
       for (int64_t it = 0; it < my_frames; ++it) {
         for (int t = 0; t < kT1; t += 2, u1 += 2) {
           const uint64_t ug = u1 >> 2;           // global window-group sequence
-          int a[2];
-          for (int q = 0; q < 2; ++q) {
-            const uint64_t u = u1 + q;
-            a[q] = (int)(u % kA1Stages);
-            mbar_wait(&a1_full[a[q]], (uint32_t)((u / kA1Stages) & 1));
-          }
+          // A1 slots come in pairs (slot 2p, 2p+1 = window members of one pair),
+          // one barrier each way per pair
+          const int pr = (int)((u1 >> 1) & 1);
+          const int a[2] = {2 * pr, 2 * pr + 1};
+          mbar_wait(&a1_full[pr], (uint32_t)((u1 >> 2) & 1));
           tc_fence_after();
 #pragma unroll
           for (int h = 0; h < kHalves; ++h) {
@@ -260,7 +259,7 @@ conv12_fused_kernel(FusedArgs A) {
                              tmem + kColA1 + a[q] * kA1Cols + kk * 8,
                              bd0 + (uint64_t)((kk * 2 * C1t * 16 + h * C1 * 16) >> 4), id1, kk);
           }
-          for (int q = 0; q < 2; ++q) umma_commit(&a1_empty[a[q]]);
+          umma_commit(&a1_empty[pr]);
           if (((u1 + 1) & 3) == 3)                 // window group complete (all halves)
             for (int h = 0; h < kHalves; ++h) umma_commit(&t1_full[(int)((ug * kHalves + h) % kNG1)]);
         }
@@ -358,9 +357,8 @@ conv12_fused_kernel(FusedArgs A) {
         }
 #pragma unroll
         for (int pq = 0; pq < 4; ++pq) {
-          const uint64_t u = u1 + pq;
-          const int a = (int)(u % kA1Stages);
-          if (u >= kA1Stages) mbar_wait(&a1_empty[a], (uint32_t)(((u / kA1Stages) - 1) & 1));
+          const int a = pq, pr = pq >> 1;       // u1 % 4 == 0: member pq -> A1 slot pq, pair pq/2
+          if ((pq & 1) == 0 && u1 >= kA1Stages) mbar_wait(&a1_empty[pr], (uint32_t)(((u1 >> 2) - 1) & 1));
           const int dy = pq >> 1, dx = pq & 1;
           uint32_t h[27];  // 27 bf16 in (tap, channel) order, one per 32-bit register
 #pragma unroll
@@ -383,9 +381,11 @@ conv12_fused_kernel(FusedArgs A) {
           v[15] = 0;
           tc_fence_after();
           tmem_st16(tmem + ((uint32_t)lg << 16) + kColA1 + a * kA1Cols, v);
-          if (!(NS_EXP & 128)) tmem_st_wait();
-          tc_fence_before();
-          mbar_arrive(&a1_full[a]);
+          if (pq & 1) {                        // pair complete: publish both members
+            if (!(NS_EXP & 128)) tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&a1_full[pr]);
+          }
         }
       }
     }
