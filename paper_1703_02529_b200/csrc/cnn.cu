@@ -211,7 +211,7 @@ fc_kernel(FcArgs A) {
   if (warp == 0) tmem_dealloc_rt(tmem, A.tmem_cols);
 }
 
-static int fc_ksplit(int K) { return std::max(1, std::min(8, K / 1152)); }
+static int fc_ksplit(int K) { return std::max(1, std::min(4, K / 2304)); }
 
 // =================================================================== host plan
 struct CnnPlan {
