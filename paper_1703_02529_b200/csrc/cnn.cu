@@ -20,7 +20,7 @@ namespace ns {
 
 constexpr int kCnnThreads = 128;
 constexpr int kBStages = 4;
-constexpr int64_t kCnnChunk = 8192;   // frames per internal chunk (workspace bound)
+constexpr int64_t kCnnChunk = 32768;  // frames per internal chunk (workspace bound)
 
 NS_DEV uint16_t f2bf(float v) {
   __nv_bfloat16 h = __float2bfloat16_rn(v);
