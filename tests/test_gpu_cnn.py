@@ -146,11 +146,12 @@ def test_cnn_zero_and_bias_weights():
 
 @pytest.mark.parametrize("L,C", [(2, 64), (4, 64), (4, 32)])
 def test_cnn_multi_chunk_sampled(L, C):
-    """More frames than one internal chunk (8,192): the generic layer kernels see
+    """More frames than one internal chunk: the layer kernels see
     chunk_base > 0 and a ragged last chunk.  Sampled frames from both chunks,
     including the chunk boundary, against the oracle."""
     nsm = ns()
-    n = 8192 + 301
+    chunk = nsm.debug_cnn_layout(nsm.Arch(L, C, 32), 1 << 20)[18]      # internal chunk size
+    n = chunk + 301
     sc, fr = scene_frames(50, 50, n, seed=19, prevalence=0.4)
     small = np.zeros((n, 7504), np.uint8)
     small[:, :7500] = fr[:, :7500]
@@ -159,7 +160,7 @@ def test_cnn_multi_chunk_sampled(L, C):
     z = nsm.noscope_specialized_infer(nsm.Arch(L, C, 32), nsm.Weights(w), torch.from_numpy(small).cuda())
     torch.cuda.synchronize()
     z = z.cpu().numpy()
-    pick = np.array([0, 1, 4095, 8190, 8191, 8192, 8193, 8300, n - 2, n - 1])
+    pick = np.array([0, 1, chunk // 2, chunk - 2, chunk - 1, chunk, chunk + 1, chunk + 108, n - 2, n - 1])
     z_o = O.cnn_logits(hw3(fr[pick], 50, 50), arch, w)
     assert np.abs(z[pick] - z_o).max() <= TOL
     assert np.isfinite(z).all()
