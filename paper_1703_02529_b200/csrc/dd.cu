@@ -35,7 +35,7 @@ uint64_t& launch_counter() {
 constexpr int kV = 128;                 // vertical-sum group
 constexpr int kHz = 160;                // box-mean / score group (out_w*3 <= 160)
 constexpr int kDsThreads = kV + kHz;
-constexpr int kDsStages = 4;
+constexpr int kDsMaxStages = 8;          // band ring depth: as many as fit 2 CTAs/SM
 // named barrier ids (0 = __syncthreads)
 constexpr int kBarFull0 = 1, kBarEmpty0 = 3, kBarV = 5, kBarH = 6;
 
@@ -70,7 +70,7 @@ struct DsArgs {
   uint8_t* disp;
   uint32_t* status;
   unsigned* done;  // [gridDim.x] completion flags, zeroed before launch (mode 1)
-  int stage_bytes, fast, rlo;
+  int stage_bytes, fast, rlo, nstages;
 };
 
 struct BandInfo {   // per output row i
@@ -158,10 +158,10 @@ dd_kernel(DsArgs A) {
   const int gg = A.grid * A.grid;
   const int small_bytes = A.out_w * A.out_h * 3;
   uint8_t* stages = smem;
-  uint16_t* cs = reinterpret_cast<uint16_t*>(smem + kDsStages * A.stage_bytes);   // 2 x RBp
+  uint16_t* cs = reinterpret_cast<uint16_t*>(smem + A.nstages * A.stage_bytes);   // 2 x RBp
   BandInfo* band = reinterpret_cast<BandInfo*>(cs + 2 * A.RBp);
   uint8_t* ref_s = reinterpret_cast<uint8_t*>(band + A.out_h);
-  uint32_t* blk = reinterpret_cast<uint32_t*>(ref_s + ((small_bytes + 15) & ~15));
+  uint32_t* blk = reinterpret_cast<uint32_t*>(ref_s + (A.mode == 0 ? ((small_bytes + 15) & ~15) : 0));
   uint32_t* blkn = blk + ((gg + 1) & ~1);
   double* wlr = reinterpret_cast<double*>(blkn + ((gg + 1) & ~1));
   double* pk = wlr + gg;
@@ -198,7 +198,7 @@ dd_kernel(DsArgs A) {
     }
   }
   if (tid == 0) {
-    for (int s = 0; s < kDsStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < A.nstages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -217,7 +217,7 @@ dd_kernel(DsArgs A) {
       bulk_g2s_evict_first(stages + (size_t)p_s * A.stage_bytes, p_frame + bd.a0, (uint32_t)bd.bytes,
                            &full[p_s], pol);
       ++p_seq;
-      p_s = p_s + 1 == kDsStages ? 0 : p_s + 1;
+      p_s = p_s + 1 == A.nstages ? 0 : p_s + 1;
       if (++p_i == A.out_h) {
         p_i = 0;
         ++p_m;
@@ -225,7 +225,7 @@ dd_kernel(DsArgs A) {
       }
     };
     if (vt == 0)
-      while (p_seq < kDsStages && p_seq < total) issue();
+      while (p_seq < A.nstages && p_seq < total) issue();
 
     int i = 0, s = 0;
     uint32_t ph = 0;
@@ -267,7 +267,7 @@ dd_kernel(DsArgs A) {
       bar_sync(kBarV, kV);  // every V thread is done with stage s
       if (vt == 0 && p_seq < total) issue();
       bar_arrive(kBarFull0 + b, kDsThreads);
-      s = s + 1 == kDsStages ? 0 : s + 1;
+      s = s + 1 == A.nstages ? 0 : s + 1;
       if (s == 0) ph ^= 1u;
       if (++i == A.out_h) i = 0;
     }
@@ -406,7 +406,7 @@ __global__ void dd_state_update_kernel(const uint8_t* small, int64_t small_pitch
 }
 
 // ===================================================================== host
-static size_t ds_smem_bytes(const DsArgs& A, int* stage_bytes_out) {
+static size_t ds_smem_bytes(const DsArgs& A, int* stage_bytes_out, int* nstages_out) {
   int stage = 0;
   for (int i = 0; i < A.out_h; ++i) {
     const int r0 = (i * A.H) / A.out_h, r1 = ((i + 1) * A.H) / A.out_h;
@@ -418,14 +418,19 @@ static size_t ds_smem_bytes(const DsArgs& A, int* stage_bytes_out) {
   *stage_bytes_out = stage;
   const int gg = A.grid * A.grid;
   const int small_bytes = A.out_w * A.out_h * 3;
-  size_t b = (size_t)kDsStages * stage;
-  b += 2 * (size_t)A.RBp * sizeof(uint16_t);
+  size_t b = 2 * (size_t)A.RBp * sizeof(uint16_t);
   b += (size_t)A.out_h * sizeof(BandInfo);
-  b += (size_t)((small_bytes + 15) & ~15);
+  b += A.mode == 0 ? (size_t)((small_bytes + 15) & ~15) : 0;   // reference image (mode 0)
   b += 2 * (size_t)((gg + 1) & ~1) * 4;
   b += 2 * (size_t)gg * 8;
-  b += 8 * 8 + kDsStages * 8 + 16;
-  return b;
+  b += 8 * 8 + kDsMaxStages * 8 + 16;
+  // ring depth: as many bands as fit with 2 CTAs per SM (227 KB per SM minus the
+  // 1 KB per-CTA reservation), at least 2
+  const size_t per_cta = (227 * 1024) / 2 - 1024;
+  int ns = per_cta > b ? (int)((per_cta - b) / stage) : 0;
+  ns = std::max(2, std::min(kDsMaxStages, ns));
+  *nstages_out = ns;
+  return b + (size_t)ns * stage;
 }
 
 size_t dd_flags_bytes() { return (size_t)4 * kNumSMs * 4; }
@@ -465,7 +470,7 @@ noscope_status launch_diff_detect(const noscope_dd_config& cfg, const uint8_t* f
   A.done = flags;
   A.fast = (A.RB % 16) == 0;
   A.rlo = A.H / A.out_h;
-  const size_t smem = ds_smem_bytes(A, &A.stage_bytes);
+  const size_t smem = ds_smem_bytes(A, &A.stage_bytes, &A.nstages);
   const int64_t frames_needed = A.need.m1 - A.need.m0;
   if (frames_needed > 0) {
     static bool attr_set = false;
