@@ -1,27 +1,36 @@
 // dd.cu — frame downsampling + difference detector (§5),
 // one fused, warp-specialised pass over the source frames.
 //
-// dd_kernel (persistent, 2 CTAs/SM, 288 threads):
+// dd_kernel (persistent, normally 1 CTA/SM):
 //   * each CTA owns a CONTIGUOUS range of the frames that must be downsampled
 //     (checked frames, plus mode-1 anchors), one output row ("band") at a time;
 //   * a band = source rows [floor(iH/h), floor((i+1)H/h)) = one contiguous byte
-//     range of the frame, fetched by one cp.async.bulk (TMA 1-D engine) into a
-//     4-stage shared-memory ring (mbarrier completion, L2 evict-first: every
-//     source byte is read exactly once);
-//   * warps 0-3 ("V"): vertical byte-column sums of the band, SWAR with two
-//     16-bit lanes per 32-bit register (PRMT unpack, 16-byte smem vectors);
-//   * warps 4-8 ("H"): box means G = floor((2S+n)/2n) (O1, reading R-1) via a
-//     per-column magic reciprocal, the small-frame row store (CNN input), and
-//     the exact integer SSD against the anchor row — the reference image kept
-//     in smem (mode 0) or frame t-k (mode 1), which this same CTA wrote k
-//     frames earlier (it stays L2-resident) — accumulated per thread / per LR
-//     block; at frame end the fp64 score (O3) and the disposition (O4);
-//   * V and H hand over double-buffered column sums through named barriers,
-//     so the two halves of the work overlap band by band;
+//     range of the frame, fetched by one cp.async.bulk (TMA 1-D engine, L2
+//     evict-first: every source byte is read exactly once) into a shared-memory
+//     ring issued by one producer thread (warp 0);
+//   * bands are dealt round-robin to NG worker GROUPS (band i -> group i % NG),
+//     each with its own ring of stages (full/empty mbarriers), so groups work on
+//     different bands at once and no CTA-wide barrier sits on the path;
+//   * a group = NS worker warps, one per column SEGMENT of the output row (a run
+//     of output pixels and the source bytes under them).  A worker warp forms the
+//     vertical byte-column sums of its segment (SWAR, two 16-bit lanes per word,
+//     PRMT unpack of 16-byte smem vectors) into a warp-private buffer, releases
+//     the stage, then each lane owns one output value (pixel j, channel c): the
+//     box mean G = floor((2S+n)/2n) (O1, reading R-1) via an exact magic
+//     reciprocal, the small-frame store (CNN input) and the exact integer SSD
+//     against the anchor — the reference image in smem (mode 0) or frame t-k
+//     (mode 1), which the SAME lane wrote k frames earlier (program order, no
+//     fence) — accumulated per LR block (u64 smem atomics, once per block row);
+//   * warp 1 scores each frame when all workers have arrived on its frame
+//     barrier: fp64 block means, w_k*m_k and the fixed-order sum (O3), the
+//     disposition (O4); per-frame block sums are double-buffered by frame parity;
 //   * the few frames whose anchor lies in the previous CTA's range are scored
 //     after that CTA publishes its completion flag (no second kernel).
 // dd_state_update_kernel carries the last k small frames / labels of a chunk
 // into the caller's stream state.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -32,15 +41,13 @@ uint64_t& launch_counter() {
   return c;
 }
 
-constexpr int kV = 128;                 // vertical-sum group
-constexpr int kHz = 160;                // box-mean / score group (out_w*3 <= 160)
-constexpr int kDsThreads = kV + kHz;
-constexpr int kDsMaxStages = 8;          // band ring depth: as many as fit 2 CTAs/SM
-// named barrier ids (0 = __syncthreads)
-constexpr int kBarFull0 = 1, kBarEmpty0 = 3, kBarV = 5, kBarH = 6;
+constexpr int kDsMaxStages = 16;        // all groups' rings together
+constexpr int kDsMaxGroups = 5;
+constexpr int kDsMaxWorkers = 25;       // NG * NS worker warps
+constexpr int kDsMaxThreads = (2 + kDsMaxWorkers) * 32;
+constexpr int kBarEnd = 1;              // named barrier: all warps but the producer
 
 NS_DEV void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-NS_DEV void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 NS_DEV unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -53,7 +60,7 @@ NS_DEV void st_release_u32(unsigned* p, unsigned v) {
 struct DsArgs {
   const uint8_t* frames;
   int64_t frame_pitch;
-  int W, H, RB, RBp;  // RB = W*3 bytes per source row, RBp = RB rounded to 16
+  int W, H, RB;  // RB = W*3 bytes per source row
   int out_w, out_h;
   uint8_t* small;
   int64_t small_pitch;
@@ -70,7 +77,9 @@ struct DsArgs {
   uint8_t* disp;
   uint32_t* status;
   unsigned* done;  // [gridDim.x] completion flags, zeroed before launch (mode 1)
-  int stage_bytes, fast, rlo, nstages;
+  int stage_bytes, fast, rlo;
+  int ng, ns, nsg;  // worker groups, segments (warps) per group, ring stages per group
+  int cs_stride;    // u16 words of column sums per worker warp (multiple of 8)
 };
 
 struct BandInfo {   // per output row i
@@ -92,41 +101,74 @@ NS_DEV int64_t range_start(const NeededSet& s, int c, int G) {
   return s.m0 + ((s.m1 - s.m0) * (int64_t)c) / G;
 }
 
-struct HzState {  // per box-mean thread
-  int t, j, colbase, ncols, bj;
-  uint32_t mlo, mhi;
-  uint64_t total;
-  uint32_t blk;
-  int cur_bi;
+// Column segment of worker `seg` (host and device agree on this split): output
+// pixels [j0, j1), source bytes of a row [xb, xb + span) (xb 16-aligned on the
+// vector path; span a multiple of 16 there).
+struct Seg {
+  int j0, j1, xb, span;
 };
+__host__ __device__ inline Seg segment_of(int seg, int ns, int out_w, int W, bool fast) {
+  const int P = (out_w + ns - 1) / ns;
+  Seg g;
+  g.j0 = min(seg * P, out_w);
+  g.j1 = min(g.j0 + P, out_w);
+  const int xs = (int)(((int64_t)g.j0 * W) / out_w) * 3;
+  const int xe = (int)(((int64_t)g.j1 * W) / out_w) * 3;
+  if (fast) {
+    g.xb = xs & ~15;
+    g.span = ((xe + 15) & ~15) - g.xb;
+  } else {
+    g.xb = xs;
+    g.span = xe - xs;
+  }
+  if (g.j1 <= g.j0) g.span = 0;
+  return g;
+}
 
-// Frame-end scoring by the H group (all 160 threads call it).
-NS_DEV void finish_score(const DsArgs& A, HzState& h, int hz, uint32_t* blk, const uint32_t* blkn,
-                         const double* wlr, double* pk, unsigned long long* red, int64_t f,
-                         bool active) {
+// Per-frame role flags, identical in every role (O4 order).
+struct FrameCtx {
+  int64_t f, tau;
+  bool scoring, forced;
+  const uint8_t* anchor;  // mode 1: global frame t-k (small buffer or state ring)
+};
+NS_DEV FrameCtx frame_ctx(const DsArgs& A, int64_t m, int64_t tau_first) {
+  FrameCtx c;
+  c.f = frame_of(A.need, m);
+  c.tau = A.tau0 + c.f;
+  const bool checked = (c.tau % A.t_skip) == 0;
+  c.forced = A.mode == 1 && checked && c.tau < A.k;
+  c.scoring = checked && !c.forced;
+  c.anchor = nullptr;
+  if (c.scoring && A.mode == 1) {
+    const int64_t fa = c.f - A.k;
+    if (fa >= 0) {
+      c.anchor = A.small + fa * A.small_pitch;
+      if (c.tau - A.k < tau_first) c.scoring = false;  // anchor owned by another CTA: deferred
+    } else {
+      c.anchor = A.ring + ((c.tau - A.k) % A.k) * A.ring_pitch;
+    }
+  }
+  return c;
+}
+
+// Score of one frame from its per-block SSDs (one warp): O3, fixed order.
+NS_DEV void score_frame(const DsArgs& A, uint32_t* blk, const uint32_t* blkn,
+                        const double* wlr, double* pk, int64_t f, int lane) {
   if (A.metric == 0) {
-    unsigned long long v = active ? h.total : 0ull;
-    v = warp_sum(v);
-    if ((hz & 31) == 0) red[hz >> 5] = v;
-    bar_sync(kBarH, kHz);
-    if (hz == 0) {
-      unsigned long long s = 0;
-      for (int w = 0; w < kHz / 32; ++w) s += red[w];
-      const double sc = (double)s / (double)(A.out_w * A.out_h * 3);
+    if (lane == 0) {
+      const double sc = (double)blk[0] / (double)(A.out_w * A.out_h * 3);
+      blk[0] = 0u;
       A.score[f] = sc;
       A.disp[f] = sc > A.delta ? NOSCOPE_FIRED : NOSCOPE_SUPPRESSED;
     }
-    bar_sync(kBarH, kHz);  // red[] reuse
   } else {
     const int gg = A.grid * A.grid;
-    if (active && h.cur_bi >= 0 && h.blk) atomicAdd(&blk[h.cur_bi * A.grid + h.bj], h.blk);
-    bar_sync(kBarH, kHz);
-    for (int q = hz; q < gg; q += kHz) {
+    for (int q = lane; q < gg; q += 32) {
       pk[q] = __dmul_rn(wlr[q], (double)blk[q] / (double)blkn[q]);  // w_k * m_k, rounded
       blk[q] = 0u;
     }
-    bar_sync(kBarH, kHz);
-    if (hz == 0) {
+    __syncwarp();
+    if (lane == 0) {
       double z = (double)A.lr_b;
       for (int q = 0; q < gg; ++q) z = __dadd_rn(z, pk[q]);  // fixed order, no FMA
       if (z != z) atomicOr(A.status, 1u);
@@ -134,45 +176,103 @@ NS_DEV void finish_score(const DsArgs& A, HzState& h, int hz, uint32_t* blk, con
       A.disp[f] = z > A.delta ? NOSCOPE_FIRED : NOSCOPE_SUPPRESSED;
     }
   }
-  h.total = 0;
-  h.blk = 0;
-  h.cur_bi = -1;
+  __syncwarp();
 }
 
-NS_DEV void ssd_acc(const DsArgs& A, HzState& h, uint32_t d2, int bi, uint32_t* blk) {
-  if (A.metric == 0) {
-    h.total += d2;
-  } else {
-    if (bi != h.cur_bi) {
-      if (h.cur_bi >= 0 && h.blk) atomicAdd(&blk[h.cur_bi * A.grid + h.bj], h.blk);
-      h.cur_bi = bi;
-      h.blk = 0;
-    }
-    h.blk += d2;
+// Warp-wide flush of the lanes' block-row SSDs: one reduction + one u32 smem atomic
+// per LR block column the warp covers (bi is warp-uniform: all lanes are on one band).
+NS_DEV void flush_blocks(uint32_t* b, int bi, int grid, int bj, int bj_lo, int bj_hi, uint32_t acc,
+                         int lane) {
+  for (int q = bj_lo; q <= bj_hi; ++q) {
+    const uint32_t v = __reduce_add_sync(0xffffffffu, bj == q ? acc : 0u);
+    if (lane == 0 && v) atomicAdd(&b[bi * grid + q], v);
   }
 }
 
-__global__ void __launch_bounds__(kDsThreads, 2)
+// Vertical byte-column sums of one band (fast path), SWAR: two 16-bit lanes per
+// word (PRMT unpack), two source rows folded per IADD3.  RLO > 0: rows = RLO or
+// RLO + 1 (compile-time unrolled); STRIDE16 > 0: compile-time row stride in uint4.
+template <int RLO, int STRIDE16>
+NS_DEV void vsum(const uint4* p, int nrows, int stride16, uint32_t (&l)[4], uint32_t (&h)[4]) {
+  const int st = STRIDE16 > 0 ? STRIDE16 : stride16;
+#define NS_ACC1(V_)                                                                   \
+  l[0] += __byte_perm(V_.x, 0u, 0x4240); h[0] += __byte_perm(V_.x, 0u, 0x4341);        \
+  l[1] += __byte_perm(V_.y, 0u, 0x4240); h[1] += __byte_perm(V_.y, 0u, 0x4341);        \
+  l[2] += __byte_perm(V_.z, 0u, 0x4240); h[2] += __byte_perm(V_.z, 0u, 0x4341);        \
+  l[3] += __byte_perm(V_.w, 0u, 0x4240); h[3] += __byte_perm(V_.w, 0u, 0x4341);
+#define NS_ACC2(P_, Q_)                                                                        \
+  l[0] += __byte_perm(P_.x, 0u, 0x4240) + __byte_perm(Q_.x, 0u, 0x4240);                       \
+  h[0] += __byte_perm(P_.x, 0u, 0x4341) + __byte_perm(Q_.x, 0u, 0x4341);                       \
+  l[1] += __byte_perm(P_.y, 0u, 0x4240) + __byte_perm(Q_.y, 0u, 0x4240);                       \
+  h[1] += __byte_perm(P_.y, 0u, 0x4341) + __byte_perm(Q_.y, 0u, 0x4341);                       \
+  l[2] += __byte_perm(P_.z, 0u, 0x4240) + __byte_perm(Q_.z, 0u, 0x4240);                       \
+  h[2] += __byte_perm(P_.z, 0u, 0x4341) + __byte_perm(Q_.z, 0u, 0x4341);                       \
+  l[3] += __byte_perm(P_.w, 0u, 0x4240) + __byte_perm(Q_.w, 0u, 0x4240);                       \
+  h[3] += __byte_perm(P_.w, 0u, 0x4341) + __byte_perm(Q_.w, 0u, 0x4341);
+  if (RLO > 0) {
+#pragma unroll
+    for (int r = 0; r + 1 < RLO; r += 2) {
+      const uint4 a = p[r * st], b = p[(r + 1) * st];
+      NS_ACC2(a, b)
+    }
+    if (RLO & 1) {
+      const uint4 a = p[(RLO - 1) * st];
+      if (nrows > RLO) {
+        const uint4 b = p[RLO * st];
+        NS_ACC2(a, b)
+      } else {
+        NS_ACC1(a)
+      }
+    } else if (nrows > RLO) {
+      const uint4 a = p[RLO * st];
+      NS_ACC1(a)
+    }
+  } else {
+    int r = 0;
+    for (; r + 1 < nrows; r += 2) {
+      const uint4 a = p[r * st], b = p[(r + 1) * st];
+      NS_ACC2(a, b)
+    }
+    if (r < nrows) {
+      const uint4 a = p[r * st];
+      NS_ACC1(a)
+    }
+  }
+#undef NS_ACC1
+#undef NS_ACC2
+}
+
+// RLO / CLO > 0: the band height / box width is RLO or RLO+1 rows / CLO or CLO+1
+// pixels (compile-time unrolled loops); STRIDE16 > 0: source row stride in uint4.
+// <0, 0, 0> is the generic kernel.
+template <int RLO, int CLO, int STRIDE16>
+__global__ void __launch_bounds__(kDsMaxThreads, 1)
 dd_kernel(DsArgs A) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int gg = A.grid * A.grid;
+  const int gg2 = (gg + 1) & ~1;
   const int small_bytes = A.out_w * A.out_h * 3;
+  const int n_out = A.out_w * 3;
+  const int nstages = A.ng * A.nsg;
+  const int nworkers = A.ng * A.ns;
   uint8_t* stages = smem;
-  uint16_t* cs = reinterpret_cast<uint16_t*>(smem + A.nstages * A.stage_bytes);   // 2 x RBp
-  BandInfo* band = reinterpret_cast<BandInfo*>(cs + 2 * A.RBp);
+  uint16_t* csbuf = reinterpret_cast<uint16_t*>(smem + (size_t)nstages * A.stage_bytes);
+  uint32_t* blk = reinterpret_cast<uint32_t*>(csbuf + (size_t)nworkers * A.cs_stride);
+  double* wlr = reinterpret_cast<double*>(blk + 2 * gg2);  // gg2 even: 8-byte aligned
+  double* pk = wlr + gg2;
+  uint64_t* full = reinterpret_cast<uint64_t*>(pk + gg2);
+  uint64_t* empty = full + kDsMaxStages;
+  uint64_t* fdone = empty + kDsMaxStages;   // [2] all workers finished frame m (parity m & 1)
+  uint64_t* bfree = fdone + 2;              // [2] scorer released the block sums of frame m
+  uint32_t* blkn = reinterpret_cast<uint32_t*>(bfree + 2);
+  BandInfo* band = reinterpret_cast<BandInfo*>(blkn + gg2);
   uint8_t* ref_s = reinterpret_cast<uint8_t*>(band + A.out_h);
-  uint32_t* blk = reinterpret_cast<uint32_t*>(ref_s + (A.mode == 0 ? ((small_bytes + 15) & ~15) : 0));
-  uint32_t* blkn = blk + ((gg + 1) & ~1);
-  double* wlr = reinterpret_cast<double*>(blkn + ((gg + 1) & ~1));
-  double* pk = wlr + gg;
-  unsigned long long* red = reinterpret_cast<unsigned long long*>(pk + gg);
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + 8);
 
   const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int64_t mA = range_start(A.need, blockIdx.x, gridDim.x);
   const int64_t mB = range_start(A.need, blockIdx.x + 1, gridDim.x);
   const int64_t my_frames = mB - mA;
-  const int64_t total = my_frames * A.out_h;
 
   // ---- one-time tables
   for (int i = tid; i < A.out_h; i += blockDim.x) {
@@ -186,178 +286,192 @@ dd_kernel(DsArgs A) {
   }
   if (A.mode == 0)
     for (int t = tid; t < small_bytes; t += blockDim.x) ref_s[t] = A.ref[t];
+  for (int q = tid; q < 2 * gg2; q += blockDim.x) blk[q] = 0u;
   if (A.metric == 1) {
     const int sh = A.out_h / A.grid, sw = A.out_w / A.grid;
     for (int q = tid; q < gg; q += blockDim.x) {
       const int bi = q / A.grid, bj = q % A.grid;
       const int rows = bi < A.grid - 1 ? sh : A.out_h - (A.grid - 1) * sh;
       const int cols = bj < A.grid - 1 ? sw : A.out_w - (A.grid - 1) * sw;
-      blk[q] = 0u;
       blkn[q] = (uint32_t)(rows * cols * 3);
       wlr[q] = (double)A.lr_w[q];
     }
   }
   if (tid == 0) {
-    for (int s = 0; s < A.nstages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < nstages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], (uint32_t)A.ns);
+    }
+    for (int p = 0; p < 2; ++p) {
+      mbar_init(&fdone[p], (uint32_t)nworkers);
+      mbar_init(&bfree[p], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
+  const int64_t tau_first = my_frames > 0 ? A.tau0 + frame_of(A.need, mA) : 0;
 
-  if (tid < kV) {
-    // =========================================================== V group
-    const int vt = tid;
-    // producer (vt == 0): issue bands ahead into the ring
-    int64_t p_seq = 0, p_m = mA;
-    int p_i = 0, p_s = 0;
+  if (warp == 0) {
+    // ======================================================= producer
+    if (lane != 0) return;
     const uint64_t pol = policy_evict_first();
-    const uint8_t* p_frame = A.frames + frame_of(A.need, p_m) * A.frame_pitch;
-    auto issue = [&]() {
-      const BandInfo bd = band[p_i];
-      mbar_arrive_expect_tx(&full[p_s], (uint32_t)bd.bytes);
-      bulk_g2s_evict_first(stages + (size_t)p_s * A.stage_bytes, p_frame + bd.a0, (uint32_t)bd.bytes,
-                           &full[p_s], pol);
-      ++p_seq;
-      p_s = p_s + 1 == A.nstages ? 0 : p_s + 1;
-      if (++p_i == A.out_h) {
-        p_i = 0;
-        ++p_m;
-        if (p_m < mB) p_frame = A.frames + frame_of(A.need, p_m) * A.frame_pitch;
-      }
-    };
-    if (vt == 0)
-      while (p_seq < A.nstages && p_seq < total) issue();
-
-    int i = 0, s = 0;
-    uint32_t ph = 0;
-    const int RB16 = A.RB >> 4;
-    for (int64_t seq = 0; seq < total; ++seq) {
-      const int b = (int)(seq & 1);
-      if (seq >= 2) bar_sync(kBarEmpty0 + b, kDsThreads);
-      mbar_wait(&full[s], ph);
-      const int offrows = band[i].offrows;
-      const int nrows = offrows & 0xFFFF, off = offrows >> 16;
-      const uint8_t* src = stages + (size_t)s * A.stage_bytes + off;
-      uint16_t* dst = cs + b * A.RBp;
-      if (A.fast) {
-        for (int u = vt; u < RB16; u += kV) {
-          const uint4* p = reinterpret_cast<const uint4*>(src) + u;
-          uint32_t l0 = 0, h0 = 0, l1 = 0, h1 = 0, l2 = 0, h2 = 0, l3 = 0, h3 = 0;
-          for (int r = 0; r < nrows; ++r) {
-            const uint4 w = p[(size_t)r * RB16];
-            l0 += __byte_perm(w.x, 0u, 0x4240); h0 += __byte_perm(w.x, 0u, 0x4341);
-            l1 += __byte_perm(w.y, 0u, 0x4240); h1 += __byte_perm(w.y, 0u, 0x4341);
-            l2 += __byte_perm(w.z, 0u, 0x4240); h2 += __byte_perm(w.z, 0u, 0x4341);
-            l3 += __byte_perm(w.w, 0u, 0x4240); h3 += __byte_perm(w.w, 0u, 0x4341);
-          }
-          uint4 o0, o1;
-          o0.x = (l0 & 0xFFFFu) | (h0 << 16); o0.y = (l0 >> 16) | (h0 & 0xFFFF0000u);
-          o0.z = (l1 & 0xFFFFu) | (h1 << 16); o0.w = (l1 >> 16) | (h1 & 0xFFFF0000u);
-          o1.x = (l2 & 0xFFFFu) | (h2 << 16); o1.y = (l2 >> 16) | (h2 & 0xFFFF0000u);
-          o1.z = (l3 & 0xFFFFu) | (h3 << 16); o1.w = (l3 >> 16) | (h3 & 0xFFFF0000u);
-          reinterpret_cast<uint4*>(dst)[2 * u] = o0;
-          reinterpret_cast<uint4*>(dst)[2 * u + 1] = o1;
+    int gs[kDsMaxGroups] = {};
+    uint32_t gph[kDsMaxGroups] = {};
+    int64_t issued[kDsMaxGroups] = {};
+    for (int64_t m = mA; m < mB; ++m) {
+      const uint8_t* fr = A.frames + frame_of(A.need, m) * A.frame_pitch;
+      int g = 0;
+      for (int i = 0; i < A.out_h; ++i) {
+        const BandInfo bd = band[i];
+        const int st = g * A.nsg + gs[g];
+        if (issued[g] >= A.nsg) mbar_wait(&empty[st], gph[g] ^ 1u);
+        mbar_arrive_expect_tx(&full[st], (uint32_t)bd.bytes);
+        bulk_g2s_evict_first(stages + (size_t)st * A.stage_bytes, fr + bd.a0, (uint32_t)bd.bytes,
+                             &full[st], pol);
+        ++issued[g];
+        if (++gs[g] == A.nsg) {
+          gs[g] = 0;
+          gph[g] ^= 1u;
         }
-      } else {
-        for (int x = vt; x < A.RB; x += kV) {
-          uint32_t sum = 0;
-          for (int r = 0; r < nrows; ++r) sum += src[(size_t)r * A.RB + x];
-          dst[x] = (uint16_t)sum;
-        }
+        if (++g == A.ng) g = 0;
       }
-      bar_sync(kBarV, kV);  // every V thread is done with stage s
-      if (vt == 0 && p_seq < total) issue();
-      bar_arrive(kBarFull0 + b, kDsThreads);
-      s = s + 1 == A.nstages ? 0 : s + 1;
-      if (s == 0) ph ^= 1u;
-      if (++i == A.out_h) i = 0;
     }
-    for (int64_t seq = total > 2 ? total - 2 : 0; seq < total; ++seq)
-      bar_sync(kBarEmpty0 + (int)(seq & 1), kDsThreads);  // drain the last EMPTY arrivals
     return;
   }
 
-  // ============================================================== H group
-  const int hz = tid - kV;
-  const int n_out = A.out_w * 3;
-  const bool active = hz < n_out;
-  HzState h{};
-  h.t = hz;
-  h.j = hz / 3;
-  h.cur_bi = -1;
-  if (active) {
-    const int c = hz - 3 * h.j;
-    const int q0 = (h.j * A.W) / A.out_w, q1 = ((h.j + 1) * A.W) / A.out_w;
-    h.colbase = q0 * 3 + c;
-    h.ncols = q1 - q0;
-    // magic reciprocals of 2n for the two possible band heights (rlo, rlo+1)
-    const uint32_t n_lo = (uint32_t)(A.rlo * h.ncols), n_hi = (uint32_t)((A.rlo + 1) * h.ncols);
-    h.mlo = (uint32_t)(0x100000000ull / (2ull * n_lo)) + 1u;
-    h.mhi = (uint32_t)(0x100000000ull / (2ull * n_hi)) + 1u;
-    h.bj = A.metric == 1 ? block_of(h.j, A.out_w, A.grid) : 0;
-  }
-  const int64_t tau_first = my_frames > 0 ? A.tau0 + frame_of(A.need, mA) : 0;
-
-  int i = 0;
-  int64_t m = mA;
-  int64_t f = 0, tau = 0;
-  bool checked = false, scoring = false, forced = false;
-  const uint8_t* anchor = nullptr;
-  uint8_t* dstf = nullptr;
-  for (int64_t seq = 0; seq < total; ++seq) {
-    if (i == 0) {  // frame start
-      f = frame_of(A.need, m);
-      tau = A.tau0 + f;
-      checked = (tau % A.t_skip) == 0;
-      forced = A.mode == 1 && checked && tau < A.k;
-      scoring = checked && !forced;
-      if (scoring && A.mode == 1) {
-        const int64_t fa = f - A.k;
-        if (fa >= 0) {
-          anchor = A.small + fa * A.small_pitch;
-          if (tau - A.k < tau_first) scoring = false;  // anchor owned by another CTA: deferred
-        } else {
-          anchor = A.ring + ((tau - A.k) % A.k) * A.ring_pitch;
-        }
-      } else if (A.mode == 0) {
-        anchor = ref_s;
+  if (warp == 1) {
+    // ========================================================= scorer
+    for (int64_t m = mA; m < mB; ++m) {
+      const int64_t lm = m - mA;
+      mbar_wait(&fdone[lm & 1], (uint32_t)((lm >> 1) & 1));
+      const FrameCtx c = frame_ctx(A, m, tau_first);
+      uint32_t* b = blk + (lm & 1) * gg2;
+      if (c.scoring) {
+        score_frame(A, b, blkn, wlr, pk, c.f, lane);
+      } else if (c.forced && lane == 0) {
+        A.score[c.f] = __longlong_as_double(0x7FF0000000000000ll);  // +inf
+        A.disp[c.f] = NOSCOPE_FIRED;
       }
-      dstf = A.small + f * A.small_pitch;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bfree[lm & 1]);
     }
-    const int b = (int)(seq & 1);
-    bar_sync(kBarFull0 + b, kDsThreads);
+  } else {
+    // ========================================================= workers
+    const int wk = warp - 2;
+    const int grp = wk / A.ns, seg = wk % A.ns;
+    const Seg sg = segment_of(seg, A.ns, A.out_w, A.W, A.fast != 0);
+    uint16_t* csw = csbuf + (size_t)wk * A.cs_stride;
+    const int nout = (sg.j1 - sg.j0) * 3;
+    const bool active = lane < nout;
+    const int tg = sg.j0 * 3 + lane;  // output value (row-local index) owned by this lane
+    int colbase = 0, ncols = 0, bj = 0;
+    uint32_t mlo = 0, mhi = 0;
     if (active) {
-      const BandInfo bd = band[i];
-      const int nrows = bd.offrows & 0xFFFF;
-      uint32_t av = 0;
-      if (scoring) av = anchor[i * n_out + h.t];
-      const uint16_t* c0 = cs + b * A.RBp + h.colbase;
-      uint32_t S = 0;
-      for (int q = 0; q < h.ncols; ++q) S += c0[3 * q];
-      const uint32_t n = (uint32_t)nrows * (uint32_t)h.ncols;
-      const uint32_t G = __umulhi(2u * S + n, nrows == A.rlo ? h.mlo : h.mhi);
-      dstf[i * n_out + h.t] = (uint8_t)G;
-      if (scoring) {
-        const int d = (int)G - (int)av;
-        ssd_acc(A, h, (uint32_t)(d * d), bd.bi, blk);
-      }
+      const int j = tg / 3, c = tg - 3 * j;
+      const int q0 = (int)(((int64_t)j * A.W) / A.out_w), q1 = (int)(((int64_t)(j + 1) * A.W) / A.out_w);
+      colbase = q0 * 3 + c - sg.xb;
+      ncols = q1 - q0;
+      // magic reciprocals of 2n for the two possible band heights (rlo, rlo+1)
+      const uint32_t n_lo = (uint32_t)(A.rlo * ncols), n_hi = (uint32_t)((A.rlo + 1) * ncols);
+      mlo = (uint32_t)(0x100000000ull / (2ull * n_lo)) + 1u;
+      mhi = (uint32_t)(0x100000000ull / (2ull * n_hi)) + 1u;
+      bj = A.metric == 1 ? block_of(j, A.out_w, A.grid) : 0;
     }
-    bar_arrive(kBarEmpty0 + b, kDsThreads);
-    if (++i == A.out_h) {  // frame end
-      i = 0;
-      if (scoring) {
-        finish_score(A, h, hz, blk, blkn, wlr, pk, red, f, active);
-      } else if (forced && hz == 0) {
-        A.score[f] = __longlong_as_double(0x7FF0000000000000ll);  // +inf
-        A.disp[f] = NOSCOPE_FIRED;
+    // LR block columns this warp covers (warp-uniform)
+    const int bj_lo = A.metric == 1 && sg.j1 > sg.j0 ? block_of(sg.j0, A.out_w, A.grid) : 0;
+    const int bj_hi = A.metric == 1 && sg.j1 > sg.j0 ? block_of(sg.j1 - 1, A.out_w, A.grid) : 0;
+    const int nvec = sg.span >> 4;
+    const int RB16 = A.RB >> 4;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t m = mA; m < mB; ++m) {
+      const int64_t lm = m - mA;
+      const FrameCtx c = frame_ctx(A, m, tau_first);
+      const uint8_t* anchor = A.mode == 0 ? ref_s : c.anchor;
+      uint8_t* dstf = A.small + c.f * A.small_pitch;
+      if (lm >= 2) mbar_wait(&bfree[lm & 1], (uint32_t)(((lm >> 1) - 1) & 1));
+      uint32_t* b = blk + (lm & 1) * gg2;
+      uint32_t acc = 0u;
+      int cur_bi = -1;
+      // anchor values are fetched one band ahead (t-k frames come from L2)
+      uint32_t av_next = (c.scoring && active && grp < A.out_h) ? anchor[grp * n_out + tg] : 0u;
+      for (int i = grp; i < A.out_h; i += A.ng) {
+        const uint32_t av = av_next;
+        if (c.scoring && active && i + A.ng < A.out_h) av_next = anchor[(i + A.ng) * n_out + tg];
+        const int offrows = band[i].offrows;
+        const int nrows = offrows & 0xFFFF, off = offrows >> 16;
+        const uint8_t* src = stages + (size_t)(grp * A.nsg + s) * A.stage_bytes + off;
+        mbar_wait(&full[grp * A.nsg + s], ph);
+        if (A.fast) {
+          const uint4* p0 = reinterpret_cast<const uint4*>(src + sg.xb);
+          for (int u = lane; u < nvec; u += 32) {
+            uint32_t l[4] = {0u, 0u, 0u, 0u}, h[4] = {0u, 0u, 0u, 0u};
+            vsum<RLO, STRIDE16>(p0 + u, nrows, RB16, l, h);
+            const uint32_t l0 = l[0], l1 = l[1], l2 = l[2], l3 = l[3];
+            const uint32_t h0 = h[0], h1 = h[1], h2 = h[2], h3 = h[3];
+            uint4 o0, o1;
+            o0.x = (l0 & 0xFFFFu) | (h0 << 16); o0.y = (l0 >> 16) | (h0 & 0xFFFF0000u);
+            o0.z = (l1 & 0xFFFFu) | (h1 << 16); o0.w = (l1 >> 16) | (h1 & 0xFFFF0000u);
+            o1.x = (l2 & 0xFFFFu) | (h2 << 16); o1.y = (l2 >> 16) | (h2 & 0xFFFF0000u);
+            o1.z = (l3 & 0xFFFFu) | (h3 << 16); o1.w = (l3 >> 16) | (h3 & 0xFFFF0000u);
+            reinterpret_cast<uint4*>(csw)[2 * u] = o0;
+            reinterpret_cast<uint4*>(csw)[2 * u + 1] = o1;
+          }
+        } else {
+          const uint8_t* p0 = src + sg.xb;
+          for (int x = lane; x < sg.span; x += 32) {
+            uint32_t sum = 0;
+            for (int r = 0; r < nrows; ++r) sum += p0[(size_t)r * A.RB + x];
+            csw[x] = (uint16_t)sum;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[grp * A.nsg + s]);  // stage consumed
+        if (++s == A.nsg) {
+          s = 0;
+          ph ^= 1u;
+        }
+        uint32_t dd2 = 0u;
+        if (active) {
+          const uint16_t* c0 = csw + colbase;
+          uint32_t S = 0;
+          if (CLO > 0) {
+#pragma unroll
+            for (int q = 0; q < CLO; ++q) S += c0[3 * q];
+            if (ncols > CLO) S += c0[3 * CLO];
+          } else {
+#pragma unroll 4
+            for (int q = 0; q < ncols; ++q) S += c0[3 * q];
+          }
+          const uint32_t n = (uint32_t)nrows * (uint32_t)ncols;
+          const uint32_t G = __umulhi(2u * S + n, nrows == A.rlo ? mlo : mhi);
+          dstf[i * n_out + tg] = (uint8_t)G;
+          const int d = (int)G - (int)av;
+          dd2 = (uint32_t)(d * d);
+        }
+        if (c.scoring) {  // warp-uniform
+          const int bi = band[i].bi;
+          if (bi != cur_bi) {
+            if (cur_bi >= 0) flush_blocks(b, cur_bi, A.grid, bj, bj_lo, bj_hi, acc, lane);
+            cur_bi = bi;
+            acc = 0u;
+          }
+          acc += dd2;
+        }
+        __syncwarp();  // csw reuse by the next band
       }
-      ++m;
+      if (cur_bi >= 0) flush_blocks(b, cur_bi, A.grid, bj, bj_lo, bj_hi, acc, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&fdone[lm & 1]);
     }
   }
 
   // ---- publish completion, then score deferred frames (mode 1 only)
   if (A.mode != 1) return;
-  bar_sync(kBarH, kHz);
-  if (hz == 0) {
+  const int nthr = blockDim.x - 32;  // every warp but the producer
+  const int et = tid - 32;
+  bar_sync(kBarEnd, nthr);
+  if (et == 0) {
     __threadfence();
     st_release_u32(&A.done[blockIdx.x], 1u);
   }
@@ -367,21 +481,41 @@ dd_kernel(DsArgs A) {
     if (tt - A.k >= tau_first) break;
     if ((tt % A.t_skip) != 0 || tt < A.k || ff - A.k < 0) continue;
     const int64_t fa = ff - A.k;
-    if (hz == 0) {  // wait for the CTA owning the anchor frame
+    if (et == 0) {  // wait for the CTA owning the anchor frame
       int c = (int)blockIdx.x - 1;
       while (c > 0 && frame_of(A.need, range_start(A.need, c, gridDim.x)) > fa) --c;
       while (ld_acquire_u32(&A.done[c]) == 0u) {
       }
     }
-    bar_sync(kBarH, kHz);
-    const uint8_t* G = A.small + ff * A.small_pitch;
-    const uint8_t* An = A.small + fa * A.small_pitch;
-    if (active)
-      for (int r = 0; r < A.out_h; ++r) {
-        const int d = (int)G[r * n_out + h.t] - (int)An[r * n_out + h.t];
-        ssd_acc(A, h, (uint32_t)(d * d), band[r].bi, blk);
+    bar_sync(kBarEnd, nthr);
+    if (warp >= 2) {  // same lane -> output mapping as the main loop; few atomics
+      const int wk = warp - 2;
+      const int grp = wk / A.ns;
+      const Seg sg = segment_of(wk % A.ns, A.ns, A.out_w, A.W, A.fast != 0);
+      const int tg = sg.j0 * 3 + lane;
+      const bool act = lane < (sg.j1 - sg.j0) * 3;
+      const int bj = A.metric == 1 && act ? block_of(tg / 3, A.out_w, A.grid) : 0;
+      const int bj_lo = A.metric == 1 && sg.j1 > sg.j0 ? block_of(sg.j0, A.out_w, A.grid) : 0;
+      const int bj_hi = A.metric == 1 && sg.j1 > sg.j0 ? block_of(sg.j1 - 1, A.out_w, A.grid) : 0;
+      const uint8_t* G = A.small + ff * A.small_pitch;
+      const uint8_t* An = A.small + fa * A.small_pitch;
+      uint32_t acc = 0u;
+      int cur_bi = -1;
+      for (int i = grp; i < A.out_h; i += A.ng) {
+        const int d = act ? (int)G[i * n_out + tg] - (int)An[i * n_out + tg] : 0;
+        const int bi = band[i].bi;
+        if (bi != cur_bi) {
+          if (cur_bi >= 0) flush_blocks(blk, cur_bi, A.grid, bj, bj_lo, bj_hi, acc, lane);
+          cur_bi = bi;
+          acc = 0u;
+        }
+        acc += (uint32_t)(d * d);
       }
-    finish_score(A, h, hz, blk, blkn, wlr, pk, red, ff, active);
+      if (cur_bi >= 0) flush_blocks(blk, cur_bi, A.grid, bj, bj_lo, bj_hi, acc, lane);
+    }
+    bar_sync(kBarEnd, nthr);
+    if (warp == 1) score_frame(A, blk, blkn, wlr, pk, ff, lane);
+    bar_sync(kBarEnd, nthr);
   }
 }
 
@@ -406,7 +540,9 @@ __global__ void dd_state_update_kernel(const uint8_t* small, int64_t small_pitch
 }
 
 // ===================================================================== host
-static size_t ds_smem_bytes(const DsArgs& A, int* stage_bytes_out, int* nstages_out) {
+// Launch geometry of dd_kernel: band stage size, worker groups (NG) x column
+// segments (NS), ring stages per group, per-warp column-sum words, dynamic smem.
+static size_t ds_plan(DsArgs& A, int ctas_per_sm) {
   int stage = 0;
   for (int i = 0; i < A.out_h; ++i) {
     const int r0 = (i * A.H) / A.out_h, r1 = ((i + 1) * A.H) / A.out_h;
@@ -414,23 +550,29 @@ static size_t ds_smem_bytes(const DsArgs& A, int* stage_bytes_out, int* nstages_
     const int64_t a0 = b0 & ~15ll, a1 = (b1 + 15) & ~15ll;
     if ((int)(a1 - a0) > stage) stage = (int)(a1 - a0);
   }
-  stage = (stage + 127) & ~127;
-  *stage_bytes_out = stage;
-  const int gg = A.grid * A.grid;
+  A.stage_bytes = (stage + 127) & ~127;
+  // segments of <= 10 output pixels (<= 30 lanes own one output value each)
+  A.ns = std::max(1, (A.out_w + 9) / 10);
+  int ng = 4;  // 4 bands in flight per CTA (A/B on B200: 2 -> 17.3 ms, 3 -> 15.8, 4 -> 15.0, 5 -> 15.2)
+  if (const char* e = std::getenv("NOSCOPE_DD_NG")) ng = std::atoi(e);
+  ng = std::max(1, std::min({ng, kDsMaxGroups, A.out_h, kDsMaxWorkers / A.ns}));
+  A.ng = ng;
+  int cs = 0;
+  for (int g = 0; g < A.ns; ++g) cs = std::max(cs, segment_of(g, A.ns, A.out_w, A.W, A.fast != 0).span);
+  A.cs_stride = (cs + 7) & ~7;
+  const int gg2 = ((A.grid * A.grid) + 1) & ~1;
   const int small_bytes = A.out_w * A.out_h * 3;
-  size_t b = 2 * (size_t)A.RBp * sizeof(uint16_t);
-  b += (size_t)A.out_h * sizeof(BandInfo);
+  size_t b = (size_t)A.ng * A.ns * A.cs_stride * sizeof(uint16_t);
+  b += 2 * (size_t)gg2 * 8 + 2 * (size_t)gg2 * 8;      // blk[2], wlr, pk
+  b += (2 * kDsMaxStages + 4) * 8;                      // mbarriers
+  b += (size_t)gg2 * 4 + (size_t)A.out_h * sizeof(BandInfo);
   b += A.mode == 0 ? (size_t)((small_bytes + 15) & ~15) : 0;   // reference image (mode 0)
-  b += 2 * (size_t)((gg + 1) & ~1) * 4;
-  b += 2 * (size_t)gg * 8;
-  b += 8 * 8 + kDsMaxStages * 8 + 16;
-  // ring depth: as many bands as fit with 2 CTAs per SM (227 KB per SM minus the
-  // 1 KB per-CTA reservation), at least 2
-  const size_t per_cta = (227 * 1024) / 2 - 1024;
-  int ns = per_cta > b ? (int)((per_cta - b) / stage) : 0;
-  ns = std::max(2, std::min(kDsMaxStages, ns));
-  *nstages_out = ns;
-  return b + (size_t)ns * stage;
+  // ring: as many stages per group as fit (227 KB per SM less the 1 KB per-CTA reservation)
+  const size_t per_cta = (size_t)(227 * 1024) / ctas_per_sm - 1024;
+  int nsg = per_cta > b ? (int)((per_cta - b) / ((size_t)A.ng * A.stage_bytes)) : 0;
+  nsg = std::min(nsg, kDsMaxStages / A.ng);
+  A.nsg = nsg;
+  return b + (size_t)A.ng * nsg * A.stage_bytes;
 }
 
 size_t dd_flags_bytes() { return (size_t)4 * kNumSMs * 4; }
@@ -446,7 +588,6 @@ noscope_status launch_diff_detect(const noscope_dd_config& cfg, const uint8_t* f
   A.W = desc.width;
   A.H = desc.height;
   A.RB = desc.width * 3;
-  A.RBp = (A.RB + 15) & ~15;
   A.out_w = cfg.out_w;
   A.out_h = cfg.out_h;
   A.small = small;
@@ -470,24 +611,36 @@ noscope_status launch_diff_detect(const noscope_dd_config& cfg, const uint8_t* f
   A.done = flags;
   A.fast = (A.RB % 16) == 0;
   A.rlo = A.H / A.out_h;
-  const size_t smem = ds_smem_bytes(A, &A.stage_bytes, &A.nstages);
+  // per-block / per-frame SSDs are u32 (255^2 per output value)
+  if ((int64_t)A.out_w * A.out_h * 3 * 65025 >= ((int64_t)1 << 32)) return NOSCOPE_SHAPE;
+  int cps = 1;  // CTAs per SM (timing experiments: NOSCOPE_DD_CPS)
+  if (const char* e = std::getenv("NOSCOPE_DD_CPS")) cps = std::max(1, std::min(4, std::atoi(e)));
+  size_t smem = ds_plan(A, cps);
+  while (A.nsg < 2 && cps > 1) smem = ds_plan(A, --cps);
+  if (A.nsg < 2) return NOSCOPE_SHAPE;
+  const int threads = (2 + A.ng * A.ns) * 32;
+  // compile-time geometry for the 640x480 -> 50x50 webcam stream (bands of 9/10 rows,
+  // boxes of 12/13 pixels, 1,920-byte rows); everything else takes the generic kernel
+  void (*kern)(DsArgs) = dd_kernel<0, 0, 0>;
+  if (A.fast && A.rlo == 9 && A.W / A.out_w == 12 && A.RB == 1920) kern = dd_kernel<9, 12, 120>;
   const int64_t frames_needed = A.need.m1 - A.need.m0;
   if (frames_needed > 0) {
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(dd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      attr_set = true;
+    static bool attr_set[2] = {false, false};
+    const int ki = kern == dd_kernel<0, 0, 0> ? 0 : 1;
+    if (!attr_set[ki]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      attr_set[ki] = true;
     }
     int per_sm = 0;
-    NS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dd_kernel, kDsThreads, smem));
+    NS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
     if (per_sm < 1) return NOSCOPE_SHAPE;
     int sms = kNumSMs, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // all CTAs co-resident (deferred scoring waits on earlier CTAs' flags)
-    const int grid = (int)std::min<int64_t>(frames_needed, (int64_t)std::min(per_sm, 4) * sms);
+    const int grid = (int)std::min<int64_t>(frames_needed, (int64_t)std::min(per_sm, cps) * sms);
     if (cfg.mode == 1) NS_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)grid * 4, st));
-    dd_kernel<<<grid, kDsThreads, smem, st>>>(A);
+    kern<<<grid, threads, smem, st>>>(A);
     NS_LAUNCH_CHECK();
     count_launch();
   }
