@@ -501,15 +501,27 @@ dd_kernel(DsArgs A) {
       const uint8_t* An = A.small + fa * A.small_pitch;
       uint32_t acc = 0u;
       int cur_bi = -1;
-      for (int i = grp; i < A.out_h; i += A.ng) {
-        const int d = act ? (int)G[i * n_out + tg] - (int)An[i * n_out + tg] : 0;
-        const int bi = band[i].bi;
-        if (bi != cur_bi) {
-          if (cur_bi >= 0) flush_blocks(blk, cur_bi, A.grid, bj, bj_lo, bj_hi, acc, lane);
-          cur_bi = bi;
-          acc = 0u;
+      constexpr int kB = 8;  // rows loaded per batch (L2 latency overlapped)
+      for (int i0 = grp; i0 < A.out_h; i0 += kB * A.ng) {
+        int dv[kB];
+#pragma unroll
+        for (int t = 0; t < kB; ++t) {
+          const int i = i0 + t * A.ng;
+          dv[t] = act && i < A.out_h ? (int)G[i * n_out + tg] - (int)An[i * n_out + tg] : 0;
         }
-        acc += (uint32_t)(d * d);
+#pragma unroll
+        for (int t = 0; t < kB; ++t) {
+          const int i = i0 + t * A.ng;
+          if (i < A.out_h) {  // warp-uniform
+            const int bi = band[i].bi;
+            if (bi != cur_bi) {
+              if (cur_bi >= 0) flush_blocks(blk, cur_bi, A.grid, bj, bj_lo, bj_hi, acc, lane);
+              cur_bi = bi;
+              acc = 0u;
+            }
+            acc += (uint32_t)(dv[t] * dv[t]);
+          }
+        }
       }
       if (cur_bi >= 0) flush_blocks(blk, cur_bi, A.grid, bj, bj_lo, bj_hi, acc, lane);
     }
