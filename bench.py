@@ -32,6 +32,10 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# streaming-read ceilings of this part, measured by tools/read_bw.cu (grid-stride uint4
+# loads) and tools/bulk_ring_bw.cu (dd_kernel's band ring with no compute), GB/s
+READ_CEIL_LDG = 6970.3
+READ_CEIL_BULK = 7534.6
 sys.path.insert(0, ROOT)
 
 W_SRC, H_SRC, OUT = 640, 480, 50
@@ -262,7 +266,11 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "kernel": "dd_kernel", "achieved": round(achieved, 1),
                      "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
                      "peak_source": peak_kind, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": ds_bytes, "avg_launch_ms": round(ds_ms, 4)},
+                     "algorithmic_bytes_per_launch": ds_bytes, "avg_launch_ms": round(ds_ms, 4),
+                     # dd_kernel's traffic is >99% reads; the copy peak above counts read+write.
+                     # Streaming-read ceilings measured on B200 (profiles/r01/read_ceiling.txt):
+                     "read_ceilings_GBps": {"ldg_stream": READ_CEIL_LDG, "bulk_ring": READ_CEIL_BULK},
+                     "frac_of_bulk_ring_ceiling": round(achieved / READ_CEIL_BULK, 4)},
         "stage_ms": {k: round(float(v), 4) for k, v in zip(
             ["dd_kernel", "dd_tail", "compaction", "cnn", "routing", "labeller",
              "labels_state"], stage)},
@@ -468,6 +476,29 @@ def run_extras(device, timing=(1000, 20000, 12_500_000_000)):
                              "smem_atomics_per_record": round((M9 + n_h1) / M9, 3),
                              "atomic_floor_ms": round(floor_ms, 3), "frac_of_atomic_floor": round(floor_ms / ms9, 3)}
     del s9, z9, y9, a9
+    # compaction (H4) and routing (H6) scale points: at the webcam hour they are ~10 us
+    # launches, so their HBM fraction is shown on 2^30 dispositions / 2^28 logits
+    hbm = measured_peaks()[0]
+    NC = 1 << 30
+    dsp = torch.where(torch.rand(NC, device=device, generator=g) < 0.15,
+                      torch.full((), 2, dtype=torch.uint8, device=device),
+                      torch.full((), 1, dtype=torch.uint8, device=device))
+    nf = int((dsp == 2).sum())
+    ms = _time_ms(lambda: N.noscope_compact_fired(dsp))
+    byt = NC + 4 * nf                              # disposition read + index write
+    out["compaction_2e30"] = {"frames": NC, "fired": nf, "ms": round(ms, 3), "GBps": round(byt / ms / 1e6, 1),
+                              "frac_of_hbm": round(byt / ms / 1e6 / hbm, 4),
+                              "algorithmic_bytes": byt}
+    del dsp
+    NR = 1 << 28
+    zr = torch.randn(NR, device=device, generator=g)
+    lo, hi = -0.5, 0.5
+    nu = int(((zr >= lo) & (zr <= hi)).sum())
+    ms = _time_ms(lambda: N.noscope_route_logits(lo, hi, zr))
+    byt = 4 * NR + NR + 4 * nu                     # logits read + route write + uncertain index write
+    out["routing_2e28"] = {"logits": NR, "uncertain": nu, "ms": round(ms, 3), "GBps": round(byt / ms / 1e6, 1),
+                           "frac_of_hbm": round(byt / ms / 1e6 / hbm, 4), "algorithmic_bytes": byt}
+    del zr
     return out
 
 

@@ -236,6 +236,20 @@ noscope_status noscope_route_logits(noscope_route r, const float* logits, const 
                                     int64_t n_max, uint8_t* route_out, int32_t* unc_idx_out,
                                     int64_t* n_unc_dev, noscope_stream_t stream);
 
+/* Stable compaction helper (step H4, "batch input images before
+ * passing them to the GPU"): idx_out[0 .. *n_out_dev) = the ascending
+ * positions i < n with disposition[i] == NOSCOPE_FIRED.  Positions whose
+ * tau = seg_offset + i has tau mod t_skip != 0 are first rewritten to
+ * NOSCOPE_SKIPPED in place (the t_skip rule; diff_detect applies
+ * the same rule before it compacts).
+ *  disposition: device u8 [n] (inout); idx_out: device i32 [n];
+ *  n_out_dev:   device i64.  Scan scratch comes from the stream-ordered pool.
+ *  Errors: NOSCOPE_INVALID_ARGUMENT for null buffers (n > 0), n < 0, n >= 2^31
+ *  or t_skip < 1.                                                            */
+noscope_status noscope_compact_fired(uint8_t* disposition, int64_t n, int64_t seg_offset,
+                                     int32_t t_skip, int32_t* idx_out, int64_t* n_out_dev,
+                                     noscope_stream_t stream);
+
 /* The whole cascade on one chunk of one unit:
  * diff_detect -> compaction -> specialized CNN on fired frames -> routing ->
  * labeller on uncertain frames -> per-frame labels:

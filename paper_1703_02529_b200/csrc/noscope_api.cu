@@ -278,6 +278,23 @@ noscope_status noscope_route_logits(noscope_route r, const float* logits, const 
   return s;
 }
 
+noscope_status noscope_compact_fired(uint8_t* disposition, int64_t n, int64_t seg_offset,
+                                     int32_t t_skip, int32_t* idx_out, int64_t* n_out_dev,
+                                     noscope_stream_t stream) {
+  if (n < 0 || n >= ((int64_t)1 << 31) || t_skip < 1 || seg_offset < 0 || !n_out_dev)
+    return NOSCOPE_INVALID_ARGUMENT;
+  if (n > 0 && (!disposition || !idx_out)) return NOSCOPE_INVALID_ARGUMENT;
+  noscope_status s = check_device();
+  if (s != NOSCOPE_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  void* scratch = nullptr;
+  NS_CUDA_TRY(cudaMallocAsync(&scratch, compact_ws_bytes(n), st));
+  s = launch_compact_fired(disposition, disposition, nullptr, n, seg_offset, t_skip, idx_out,
+                           n_out_dev, scratch, st);
+  cudaFreeAsync(scratch, st);
+  return s;
+}
+
 static noscope_status cascade_impl(const noscope_dd_config* dd, const noscope_cnn_arch* arch,
                                    const noscope_cnn_weights* weights, noscope_route route,
                                    const uint8_t* frames, noscope_frames_desc desc, int64_t n,

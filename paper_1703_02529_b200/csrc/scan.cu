@@ -1,11 +1,13 @@
 // scan.cu — stream compaction ("batch input images"), routing
 // and per-frame label resolution.
 //
-// Compaction is a single-pass decoupled look-back scan: tiles of 4096 items
-// are claimed in launch order through an atomic counter, each tile publishes
-// its aggregate then its inclusive prefix in one 64-bit word (flag | count),
-// and successors accumulate predecessors' words walking backwards.  Output
-// order is ascending (stable), so results are bit-identical to a serial scan.
+// Compaction of the FIRED frames is one persistent two-phase launch (count per
+// contiguous range, grid barrier, write) — see compact_fired_kernel.  Routing's
+// compaction of the uncertain frames is a single-pass decoupled look-back scan:
+// tiles of 8192 items are claimed in launch order through an atomic counter,
+// each tile publishes its aggregate then its inclusive prefix in one 64-bit word
+// (flag | count), and successors accumulate predecessors' words walking
+// backwards.  Both outputs are ascending (stable), bit-identical to a serial scan.
 //
 // Label resolution follows the backward pointers of O8 without pointer
 // chasing: among checked frames (tau = p * t_skip) a mode-1 suppression copies
@@ -18,7 +20,7 @@
 
 namespace ns {
 
-constexpr int kScanThreads = 256;
+constexpr int kScanThreads = 512;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
@@ -76,26 +78,37 @@ NS_DEV uint32_t block_excl_scan(uint32_t v, uint32_t* warp_sums, uint32_t* total
   return pre + x - v;
 }
 
-// Decoupled look-back: exclusive prefix of this tile (thread 0 does the walk).
-NS_DEV uint64_t tile_lookback(ScanWs ws, int tile, uint32_t agg, uint64_t* s_excl) {
-  if (threadIdx.x == 0) {
+// Decoupled look-back: exclusive prefix of this tile.  Warp 0 inspects the 32
+// preceding tiles' status words at once: if one of them holds an inclusive prefix,
+// the nearest such tile ends the walk (sum of the words up to it); otherwise all 32
+// aggregates are added and the window moves 32 tiles back.
+NS_DEV uint64_t tile_lookback(ScanWs ws, int tile, uint32_t agg, uint64_t* s_excl) {  // NOLINT
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
     uint64_t excl = 0;
     if (tile == 0) {
-      st_relaxed(&ws.status[0], kFlagIncl | agg);
+      if (lane == 0) st_relaxed(&ws.status[0], kFlagIncl | agg);
     } else {
-      st_relaxed(&ws.status[tile], kFlagAgg | agg);
-      int p = tile - 1;
+      if (lane == 0) st_relaxed(&ws.status[tile], kFlagAgg | agg);
+      int p = tile - 1;  // window [p - 31, p]; lane l reads tile p - l
       while (true) {
-        unsigned long long v = ld_relaxed(&ws.status[p]);
-        unsigned long long flag = v & ~kValMask;
-        if (flag == 0) continue;
-        excl += v & kValMask;
-        if (flag == kFlagIncl) break;
-        --p;
+        const int q = p - lane;
+        unsigned long long v = q >= 0 ? ld_relaxed(&ws.status[q]) : kFlagIncl;
+        while (__any_sync(0xffffffffu, (v & ~kValMask) == 0)) {
+          if ((v & ~kValMask) == 0) v = ld_relaxed(&ws.status[q]);
+        }
+        const unsigned incl = __ballot_sync(0xffffffffu, (v & ~kValMask) == kFlagIncl);
+        const int stop = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive tile (or the window)
+        uint64_t x = lane <= stop ? (v & kValMask) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        excl += x;
+        if (incl) break;
+        p -= 32;
       }
-      st_relaxed(&ws.status[tile], kFlagIncl | (excl + agg));
+      if (lane == 0) st_relaxed(&ws.status[tile], kFlagIncl | (excl + agg));
     }
-    *s_excl = excl;
+    if (lane == 0) *s_excl = excl;
   }
   __syncthreads();
   return *s_excl;
@@ -108,42 +121,159 @@ NS_DEV int claim_tile(ScanWs ws, int* s_tile) {
 }
 
 // ------------------------------------------------------------ fired frames
-__global__ void __launch_bounds__(kScanThreads)
-compact_fired_kernel(uint8_t* disp, double* score, int64_t n, int64_t tau0, int t_skip,
-                     int32_t* idx_out, int64_t* count_out, ScanWs ws, int ntiles) {
-  __shared__ uint32_t warp_sums[32];
-  __shared__ uint64_t s_excl;
-  __shared__ int s_tile;
-  const int tile = claim_tile(ws, &s_tile);
-  const int64_t base = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
-  uint32_t flags = 0, cnt = 0;
-#pragma unroll
-  for (int e = 0; e < kScanItems; ++e) {
-    const int64_t f = base + e;
-    if (f < n) {
-      const int64_t tau = tau0 + f;
-      if (tau % t_skip != 0) {
-        disp[f] = NOSCOPE_SKIPPED;
-        if (score) score[f] = __longlong_as_double(0xFFF0000000000000ll);  // -inf
-      } else if (disp[f] == NOSCOPE_FIRED) {
-        flags |= 1u << e;
-        ++cnt;
-      }
-    }
-  }
-  uint32_t total;
-  uint32_t local = block_excl_scan(cnt, warp_sums, &total);
-  uint64_t excl = tile_lookback(ws, tile, total, &s_excl);
-  uint64_t pos = excl + local;
-  if (idx_out) {
-#pragma unroll
-    for (int e = 0; e < kScanItems; ++e)
-      if (flags & (1u << e)) idx_out[pos++] = (int32_t)(base + e);
-  }
-  if (count_out && tile == ntiles - 1 && threadIdx.x == 0) *count_out = (int64_t)(excl + total);
+// Tile-local stable write-out: the tile's selected indices are staged in smem in
+// scan order, then stored as one coalesced run at the tile's global offset.
+NS_DEV void store_run(int32_t* out, uint64_t excl, uint32_t total, const int32_t* idx_s) {
+  for (uint32_t k = threadIdx.x; k < total; k += blockDim.x) out[excl + k] = idx_s[k];
 }
 
-size_t compact_fired_tiles(int64_t n) { return (n + kScanTile - 1) / kScanTile; }
+// Compaction of the FIRED frames (O5) as one persistent launch in two phases,
+// all G CTAs co-resident, CTA c owning the contiguous tile range
+// [c*T/G, (c+1)*T/G) of 8,192-frame tiles:
+//   phase 1: stream the range, count FIRED frames (and apply the t_skip rewrite:
+//            SKIPPED + score -inf in global memory); publish the range count;
+//   grid barrier (atomic arrival counter, acquire spin);
+//   phase 2: offset = sum of the lower ranges' counts; stream the range again and
+//            write the ascending indices, tile by tile (block scan, indices staged
+//            in smem, one coalesced run per tile).
+// Both phases prefetch kCStages tiles ahead with cp.async.bulk into a smem ring
+// (one mbarrier per stage), so every pass streams at HBM rate; there is no
+// look-back chain (a single-pass decoupled look-back is bound by one L2 round trip
+// per round of G tiles).  At the cascade's chunk sizes phase 2 re-reads from L2.
+// Tail or misaligned tiles are read directly from global memory.
+constexpr int kCThreads = 256, kCItems = 32, kCTile = kCThreads * kCItems, kCStages = 4;
+static_assert(NOSCOPE_FIRED == 2, "SWAR compare below tests bytes == 0x02");
+
+NS_DEV unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(kCThreads)
+compact_fired_kernel(uint8_t* disp, double* score, int64_t n, int64_t tau0, int t_skip,
+                     int32_t* idx_out, int64_t* count_out, ScanWs ws, int ntiles, int vec) {
+  extern __shared__ __align__(128) uint8_t csm[];
+  uint8_t* ring = csm;                                            // kCStages x kCTile
+  uint64_t* full = reinterpret_cast<uint64_t*>(csm + kCStages * kCTile);
+  uint32_t* warp_sums = reinterpret_cast<uint32_t*>(full + kCStages);  // [32]
+  uint64_t* s_off = reinterpret_cast<uint64_t*>(warp_sums + 32);
+  int32_t* idx_s = reinterpret_cast<int32_t*>(s_off + 2);         // kCTile staged indices
+  const int tid = threadIdx.x, G = gridDim.x, c = blockIdx.x;
+  const int t0 = (int)(((int64_t)ntiles * c) / G), t1 = (int)(((int64_t)ntiles * (c + 1)) / G);
+  const int nt = t1 - t0;
+  auto bulk_ok = [&](int t) { return vec && (int64_t)(t + 1) * kCTile <= n; };
+  // k-th fill of the ring (k counts over both passes): tile t0 + k % nt into stage k % kCStages
+  auto fill = [&](int k) {
+    const int st = k % kCStages;
+    const int t = t0 + (k < nt ? k : k - nt);
+    if (k < 2 * nt && bulk_ok(t)) {
+      mbar_arrive_expect_tx(&full[st], (uint32_t)kCTile);
+      bulk_g2s(ring + (size_t)st * kCTile, disp + (int64_t)t * kCTile, (uint32_t)kCTile, &full[st]);
+    } else {
+      mbar_arrive(&full[st]);  // keeps the stage's phase count in step
+    }
+  };
+  if (tid == 0) {
+    for (int st = 0; st < kCStages; ++st) mbar_init(&full[st], 1);
+    fence_mbar_init();
+    for (int k = 0; k < kCStages; ++k) fill(k);
+  }
+  __syncthreads();
+  // this thread's 16 frames of the k-th tile of the range: FIRED flags after the t_skip rule
+  auto load_flags = [&](int k, bool rewrite) -> uint32_t {
+    const int st = k % kCStages;
+    mbar_wait(&full[st], (uint32_t)((k / kCStages) & 1));
+    const int t = t0 + (k < nt ? k : k - nt);
+    const int64_t base = (int64_t)t * kCTile + (int64_t)tid * kCItems;
+    uint8_t d[kCItems];
+    if (bulk_ok(t)) {
+      const uint4* vp = reinterpret_cast<const uint4*>(ring + (size_t)st * kCTile + tid * kCItems);
+      const uint4 v0 = vp[0], v1 = vp[1];
+      const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      if (t_skip == 1) {  // SWAR: FIRED bytes -> 4-bit masks (byte e -> bit e)
+        uint32_t flags = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          flags |= (((__vcmpeq4(w[j], 0x02020202u) & 0x01010101u) * 0x01020408u) >> 24) << (4 * j);
+        return flags;
+      }
+#pragma unroll
+      for (int e = 0; e < kCItems; ++e) d[e] = (uint8_t)(w[e >> 2] >> (8 * (e & 3)));
+    } else {
+#pragma unroll
+      for (int e = 0; e < kCItems; ++e) d[e] = base + e < n ? disp[base + e] : (uint8_t)0;
+    }
+    uint32_t flags = 0;
+    if (t_skip == 1) {
+#pragma unroll
+      for (int e = 0; e < kCItems; ++e)
+        if (d[e] == NOSCOPE_FIRED && base + e < n) flags |= 1u << e;
+    } else {
+      int r = (int)((tau0 + base) % t_skip);  // tau mod t_skip, advanced incrementally
+#pragma unroll
+      for (int e = 0; e < kCItems; ++e) {
+        const int64_t f = base + e;
+        if (f < n) {
+          if (r != 0) {
+            if (rewrite) {
+              disp[f] = NOSCOPE_SKIPPED;
+              if (score) score[f] = __longlong_as_double(0xFFF0000000000000ll);  // -inf
+            }
+          } else if (d[e] == NOSCOPE_FIRED) {
+            flags |= 1u << e;
+          }
+        }
+        if (++r == t_skip) r = 0;
+      }
+    }
+    return flags;
+  };
+
+  // ---- phase 1: count
+  uint32_t mine = 0;
+  for (int k = 0; k < nt; ++k) {
+    mine += __popc(load_flags(k, true));
+    __syncthreads();                    // every thread is done with stage k % kCStages
+    if (tid == 0) fill(k + kCStages);
+  }
+  uint32_t range_total;
+  block_excl_scan(mine, warp_sums, &range_total);
+  if (tid == 0) {
+    st_relaxed(&ws.status[c], (unsigned long long)range_total);
+    __threadfence();
+    atomicAdd(ws.counter, 1u);
+    while (ld_acquire_gpu(ws.counter) < (unsigned)G) {
+    }
+    uint64_t off = 0;
+    for (int q = 0; q < c; ++q) off += ld_relaxed(&ws.status[q]);
+    *s_off = off;
+    if (c == G - 1 && count_out) *count_out = (int64_t)(off + range_total);
+  }
+  __syncthreads();
+  uint64_t off = *s_off;
+
+  // ---- phase 2: write the ascending indices
+  for (int k = nt; k < 2 * nt; ++k) {
+    const uint32_t flags = load_flags(k, false);
+    uint32_t total;
+    const uint32_t local = block_excl_scan((uint32_t)__popc(flags), warp_sums, &total);
+    if (tid == 0) fill(k + kCStages);   // block_excl_scan synced: stage free
+    const int64_t base = (int64_t)(t0 + k - nt) * kCTile + (int64_t)tid * kCItems;
+    uint32_t q = local;
+    for (uint32_t f = flags; f; f &= f - 1) idx_s[q++] = (int32_t)(base + __ffs(f) - 1);
+    __syncthreads();
+    if (idx_out) store_run(idx_out, off, total, idx_s);
+    off += total;
+    __syncthreads();                    // idx_s / warp_sums reuse
+  }
+}
+
+static size_t compact_smem_bytes() {
+  return (size_t)kCStages * kCTile + kCStages * 8 + 32 * 4 + 16 + (size_t)kCTile * 4;
+}
+
+size_t compact_fired_tiles(int64_t n) { return (n + kCTile - 1) / kCTile; }
 
 noscope_status launch_compact_fired(const uint8_t* /*disp_in*/, uint8_t* disp, double* score,
                                     int64_t n, int64_t tau0, int t_skip, int32_t* idx_out,
@@ -154,8 +284,21 @@ noscope_status launch_compact_fired(const uint8_t* /*disp_in*/, uint8_t* disp, d
     return NOSCOPE_OK;
   }
   NS_CUDA_TRY(cudaMemsetAsync(scan_ws, 0, compact_ws_bytes(n), st));
-  compact_fired_kernel<<<ntiles, kScanThreads, 0, st>>>(disp, score, n, tau0, t_skip, idx_out,
-                                                        count_out, scan_ws_of(scan_ws, n), ntiles);
+  const int vec = (reinterpret_cast<uintptr_t>(disp) & 15) == 0;
+  const size_t smem = compact_smem_bytes();
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaFuncSetAttribute(compact_fired_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    NS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compact_fired_kernel, kCThreads, smem));
+    if (per_sm < 1) per_sm = 1;
+  }
+  int sms = kNumSMs, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // persistent and co-resident (look-back waits only on earlier-claimed tiles)
+  const int grid = std::min(ntiles, per_sm * sms);
+  compact_fired_kernel<<<grid, kCThreads, smem, st>>>(disp, score, n, tau0, t_skip, idx_out, count_out,
+                                                      scan_ws_of(scan_ws, n), ntiles, vec);
   NS_LAUNCH_CHECK();
   count_launch();
   return NOSCOPE_OK;
@@ -176,6 +319,7 @@ struct RouteArgs {
   float* logits_pf;          // per-frame logits via frame_idx (nullable)
   unsigned long long* counters;  // [0] NEG, [1] POS (nullable)
   uint32_t* status;
+  int vec;                   // logits and route_out 16-byte aligned
 };
 
 __global__ void __launch_bounds__(kScanThreads)
@@ -184,6 +328,7 @@ route_kernel(RouteArgs A, ScanWs ws) {
   __shared__ uint64_t s_excl;
   __shared__ int s_tile;
   __shared__ unsigned int s_neg, s_pos;
+  __shared__ int32_t idx_s[kScanTile];
   const int64_t n = A.n_dev ? min(*A.n_dev, A.n_max) : A.n_max;
   const int ntiles = (int)((n + kScanTile - 1) / kScanTile);
   const int tile = claim_tile(ws, &s_tile);
@@ -194,32 +339,58 @@ route_kernel(RouteArgs A, ScanWs ws) {
   if (tile >= ntiles) return;
   if (threadIdx.x == 0) s_neg = s_pos = 0;
   const int64_t base = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
-  uint32_t flags = 0, cnt = 0, nneg = 0, npos = 0;
+  const bool full = A.vec && base + kScanItems <= n;
+  float zv[kScanItems];
+  if (full) {
+#pragma unroll
+    for (int q = 0; q < kScanItems / 4; ++q) {
+      const float4 v = reinterpret_cast<const float4*>(A.logits + base)[q];
+      zv[4 * q] = v.x; zv[4 * q + 1] = v.y; zv[4 * q + 2] = v.z; zv[4 * q + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < kScanItems; ++e) zv[e] = base + e < n ? A.logits[base + e] : 0.f;
+  }
+  uint32_t flags = 0, cnt = 0, nneg = 0, npos = 0, nan = 0;
+  uint8_t code[kScanItems];
 #pragma unroll
   for (int e = 0; e < kScanItems; ++e) {
-    const int64_t i = base + e;
-    if (i < n) {
-      const float z = A.logits[i];
-      uint8_t code;
-      if (z < A.lo) {
-        code = NOSCOPE_R_NEG;
-        ++nneg;
-      } else if (z > A.hi) {
-        code = NOSCOPE_R_POS;
-        ++npos;
-      } else {
-        code = NOSCOPE_R_UNC;
+    const float z = zv[e];
+    const bool in = base + e < n;
+    // NEG iff z < lo, POS iff z > hi, else UNCERTAIN (R-5; NaN -> UNCERTAIN + status)
+    code[e] = z < A.lo ? NOSCOPE_R_NEG : (z > A.hi ? NOSCOPE_R_POS : NOSCOPE_R_UNC);
+    if (in) {
+      nneg += code[e] == NOSCOPE_R_NEG;
+      npos += code[e] == NOSCOPE_R_POS;
+      if (code[e] == NOSCOPE_R_UNC) {
         flags |= 1u << e;
         ++cnt;
       }
-      if (z != z) atomicOr(A.status, 2u);
-      if (A.route_out) A.route_out[i] = code;
-      if (A.frame_idx) {
-        const int32_t f = A.frame_idx[i];
-        if (A.route_pf) A.route_pf[f] = code;
-        if (A.logits_pf) A.logits_pf[f] = z;
-      }
+      nan |= z != z;
     }
+  }
+  if (nan) atomicOr(A.status, 2u);
+  if (A.route_out) {
+    if (full) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        w[q] = code[4 * q] | (code[4 * q + 1] << 8) | (code[4 * q + 2] << 16) | ((uint32_t)code[4 * q + 3] << 24);
+      *reinterpret_cast<uint4*>(A.route_out + base) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < kScanItems; ++e)
+        if (base + e < n) A.route_out[base + e] = code[e];
+    }
+  }
+  if (A.frame_idx) {
+#pragma unroll
+    for (int e = 0; e < kScanItems; ++e)
+      if (base + e < n) {
+        const int32_t f = A.frame_idx[base + e];
+        if (A.route_pf) A.route_pf[f] = code[e];
+        if (A.logits_pf) A.logits_pf[f] = zv[e];
+      }
   }
   uint32_t total;
   uint32_t local = block_excl_scan(cnt, warp_sums, &total);
@@ -227,16 +398,20 @@ route_kernel(RouteArgs A, ScanWs ws) {
     if (nneg) atomicAdd(&s_neg, nneg);
     if (npos) atomicAdd(&s_pos, npos);
   }
-  uint64_t excl = tile_lookback(ws, tile, total, &s_excl);
-  uint64_t pos = excl + local;
+  {
+    uint32_t q = local;
 #pragma unroll
-  for (int e = 0; e < kScanItems; ++e)
-    if (flags & (1u << e)) {
-      const int64_t i = base + e;
-      const int32_t f = A.frame_idx ? A.frame_idx[i] : (int32_t)i;
-      if (A.unc_pos_pf) A.unc_pos_pf[f] = (int32_t)pos;
-      A.unc_out[pos++] = f;
-    }
+    for (int e = 0; e < kScanItems; ++e)
+      if (flags & (1u << e)) idx_s[q++] = A.frame_idx ? A.frame_idx[base + e] : (int32_t)(base + e);
+  }
+  uint64_t excl = tile_lookback(ws, tile, total, &s_excl);  // ends with __syncthreads
+  if (A.unc_pos_pf) {
+    uint64_t pos = excl + local;
+#pragma unroll
+    for (int e = 0; e < kScanItems; ++e)
+      if (flags & (1u << e)) A.unc_pos_pf[A.frame_idx ? A.frame_idx[base + e] : (int32_t)(base + e)] = (int32_t)pos++;
+  }
+  store_run(A.unc_out, excl, total, idx_s);
   if (threadIdx.x == 0) {
     if (A.counters) {
       atomicAdd(&A.counters[0], (unsigned long long)s_neg);
@@ -256,7 +431,8 @@ noscope_status launch_route(noscope_route r, const float* logits, const int64_t*
   NS_CUDA_TRY(cudaMemsetAsync(scan_ws, 0, compact_ws_bytes(n_max), st));
   RouteArgs A{r.lo_logit, r.hi_logit, logits, n_dev, n_max, frame_idx, route_out, route_pf,
               unc_out, n_unc, unc_pos_pf, logits_pf,
-              reinterpret_cast<unsigned long long*>(counters), status};
+              reinterpret_cast<unsigned long long*>(counters), status,
+              (int)(((reinterpret_cast<uintptr_t>(logits) | reinterpret_cast<uintptr_t>(route_out)) & 15) == 0)};
   route_kernel<<<ntiles, kScanThreads, 0, st>>>(A, scan_ws_of(scan_ws, n_max));
   NS_LAUNCH_CHECK();
   count_launch();

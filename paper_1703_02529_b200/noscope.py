@@ -134,6 +134,8 @@ def lib():
                                             c_p, c_p, c_i64, c_p, c_p, c_sz, c_p]
     L.noscope_route_logits.restype = c_i32
     L.noscope_route_logits.argtypes = [Route, c_p, c_p, c_i64, c_p, c_p, c_p, c_p]
+    L.noscope_compact_fired.restype = c_i32
+    L.noscope_compact_fired.argtypes = [c_p, c_i64, c_i64, c_i32, c_p, c_p, c_p]
     L.noscope_cascade_run.restype = c_i32
     L.noscope_cascade_run.argtypes = [C.POINTER(DDConfig), C.POINTER(CnnArchC),
                                       C.POINTER(CnnWeightsC), Route, c_p, FramesDesc, c_i64, c_i64,
@@ -322,6 +324,17 @@ def noscope_route_logits(lo: float, hi: float, logits: torch.Tensor, n_dev=None,
     _check(lib().noscope_route_logits(Route(lo, hi), _ptr(logits), _ptr(n_dev), n, _ptr(route),
                                       _ptr(unc), _ptr(nunc), _stream(stream)), "noscope_route_logits")
     return route[:n], unc, nunc
+
+
+def noscope_compact_fired(disposition: torch.Tensor, seg_offset=0, t_skip=1, stream=None):
+    """Stable list of FIRED positions (disposition u8, rewritten in place for t_skip)."""
+    n = disposition.numel()
+    dev = disposition.device
+    idx = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    _check(lib().noscope_compact_fired(_ptr(disposition), n, seg_offset, t_skip, _ptr(idx), _ptr(cnt),
+                                       _stream(stream)), "noscope_compact_fired")
+    return idx, cnt
 
 
 def noscope_cascade_run(dd: DD, arch: Arch, weights: Weights, lo: float, hi: float,

@@ -124,3 +124,27 @@ def test_sweep_1m_records_sampled():
         fp, fn, F, UU = O.triple_counts(T, jj, ll, hh)
         if fp <= lim and fn <= lim:
             assert O.cost_ps(checked, F, UU, *timing) >= best["cost_ps"]
+
+
+@pytest.mark.parametrize("n", [0, 1, 15, 16, 17, 4095, 4096, 4097, 100003])
+@pytest.mark.parametrize("t_skip,seg", [(1, 0), (3, 7), (15, 0)])
+def test_compact_fired_bit_exact(n, t_skip, seg):
+    """H4 stable compaction (+ the t_skip rewrite) vs the oracle's O5 loop, on the
+    aligned (16-byte vector) and misaligned (scalar) load paths."""
+    nsm = ns()
+    rng = np.random.default_rng(n * 31 + t_skip)
+    disp = rng.choice([O.SUPPRESSED, O.FIRED], size=n, p=[0.85, 0.15]).astype(np.uint8)
+    want = disp.copy()
+    tau = seg + np.arange(n)
+    want[tau % t_skip != 0] = O.SKIPPED
+    want_idx = O.compact(want)
+    for off in (0, 1):
+        buf = torch.zeros(n + 16, dtype=torch.uint8, device="cuda")
+        d = buf[off:off + n]
+        d.copy_(torch.from_numpy(disp))
+        idx, cnt = nsm.noscope_compact_fired(d, seg_offset=seg, t_skip=t_skip)
+        torch.cuda.synchronize()
+        k = int(cnt.item())
+        assert k == len(want_idx)
+        assert np.array_equal(idx.cpu().numpy()[:k], want_idx)
+        assert np.array_equal(d.cpu().numpy(), want)

@@ -1,0 +1,34 @@
+"""Scale points of the compaction (H4) and routing (H6) kernels: 2^30 dispositions,
+2^28 logits.  usage: python tools/prof_scan.py"""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_1703_02529_b200 import noscope as N
+
+
+def t_ms(fn, reps=5):
+    fn(); torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record(); torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+g = torch.Generator(device="cuda").manual_seed(4)
+for frac in (0.15, 0.5):
+    NC = 1 << 30
+    d = torch.where(torch.rand(NC, device="cuda", generator=g) < frac, torch.full((), 2, dtype=torch.uint8, device="cuda"),
+                    torch.full((), 1, dtype=torch.uint8, device="cuda"))
+    nf = int((d == 2).sum())
+    ms = t_ms(lambda: N.noscope_compact_fired(d))
+    byt = NC + 4 * nf
+    print(f"compaction 2^30 fired {frac}: {ms:.3f} ms  {byt / ms / 1e6:.1f} GB/s")
+    del d
+NR = 1 << 28
+z = torch.randn(NR, device="cuda", generator=g)
+nu = int(((z >= -0.5) & (z <= 0.5)).sum())
+ms = t_ms(lambda: N.noscope_route_logits(-0.5, 0.5, z))
+byt = 5 * NR + 4 * nu
+print(f"routing 2^28: {ms:.3f} ms  {byt / ms / 1e6:.1f} GB/s")
