@@ -2,6 +2,7 @@
 against the oracle on the same seeded inputs.  Dispositions and compaction are
 compared bit-exact, downsampled frames byte-exact, scores to rel 1e-5 (the
 north-star bound; the implementation is expected to be exactly equal)."""
+import functools
 import math
 
 import numpy as np
@@ -137,3 +138,37 @@ def test_validation_errors():
     _, g = dd_pair(nsm, 1, 0)
     with pytest.raises(nsm.NoScopeError):
         nsm.noscope_diff_detect(g, fr[:, :7500], 50, 50)  # pitch not /16
+
+
+@functools.lru_cache(maxsize=None)
+def _geom_frames(W, H, out):
+    # 640x480: ~1.4 frames per CTA, so t-5 anchors sit several CTAs back (deferred path)
+    n = {640: 200, 101: 3000, 160: 1200}[W]
+    sc, fr = scene_frames(W, H, n, seed=11, prevalence=0.6)
+    return fr, O.downsample(hw3(fr, W, H), out, out)
+
+
+@pytest.mark.parametrize("ng,cps", [(1, 1), (2, 1), (3, 1), (5, 1), (2, 2)])
+@pytest.mark.parametrize("geom", [(640, 480, 50, 1, 1), (101, 77, 23, 1, 0), (160, 120, 50, 0, 1)])
+def test_dd_kernel_launch_geometries(monkeypatch, ng, cps, geom):
+    """dd_kernel parity for every worker-group count / CTAs-per-SM the launch can take
+    (the default is NG = 4, 1 CTA/SM): band ring per group, segment warps, scorer and
+    deferred-anchor scoring must give the same bytes and scores in every geometry."""
+    W, H, out, mode, metric = geom
+    monkeypatch.setenv("NOSCOPE_DD_NG", str(ng))
+    monkeypatch.setenv("NOSCOPE_DD_CPS", str(cps))
+    nsm = ns()
+    fr, small_o = _geom_frames(W, H, out)
+    n = fr.shape[0]
+    grid = 10 if out % 10 == 0 else 4
+    lr = sg.lr_weights(grid, 7)
+    ref = small_o[0].copy()
+    cfg0 = O.DDConfig(mode=mode, metric=metric, out_w=out, out_h=out, grid=grid, t_diff_frames=5,
+                      t_skip_frames=1, delta_diff=0.0, ref_image=ref, lr_w=lr[0], lr_b=lr[1])
+    s_tmp, _ = O.diff_detect(small_o, cfg0)
+    fin = s_tmp[np.isfinite(s_tmp)]
+    delta = float(np.quantile(fin, 0.5))
+    ocfg, g = dd_pair(nsm, mode, metric, out=out, grid=grid, k=5, t_skip=1, delta=delta, ref=ref, lr=lr)
+    s_o, d_o = O.diff_detect(small_o, ocfg)
+    res = _run(nsm, g, fr, W, H)
+    _compare(res, small_o, s_o, d_o, out=out)
