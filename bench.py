@@ -284,6 +284,8 @@ def run_ours(args):
         line["clocks"] = clk.summary()
     if not args.no_e2e:
         line["e2e"] = run_e2e(args, S, device, world)
+    if not args.no_extras and rank == 0:
+        line["tskip15"] = run_tskip(S, device, 15)
     del S["frames"]
     torch.cuda.empty_cache()
     if not args.no_extras and rank == 0:
@@ -299,6 +301,50 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_tskip(S, device, t_skip, steps=5):
+    """The same webcam hour with the paper's frame skipping ("every 15
+    frames"): only frames with tau mod t_skip == 0 are read and scored (their t-30
+    anchors are checked frames too), skipped frames inherit the last checked label.
+    Same thresholds; device-timed like the main line, whole cascade per step."""
+    import copy
+    import ctypes
+    import torch
+    from paper_1703_02529_b200 import noscope as N
+    from synthgen.gpu import truth_labeller_address
+    dd = copy.copy(S["dd"])
+    dd.t_skip_frames = t_skip
+    n = S["frames"].shape[0]
+    ws = N.workspace(N.OP_CASCADE_RUN, dd, S["arch"], n, device=device)
+    state = torch.empty(max(1, N.lib().noscope_stream_state_bytes(ctypes.byref(dd.c()))), dtype=torch.uint8,
+                        device=device)
+    labels = torch.empty(n, dtype=torch.uint8, device=device)
+    lab_fn = truth_labeller_address()
+    stats = {}
+
+    def step():
+        N.lib().noscope_stream_state_init(ctypes.byref(dd.c()), N._ptr(state), N._stream())
+        out = N.noscope_cascade_run(dd, S["arch"], S["W"], S["lo"], S["hi"], S["frames"], W_SRC, H_SRC, state,
+                                    lab_fn, S["gs"].truth, ws=ws, labels=labels, want_stats=not stats)
+        if "stats" in out:
+            stats.update(out["stats"])
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    checked = n - stats.get("n_skipped", 0)
+    src = checked * (W_SRC * H_SRC * 3 + OUT * OUT * 3)
+    return {"t_skip": t_skip, "frames": n, "checked": checked, "ms_per_step": round(ms, 4),
+            "fps": round(n / (ms / 1e3), 1), "checked_source_GBps": round(src / ms / 1e6, 1),
+            "run_stats": stats}
 
 
 def cnn_flops_per_frame(arch):
