@@ -43,9 +43,10 @@ uint64_t& launch_counter() {
 
 constexpr int kDsMaxStages = 16;        // all groups' rings together
 constexpr int kDsMaxGroups = 5;
-constexpr int kDsMaxWorkers = 25;       // NG * NS worker warps
+constexpr int kDsMaxWorkers = 20;       // NG * NS worker warps (launch bound: 22 warps)
 constexpr int kDsMaxThreads = (2 + kDsMaxWorkers) * 32;
 constexpr int kBarEnd = 1;              // named barrier: all warps but the producer
+constexpr int kDsHeadBytes = 320;       // mbarriers: full/empty[16], fdone/bfree[2]
 
 NS_DEV void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 NS_DEV unsigned ld_acquire_u32(const unsigned* p) {
@@ -80,6 +81,8 @@ struct DsArgs {
   int stage_bytes, fast, rlo;
   int ng, ns, nsg;  // worker groups, segments (warps) per group, ring stages per group
   int cs_stride;    // u16 words of column sums per worker warp (multiple of 8)
+  // dynamic smem byte offsets (host-planned, ds_plan)
+  int off_ref, off_blkn, off_blk, off_wlr, off_cs, off_stages;
 };
 
 struct BandInfo {   // per output row i
@@ -255,18 +258,21 @@ dd_kernel(DsArgs A) {
   const int n_out = A.out_w * 3;
   const int nstages = A.ng * A.nsg;
   const int nworkers = A.ng * A.ns;
-  uint8_t* stages = smem;
-  uint16_t* csbuf = reinterpret_cast<uint16_t*>(smem + (size_t)nstages * A.stage_bytes);
-  uint32_t* blk = reinterpret_cast<uint32_t*>(csbuf + (size_t)nworkers * A.cs_stride);
-  double* wlr = reinterpret_cast<double*>(blk + 2 * gg2);  // gg2 even: 8-byte aligned
-  double* pk = wlr + gg2;
-  uint64_t* full = reinterpret_cast<uint64_t*>(pk + gg2);
+  // fixed-offset head (mbarriers, band table), then the host-planned variable part
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kDsMaxStages;
   uint64_t* fdone = empty + kDsMaxStages;   // [2] all workers finished frame m (parity m & 1)
   uint64_t* bfree = fdone + 2;              // [2] scorer released the block sums of frame m
-  uint32_t* blkn = reinterpret_cast<uint32_t*>(bfree + 2);
-  BandInfo* band = reinterpret_cast<BandInfo*>(blkn + gg2);
-  uint8_t* ref_s = reinterpret_cast<uint8_t*>(band + A.out_h);
+  BandInfo* band = reinterpret_cast<BandInfo*>(smem + kDsHeadBytes);
+  uint8_t* ref_s = smem + A.off_ref;
+  uint32_t* blkn = reinterpret_cast<uint32_t*>(smem + A.off_blkn);
+  uint32_t* blk = reinterpret_cast<uint32_t*>(smem + A.off_blk);
+  double* wlr = reinterpret_cast<double*>(smem + A.off_wlr);
+  double* pk = wlr + gg2;
+  uint16_t* csbuf = reinterpret_cast<uint16_t*>(smem + A.off_cs);
+  uint8_t* stages = smem + A.off_stages;
+  (void)nstages;
+  (void)nworkers;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -574,11 +580,19 @@ static size_t ds_plan(DsArgs& A, int ctas_per_sm) {
   A.cs_stride = (cs + 7) & ~7;
   const int gg2 = ((A.grid * A.grid) + 1) & ~1;
   const int small_bytes = A.out_w * A.out_h * 3;
-  size_t b = (size_t)A.ng * A.ns * A.cs_stride * sizeof(uint16_t);
-  b += 2 * (size_t)gg2 * 8 + 2 * (size_t)gg2 * 8;      // blk[2], wlr, pk
-  b += (2 * kDsMaxStages + 4) * 8;                      // mbarriers
-  b += (size_t)gg2 * 4 + (size_t)A.out_h * sizeof(BandInfo);
+  auto up = [](size_t x, size_t a) { return (x + a - 1) / a * a; };
+  size_t b = kDsHeadBytes + (size_t)A.out_h * sizeof(BandInfo);
+  A.off_ref = (int)b;
   b += A.mode == 0 ? (size_t)((small_bytes + 15) & ~15) : 0;   // reference image (mode 0)
+  A.off_blkn = (int)(b = up(b, 16));
+  b += (size_t)gg2 * 4;
+  A.off_blk = (int)(b = up(b, 16));
+  b += 2 * (size_t)gg2 * 4;                                   // blk[2] (frame parity)
+  A.off_wlr = (int)(b = up(b, 16));
+  b += 2 * (size_t)gg2 * 8;                                   // wlr, pk
+  A.off_cs = (int)(b = up(b, 16));
+  b += (size_t)A.ng * A.ns * A.cs_stride * sizeof(uint16_t);
+  A.off_stages = (int)(b = up(b, 128));
   // ring: as many stages per group as fit (227 KB per SM less the 1 KB per-CTA reservation)
   const size_t per_cta = (size_t)(227 * 1024) / ctas_per_sm - 1024;
   int nsg = per_cta > b ? (int)((per_cta - b) / ((size_t)A.ng * A.stage_bytes)) : 0;
