@@ -138,7 +138,7 @@ NS_DEV FrameCtx frame_ctx(const DsArgs& A, int64_t m, int64_t tau_first) {
   FrameCtx c;
   c.f = frame_of(A.need, m);
   c.tau = A.tau0 + c.f;
-  const bool checked = (c.tau % A.t_skip) == 0;
+  const bool checked = A.t_skip == 1 || (c.tau % A.t_skip) == 0;
   c.forced = A.mode == 1 && checked && c.tau < A.k;
   c.scoring = checked && !c.forced;
   c.anchor = nullptr;
@@ -371,11 +371,17 @@ dd_kernel(DsArgs A) {
     const bool active = lane < nout;
     const int tg = sg.j0 * 3 + lane;  // output value (row-local index) owned by this lane
     int colbase = 0, ncols = 0, bj = 0;
+    int hoff[4] = {0, 0, 0, 0};  // u16 slots of columns colbase + 3q, q < 4
     uint32_t mlo = 0, mhi = 0;
     if (active) {
       const int j = tg / 3, c = tg - 3 * j;
       const int q0 = (int)(((int64_t)j * A.W) / A.out_w), q1 = (int)(((int64_t)(j + 1) * A.W) / A.out_w);
       colbase = q0 * 3 + c - sg.xb;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int x = colbase + 3 * q;
+        hoff[q] = A.fast ? ((x & ~3) | ((x & 1) << 1) | ((x >> 1) & 1)) : x;
+      }
       ncols = q1 - q0;
       // magic reciprocals of 2n for the two possible band heights (rlo, rlo+1)
       const uint32_t n_lo = (uint32_t)(A.rlo * ncols), n_hi = (uint32_t)((A.rlo + 1) * ncols);
@@ -413,15 +419,10 @@ dd_kernel(DsArgs A) {
           for (int u = lane; u < nvec; u += 32) {
             uint32_t l[4] = {0u, 0u, 0u, 0u}, h[4] = {0u, 0u, 0u, 0u};
             vsum<RLO, STRIDE16>(p0 + u, nrows, RB16, l, h);
-            const uint32_t l0 = l[0], l1 = l[1], l2 = l[2], l3 = l[3];
-            const uint32_t h0 = h[0], h1 = h[1], h2 = h[2], h3 = h[3];
-            uint4 o0, o1;
-            o0.x = (l0 & 0xFFFFu) | (h0 << 16); o0.y = (l0 >> 16) | (h0 & 0xFFFF0000u);
-            o0.z = (l1 & 0xFFFFu) | (h1 << 16); o0.w = (l1 >> 16) | (h1 & 0xFFFF0000u);
-            o1.x = (l2 & 0xFFFFu) | (h2 << 16); o1.y = (l2 >> 16) | (h2 & 0xFFFF0000u);
-            o1.z = (l3 & 0xFFFFu) | (h3 << 16); o1.w = (l3 >> 16) | (h3 & 0xFFFF0000u);
-            reinterpret_cast<uint4*>(csw)[2 * u] = o0;
-            reinterpret_cast<uint4*>(csw)[2 * u + 1] = o1;
+            // stored as computed: u16 slot of column byte b is b with bits 0 and 1 swapped
+            // (l_j = columns 4j, 4j+2; h_j = columns 4j+1, 4j+3); see hoff below
+            reinterpret_cast<uint4*>(csw)[2 * u] = make_uint4(l[0], h[0], l[1], h[1]);
+            reinterpret_cast<uint4*>(csw)[2 * u + 1] = make_uint4(l[2], h[2], l[3], h[3]);
           }
         } else {
           const uint8_t* p0 = src + sg.xb;
@@ -439,15 +440,21 @@ dd_kernel(DsArgs A) {
         }
         uint32_t dd2 = 0u;
         if (active) {
-          const uint16_t* c0 = csw + colbase;
+          // column colbase + 3q sits at hoff[q & 3] + 12 * (q >> 2) (12 = 0 mod 4 keeps
+          // the swapped bits), so every load has a compile-time offset from 4 bases
           uint32_t S = 0;
           if (CLO > 0) {
 #pragma unroll
-            for (int q = 0; q < CLO; ++q) S += c0[3 * q];
-            if (ncols > CLO) S += c0[3 * CLO];
+            for (int q = 0; q < CLO; ++q) S += csw[hoff[q & 3] + 12 * (q >> 2)];
+            if (ncols > CLO) S += csw[hoff[CLO & 3] + 12 * (CLO >> 2)];
           } else {
-#pragma unroll 4
-            for (int q = 0; q < ncols; ++q) S += c0[3 * q];
+            for (int q = 0; q < ncols; q += 4) {
+              const int b = 3 * q;
+              S += csw[hoff[0] + b];
+              if (q + 1 < ncols) S += csw[hoff[1] + b];
+              if (q + 2 < ncols) S += csw[hoff[2] + b];
+              if (q + 3 < ncols) S += csw[hoff[3] + b];
+            }
           }
           const uint32_t n = (uint32_t)nrows * (uint32_t)ncols;
           const uint32_t G = __umulhi(2u * S + n, nrows == A.rlo ? mlo : mhi);
