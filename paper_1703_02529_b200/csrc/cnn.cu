@@ -2,7 +2,7 @@
 // conv+ReLU+maxpool layers, a dense layer and a sigmoid") on tcgen05 tensor
 // cores: bf16 operands from shared memory (or TMEM), fp32 accumulators in TMEM.
 //
-// Layer schedule per chunk of <= 8192 frames:
+// Layer schedule per chunk of <= 32768 frames (kCnnChunk):
 //   base_filters = 32: conv1+conv2 fused in one kernel (cnn_fused.cu; the conv1
 //     map never leaves the SM), then conv3/conv4 (L = 4) on the generic layer
 //     kernel (cnn_gemm.cu);
