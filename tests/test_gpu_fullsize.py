@@ -75,8 +75,10 @@ def test_webcam_hour_sampled_parity():
 
     # ---- sampled frames recomputed by the oracle
     rng = np.random.default_rng(0)
-    per_cta = N / 296.0
-    boundary = [int(math.floor(c * per_cta)) + d for c in (1, 2, 77, 295) for d in (0, 1, 29, 30)]
+    # dd_kernel runs one CTA per SM (148) over contiguous ranges (NOSCOPE_DD_CPS=2
+    # gives 296); frames around each boundary take their t-30 anchor from another CTA
+    boundary = [int(math.floor(c * N / G)) + d for G, cs in ((148, (1, 2, 77, 147)), (296, (1, 295)))
+                for c in cs for d in (-1, 0, 1, 29, 30)]
     samples = sorted(set([0, 1, 29, 30, 31, N - 1] + boundary + rng.integers(K, N, 10).tolist()))
     bg = sg.background(sc.spec)
     fired_samples = []
