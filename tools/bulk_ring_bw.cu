@@ -90,7 +90,8 @@ int main() {
       {48, 2, 5, 1, 1}, {48, 2, 5, 1, 0}, {48, 2, 4, 1, 1}, {48, 2, 5, 4, 1}, {48, 3, 3, 1, 1},
       {48, 3, 3, 1, 0}, {48, 4, 2, 1, 1}, {96, 2, 10, 1, 1}, {96, 3, 7, 1, 1}, {96, 4, 5, 1, 1},
       {96, 6, 3, 1, 1}, {192, 4, 10, 1, 1}, {192, 6, 7, 1, 1}, {192, 8, 5, 1, 1}, {24, 2, 2, 1, 1},
-      {24, 1, 5, 1, 1}, {48, 1, 10, 1, 1}};
+      {24, 1, 5, 1, 1}, {48, 1, 10, 1, 1}, {48, 1, 8, 1, 1}, {48, 1, 6, 1, 1}, {48, 1, 9, 1, 1},
+      {48, 1, 11, 1, 1}};
   for (const Cfg& c : cfgs) {
     Args A{fr, n, pitch, (int)(pitch / c.bpf), c.bpf, c.split, c.stages, c.read, sink};
     const size_t smem = 256 + (size_t)c.stages * A.band_bytes;
