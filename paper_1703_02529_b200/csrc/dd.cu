@@ -41,12 +41,12 @@ uint64_t& launch_counter() {
   return c;
 }
 
-constexpr int kDsMaxStages = 16;        // all groups' rings together
+constexpr int kDsMaxStages = 128;       // all groups' rings together (deep rings for small bands)
 constexpr int kDsMaxGroups = 5;
 constexpr int kDsMaxWorkers = 20;       // NG * NS worker warps (launch bound: 22 warps)
 constexpr int kDsMaxThreads = (2 + kDsMaxWorkers) * 32;
 constexpr int kBarEnd = 1;              // named barrier: all warps but the producer
-constexpr int kDsHeadBytes = 320;       // mbarriers: full/empty[16], fdone/bfree[2]
+constexpr int kDsHeadBytes = 2 * kDsMaxStages * 8 + 4 * 8 + 32;  // mbarriers: full/empty, fdone/bfree[2]
 
 NS_DEV void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 NS_DEV unsigned ld_acquire_u32(const unsigned* p) {
@@ -544,6 +544,125 @@ dd_kernel(DsArgs A) {
   }
 }
 
+// ------------------------------------------------- identity downsample (out == source)
+// When the target resolution equals the source (BASELINE configs[0]: 50x50 frames),
+// O1 is the identity, so the source frame IS the small frame and the t-k anchor is
+// source frame f-k itself (or the state ring before tau0): no band pipeline and no
+// cross-CTA anchor hand-off are needed.  One CTA per needed frame (grid-stride):
+// 16-byte vectors are copied to the small-frame buffer and, for scored frames, the
+// integer SSD against the anchor is accumulated per LR block (per-thread partials,
+// u32 smem atomics when the block changes); then the fp64 score in the fixed order
+// of O3 and the disposition of O4 — the same arithmetic as dd_kernel.
+constexpr int kIdThreads = 256;
+
+__global__ void __launch_bounds__(kIdThreads)
+dd_identity_kernel(DsArgs A) {
+  __shared__ uint32_t blk[kMaxGrid * kMaxGrid + 2];
+  __shared__ uint32_t blkn[kMaxGrid * kMaxGrid + 2];
+  __shared__ double wlr[kMaxGrid * kMaxGrid + 2];
+  __shared__ double pk[kMaxGrid * kMaxGrid + 2];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int gg = A.grid * A.grid;
+  const int n_out = A.out_w * 3;
+  const int small_bytes = n_out * A.out_h;
+  const int nvec = (small_bytes + 15) >> 4;
+  if (A.metric == 1) {
+    const int sh = A.out_h / A.grid, sw = A.out_w / A.grid;
+    for (int q = tid; q < gg; q += blockDim.x) {
+      const int bi = q / A.grid, bj = q % A.grid;
+      const int rows = bi < A.grid - 1 ? sh : A.out_h - (A.grid - 1) * sh;
+      const int cols = bj < A.grid - 1 ? sw : A.out_w - (A.grid - 1) * sw;
+      blkn[q] = (uint32_t)(rows * cols * 3);
+      wlr[q] = (double)A.lr_w[q];
+    }
+  }
+  for (int q = tid; q < gg; q += blockDim.x) blk[q] = 0u;
+  __syncthreads();
+  for (int64_t m = A.need.m0 + blockIdx.x; m < A.need.m1; m += gridDim.x) {
+    const int64_t f = frame_of(A.need, m);
+    const int64_t tau = A.tau0 + f;
+    const bool checked = A.t_skip == 1 || (tau % A.t_skip) == 0;
+    const bool forced = A.mode == 1 && checked && tau < A.k;
+    const bool scoring = checked && !forced;
+    const uint8_t* src = A.frames + f * A.frame_pitch;
+    uint8_t* dst = A.small + f * A.small_pitch;
+    const uint8_t* anc = A.ref;
+    if (A.mode == 1 && scoring)
+      anc = f - A.k >= 0 ? A.frames + (f - A.k) * A.frame_pitch : A.ring + ((tau - A.k) % A.k) * A.ring_pitch;
+    for (int v = tid; v < nvec; v += blockDim.x) {
+      const uint4 w = reinterpret_cast<const uint4*>(src)[v];
+      reinterpret_cast<uint4*>(dst)[v] = w;  // pitches are 16-byte multiples
+      if (!scoring) continue;
+      const int x0 = v << 4;
+      uint32_t a[4];
+      if (x0 + 16 <= small_bytes && (reinterpret_cast<uintptr_t>(anc) & 15) == 0) {
+        const uint4 av = *reinterpret_cast<const uint4*>(anc + x0);
+        a[0] = av.x; a[1] = av.y; a[2] = av.z; a[3] = av.w;
+      } else {  // tail or unaligned reference image: byte loads inside the image only
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint32_t word = 0;
+          for (int b = 0; b < 4; ++b)
+            if (x0 + 4 * j + b < small_bytes) word |= (uint32_t)anc[x0 + 4 * j + b] << (8 * b);
+          a[j] = word;
+        }
+      }
+      const uint32_t s[4] = {w.x, w.y, w.z, w.w};
+      int row = x0 / n_out, colb = x0 - row * n_out;  // byte column within the row
+      uint32_t acc = 0u;
+      int cur = -1;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        if (x0 + e < small_bytes) {
+          const int d = (int)((s[e >> 2] >> (8 * (e & 3))) & 0xFFu) - (int)((a[e >> 2] >> (8 * (e & 3))) & 0xFFu);
+          const int q = A.metric == 1 ? block_of(row, A.out_h, A.grid) * A.grid + block_of(colb / 3, A.out_w, A.grid) : 0;
+          if (q != cur) {
+            if (cur >= 0 && acc) atomicAdd(&blk[cur], acc);
+            cur = q;
+            acc = 0u;
+          }
+          acc += (uint32_t)(d * d);
+        }
+        if (++colb == n_out) {
+          colb = 0;
+          ++row;
+        }
+      }
+      if (cur >= 0 && acc) atomicAdd(&blk[cur], acc);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      if (scoring) {
+        if (A.metric == 0) {
+          if (lane == 0) {
+            const double sc = (double)blk[0] / (double)small_bytes;
+            blk[0] = 0u;
+            A.score[f] = sc;
+            A.disp[f] = sc > A.delta ? NOSCOPE_FIRED : NOSCOPE_SUPPRESSED;
+          }
+        } else {
+          for (int q = lane; q < gg; q += 32) {
+            pk[q] = __dmul_rn(wlr[q], (double)blk[q] / (double)blkn[q]);  // w_k * m_k, rounded
+            blk[q] = 0u;
+          }
+          __syncwarp();
+          if (lane == 0) {
+            double z = (double)A.lr_b;
+            for (int q = 0; q < gg; ++q) z = __dadd_rn(z, pk[q]);  // fixed order, no FMA
+            if (z != z) atomicOr(A.status, 1u);
+            A.score[f] = z;
+            A.disp[f] = z > A.delta ? NOSCOPE_FIRED : NOSCOPE_SUPPRESSED;
+          }
+        }
+      } else if (forced && lane == 0) {
+        A.score[f] = __longlong_as_double(0x7FF0000000000000ll);  // +inf
+        A.disp[f] = NOSCOPE_FIRED;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------ state update
 __global__ void dd_state_update_kernel(const uint8_t* small, int64_t small_pitch, uint8_t* ring,
                                        int64_t ring_pitch, int k, int small_bytes, int64_t tau0,
@@ -657,6 +776,16 @@ noscope_status launch_diff_detect(const noscope_dd_config& cfg, const uint8_t* f
   void (*kern)(DsArgs) = dd_kernel<0, 0, 0>;
   if (A.fast && A.rlo == 9 && A.W / A.out_w == 12 && A.RB == 1920) kern = dd_kernel<9, 12, 120>;
   const int64_t frames_needed = A.need.m1 - A.need.m0;
+  if (A.W == A.out_w && A.H == A.out_h && A.grid <= kMaxGrid) {  // O1 is the identity
+    if (frames_needed > 0) {
+      const int grid = (int)std::min<int64_t>(frames_needed, (int64_t)kNumSMs * 8);
+      dd_identity_kernel<<<grid, kIdThreads, 0, st>>>(A);
+      NS_LAUNCH_CHECK();
+      count_launch();
+    }
+    prof_mark(prof, st);
+    return NOSCOPE_OK;
+  }
   if (frames_needed > 0) {
     static bool attr_set[2] = {false, false};
     const int ki = kern == dd_kernel<0, 0, 0> ? 0 : 1;

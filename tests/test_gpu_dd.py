@@ -172,3 +172,40 @@ def test_dd_kernel_launch_geometries(monkeypatch, ng, cps, geom):
     s_o, d_o = O.diff_detect(small_o, ocfg)
     res = _run(nsm, g, fr, W, H)
     _compare(res, small_o, s_o, d_o, out=out)
+
+
+@pytest.mark.parametrize("mode,metric,t_skip,k", [(0, 0, 1, 1), (0, 1, 3, 1), (1, 0, 1, 1), (1, 1, 1, 30),
+                                                  (1, 1, 4, 7), (1, 0, 3, 2)])
+@pytest.mark.parametrize("size,grid", [(50, 10), (23, 4)])
+def test_identity_downsample_path(mode, metric, t_skip, k, size, grid):
+    """out == source size (BASELINE configs[0]): the identity kernel (source frame = small
+    frame, t-k anchors read straight from the source frames), whole unit and in chunks
+    with carried state (anchors from the state ring)."""
+    nsm = ns()
+    n = 1500
+    sc, fr = scene_frames(size, size, n, seed=13, prevalence=0.4)
+    small_o = hw3(fr, size, size)
+    lr = sg.lr_weights(grid, 9)
+    ref = sg.background(sc.spec)
+    cfg0 = O.DDConfig(mode=mode, metric=metric, out_w=size, out_h=size, grid=grid, t_diff_frames=k,
+                      t_skip_frames=t_skip, delta_diff=0.0, ref_image=ref, lr_w=lr[0], lr_b=lr[1])
+    s_tmp, _ = O.diff_detect(small_o, cfg0)
+    fin = s_tmp[np.isfinite(s_tmp)]
+    delta = float(np.quantile(fin, 0.5))
+    ocfg, g = dd_pair(nsm, mode, metric, out=size, grid=grid, k=k, t_skip=t_skip, delta=delta, ref=ref, lr=lr)
+    s_o, d_o = O.diff_detect(small_o, ocfg)
+    assert 0 < (d_o == O.FIRED).sum() < n
+    need = [t for t in range(n) if t % t_skip == 0 or (mode == 1 and (t + k) % t_skip == 0)]
+    res = _run(nsm, g, fr, size, size)
+    _compare(res, small_o, s_o, d_o, out=size, needed=np.array(need))
+    state = nsm.noscope_stream_state_init(g)
+    disp = np.empty(n, np.uint8)
+    score = np.empty(n)
+    pos = 0
+    for c in (1, 499, 3, 997):
+        r = _run(nsm, g, fr[pos:pos + c], size, size, seg_offset=pos, state=state)
+        disp[pos:pos + c] = r["disp"][:c]
+        score[pos:pos + c] = r["score"][:c]
+        pos += c
+    assert np.array_equal(disp, d_o)
+    assert np.array_equal(score[np.isfinite(s_o)], s_o[np.isfinite(s_o)])
