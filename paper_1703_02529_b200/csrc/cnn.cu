@@ -37,21 +37,6 @@ static uint32_t tmem_cols_host(int c) {
 
 // ------------------------------------------------------------ weight packing
 // out[((p*nkc + kc)*pn + n)*8 + e] = w[(p*pn + n)*Kreal + kc*8 + e] (0 beyond Kreal)
-__global__ void pack_kernel(const uint16_t* __restrict__ w, int rows, int Kreal, int Kpad, int pn,
-                            uint16_t* __restrict__ out) {
-  const int nkc = Kpad / 8;
-  const int64_t total = (int64_t)rows * Kpad;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int e = (int)(t & 7);
-    const int64_t r = t >> 3;
-    const int n_all = (int)(r % rows);
-    const int kc = (int)(r / rows);
-    const int p = n_all / pn, n = n_all % pn;
-    const int k = kc * 8 + e;
-    out[(((int64_t)p * nkc + kc) * pn + n) * 8 + e] = k < Kreal ? w[(int64_t)n_all * Kreal + k] : 0;
-  }
-}
 
 
 // =================================================================== FC
@@ -308,13 +293,47 @@ bool cnn_debug_layout(const noscope_cnn_arch& a, int64_t n_max, int64_t* out) {
   return true;
 }
 
-static void pack(const uint16_t* w, int rows, int Kreal, int Kpad, int pn, uint8_t* out,
-                 cudaStream_t st) {
-  int64_t total = (int64_t)rows * Kpad;
-  int grid = (int)std::min<int64_t>((total + 255) / 256, 4 * kNumSMs);
-  pack_kernel<<<grid, 256, 0, st>>>(w, rows, Kreal, Kpad, pn, reinterpret_cast<uint16_t*>(out));
-  count_launch();
+// All weight repacks of one call in ONE launch (the call is launch-latency bound
+// for small batches): jobs share one flat index space; job 0 (conv1) also writes
+// the fp32 bias as a bf16 hi/lo pair into K columns 27/28 (against A = 1.0).
+struct PackJob {
+  const uint16_t* w;
+  uint16_t* out;
+  int rows, Kreal, Kpad, pn;
+  int64_t total;
+};
+struct PackJobs {
+  PackJob j[3];
+  int n;
+  const float* bias1;  // conv1 bias (job 0), nullable
+};
+__global__ void pack_multi_kernel(PackJobs J) {
+  int64_t start = 0;
+  for (int q = 0; q < J.n; ++q) {
+    const PackJob b = J.j[q];
+    const int nkc = b.Kpad / 8;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - start; t < b.total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+      if (t < 0) continue;
+      const int e = (int)(t & 7);
+      const int64_t r = t >> 3;
+      const int n_all = (int)(r % b.rows);
+      const int kc = (int)(r / b.rows);
+      const int p = n_all / b.pn, n = n_all % b.pn;
+      const int k = kc * 8 + e;
+      uint16_t v = k < b.Kreal ? b.w[(int64_t)n_all * b.Kreal + k] : (uint16_t)0;
+      if (q == 0 && J.bias1 && (k == 27 || k == 28)) {
+        const float x = J.bias1[n_all];
+        const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+        const __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+        v = *reinterpret_cast<const uint16_t*>(k == 27 ? &hi : &lo);
+      }
+      b.out[(((int64_t)p * nkc + kc) * b.pn + n) * 8 + e] = v;
+    }
+    start += b.total;
+  }
 }
+
 
 noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& w,
                           const uint8_t* small, int64_t small_pitch, const int32_t* idx,
@@ -326,17 +345,27 @@ noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& 
   if (n_max <= 0) return NOSCOPE_OK;
   uint8_t* ws = reinterpret_cast<uint8_t*>(ws_v);
   // pack weights into the canonical UMMA layouts
-  pack(w.conv_w[0], P.C, 27, 32, P.C, ws + P.w1_off, st);
-  if (P.fused) pack(w.conv_w[1], 2 * P.C, 9 * P.C, 9 * P.C, 2 * P.C, ws + P.w2_off, st);
-  NS_LAUNCH_CHECK();
-  noscope_status sb = pack_conv12_bias(w.conv_b[0], P.C, ws + P.w1_off, st);  // bias in K 27/28
-  if (sb != NOSCOPE_OK) return sb;
+  {
+    PackJobs J{};
+    auto job = [&](const uint16_t* wsrc, int rows, int Kreal, int Kpad, int pn, uint8_t* out) {
+      J.j[J.n++] = PackJob{wsrc, reinterpret_cast<uint16_t*>(out), rows, Kreal, Kpad, pn,
+                           (int64_t)rows * Kpad};
+    };
+    job(w.conv_w[0], P.C, 27, 32, P.C, ws + P.w1_off);  // + bias in K 27/28
+    if (P.fused) job(w.conv_w[1], 2 * P.C, 9 * P.C, 9 * P.C, 2 * P.C, ws + P.w2_off);
+    job(w.fc1_w, P.D, P.K, P.K, P.D, ws + P.fc_off);
+    J.bias1 = w.conv_b[0];
+    int64_t total = 0;
+    for (int q = 0; q < J.n; ++q) total += J.j[q].total;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, 4 * kNumSMs);
+    pack_multi_kernel<<<grid, 256, 0, st>>>(J);
+    NS_LAUNCH_CHECK();
+    count_launch();
+  }
   for (int l = P.first_g; l < P.L; ++l) {
     noscope_status s = pack_convg(w.conv_w[l], P.g[l], ws + P.gw_off[l], st);
     if (s != NOSCOPE_OK) return s;
   }
-  pack(w.fc1_w, P.D, P.K, P.K, P.D, ws + P.fc_off, st);
-  NS_LAUNCH_CHECK();
 
   static bool attr = false;
   if (!attr) {

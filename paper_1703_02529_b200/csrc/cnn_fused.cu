@@ -562,26 +562,6 @@ conv12_fused_kernel(FusedArgs A) {
 
 size_t conv12_fused_smem() { return (size_t)fz::kSmem; }
 
-// conv1 packed weights [4 kc][C][8]: K index 27 <- bf16(bias), 28 <- bf16(bias -
-// bf16(bias)); with A[., 27] = A[., 28] = 1.0 the tensor core accumulates the
-// fp32 bias to ~2^-17 relative.
-__global__ void pack_conv1_bias_kernel(const float* __restrict__ b, int C, uint16_t* __restrict__ out) {
-  const int n = threadIdx.x;
-  if (n >= C) return;
-  const float v = b[n];
-  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-  const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
-  out[(3 * C + n) * 8 + 3] = *reinterpret_cast<const uint16_t*>(&hi);
-  out[(3 * C + n) * 8 + 4] = *reinterpret_cast<const uint16_t*>(&lo);
-}
-
-noscope_status pack_conv12_bias(const float* b1, int C, uint8_t* w1_packed, cudaStream_t st) {
-  pack_conv1_bias_kernel<<<1, 64, 0, st>>>(b1, C, reinterpret_cast<uint16_t*>(w1_packed));
-  NS_LAUNCH_CHECK();
-  count_launch();
-  return NOSCOPE_OK;
-}
-
 template <int kHalves, bool kConv2>
 static noscope_status launch_variant(const FusedArgs& a, int grid, cudaStream_t st) {
   static bool attr = false;

@@ -170,7 +170,6 @@ noscope_status launch_convg(const ConvGArgs& a, cudaStream_t st);
 bool make_convt_geom(int cin, int cout, int H, int64_t chunk, ConvGGeom* g);
 noscope_status launch_convt(const ConvGArgs& a, cudaStream_t st);
 noscope_status pack_convg(const uint16_t* w, const ConvGGeom& g, uint8_t* out, cudaStream_t st);
-noscope_status pack_conv12_bias(const float* b1, int C, uint8_t* w1_packed, cudaStream_t st);
 noscope_status launch_conv12_fused(const FusedArgs& a, int grid, cudaStream_t st);
 size_t cnn_ws_bytes(const noscope_cnn_arch& a, int64_t n_max);
 noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& w,
