@@ -1,6 +1,7 @@
 // common.cuh — sm_100a PTX helpers shared by the NoScope kernels (CUDA side only).
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
@@ -190,6 +191,25 @@ NS_DEV T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Launch with the cooperative attribute: the driver guarantees every CTA of the grid
+// is co-resident (or fails the launch), which the in-kernel grid barriers / cross-CTA
+// flag waits rely on.  Capturable into CUDA graphs.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_cooperative(void (*kern)(KArgs...), int grid, int threads, size_t smem,
+                                      cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 }  // namespace ns

@@ -802,7 +802,7 @@ noscope_status launch_diff_detect(const noscope_dd_config& cfg, const uint8_t* f
     // all CTAs co-resident (deferred scoring waits on earlier CTAs' flags)
     const int grid = (int)std::min<int64_t>(frames_needed, (int64_t)std::min(per_sm, cps) * sms);
     if (cfg.mode == 1) NS_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)grid * 4, st));
-    kern<<<grid, threads, smem, st>>>(A);
+    NS_CUDA_TRY(launch_cooperative(kern, grid, threads, smem, st, A));  // deferred anchors wait on earlier CTAs
     NS_LAUNCH_CHECK();
     count_launch();
   }

@@ -297,8 +297,8 @@ noscope_status launch_compact_fired(const uint8_t* /*disp_in*/, uint8_t* disp, d
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // persistent and co-resident (look-back waits only on earlier-claimed tiles)
   const int grid = std::min(ntiles, per_sm * sms);
-  compact_fired_kernel<<<grid, kCThreads, smem, st>>>(disp, score, n, tau0, t_skip, idx_out, count_out,
-                                                      scan_ws_of(scan_ws, n), ntiles, vec);
+  NS_CUDA_TRY(launch_cooperative(compact_fired_kernel, grid, kCThreads, smem, st, disp, score, n, tau0, t_skip,
+                                 idx_out, count_out, scan_ws_of(scan_ws, n), ntiles, vec));
   NS_LAUNCH_CHECK();
   count_launch();
   return NOSCOPE_OK;
