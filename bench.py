@@ -172,10 +172,10 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
+    if world > 1:   # one process per GPU; bind the NCCL communicator to this rank's device
+        dist.init_process_group("nccl", device_id=device)
     n = args.frames
     S = setup_gpu(rank, n, device)
     dd, arch, W = S["dd"], S["arch"], S["W"]
