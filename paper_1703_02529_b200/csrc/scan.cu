@@ -82,7 +82,7 @@ NS_DEV uint32_t block_excl_scan(uint32_t v, uint32_t* warp_sums, uint32_t* total
 // preceding tiles' status words at once: if one of them holds an inclusive prefix,
 // the nearest such tile ends the walk (sum of the words up to it); otherwise all 32
 // aggregates are added and the window moves 32 tiles back.
-NS_DEV uint64_t tile_lookback(ScanWs ws, int tile, uint32_t agg, uint64_t* s_excl) {  // NOLINT
+NS_DEV uint64_t tile_lookback(ScanWs ws, int tile, uint32_t agg, uint64_t* s_excl) {
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     uint64_t excl = 0;
