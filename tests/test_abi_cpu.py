@@ -112,3 +112,34 @@ def test_next_row_entry_points_validate_before_device_use(lib):
     res = N.CboResult()
     assert lib.noscope_cbo_search(None, 0, None, 0, v, N.FramesDesc(50, 50, 7504), 10, v, v, 3, 1, 1, 0, 0,
                                   ctypes.byref(res), v, 1 << 20, None) == 1
+
+
+def test_compact_fired_validates_before_device_use(lib):
+    """noscope_compact_fired (H4 helper) rejects bad arguments on the host."""
+    one = ctypes.c_void_p(16)
+    assert lib.noscope_compact_fired(None, 10, 0, 1, one, one, None) == 1        # null dispositions
+    assert lib.noscope_compact_fired(one, 10, 0, 0, one, one, None) == 1         # t_skip < 1
+    assert lib.noscope_compact_fired(one, -1, 0, 1, one, one, None) == 1         # n < 0
+    assert lib.noscope_compact_fired(one, 1 << 31, 0, 1, one, one, None) == 1    # n >= 2^31
+    assert lib.noscope_compact_fired(one, 10, -1, 1, one, one, None) == 1        # seg_offset < 0
+    assert lib.noscope_compact_fired(one, 10, 0, 1, one, None, None) == 1        # null count
+
+
+def test_bench_reference_arm_prints_one_contract_line():
+    """bench.py --impl reference (the CPU oracle arm the driver runs) prints one JSON
+    line with the contract keys and an e2e object with zero copy bytes."""
+    import json
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["kind"] == "oracle"
