@@ -5,8 +5,8 @@
 //   * each CTA owns a CONTIGUOUS range of the frames that must be downsampled
 //     (checked frames, plus mode-1 anchors), one output row ("band") at a time;
 //   * a band = source rows [floor(iH/h), floor((i+1)H/h)) = one contiguous byte
-//     range of the frame, fetched by one cp.async.bulk (TMA 1-D engine, L2
-//     evict-first: every source byte is read exactly once) into a shared-memory
+//     range of the frame, fetched by one cp.async.bulk (TMA 1-D engine; every
+//     source byte is read exactly once) into a shared-memory
 //     ring issued by one producer thread (warp 0);
 //   * bands are dealt round-robin to NG worker GROUPS (band i -> group i % NG),
 //     each with its own ring of stages (full/empty mbarriers), so groups work on
@@ -320,7 +320,6 @@ dd_kernel(DsArgs A) {
   if (warp == 0) {
     // ======================================================= producer
     if (lane != 0) return;
-    const uint64_t pol = policy_evict_first();
     int gs[kDsMaxGroups] = {};
     uint32_t gph[kDsMaxGroups] = {};
     int64_t issued[kDsMaxGroups] = {};
@@ -332,8 +331,7 @@ dd_kernel(DsArgs A) {
         const int st = g * A.nsg + gs[g];
         if (issued[g] >= A.nsg) mbar_wait(&empty[st], gph[g] ^ 1u);
         mbar_arrive_expect_tx(&full[st], (uint32_t)bd.bytes);
-        bulk_g2s_evict_first(stages + (size_t)st * A.stage_bytes, fr + bd.a0, (uint32_t)bd.bytes,
-                             &full[st], pol);
+        bulk_g2s(stages + (size_t)st * A.stage_bytes, fr + bd.a0, (uint32_t)bd.bytes, &full[st]);
         ++issued[g];
         if (++gs[g] == A.nsg) {
           gs[g] = 0;
