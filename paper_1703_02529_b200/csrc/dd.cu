@@ -48,6 +48,19 @@ constexpr int kDsMaxThreads = (2 + kDsMaxWorkers) * 32;
 constexpr int kBarEnd = 1;              // named barrier: all warps but the producer
 constexpr int kDsHeadBytes = 2 * kDsMaxStages * 8 + 4 * 8 + 32;  // mbarriers: full/empty, fdone/bfree[2]
 
+// mbarrier phase wait without a suspend-time hint (spins on try_wait; the band
+// hand-offs are short, so no sleep/wake latency on the critical path)
+NS_DEV void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar), done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!done);
+}
 NS_DEV void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 NS_DEV unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -411,7 +424,7 @@ dd_kernel(DsArgs A) {
         const int offrows = band[i].offrows;
         const int nrows = offrows & 0xFFFF, off = offrows >> 16;
         const uint8_t* src = stages + (size_t)(grp * A.nsg + s) * A.stage_bytes + off;
-        mbar_wait(&full[grp * A.nsg + s], ph);
+        mbar_wait_spin(&full[grp * A.nsg + s], ph);
         if (A.fast) {
           const uint4* p0 = reinterpret_cast<const uint4*>(src + sg.xb);
           for (int u = lane; u < nvec; u += 32) {
