@@ -148,3 +148,26 @@ def test_compact_fired_bit_exact(n, t_skip, seg):
         assert k == len(want_idx)
         assert np.array_equal(idx.cpu().numpy()[:k], want_idx)
         assert np.array_equal(d.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("t_skip", [1, 3])
+def test_compact_fired_multi_window(t_skip):
+    """More than one 64 MB compaction window (8,192 tiles of 8,192 frames): the running
+    offset carried across windows, ragged tail; checked against numpy.flatnonzero (the
+    O5 pin) on 70,000,123 dispositions."""
+    nsm = ns()
+    n = 70_000_123
+    g = torch.Generator(device="cuda").manual_seed(17)
+    d = torch.where(torch.rand(n, device="cuda", generator=g) < 0.15,
+                    torch.full((), O.FIRED, dtype=torch.uint8, device="cuda"),
+                    torch.full((), O.SUPPRESSED, dtype=torch.uint8, device="cuda"))
+    disp = d.cpu().numpy()
+    want = disp.copy()
+    want[(5 + np.arange(n)) % t_skip != 0] = O.SKIPPED
+    idx, cnt = nsm.noscope_compact_fired(d, seg_offset=5, t_skip=t_skip)
+    torch.cuda.synchronize()
+    ref = np.flatnonzero(want == O.FIRED)
+    k = int(cnt.item())
+    assert k == len(ref)
+    assert np.array_equal(idx[:k].cpu().numpy(), ref)
+    assert np.array_equal(d.cpu().numpy(), want)
