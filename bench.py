@@ -636,11 +636,14 @@ def next_rows_extras(device, sc, gs, small, n):
     F = feats[k:].contiguous()
     t = (y[k:] != y[:-k]).to(torch.uint8).contiguous()
     wsl = N.fit_workspace(F.shape[0], g * g, 0, device)
-    iters = 100
-    ms = _time_ms(lambda: N.noscope_lr_fit(F, t, iters, l2=1e-3, ws=wsl), reps=2)
-    gb = iters * 2 * F.numel() * 8 / ms / 1e6
-    out["lr_fit"] = {"examples": F.shape[0], "features": g * g, "iters": iters, "ms": round(ms, 3),
-                     "ms_per_iter": round(ms / iters, 4), "GBps_per_iter_stream": round(gb, 1)}
+    info = {}
+    ms = _time_ms(lambda: N.noscope_lr_fit(F, t, ws=wsl, info=info), reps=2)
+    # per Newton step: one gradient/Hessian pass (n * E^2 / 2 fp64 FMAs) + one trial pass
+    E = g * g + 1
+    fl = (info["iters"] + 1) * F.shape[0] * (E * E + 4 * E) * 2 / ms / 1e9
+    out["lr_fit"] = {"examples": F.shape[0], "features": g * g, "newton_steps": info["iters"],
+                     "grad_inf": info["grad_inf"], "stop": info["stop"], "ms_incl_sync": round(ms, 3),
+                     "fp64_TFLOPs": round(fl, 2)}
     big = torch.randint(0, 2, (256 * 1024 * 1024,), dtype=torch.uint8, device=device)
     ref2 = big.roll(7)
     ms = _time_ms(lambda: N.noscope_eval_labels(big, ref2))
@@ -676,7 +679,7 @@ def next_rows_extras(device, sc, gs, small, n):
     N.noscope_cnn_train(A, p.clone(), small, y, perms[:1, :128].contiguous(), val[:64], batch=64)   # warm-up
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    hist, run = N.noscope_cnn_train(A, p, small, y, perms, val, batch=64, patience=ep)
+    hist, run = N.noscope_cnn_train(A, p, small, y, perms, val, batch=64)
     dt = time.perf_counter() - t0
     fwd = cnn_flops_per_frame((2, 32, 32))
     conv1 = 2 * 2500 * 27 * 32

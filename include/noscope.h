@@ -366,22 +366,31 @@ noscope_status noscope_block_features(const noscope_dd_config* dd, const uint8_t
                                       noscope_stream_t stream);
 
 /* Blocked-LR fit ("trains a logistic regression (LR) classifier to
- * weigh each block"; SPEC train_block_weights S:209-217; reading
- * R-22): full-batch gradient descent in fp64 on the mean log loss
- * (+ l2/2 |w|^2) over z-scored features (population mean/std per feature;
- * constant features std := 1), w = b = 0, `iters` steps
- *   r = sigmoid(X w + b) - t;  w -= lr (X^T r / n + l2 w);  b -= lr mean(r)
- * (lr <= 0 selects 4/(d+1)); returned in raw-feature form: w_host[k] = w_k/sd_k,
+ * weigh each block", P:850-853 (scikit-learn); SPEC train_block_weights
+ * S:209-217; reading R-22): the minimiser, in fp64, of
+ *   J(w, b) = mean_i [log(1 + exp(z_i)) - t_i z_i] + l2/2 |w|^2,  z_i = x_i.w + b
+ * over z-scored features x (population mean/std per feature; constant
+ * features std := 1).  l2 > 0 makes J strictly convex (a unique minimiser even
+ * on separable data; l2 = 1/n is scikit-learn's default C = 1 per example).
+ * Newton's method from w = b = 0: g = grad J; stop when max|g| <= tol;
+ * H = [X 1]^T diag(p(1-p)) [X 1]/n + l2 diag(1..1, 0); Delta = -H^{-1} g
+ * (Cholesky); step = the first of 1, 1/2, ..., 2^-15 meeting Armijo
+ * J(v + s Delta) <= J(v) + 1e-4 s g.Delta (none: stop, the rounding floor is
+ * reached); at most max_iters steps.  Reductions run in a fixed order
+ * (bitwise reproducible).  Returned in raw-feature form: w_host[k] = w_k/sd_k,
  * w_host[d] = b - sum_k w_k mu_k / sd_k, so the DD logit b + sum w_k m_k of
  * noscope_dd_config (lr_weights = (float)w_host[0..d), lr_bias = (float)w_host[d])
- * reproduces the fitted model.  feats: device fp64 [n][d] (finite); targets:
- * device u8 [n] (nonzero = 1); w_host: host fp64 [d + 1].  Synchronous.
- * NOSCOPE_DATA: n < 2, one class only, or a non-finite feature (use the
- * global metric).  NOSCOPE_SHAPE if n / min(1024, ceil(n/256)) rows per CTA
- * exceed shared memory (n > ~28 M).                                         */
+ * reproduces the fitted model.  feats: device fp64 [n][d] (finite), d <= 256;
+ * targets: device u8 [n] (nonzero = 1); w_host: host fp64 [d + 1]; info_host
+ * (nullable): host fp64 [4] = accepted Newton steps, max|g| at the result, J
+ * at the result, stop reason (1 tol met, 2 no Armijo step, 3 max_iters).
+ * Synchronous (one host sync per Newton step).
+ * NOSCOPE_INVALID_ARGUMENT: l2 <= 0, tol < 0 or NaN, max_iters < 0.
+ * NOSCOPE_SHAPE: d > 256.  NOSCOPE_DATA: n < 2, one class only, or a
+ * non-finite feature (use the global metric).                        */
 noscope_status noscope_lr_fit(const double* feats, const uint8_t* targets, int64_t n, int32_t d,
-                              int32_t iters, double lr, double l2, double* w_host, void* ws,
-                              size_t ws_bytes, noscope_stream_t stream);
+                              int32_t max_iters, double tol, double l2, double* w_host, double* info_host,
+                              void* ws, size_t ws_bytes, noscope_stream_t stream);
 
 /* ---- Full CBO search -------------------------------
  * the CBO profiles every difference detector and every specialized
@@ -445,9 +454,13 @@ noscope_status noscope_eval_labels(const uint8_t* pred, const uint8_t* ref, int6
  *   v <- rho v + (1-rho) g^2;  p <- p - lr g / (sqrt(v) + eps)
  * on every parameter, one step per mini-batch of `batch` frames (last partial).
  * Epoch e visits perms[e][0..n_train) (device int32 frame indices into small,
- * the shuffled order is the caller's); after each epoch the mean loss over
- * val_idx decides early stopping: stop after `patience` epochs without a new
- * best, and leave the best epoch's parameters in `params`.
+ * the shuffled order is the caller's).  An epoch's training loss is the mean
+ * over its samples of the loss of their mini-batch before that batch's update;
+ * after each epoch the mean loss over val_idx (cross-validation) is recorded.
+ * Training stops after the first epoch e >= 1 whose training loss exceeds
+ * epoch e-1's ("early stopping if the training loss increases",
+ * S:317), or after cfg.epochs epochs; `params` is left holding the parameters
+ * of the epoch with the lowest cross-validation loss (earliest on ties).
  * params: device fp32 [noscope_cnn_param_count] in this order, each row-major:
  *   for each conv layer l: w [Cout][3][3][Cin], b [Cout]; then fc1 w [D][K]
  *   ((h, w, c) feature order), fc1 b [D], fc2 w [D], fc2 b [1].
@@ -456,7 +469,7 @@ noscope_status noscope_eval_labels(const uint8_t* pred, const uint8_t* ref, int6
  * explicit im2col rows (plain library GEMMs); everything else in this
  * library's kernels.  Synchronous (one host sync per epoch).                 */
 typedef struct {
-  int32_t batch, epochs, patience;
+  int32_t batch, epochs;   /* mini-batch size; maximum epochs (the paper's 1-5) */
   float lr, rho, eps;
 } noscope_train_config;
 int64_t noscope_cnn_param_count(const noscope_cnn_arch* arch);

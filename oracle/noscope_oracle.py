@@ -475,8 +475,9 @@ def sweep_greedy_paper(s, z, y, a, delta, u, timing, fp_limit, fn_limit):
 #    P:577-581 / P:850-853 "trains a logistic regression (LR) classifier to weigh
 #    each block"; SPEC build_reference_image S:134-142, train_block_weights
 #    S:209-217.  Readings: R-21 rounding half up, on the 50x50 small
-#    frames the DD compares; R-22 LR = full-batch gradient descent on the mean log
-#    loss (+ l2/2 |w|^2) over z-scored features, folded back to raw features.
+#    frames the DD compares; R-22 LR = the minimiser of the mean log loss
+#    (+ l2/2 |w|^2, l2 > 0) over z-scored features (Newton's method to a gradient
+#    tolerance), folded back to raw features.
 # --------------------------------------------------------------------------
 def reference_image(small: np.ndarray, labels: np.ndarray) -> np.ndarray:
     """small uint8 [n, h, w, 3], labels [n] (0 = no object).  Per-pixel mean over
@@ -505,39 +506,72 @@ def block_features(small: np.ndarray, grid: int, mode: int, ref=None, k: int = 0
     return out
 
 
-def lr_fit(F: np.ndarray, t: np.ndarray, iters: int, lr: float = 0.0, l2: float = 0.0):
-    """Logistic regression by full-batch gradient descent (R-22), fp64.
+LR_STEP_LADDER = [2.0 ** -i for i in range(16)]     # backtracking steps 1, 1/2, ..., 2^-15
+LR_ARMIJO_C = 1e-4
 
-    X = (F - mu) / sd per feature (sd = population std; constant features sd := 1),
-    w = 0, b = 0; each iteration, in this order:
-        p = 1 / (1 + exp(-(X w + b)));  r = p - t
-        w <- w - lr * (X^T r / n + l2 * w);  b <- b - lr * mean(r)
-    lr <= 0 selects 4 / (d + 1) (the log loss Hessian is <= (d + 1) / 4 on
-    z-scored features, so the step is a guaranteed descent).  Returns raw-feature
-    parameters (w / sd, b - sum(w * mu / sd)) so that the scorer's logit
-    b + sum_k w_k m_k equals the fitted model's.  Errors: n < 2 or one class only
-    (S:212, "advising global metric")."""
+
+def lr_objective(X, t, v, l2: float) -> float:
+    """J(w, b) = mean_i [softplus(z_i) - t_i z_i] + l2/2 |w|^2,  z = X w + b (X z-scored)."""
+    z = X @ v[:-1] + v[-1]
+    return float(np.mean(np.logaddexp(0.0, z) - t * z) + 0.5 * l2 * np.dot(v[:-1], v[:-1]))
+
+
+def lr_fit(F: np.ndarray, t: np.ndarray, l2: float | None = None, tol: float = 1e-9, max_iters: int = 100,
+           info: dict | None = None):
+    """Logistic regression (R-22), fp64: the minimiser of
+        J(w, b) = mean_i [log(1 + exp(z_i)) - t_i z_i] + l2/2 |w|^2,   z_i = x_i . w + b,
+    x_i = (F_i - mu) / sd per feature (population mean / std; constant features sd := 1).
+    l2 > 0 (default 1/n: scikit-learn's C = 1 written per example, P:850-851 names
+    scikit-learn) makes J strictly convex, so the minimiser exists and is unique even on
+    separable data.  Found by Newton's method from v = (w, b) = 0; each iteration:
+        p = sigmoid(z);  g = [X^T (p - t) / n + l2 w ;  mean(p - t)]
+        stop if max|g| <= tol
+        H = [X 1]^T diag(p (1 - p)) [X 1] / n + l2 diag(1, .., 1, 0)
+        Delta = -H^{-1} g                                  (Cholesky solve)
+        s = first of 1, 1/2, ..., 2^-15 with J(v + s Delta) <= J(v) + 1e-4 s g.Delta
+            (Armijo backtracking); if none, stop (the rounding floor is reached)
+        v = v + s Delta
+    Returns raw-feature parameters (w / sd, b - sum(w * mu / sd)) so that the scorer's
+    logit b + sum_k w_k m_k equals the fitted model's.  info (optional dict) receives
+    iters, grad_inf (max|g| at the returned point) and J.  Errors: n < 2 or one class
+    only (S:212, "advising global metric"), l2 <= 0."""
     F = np.asarray(F, dtype=np.float64)
     t = np.asarray(t, dtype=np.float64)
     n, d = F.shape
     if n < 2 or t.min() == t.max():
         raise ValueError("LR fit needs >= 2 examples of both classes; use the global metric")
+    if l2 is None:
+        l2 = 1.0 / n
+    if not l2 > 0:
+        raise ValueError("l2 must be > 0 (a minimiser must exist)")
     mu = F.mean(axis=0)
     sd = F.std(axis=0)
     sd = np.where(sd > 0, sd, 1.0)
     X = (F - mu) / sd
-    if lr <= 0:
-        lr = 4.0 / (d + 1)
-    w = np.zeros(d)
-    b = 0.0
-    for _ in range(iters):
-        p = 1.0 / (1.0 + np.exp(-(X @ w + b)))
-        r = p - t
-        gw = X.T @ r / n + l2 * w
-        gb = r.mean()
-        w = w - lr * gw
-        b = b - lr * gb
-    return w / sd, b - float(np.sum(w * mu / sd))
+    X1 = np.hstack([X, np.ones((n, 1))])
+    reg = np.full(d + 1, l2)
+    reg[d] = 0.0
+    v = np.zeros(d + 1)
+    it = 0
+    while True:
+        p = 1.0 / (1.0 + np.exp(-(X1 @ v)))
+        g = X1.T @ (p - t) / n + reg * v
+        if np.max(np.abs(g)) <= tol or it >= max_iters:
+            break
+        H = (X1 * (p * (1.0 - p))[:, None]).T @ X1 / n + np.diag(reg)
+        L = np.linalg.cholesky(H)
+        delta = -np.linalg.solve(L.T, np.linalg.solve(L, g))
+        J0, slope = lr_objective(X, t, v, l2), float(g @ delta)
+        step = next((s for s in LR_STEP_LADDER
+                     if lr_objective(X, t, v + s * delta, l2) <= J0 + LR_ARMIJO_C * s * slope), None)
+        if step is None:
+            break
+        v = v + step * delta
+        it += 1
+    if info is not None:
+        info.update(iters=it, grad_inf=float(np.max(np.abs(g))), J=lr_objective(X, t, v, l2))
+    w = v[:d]
+    return w / sd, v[d] - float(np.sum(w * mu / sd))
 
 
 def lr_loss(F, t, w_raw, b_raw, l2: float = 0.0) -> float:
@@ -669,7 +703,9 @@ def factor_analysis(frames_hw3, cfg: DDConfig, arch, weights, lo, hi, truth, tim
 #    the inference normalisation O6); mean binary cross-entropy on the logit;
 #    RMSprop v <- rho v + (1 - rho) g^2, w <- w - lr g / (sqrt(v) + eps); the
 #    mini-batch order is an input (a permutation per epoch); max-pool gradients go
-#    to the first maximum of each window in (dy, dx) row-major order.
+#    to the first maximum of each window in (dy, dx) row-major order; stop after
+#    the first epoch whose training loss rose, return the best
+#    cross-validation epoch.
 # --------------------------------------------------------------------------
 def cnn_params_from_weights(weights: dict) -> dict:
     """bf16-bit weight dict (synthgen layout) -> fp64 parameter dict."""
@@ -771,17 +807,30 @@ def _copy_params(P):
     return {k: ([x.copy() for x in v] if isinstance(v, list) else v.copy()) for k, v in P.items()}
 
 
+def train_should_stop(hist) -> bool:
+    """P:474-475 "early stopping if the training loss increases" ("stops early
+    when epoch-end training loss exceeds the previous epoch's"): after epoch e >= 1,
+    stop iff train_loss[e] > train_loss[e - 1] (strict)."""
+    e = len(hist) - 1
+    if e > 0 and hist[e][0] > hist[e - 1][0]:
+        return True
+    return False
+
+
 def cnn_train(small_tr, y_tr, small_va, y_va, arch, P0: dict, perms, batch: int, lr=1e-3, rho=0.9,
-              eps=1e-7, patience=1):
-    """RMSprop over epochs (len(perms)); each epoch visits perms[e] in mini-batches
-    of `batch` (last one partial); after each epoch the cross-validation loss
-    decides early stopping: stop after `patience` epochs without improvement,
-    return the best epoch's parameters.  Returns (params, history) with history
-    = list of (train_loss, val_loss) per epoch run (train loss = mean over the
-    epoch's samples of the loss of their batch before its update)."""
+              eps=1e-7):
+    """RMSprop over at most len(perms) epochs (the paper's 1-5); epoch e visits
+    perms[e] in mini-batches of `batch` (last one partial).  The epoch's training loss is
+    the mean over its samples of the loss of their batch before that batch's update
+    (Keras's reported epoch loss; P:472 names Keras).  After each epoch the
+    cross-validation loss is recorded; training stops after the first epoch whose
+    training loss exceeds the previous epoch's (train_should_stop), and the parameters
+    of the epoch with the lowest cross-validation loss (earliest on ties) are returned
+    (S:317).  Returns (params, history) with history = [(train_loss, val_loss)] per
+    epoch run."""
     P = _copy_params(P0)
     V = _zeros_like_params(P)
-    best, best_val, since, hist = _copy_params(P), math.inf, 0, []
+    best, best_val, hist = _copy_params(P), math.inf, []
     for perm in perms:
         tot = 0.0
         for s in range(0, len(perm), batch):
@@ -793,9 +842,7 @@ def cnn_train(small_tr, y_tr, small_va, y_va, arch, P0: dict, perms, batch: int,
         val = bce_with_logits(zv, y_va)
         hist.append((tot / len(perm), val))
         if val < best_val:
-            best, best_val, since = _copy_params(P), val, 0
-        else:
-            since += 1
-            if since >= patience:
-                break
+            best, best_val = _copy_params(P), val
+        if train_should_stop(hist):
+            break
     return best, hist

@@ -184,8 +184,8 @@ noscope_status launch_reference_image(const uint8_t* small, int64_t pitch, int b
                                       cudaStream_t st);
 noscope_status launch_block_features(const noscope_dd_config& c, const uint8_t* small, int64_t pitch,
                                      int64_t n, double* feats, cudaStream_t st);
-noscope_status launch_lr_fit(const double* F, const uint8_t* t, int64_t n, int d, int iters, double lr,
-                             double l2, double* wb_host, void* ws, cudaStream_t st);
+noscope_status launch_lr_fit(const double* F, const uint8_t* t, int64_t n, int d, int max_iters, double tol,
+                             double l2, double* wb_host, double* info_host, void* ws, cudaStream_t st);
 
 // CBO search helper (cbo.cu).
 noscope_status launch_records_a(const double* score, const uint8_t* y, int64_t n, int mode, int k,

@@ -496,16 +496,17 @@ noscope_status noscope_block_features(const noscope_dd_config* dd, const uint8_t
 }
 
 noscope_status noscope_lr_fit(const double* feats, const uint8_t* targets, int64_t n, int32_t d,
-                              int32_t iters, double lr, double l2, double* w_host, void* ws,
-                              size_t ws_bytes, noscope_stream_t stream) {
-  if (!feats || !targets || !w_host || !ws || d < 1 || iters < 0 || std::isnan(lr) || std::isnan(l2) ||
-      l2 < 0)
+                              int32_t max_iters, double tol, double l2, double* w_host, double* info_host,
+                              void* ws, size_t ws_bytes, noscope_stream_t stream) {
+  if (!feats || !targets || !w_host || !ws || d < 1 || max_iters < 0 || !(tol >= 0) || !(l2 > 0) ||
+      !std::isfinite(l2))
     return NOSCOPE_INVALID_ARGUMENT;
+  if (d > 256) return NOSCOPE_SHAPE;
   if (n < 2) return NOSCOPE_DATA;
   if (ws_bytes < fit_ws_bytes(n, d, 0)) return NOSCOPE_WORKSPACE_TOO_SMALL;
   noscope_status s = check_device();
   if (s != NOSCOPE_OK) return s;
-  return launch_lr_fit(feats, targets, n, d, iters, lr, l2, w_host, ws, (cudaStream_t)stream);
+  return launch_lr_fit(feats, targets, n, d, max_iters, tol, l2, w_host, info_host, ws, (cudaStream_t)stream);
 }
 
 // ---- Full CBO search (cbo.cu helper + the existing entry points)
@@ -658,7 +659,7 @@ noscope_status noscope_cnn_train(const noscope_cnn_arch* arch, const noscope_tra
   if (!arch || !cfg || !params || !small || !labels || !perms || !history_host || !epochs_run_host || !ws)
     return NOSCOPE_INVALID_ARGUMENT;
   if (!cnn_arch_supported(*arch)) return NOSCOPE_SHAPE;
-  if (cfg->batch < 1 || cfg->batch > 1024 || cfg->epochs < 1 || cfg->patience < 1 || !(cfg->lr > 0) ||
+  if (cfg->batch < 1 || cfg->batch > 1024 || cfg->epochs < 1 || !(cfg->lr > 0) ||
       !(cfg->rho >= 0 && cfg->rho < 1) || !(cfg->eps > 0) || n_train < 1 || n_val < 0 || (n_val > 0 && !val_idx))
     return NOSCOPE_INVALID_ARGUMENT;
   if (small_pitch % 16 || small_pitch < 7504) return NOSCOPE_SHAPE;

@@ -388,8 +388,8 @@ noscope_status launch_cnn_train(const noscope_cnn_arch& a, const noscope_train_c
     fill_kernel<<<grid_for(nr), kT, 0, st>>>(w.ones, nr, 1.0f);
   }
   NS_CUDA_TRY(cudaMemcpyAsync(w.best, P, p.nparams * 4, cudaMemcpyDeviceToDevice, st));
-  double best_val = INFINITY;
-  int since = 0, run = 0;
+  double best_val = INFINITY, prev_tr = INFINITY;
+  int run = 0;
   for (int e = 0; e < cfg.epochs; ++e) {
     NS_CUDA_TRY(cudaMemsetAsync(w.loss, 0, 8, st));
     for (int64_t s0 = 0; s0 < n_train; s0 += cfg.batch) {
@@ -414,13 +414,15 @@ noscope_status launch_cnn_train(const noscope_cnn_arch& a, const noscope_train_c
     hist[2 * e] = tr;
     hist[2 * e + 1] = va;
     run = e + 1;
+    // keep the best cross-validation epoch; stop after the first epoch
+    // whose training loss rose ("early stopping if the training loss
+    // increases")
     if (va < best_val) {
       best_val = va;
-      since = 0;
       NS_CUDA_TRY(cudaMemcpyAsync(w.best, P, p.nparams * 4, cudaMemcpyDeviceToDevice, st));
-    } else if (++since >= cfg.patience) {
-      break;
     }
+    if (e > 0 && tr > prev_tr) break;
+    prev_tr = tr;
   }
   NS_CUDA_TRY(cudaMemcpyAsync(P, w.best, p.nparams * 4, cudaMemcpyDeviceToDevice, st));
   NS_CUDA_TRY(cudaStreamSynchronize(st));

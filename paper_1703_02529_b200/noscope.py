@@ -91,7 +91,7 @@ class EvalCounts(C.Structure):
 
 
 class TrainConfig(C.Structure):
-    _fields_ = [("batch", c_i32), ("epochs", c_i32), ("patience", c_i32), ("lr", c_f32), ("rho", c_f32),
+    _fields_ = [("batch", c_i32), ("epochs", c_i32), ("lr", c_f32), ("rho", c_f32),
                 ("eps", c_f32)]
 
 
@@ -158,7 +158,7 @@ def lib():
     L.noscope_block_features.argtypes = [C.POINTER(DDConfig), c_p, c_i64, c_i64, c_p, c_p]
     L.noscope_lr_fit.restype = c_i32
     L.noscope_lr_fit.argtypes = [c_p, c_p, c_i64, c_i32, c_i32, C.c_double, C.c_double,
-                                 C.POINTER(C.c_double), c_p, c_sz, c_p]
+                                 C.POINTER(C.c_double), C.POINTER(C.c_double), c_p, c_sz, c_p]
     L.noscope_cbo_workspace_bytes.restype = c_sz
     L.noscope_cbo_workspace_bytes.argtypes = [C.POINTER(CboCNN), c_i32, c_i64, c_i32, c_i32]
     L.noscope_cbo_search.restype = c_i32
@@ -436,14 +436,20 @@ def noscope_block_features(dd: DD, small: torch.Tensor, n=None, feats=None, stre
     return feats
 
 
-def noscope_lr_fit(feats: torch.Tensor, targets: torch.Tensor, iters: int, lr=0.0, l2=0.0, ws=None,
-                   stream=None):
-    """feats: device f64 [n, d]; targets: device u8 [n] -> (w numpy f64 [d], b float), raw-feature form."""
+def noscope_lr_fit(feats: torch.Tensor, targets: torch.Tensor, l2=None, tol=1e-9, max_iters=100, ws=None,
+                   stream=None, info: dict | None = None):
+    """feats: device f64 [n, d]; targets: device u8 [n] -> (w numpy f64 [d], b float), raw-feature
+    form.  l2 defaults to 1/n (include/noscope.h).  `info` (optional dict) receives iters,
+    grad_inf, J and stop."""
     n, d = feats.shape
+    l2 = 1.0 / n if l2 is None else l2
     ws = ws if ws is not None else fit_workspace(n, d, 0, feats.device)
     out = (C.c_double * (d + 1))()
-    _check(lib().noscope_lr_fit(_ptr(feats), _ptr(targets), n, d, int(iters), float(lr), float(l2), out,
-                                _ptr(ws), ws.numel(), _stream(stream)), "noscope_lr_fit")
+    inf = (C.c_double * 4)()
+    _check(lib().noscope_lr_fit(_ptr(feats), _ptr(targets), n, d, int(max_iters), float(tol), float(l2), out,
+                                inf, _ptr(ws), ws.numel(), _stream(stream)), "noscope_lr_fit")
+    if info is not None:
+        info.update(iters=int(inf[0]), grad_inf=inf[1], J=inf[2], stop=int(inf[3]))
     import numpy as np
     v = np.array(out[:], dtype=np.float64)
     return v[:d], float(v[d])
@@ -506,14 +512,14 @@ def params_from_weight_dict(arch: Arch, w: dict, device="cuda"):
 
 def noscope_cnn_train(arch: Arch, params: torch.Tensor, small: torch.Tensor, labels: torch.Tensor,
                       perms: torch.Tensor, val_idx: torch.Tensor, batch=32, lr=1e-3, rho=0.9, eps=1e-7,
-                      patience=1, stream=None):
+                      stream=None):
     """params: device fp32 (updated in place to the best epoch's); perms: device int32
     [epochs, n_train]; val_idx: device int32 [n_val].  Returns (history, epochs_run)."""
     epochs, n_train = perms.shape
     ac = arch.c()
     nb = lib().noscope_cnn_train_workspace_bytes(C.byref(ac), batch)
     ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=params.device)
-    cfg = TrainConfig(batch, epochs, patience, lr, rho, eps)
+    cfg = TrainConfig(batch, epochs, lr, rho, eps)
     hist = (C.c_double * (2 * epochs))()
     run = c_i32(0)
     _check(lib().noscope_cnn_train(C.byref(ac), C.byref(cfg), _ptr(params), _ptr(small), small.shape[1],

@@ -100,10 +100,13 @@ def test_next_row_entry_points_validate_before_device_use(lib):
     assert lib.noscope_block_features(ctypes.byref(dd), v, 7504, 4, v, None) == 2
     dd = N.DD(mode=0, metric=1, grid=10).c()
     assert lib.noscope_block_features(ctypes.byref(dd), v, 7504, 4, v, None) == 1
-    # LR fit: n < 2 is a data error, negative l2 an argument error
+    # LR fit: n < 2 is a data error; l2 <= 0 (no minimiser), tol < 0 argument errors; d > 256 shape
     out = (ctypes.c_double * 3)()
-    assert lib.noscope_lr_fit(v, v, 1, 2, 10, 0.0, 0.0, out, v, 1 << 20, None) == 6
-    assert lib.noscope_lr_fit(v, v, 10, 2, 10, 0.0, -1.0, out, v, 1 << 20, None) == 1
+    assert lib.noscope_lr_fit(v, v, 1, 2, 10, 1e-9, 0.1, out, None, v, 1 << 20, None) == 6
+    assert lib.noscope_lr_fit(v, v, 10, 2, 10, 1e-9, -1.0, out, None, v, 1 << 20, None) == 1
+    assert lib.noscope_lr_fit(v, v, 10, 2, 10, 1e-9, 0.0, out, None, v, 1 << 20, None) == 1
+    assert lib.noscope_lr_fit(v, v, 10, 2, 10, -1.0, 0.1, out, None, v, 1 << 20, None) == 1
+    assert lib.noscope_lr_fit(v, v, 10, 257, 10, 1e-9, 0.1, out, None, v, 1 << 20, None) == 2
     # eval: window / agree_min consistency
     cnt = N.EvalCounts()
     assert lib.noscope_eval_labels(v, v, 90, 30, 31, ctypes.byref(cnt), v, 256, None) == 1

@@ -53,31 +53,70 @@ def test_one_step_gradients(L, C):
     assert abs(hist[0][0] - hist_o[0][0]) <= 1e-5 * abs(hist_o[0][0])     # loss before the step
 
 
-def test_training_epochs_and_early_stopping():
+def _toy(n, seed, learnable=True):
+    """The oracle pins' toy task (tests/test_oracle_train.py::_toy), in the ABI layout."""
+    rng = np.random.default_rng(seed)
+    g = rng.integers(40, 90, (n, 50, 50, 3), dtype=np.uint8)
+    t = (rng.random(n) < 0.5).astype(np.uint8)
+    if learnable:
+        for i in np.flatnonzero(t):
+            y0, x0 = rng.integers(0, 34, 2)
+            g[i, y0:y0 + 16, x0:x0 + 16, :] = 230
+    small = np.zeros((n, 7504), np.uint8)
+    small[:, :7500] = g.reshape(n, -1)
+    return rng, small, g, t
+
+
+def test_training_continues_while_val_loss_rises():
+    """stopping follows the TRAINING loss.  Cross-validation labels flipped:
+    the validation loss rises every epoch while the training loss falls, so all 4
+    epochs run on both sides and the parameters returned are epoch 1's."""
     nsm = ns()
-    n_tr, n_va = 96, 32
-    small, g, y = _data(n_tr + n_va, 7)
+    rng, small, g, t = _toy(80, 2)
     arch = sg.CnnArch(2, 32, 32)
-    w = sg.he_normal_weights(arch, 8)
+    w = sg.he_normal_weights(arch, 4)
+    perms = np.stack([rng.permutation(64) for _ in range(4)]).astype(np.int32)
+    lab = t.copy()
+    lab[64:] = 1 - lab[64:]
     A = nsm.Arch(2, 32, 32)
-    rng = np.random.default_rng(3)
-    perms = np.stack([rng.permutation(n_tr) for _ in range(4)]).astype(np.int32)
     p = nsm.params_from_weight_dict(A, w)
-    hist, run = nsm.noscope_cnn_train(A, p, torch.from_numpy(small).cuda(), torch.from_numpy(y).cuda(),
+    hist, run = nsm.noscope_cnn_train(A, p, torch.from_numpy(small).cuda(), torch.from_numpy(lab).cuda(),
                                       torch.from_numpy(perms).cuda(),
-                                      torch.arange(n_tr, n_tr + n_va, dtype=torch.int32, device="cuda"),
-                                      batch=16, lr=1e-3, patience=1)
-    P, hist_o = O.cnn_train(g[:n_tr], y[:n_tr], g[n_tr:], y[n_tr:], arch, O.cnn_params_from_weights(w),
-                            list(perms), 16, lr=1e-3, patience=1)
-    assert run == len(hist_o)
+                                      torch.arange(64, 80, dtype=torch.int32, device="cuda"), batch=16, lr=1e-3)
+    _, hist_o = O.cnn_train(g[:64], t[:64], g[64:], lab[64:], arch, O.cnn_params_from_weights(w),
+                            list(perms), 16, lr=1e-3)
+    assert run == len(hist_o) == 4
     for (a, b), (c, d) in zip(hist, hist_o):
         assert abs(a - c) <= 2e-3 * abs(c) and abs(b - d) <= 2e-3 * abs(d), (hist, hist_o)
-    # the returned parameters are the best epoch's: their val loss is the minimum
-    best = min(h[1] for h in hist)
+    # the returned parameters are epoch 1's (the lowest validation loss)
     Wt = nsm.noscope_cnn_params_to_weights(A, p, nsm.Weights(w))
-    z = nsm.noscope_specialized_infer(A, Wt, torch.from_numpy(small[n_tr:]).cuda()).cpu().numpy()
-    bce = float(np.mean(np.logaddexp(0, z) - y[n_tr:] * z))
-    assert abs(bce - best) < 0.05 * abs(best) + 0.02      # bf16 inference of the trained fp32 model
+    z = nsm.noscope_specialized_infer(A, Wt, torch.from_numpy(small[64:]).cuda()).cpu().numpy()
+    bce = float(np.mean(np.logaddexp(0, z) - lab[64:] * z))
+    assert abs(bce - hist[0][1]) < 0.05 * abs(hist[0][1]) + 0.02      # bf16 inference of the fp32 model
+
+
+def test_training_stops_when_training_loss_rises():
+    """an oversized learning rate on random labels makes the training loss rise
+    after it first fell; the GPU stops at that epoch (its own history obeys the rule:
+    every earlier epoch did not rise, the last one did) and returns its best
+    cross-validation epoch.  (This regime is chaotic, so fp32 and fp64 trajectories
+    are compared only through the rule, not value by value.)"""
+    nsm = ns()
+    rng, small, g, t = _toy(48, 2, learnable=False)
+    arch = sg.CnnArch(2, 32, 32)
+    w = sg.he_normal_weights(arch, 4)
+    perms = np.stack([rng.permutation(32) for _ in range(5)]).astype(np.int32)
+    A = nsm.Arch(2, 32, 32)
+    p = nsm.params_from_weight_dict(A, w)
+    hist, run = nsm.noscope_cnn_train(A, p, torch.from_numpy(small).cuda(), torch.from_numpy(t).cuda(),
+                                      torch.from_numpy(perms).cuda(),
+                                      torch.arange(32, 48, dtype=torch.int32, device="cuda"), batch=8, lr=3e-3)
+    assert run == len(hist) < 5
+    tr = [h[0] for h in hist]
+    assert tr[-1] > tr[-2] and all(tr[e] <= tr[e - 1] for e in range(1, run - 1))
+    _, hist_o = O.cnn_train(g[:32], t[:32], g[32:], t[32:], arch, O.cnn_params_from_weights(w),
+                            list(perms), 8, lr=3e-3)
+    assert len(hist_o) < 5          # the oracle also stops early on this instance
 
 
 def test_params_to_weights_rounding():

@@ -92,21 +92,78 @@ def test_rmsprop_matches_torch():
     assert np.allclose(P["fc1_w"], tp.detach().numpy(), rtol=1e-13, atol=1e-15)
 
 
-def test_training_learns_and_early_stops():
-    """A learnable toy task (a bright square present or not) drives the loss down;
-    early stopping returns the best epoch's parameters."""
-    rng = np.random.default_rng(2)
-    n = 96
+def _toy(n, seed, learnable=True):
+    rng = np.random.default_rng(seed)
     small = rng.integers(40, 90, (n, 50, 50, 3), dtype=np.uint8)
     t = (rng.random(n) < 0.5).astype(np.uint8)
-    for i in np.flatnonzero(t):
-        y0, x0 = rng.integers(0, 34, 2)
-        small[i, y0:y0 + 16, x0:x0 + 16, :] = 230
+    if learnable:                                           # a bright square iff positive
+        for i in np.flatnonzero(t):
+            y0, x0 = rng.integers(0, 34, 2)
+            small[i, y0:y0 + 16, x0:x0 + 16, :] = 230
+    return rng, small, t
+
+
+@pytest.mark.parametrize("hist,stop", [
+    ([(1.0, 0.5)], False),                          # epoch 1 has no predecessor
+    ([(1.0, 0.5), (0.9, 0.9)], False),              # train falls, val rises -> continue
+    ([(1.0, 0.5), (1.0, 0.4)], False),              # equal is not an increase
+    ([(1.0, 0.5), (1.1, 0.4)], True),               # train rises -> stop, even if val improved
+    ([(3.0, 1.0), (2.0, 1.0), (2.5, 0.1)], True),
+])
+def test_stop_rule_is_training_loss_increase(hist, stop):
+    """P:474-475 "early stopping if the training loss increases"; "stops early
+    when epoch-end training loss exceeds the previous epoch's"."""
+    assert O.train_should_stop(hist) is stop
+
+
+def test_training_learns_and_returns_best_val_epoch():
+    """A learnable toy task drives the training loss down over all epochs (no stop);
+    the returned parameters are the best cross-validation epoch's."""
+    rng, small, t = _toy(96, 2)
     arch = sg.CnnArch(2, 32, 32)
     P0 = O.cnn_params_from_weights(sg.he_normal_weights(arch, 4))
     perms = [rng.permutation(64) for _ in range(3)]
     P, hist = O.cnn_train(small[:64], t[:64], small[64:], t[64:], arch, P0, perms, 16, lr=1e-3)
-    assert hist[-1][0] < hist[0][0]                          # training loss decreases
+    assert len(hist) == 3 and hist[2][0] < hist[1][0] < hist[0][0]
     best = min(range(len(hist)), key=lambda e: hist[e][1])
     zb, _ = O.cnn_forward_train(small[64:], arch, P)
-    assert abs(O.bce_with_logits(zb, t[64:]) - hist[best][1]) < 1e-12   # best epoch returned
+    assert abs(O.bce_with_logits(zb, t[64:]) - hist[best][1]) < 1e-12
+
+
+def test_training_continues_while_val_loss_rises():
+    """Cross-validation labels flipped: the training loss keeps falling while the
+    validation loss rises every epoch.  The paper's rule keeps training (all 4
+    epochs run); the parameters returned are epoch 1's (lowest validation loss)."""
+    rng, small, t = _toy(80, 2)
+    arch = sg.CnnArch(2, 32, 32)
+    P0 = O.cnn_params_from_weights(sg.he_normal_weights(arch, 4))
+    perms = [rng.permutation(64) for _ in range(4)]
+    P, hist = O.cnn_train(small[:64], t[:64], small[64:], 1 - t[64:], arch, P0, perms, 16, lr=1e-3)
+    assert len(hist) == 4
+    assert all(hist[e][0] < hist[e - 1][0] and hist[e][1] > hist[e - 1][1] for e in range(1, 4))
+    zb, _ = O.cnn_forward_train(small[64:], arch, P)
+    assert abs(O.bce_with_logits(zb, 1 - t[64:]) - hist[0][1]) < 1e-12
+
+
+def test_training_stops_when_training_loss_rises():
+    """an oversized learning rate on unlearnable (random) labels makes the
+    training loss rise after it first fell -> training stops at that epoch although
+    more epochs were allowed; the best cross-validation epoch is returned."""
+    rng, small, t = _toy(48, 2, learnable=False)
+    arch = sg.CnnArch(2, 32, 32)
+    P0 = O.cnn_params_from_weights(sg.he_normal_weights(arch, 4))
+    perms = [rng.permutation(32) for _ in range(5)]
+    P, hist = O.cnn_train(small[:32], t[:32], small[32:], t[32:], arch, P0, perms, 8, lr=3e-3)
+    assert len(hist) == 3 and hist[2][0] > hist[1][0] < hist[0][0]
+    best = min(range(3), key=lambda e: hist[e][1])
+    zb, _ = O.cnn_forward_train(small[32:], arch, P)
+    assert abs(O.bce_with_logits(zb, t[32:]) - hist[best][1]) < 1e-12
+
+
+def test_training_one_epoch():
+    """max_epochs = 1 -> exactly one epoch of updates."""
+    rng, small, t = _toy(40, 3)
+    arch = sg.CnnArch(2, 32, 32)
+    P0 = O.cnn_params_from_weights(sg.he_normal_weights(arch, 5))
+    P, hist = O.cnn_train(small[:32], t[:32], small[32:], t[32:], arch, P0, [rng.permutation(32)], 8, lr=1e-3)
+    assert len(hist) == 1
