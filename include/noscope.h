@@ -22,8 +22,9 @@
  *    (any CUDA allocation visible to the current device, e.g. the PyTorch
  *    caching allocator); *_host pointers are host memory.  The caller owns
  *    every buffer; the library never allocates or frees device memory and
- *    holds no global state, so calls on different streams with distinct
- *    workspaces/states are independent.
+ *    holds no global state beyond per-device caches of kernel attributes and
+ *    (noscope_cnn_train only) one cuBLAS handle per host thread, so calls on
+ *    different streams with distinct workspaces/states are independent.
  *  - Work is enqueued asynchronously on `stream` (a cudaStream_t; 0 = legacy
  *    default stream).  Exceptions: noscope_threshold_sweep with phase 2/3 and
  *    any call given a non-null *_host output synchronise `stream` once to copy
@@ -100,7 +101,9 @@ typedef struct {
 typedef struct {
   int32_t mode;           /* 0 = reference image, 1 = earlier frame t-k */
   int32_t metric;         /* 0 = global MSE, 1 = blocked MSE + LR */
-  int32_t out_w, out_h;   /* downsample target (<= source), e.g. 50 x 50 */
+  int32_t out_w, out_h;   /* downsample target (<= source), e.g. 50 x 50; out_w <= 53
+                             and out_w*out_h*3*255^2 < 2^32 (u32 SSDs), else
+                             NOSCOPE_SHAPE */
   int32_t grid;           /* g for metric 1: 1 <= g <= min(out_w, out_h) */
   int32_t t_diff_frames;  /* k >= 1 (mode 1) */
   int32_t t_skip_frames;  /* >= 1 */
@@ -209,7 +212,12 @@ noscope_status noscope_stream_state_init(const noscope_dd_config* dd, void* stat
  *  disposition_out: device u8 [n_frames] NOSCOPE_SKIPPED/SUPPRESSED/FIRED.
  *  fired_idx_out: device i32 [n_frames] (nullable): ascending indices (into
  *                 this chunk) of fired frames; n_fired_dev: device i64 count.
- *  Errors: NOSCOPE_SHAPE if out_w > width or out_h > height or pitches not /16.  */
+ *  Errors: NOSCOPE_SHAPE if out_w > width or out_h > height, pitches not /16,
+ *  out_w > 53, out_w*out_h*3*255^2 >= 2^32, a box taller than 257 rows or
+ *  larger than 2,048 pixels, or one output row's source rows ("band",
+ *  box_h*width*3 bytes) too large for a 2-stage shared-memory ring (about
+ *  110 KB: every source size in PAPER.md Table 1, up to 1170x1080 -> 50x50,
+ *  is accepted; 1920x1080 -> 50x50 is not).                                  */
 noscope_status noscope_diff_detect(const noscope_dd_config* dd, const uint8_t* frames,
                                    noscope_frames_desc desc, int64_t n_frames,
                                    int64_t seg_offset, void* stream_state,
@@ -320,6 +328,16 @@ typedef struct {
 typedef struct {
   uint64_t *F, *FPnf, *FNnf, *FPf, *FNf, *GE, *GT;
 } noscope_sweep_tables;
+
+/* The a[] column of the sweep records for one unit (tau = i; oracle
+ * build_records; P:554-563 label inheritance): the label the cascade
+ * would emit for record i if it were NOT fired, from the reference labels y:
+ * skipped (s[i] == -inf) -> y[i - i % t_skip] (its period's checked frame);
+ * checked -> 0 in mode 0 (the reference image shows no object) or y[i - k] in
+ * mode 1 (0 for i < k).  s: device fp64 [n]; y, a_out: device u8 [n];
+ * t_skip, k >= 1.  Asynchronous.                                              */
+noscope_status noscope_sweep_records(const double* s, const uint8_t* y, int64_t n, int32_t mode, int32_t k,
+                                     int32_t t_skip, uint8_t* a_out, noscope_stream_t stream);
 
 size_t noscope_sweep_hist_words(int32_t n_delta, int32_t m);
 

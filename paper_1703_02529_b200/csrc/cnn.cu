@@ -367,11 +367,9 @@ noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& 
     if (s != NOSCOPE_OK) return s;
   }
 
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  static DeviceOnce attr;
+  if (attr.first())
+    NS_CUDA_TRY(cudaFuncSetAttribute(fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   if (fc_ksplit(P.K) > 1)   // FC split-K arrival counters start at zero (reset by their last CTA)
     NS_CUDA_TRY(cudaMemsetAsync(ws + P.cnt_off, 0, (size_t)(P.chunk / 128) * 4, st));
   for (int64_t base = 0; base < n_max; base += P.chunk) {

@@ -564,12 +564,10 @@ size_t conv12_fused_smem() { return (size_t)fz::kSmem; }
 
 template <int kHalves, bool kConv2>
 static noscope_status launch_variant(const FusedArgs& a, int grid, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(conv12_fused_kernel<kHalves, kConv2>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, fz::kSmem);
-    attr = true;
-  }
+  static DeviceOnce attr;
+  if (attr.first())
+    NS_CUDA_TRY(cudaFuncSetAttribute(conv12_fused_kernel<kHalves, kConv2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, fz::kSmem));
   conv12_fused_kernel<kHalves, kConv2><<<grid, fz::kThreads, fz::kSmem, st>>>(a);
   NS_LAUNCH_CHECK();
   count_launch();

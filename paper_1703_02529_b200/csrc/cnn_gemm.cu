@@ -383,11 +383,9 @@ convg_kernel(ConvGArgs A) {
 }
 
 noscope_status launch_convg(const ConvGArgs& a, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(convg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  static DeviceOnce attr;
+  if (attr.first())
+    NS_CUDA_TRY(cudaFuncSetAttribute(convg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   const ConvGGeom& g = a.g;
   const int64_t P = (int64_t)(g.H + 1) * (g.W + 1);
   const int64_t umax = (a.chunk_len * P + g.S - 1) / g.S;

@@ -279,11 +279,9 @@ convt_kernel(ConvGArgs A) {
 }
 
 noscope_status launch_convt(const ConvGArgs& a, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static DeviceOnce attr;
+  if (attr.first())
     NS_CUDA_TRY(cudaFuncSetAttribute(convt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
   const ConvGGeom& g = a.g;
   const int64_t umax = (a.chunk_len * (g.H + 1) + 15) / 16;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(umax, kNumSMs));

@@ -708,34 +708,54 @@ static size_t ds_plan(DsArgs& A, int ctas_per_sm) {
   A.stage_bytes = (stage + 127) & ~127;
   // segments of <= 10 output pixels (<= 30 lanes own one output value each)
   A.ns = std::max(1, (A.out_w + 9) / 10);
-  int ng = 4;  // 4 bands in flight per CTA (A/B on B200: 2 -> 17.3 ms, 3 -> 15.8, 4 -> 15.0, 5 -> 15.2)
-  if (const char* e = std::getenv("NOSCOPE_DD_NG")) ng = std::atoi(e);
-  ng = std::max(1, std::min({ng, kDsMaxGroups, A.out_h, kDsMaxWorkers / A.ns}));
-  A.ng = ng;
+  int ng_max = 4;  // 4 bands in flight per CTA (A/B on B200: 2 -> 17.3 ms, 3 -> 15.8, 4 -> 15.0, 5 -> 15.2)
+  if (const char* e = std::getenv("NOSCOPE_DD_NG")) ng_max = std::atoi(e);
+  ng_max = std::max(1, std::min({ng_max, kDsMaxGroups, A.out_h, kDsMaxWorkers / A.ns}));
   int cs = 0;
   for (int g = 0; g < A.ns; ++g) cs = std::max(cs, segment_of(g, A.ns, A.out_w, A.W, A.fast != 0).span);
   A.cs_stride = (cs + 7) & ~7;
   const int gg2 = ((A.grid * A.grid) + 1) & ~1;
   const int small_bytes = A.out_w * A.out_h * 3;
   auto up = [](size_t x, size_t a) { return (x + a - 1) / a * a; };
-  size_t b = kDsHeadBytes + (size_t)A.out_h * sizeof(BandInfo);
-  A.off_ref = (int)b;
-  b += A.mode == 0 ? (size_t)((small_bytes + 15) & ~15) : 0;   // reference image (mode 0)
-  A.off_blkn = (int)(b = up(b, 16));
-  b += (size_t)gg2 * 4;
-  A.off_blk = (int)(b = up(b, 16));
-  b += 2 * (size_t)gg2 * 4;                                   // blk[2] (frame parity)
-  A.off_wlr = (int)(b = up(b, 16));
-  b += 2 * (size_t)gg2 * 8;                                   // wlr, pk
-  A.off_cs = (int)(b = up(b, 16));
-  b += (size_t)A.ng * A.ns * A.cs_stride * sizeof(uint16_t);
-  A.off_stages = (int)(b = up(b, 128));
-  // ring: as many stages per group as fit (227 KB per SM less the 1 KB per-CTA reservation)
-  const size_t per_cta = (size_t)(227 * 1024) / ctas_per_sm - 1024;
-  int nsg = per_cta > b ? (int)((per_cta - b) / ((size_t)A.ng * A.stage_bytes)) : 0;
-  nsg = std::min(nsg, kDsMaxStages / A.ng);
-  A.nsg = nsg;
-  return b + (size_t)A.ng * nsg * A.stage_bytes;
+  const size_t per_cta = (size_t)(227 * 1024) / ctas_per_sm - 1024;  // less the 1 KB per-CTA reservation
+  // Fewer worker groups when bands are large (720p / 1080p sources): every group
+  // needs a ring of >= 2 stages of one band each.
+  size_t b = 0;
+  for (int ng = ng_max; ng >= 1; --ng) {
+    A.ng = ng;
+    b = kDsHeadBytes + (size_t)A.out_h * sizeof(BandInfo);
+    A.off_ref = (int)b;
+    b += A.mode == 0 ? (size_t)((small_bytes + 15) & ~15) : 0;   // reference image (mode 0)
+    A.off_blkn = (int)(b = up(b, 16));
+    b += (size_t)gg2 * 4;
+    A.off_blk = (int)(b = up(b, 16));
+    b += 2 * (size_t)gg2 * 4;                                   // blk[2] (frame parity)
+    A.off_wlr = (int)(b = up(b, 16));
+    b += 2 * (size_t)gg2 * 8;                                   // wlr, pk
+    A.off_cs = (int)(b = up(b, 16));
+    b += (size_t)A.ng * A.ns * A.cs_stride * sizeof(uint16_t);
+    A.off_stages = (int)(b = up(b, 128));
+    // ring: as many stages per group as fit
+    int nsg = per_cta > b ? (int)((per_cta - b) / ((size_t)A.ng * A.stage_bytes)) : 0;
+    A.nsg = std::min(nsg, kDsMaxStages / A.ng);
+    if (A.nsg >= 2) break;
+  }
+  return b + (size_t)A.ng * A.nsg * A.stage_bytes;
+}
+
+bool dd_frames_fit(const noscope_dd_config& cfg, const noscope_frames_desc& desc) {
+  if (desc.width == cfg.out_w && desc.height == cfg.out_h) return true;   // identity kernel, no bands
+  DsArgs A{};
+  A.W = desc.width;
+  A.H = desc.height;
+  A.RB = desc.width * 3;
+  A.out_w = cfg.out_w;
+  A.out_h = cfg.out_h;
+  A.mode = cfg.mode;
+  A.grid = cfg.metric == 1 ? cfg.grid : 1;
+  A.fast = (A.RB % 16) == 0;
+  ds_plan(A, 1);
+  return A.nsg >= 2;
 }
 
 size_t dd_flags_bytes() { return (size_t)4 * kNumSMs * 4; }
@@ -798,12 +818,10 @@ noscope_status launch_diff_detect(const noscope_dd_config& cfg, const uint8_t* f
     return NOSCOPE_OK;
   }
   if (frames_needed > 0) {
-    static bool attr_set[2] = {false, false};
+    static DeviceOnce attr_set[2];
     const int ki = kern == dd_kernel<0, 0, 0> ? 0 : 1;
-    if (!attr_set[ki]) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      attr_set[ki] = true;
-    }
+    if (attr_set[ki].first())
+      NS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     int per_sm = 0;
     NS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
     if (per_sm < 1) return NOSCOPE_SHAPE;

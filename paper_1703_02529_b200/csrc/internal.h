@@ -1,6 +1,7 @@
 // internal.h — host/device declarations shared by the NoScope CUDA sources.
 #pragma once
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -21,6 +22,24 @@ inline void prof_mark(Prof* p, cudaStream_t st) {
   if (p && p->n < 16) cudaEventRecord(p->ev[p->n++], st);
 }
 uint64_t& launch_counter();  // kernels launched by the calling host thread
+
+// Per-device caches.  Function attributes and occupancy belong to a device
+// context, so a process that drives several GPUs (cudaSetDevice between calls)
+// needs them once per device, keyed by the current device ordinal.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  return cudaGetDevice(&d) == cudaSuccess && d >= 0 && d < kMaxDevices ? d : 0;
+}
+struct DeviceOnce {           // first() is true once per device
+  std::atomic<bool> done[kMaxDevices]{};
+  bool first() { return !done[current_device()].exchange(true); }
+};
+struct DeviceInt {            // an int cached per device (0 = not yet known)
+  std::atomic<int> v[kMaxDevices]{};
+  int get() { return v[current_device()].load(); }
+  void set(int x) { v[current_device()].store(x); }
+};
 inline void count_launch(int k = 1) { launch_counter() += (uint64_t)k; }
 
 struct DsGeom {
@@ -86,6 +105,9 @@ noscope_status launch_diff_detect(const noscope_dd_config& cfg, const uint8_t* f
                                   uint8_t* state, uint8_t* small, int64_t small_pitch,
                                   double* score, uint8_t* disp, uint32_t* status,
                                   unsigned* flags, cudaStream_t st, Prof* prof = nullptr);
+// Whether dd_kernel's band ring (>= 2 stages of one output row's source rows per
+// worker group, at least one group) fits shared memory for this source size.
+bool dd_frames_fit(const noscope_dd_config& cfg, const noscope_frames_desc& desc);
 size_t dd_flags_bytes();  // workspace for the per-CTA completion flags
 noscope_status launch_state_update(const noscope_dd_config& cfg, const uint8_t* small,
                                    int64_t small_pitch, uint8_t* state, int64_t tau0, int64_t n,

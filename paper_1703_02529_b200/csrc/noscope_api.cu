@@ -18,15 +18,17 @@ namespace {
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 noscope_status check_device() {
-  static int cached = -1;
+  static DeviceInt cached;   // 1 supported, 2 not, per device
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return NOSCOPE_CUDA;
-  if (cached < 0) {
+  int c = cached.get();
+  if (c == 0) {
     cudaDeviceProp p;
     if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return NOSCOPE_CUDA;
-    cached = (p.major == 10 && p.minor == 0) ? 1 : 0;
+    c = (p.major == 10 && p.minor == 0) ? 1 : 2;
+    cached.set(c);
   }
-  return cached ? NOSCOPE_OK : NOSCOPE_UNSUPPORTED_DEVICE;
+  return c == 1 ? NOSCOPE_OK : NOSCOPE_UNSUPPORTED_DEVICE;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -36,6 +38,8 @@ noscope_status validate_dd(const noscope_dd_config* c, bool check_ptrs = true) {
   if (c->mode != 0 && c->mode != 1) return NOSCOPE_INVALID_ARGUMENT;
   if (c->metric != 0 && c->metric != 1) return NOSCOPE_INVALID_ARGUMENT;
   if (c->out_w < 1 || c->out_h < 1 || c->out_w > kMaxOutW) return NOSCOPE_SHAPE;
+  // per-frame / per-block SSDs are u32: out_w*out_h*3 values of at most 255^2
+  if ((int64_t)c->out_w * c->out_h * 3 * 65025 >= ((int64_t)1 << 32)) return NOSCOPE_SHAPE;
   if (c->t_skip_frames < 1) return NOSCOPE_INVALID_ARGUMENT;
   if (c->mode == 1 && c->t_diff_frames < 1) return NOSCOPE_INVALID_ARGUMENT;
   if (check_ptrs && c->mode == 0 && !c->ref_image) return NOSCOPE_INVALID_ARGUMENT;
@@ -57,8 +61,9 @@ noscope_status validate_frames(const noscope_dd_config* c, const noscope_frames_
   const int64_t box_h = (d.height + c->out_h - 1) / c->out_h;
   const int64_t box_w = (d.width + c->out_w - 1) / c->out_w;
   if (box_h > 257 || box_h * box_w > kMaxBox) return NOSCOPE_SHAPE;
-  // one band (box_h source rows) per pipeline stage: 4 stages x 2 CTAs must fit smem
-  if (box_h * d.width * 3 + 32 > 24 * 1024) return NOSCOPE_SHAPE;
+  // one band (box_h source rows) per ring stage, >= 2 stages per worker group:
+  // bands up to ~110 KB (every source in PAPER.md Table 1, up to 1170x1080 -> 50x50)
+  if (!dd_frames_fit(*c, d)) return NOSCOPE_SHAPE;
   return NOSCOPE_OK;
 }
 
@@ -579,18 +584,33 @@ noscope_status noscope_cbo_search(const noscope_cbo_dd* dds, int32_t n_dd, const
   bool have = false;
   noscope_cbo_result best{};
   uint64_t bk[4] = {0, 0, 0, 0};
+  // R-23: every CNN runs unfiltered on all n frames.  A DD launch writes only the
+  // small frames its configuration needs (checked frames and their anchors), so
+  // the CNN input comes from a t_skip = 1 pass of dds[0] (every frame checked,
+  // every frame downsampled); the same 50x50 frames serve every DD config.
+  auto cnn_pass = [&]() -> noscope_status {
+    for (int c = 0; c < n_cnn; ++c) {
+      noscope_status s = noscope_specialized_infer(cnns[c].arch, cnns[c].weights, small, 7504, nullptr, nullptr,
+                                                   n, reinterpret_cast<float*>(b + w.logits) + (size_t)c * n,
+                                                   b + w.cnn, w.cnn_bytes, stream);
+      if (s != NOSCOPE_OK) return s;
+    }
+    return NOSCOPE_OK;
+  };
+  if (dds[0].dd->t_skip_frames != 1) {
+    noscope_dd_config all = *dds[0].dd;
+    all.t_skip_frames = 1;
+    noscope_status s = noscope_diff_detect(&all, frames, desc, n, 0, nullptr, small, 7504, score, b + w.disp,
+                                           nullptr, nullptr, b + w.dd, dd_ws(n).total, stream);
+    if (s != NOSCOPE_OK) return s;
+    if ((s = cnn_pass()) != NOSCOPE_OK) return s;
+  }
   for (int d = 0; d < n_dd; ++d) {
     const noscope_dd_config& dd = *dds[d].dd;
     noscope_status s = noscope_diff_detect(&dd, frames, desc, n, 0, nullptr, small, 7504, score,
                                            b + w.disp, nullptr, nullptr, b + w.dd, dd_ws(n).total, stream);
     if (s != NOSCOPE_OK) return s;
-    if (d == 0)   // the CNN sees the same 50x50 small frames under every DD config
-      for (int c = 0; c < n_cnn; ++c) {
-        s = noscope_specialized_infer(cnns[c].arch, cnns[c].weights, small, 7504, nullptr, nullptr, n,
-                                      reinterpret_cast<float*>(b + w.logits) + (size_t)c * n, b + w.cnn,
-                                      w.cnn_bytes, stream);
-        if (s != NOSCOPE_OK) return s;
-      }
+    if (d == 0 && dd.t_skip_frames == 1 && (s = cnn_pass()) != NOSCOPE_OK) return s;
     s = launch_records_a(score, labels, n, dd.mode, dd.t_diff_frames, dd.t_skip_frames, a, st);
     if (s != NOSCOPE_OK) return s;
     for (int c = 0; c < n_cnn; ++c) {
@@ -622,6 +642,15 @@ noscope_status noscope_cbo_search(const noscope_cbo_dd* dds, int32_t n_dd, const
   }
   *result_host = best;
   return best.best.feasible ? NOSCOPE_OK : NOSCOPE_INFEASIBLE;
+}
+
+noscope_status noscope_sweep_records(const double* s, const uint8_t* y, int64_t n, int32_t mode, int32_t k,
+                                     int32_t t_skip, uint8_t* a_out, noscope_stream_t stream) {
+  if ((n > 0 && (!s || !y || !a_out)) || n < 0 || (mode != 0 && mode != 1) || k < 1 || t_skip < 1)
+    return NOSCOPE_INVALID_ARGUMENT;
+  noscope_status st = check_device();
+  if (st != NOSCOPE_OK) return st;
+  return launch_records_a(s, y, n, mode, k, t_skip, a_out, (cudaStream_t)stream);
 }
 
 noscope_status noscope_eval_labels(const uint8_t* pred, const uint8_t* ref, int64_t n, int32_t window,

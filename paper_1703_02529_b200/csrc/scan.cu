@@ -286,11 +286,13 @@ noscope_status launch_compact_fired(const uint8_t* /*disp_in*/, uint8_t* disp, d
   NS_CUDA_TRY(cudaMemsetAsync(scan_ws, 0, compact_ws_bytes(n), st));
   const int vec = (reinterpret_cast<uintptr_t>(disp) & 15) == 0;
   const size_t smem = compact_smem_bytes();
-  static int per_sm = 0;
+  static DeviceInt occ;
+  int per_sm = occ.get();
   if (per_sm == 0) {
-    cudaFuncSetAttribute(compact_fired_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    NS_CUDA_TRY(cudaFuncSetAttribute(compact_fired_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     NS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compact_fired_kernel, kCThreads, smem));
     if (per_sm < 1) per_sm = 1;
+    occ.set(per_sm);
   }
   int sms = kNumSMs, dev = 0;
   cudaGetDevice(&dev);

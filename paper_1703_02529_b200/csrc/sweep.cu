@@ -170,12 +170,39 @@ sweep_hist_kernel(const double* __restrict__ s, const float* __restrict__ z,
   if (blockIdx.x == 0 && tid == 0) atomicAdd(&hist[L.tail + 1], (unsigned long long)n);
 }
 
-// Phase 2a: per-delta tables.  One CTA per j.
+// Phase 2a: per-delta tables.
+// sweep_dsuffix_kernel: one thread per histogram column, one pass over d —
+//   G[d][b][y] = sum_{d' >= d} H2[d'][b][y]   (fired under delta_j  <=>  d > j)
+//   Pn[d][c]   = sum_{d' <= d} H1[d'][c]      (c = (a=1,y=0), (a=0,y=1); not fired <=> d <= j)
 struct Tables {
   unsigned long long *F, *FPnf, *FNnf, *FPf, *FNf, *GE, *GT;
 };
 
-__global__ void sweep_prefix_kernel(const unsigned long long* hist, int nd, int m, Tables T) {
+__global__ void sweep_dsuffix_kernel(const unsigned long long* __restrict__ hist, int nd, int m,
+                                     unsigned long long* __restrict__ G, unsigned long long* __restrict__ Pn) {
+  HistLayout L(nd, m);
+  const int cols = 2 * L.B;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < cols) {
+    unsigned long long acc = 0;
+    for (int d = nd; d >= 0; --d) {
+      acc += hist[L.h2 + (size_t)d * cols + c];
+      G[(size_t)d * cols + c] = acc;
+    }
+  } else if (c < cols + 2) {
+    const int w = c == cols ? 1 * 2 + 0 : 0 * 2 + 1;   // (a, y) = (1, 0) FP, (0, 1) FN
+    unsigned long long acc = 0;
+    for (int d = 0; d <= nd; ++d) {
+      acc += hist[L.h1 + (size_t)d * 4 + w];
+      Pn[(size_t)d * 2 + (c - cols)] = acc;
+    }
+  }
+}
+
+// One CTA per j: the fired histogram over logit bins (G at d = j + 1), then
+// suffix / prefix sums over b.
+__global__ void sweep_prefix_kernel(const unsigned long long* __restrict__ G,
+                                    const unsigned long long* __restrict__ Pn, int nd, int m, Tables T) {
   extern __shared__ __align__(16) uint8_t smem[];
   HistLayout L(nd, m);
   unsigned long long* fh0 = reinterpret_cast<unsigned long long*>(smem);
@@ -184,14 +211,10 @@ __global__ void sweep_prefix_kernel(const unsigned long long* hist, int nd, int 
   unsigned long long* SA = S0 + L.B + 1;  // suffix of fh0 + fh1
   unsigned long long* P1 = SA + L.B + 1;  // prefix (inclusive) of fh1
   const int j = blockIdx.x, tid = threadIdx.x;
+  const unsigned long long* g = G + (size_t)(j + 1) * 2 * L.B;
   for (int b = tid; b < L.B; b += blockDim.x) {
-    unsigned long long c0 = 0, c1 = 0;
-    for (int d = j + 1; d <= nd; ++d) {   // fired: d > j
-      c0 += hist[L.h2 + ((size_t)d * L.B + b) * 2 + 0];
-      c1 += hist[L.h2 + ((size_t)d * L.B + b) * 2 + 1];
-    }
-    fh0[b] = c0;
-    fh1[b] = c1;
+    fh0[b] = g[2 * b + 0];
+    fh1[b] = g[2 * b + 1];
   }
   __syncthreads();
   if (tid == 0) {
@@ -206,14 +229,9 @@ __global__ void sweep_prefix_kernel(const unsigned long long* hist, int nd, int 
       p += fh1[b];
       P1[b] = p;
     }
-    unsigned long long fp = 0, fn = 0;
-    for (int d = 0; d <= j; ++d) {         // not fired: d <= j
-      fp += hist[L.h1 + (size_t)d * 4 + 1 * 2 + 0];  // a = 1, y = 0
-      fn += hist[L.h1 + (size_t)d * 4 + 0 * 2 + 1];  // a = 0, y = 1
-    }
     T.F[j] = SA[0];
-    T.FPnf[j] = fp;
-    T.FNnf[j] = fn;
+    T.FPnf[j] = Pn[(size_t)j * 2 + 0];
+    T.FNnf[j] = Pn[(size_t)j * 2 + 1];
   }
   __syncthreads();
   for (int t = tid; t < m; t += blockDim.x) {
@@ -333,8 +351,9 @@ __global__ void sweep_final_kernel(const EvalOut* blocks, int nblocks, Tables T,
 // ===================================================================== host
 size_t sweep_ws_bytes(int32_t nd, int32_t m) {
   size_t tabs = (size_t)nd * 3 + (size_t)nd * m * 4;
+  size_t suffix = (size_t)(nd + 1) * (2 * (2 * (size_t)m + 1)) + (size_t)(nd + 1) * 2;
   size_t blocks = ((size_t)nd * m + 255) / 256;
-  return 256 + tabs * 8 + blocks * sizeof(EvalOut) + sizeof(noscope_sweep_best) + 256;
+  return 256 + (tabs + suffix) * 8 + blocks * sizeof(EvalOut) + sizeof(noscope_sweep_best) + 256;
 }
 
 noscope_status launch_sweep(int32_t phase, const double* s, const float* z, const uint8_t* y,
@@ -352,12 +371,9 @@ noscope_status launch_sweep(int32_t phase, const double* s, const float* z, cons
       size_t priv = smem + L.tail * 4;
       int privatised = priv <= 200 * 1024 ? 1 : 0;
       size_t use = privatised ? priv : smem;
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(sweep_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024);
-        attr = true;
-      }
+      // set on every call: function attributes are per device context
+      NS_CUDA_TRY(cudaFuncSetAttribute(sweep_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)use));
       int64_t want = (n + kHistThreads * 16 - 1) / (kHistThreads * 16);
       int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, kNumSMs));
       sweep_hist_kernel<<<grid, kHistThreads, use, st>>>(s, z, y, a, n, delta, nd, u, m, hist,
@@ -392,15 +408,22 @@ noscope_status launch_sweep(int32_t phase, const double* s, const float* z, cons
       T.GE = take((size_t)nd * m);
       T.GT = take((size_t)nd * m);
     }
+    unsigned long long* G = take((size_t)(nd + 1) * 2 * L.B);
+    unsigned long long* Pn = take((size_t)(nd + 1) * 2);
     const int nblocks = (int)(((int64_t)nd * m + 255) / 256);
     EvalOut* bo = reinterpret_cast<EvalOut*>(p);
     p += (size_t)nblocks * sizeof(EvalOut);
     p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
     noscope_sweep_best* best_dev = reinterpret_cast<noscope_sweep_best*>(p);
-    size_t smem = (size_t)(5 * L.B + 2) * 8;
-    sweep_prefix_kernel<<<nd, 256, smem, st>>>(hist, nd, m, T);
+    const int cols = 2 * L.B + 2;
+    sweep_dsuffix_kernel<<<(cols + 255) / 256, 256, 0, st>>>(hist, nd, m, G, Pn);
     NS_LAUNCH_CHECK();
-    count_launch(3);
+    const size_t smem = (size_t)(5 * L.B + 2) * 8;   // up to 164 KB at m = 2048
+    NS_CUDA_TRY(cudaFuncSetAttribute(sweep_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    sweep_prefix_kernel<<<nd, 256, smem, st>>>(G, Pn, nd, m, T);
+    NS_LAUNCH_CHECK();
+    count_launch(4);
     sweep_eval_kernel<<<nblocks, 256, 0, st>>>(T, hist, nd, m, tm.t_mse_ps, tm.t_snn_ps,
                                                tm.t_full_ps, fp_limit, fn_limit, bo);
     NS_LAUNCH_CHECK();

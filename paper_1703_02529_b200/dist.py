@@ -33,7 +33,7 @@ def allreduce_hist_(hist: torch.Tensor) -> torch.Tensor:
 
 
 def gather_labels(local: torch.Tensor, counts=None):
-    """C2: concatenate every rank's label track in rank order (on all ranks).
+    """C2 (all ranks receive): concatenate every rank's label track in rank order.
 
     `counts` (list of per-rank lengths) allows unequal shards; default equal."""
     world, _ = world_rank()
@@ -44,7 +44,7 @@ def gather_labels(local: torch.Tensor, counts=None):
     m = max(counts)
     buf = torch.zeros(m, dtype=local.dtype, device=local.device)
     buf[:local.numel()] = local
-    if local.device.type == "cuda":
+    if local.device.type == "cuda" and dist.get_backend() == "nccl":
         out = torch.empty(m * world, dtype=local.dtype, device=local.device)
         dist.all_gather_into_tensor(out, buf)
         parts = list(out.view(world, m))
@@ -52,6 +52,25 @@ def gather_labels(local: torch.Tensor, counts=None):
         parts = [torch.empty_like(buf) for _ in range(world)]
         dist.all_gather(parts, buf)
     return torch.cat([p[:c] for p, c in zip(parts, counts)])
+
+
+def gather_labels_to_rank0(local: torch.Tensor, out: torch.Tensor | None = None):
+    """C2: per-unit label tracks gathered to rank 0 only (dist.gather; NCCL or gloo).
+    Every rank passes an equal-length track; rank 0 returns the concatenation in
+    rank order (written into `out` [world * n] if given), other ranks None."""
+    world, rank = world_rank()
+    if world == 1:
+        if out is not None:
+            out.copy_(local)
+            return out
+        return local
+    if rank == 0:
+        out = out if out is not None else torch.empty(world * local.numel(), dtype=local.dtype,
+                                                      device=local.device)
+        dist.gather(local, gather_list=list(out.view(world, local.numel())), dst=0)
+        return out
+    dist.gather(local, dst=0)
+    return None
 
 
 def distributed_sweep(hist_fn, evaluate_fn, n_words: int, device):
@@ -80,19 +99,41 @@ def sweep_on_shard(nsm, s, z, y, a, delta, u, timing, fp_limit, fn_limit):
 
 
 def run_units(nsm, units, make_frames, dd, arch, weights, lo, hi, labeller, labeller_user_fn,
-              chunk=8192, ws=None):
+              chunk=8192, ws=None, device="cuda", timer=None, records=None):
     """Process this rank's units through noscope_cascade_run in chunks with
-    carried state; returns the concatenated label track (device)."""
+    carried stream state (R-19: no state crosses a unit boundary); returns the
+    concatenated label track.
+
+    make_frames(u, t0, m) -> device frames of unit u, ordinals [t0, t0+m) (the
+    decode stand-in; called outside the timed intervals).  timer: optional list;
+    a (start, end) CUDA event pair is appended around every cascade call, so the
+    caller can sum the cascade time without the generation.  records: optional
+    dict of per-unit lists that receives each unit's scores / logits (device)."""
     outs = []
     for u in units:
         n = u["n_frames"]
         state = nsm.noscope_stream_state_init(dd)
-        labels = torch.empty(n, dtype=torch.uint8, device="cuda")
+        labels = torch.empty(n, dtype=torch.uint8, device=device)
+        scores = logits = None
+        if records is not None:
+            scores = torch.empty(n, dtype=torch.float64, device=device)
+            logits = torch.zeros(n, dtype=torch.float32, device=device)
         for t0 in range(0, n, chunk):
             m = min(chunk, n - t0)
             frames = make_frames(u, t0, m)
+            if timer is not None:
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ev[0].record()
             nsm.noscope_cascade_run(dd, arch, weights, lo, hi, frames, u["width"], u["height"], state,
                                     labeller, labeller_user_fn(u), seg_offset=t0,
-                                    frame_index_base=t0, ws=ws, labels=labels[t0:t0 + m])
+                                    frame_index_base=t0, ws=ws, labels=labels[t0:t0 + m],
+                                    scores_out=None if scores is None else scores[t0:t0 + m],
+                                    logits_out=None if logits is None else logits[t0:t0 + m])
+            if timer is not None:
+                ev[1].record()
+                timer.append(ev)
+        if records is not None:
+            records.setdefault("scores", []).append(scores)
+            records.setdefault("logits", []).append(logits)
         outs.append(labels)
-    return torch.cat(outs) if outs else torch.empty(0, dtype=torch.uint8, device="cuda")
+    return torch.cat(outs) if outs else torch.empty(0, dtype=torch.uint8, device=device)

@@ -165,6 +165,8 @@ def lib():
     L.noscope_cbo_search.argtypes = [C.POINTER(CboDD), c_i32, C.POINTER(CboCNN), c_i32, c_p, FramesDesc,
                                      c_i64, c_p, c_p, c_i32, C.c_uint64, C.c_uint64, C.c_uint64,
                                      C.c_uint64, C.POINTER(CboResult), c_p, c_sz, c_p]
+    L.noscope_sweep_records.restype = c_i32
+    L.noscope_sweep_records.argtypes = [c_p, c_p, c_i64, c_i32, c_i32, c_i32, c_p, c_p]
     L.noscope_eval_labels.restype = c_i32
     L.noscope_eval_labels.argtypes = [c_p, c_p, c_i64, c_i32, c_i32, C.POINTER(EvalCounts), c_p, c_sz, c_p]
     L.noscope_cnn_param_count.restype = c_i64
@@ -406,6 +408,15 @@ def noscope_threshold_sweep(phase, s, z, y, a, delta, u, hist, timing=(0, 0, 0),
     if not phase & 2:
         return None, code
     return {f: getattr(best, f) for f, _ in SweepBest._fields_}, code
+
+
+def noscope_sweep_records(s: torch.Tensor, y: torch.Tensor, mode: int, k: int, t_skip: int = 1, a_out=None,
+                          stream=None):
+    """a[i] = label emitted for record i when not fired (include/noscope.h)."""
+    a_out = a_out if a_out is not None else torch.empty_like(y)
+    _check(lib().noscope_sweep_records(_ptr(s), _ptr(y), s.numel(), mode, k, t_skip, _ptr(a_out),
+                                       _stream(stream)), "noscope_sweep_records")
+    return a_out
 
 
 # ---------------------------------------------------------------- DD fitting

@@ -66,6 +66,16 @@ def test_validation_precedes_device_use(lib):
                                  0, None, ctypes.c_void_p(16), 10816, None, ctypes.c_void_p(16),
                                  None, None, ctypes.c_void_p(16), 1 << 20, None)
     assert rc == 2                                                     # S:75 target > source
+    dd = N.DD(mode=1, metric=0, out_w=53, out_h=720).c()                # u32 SSD would wrap
+    rc = lib.noscope_diff_detect(ctypes.byref(dd), ctypes.c_void_p(16), N.FramesDesc(1280, 720, 2764800), 1,
+                                 0, None, ctypes.c_void_p(16), 114480, None, ctypes.c_void_p(16),
+                                 None, None, ctypes.c_void_p(16), 1 << 30, None)
+    assert rc == 2
+    dd = N.DD(mode=1, metric=0, out_w=50, out_h=50).c()                # 1920x1080: 126 KB band
+    rc = lib.noscope_diff_detect(ctypes.byref(dd), ctypes.c_void_p(16), N.FramesDesc(1920, 1080, 6220800), 1,
+                                 0, None, ctypes.c_void_p(16), 7504, None, ctypes.c_void_p(16),
+                                 None, None, ctypes.c_void_p(16), 1 << 30, None)
+    assert rc == 2
     rc = lib.noscope_threshold_sweep(4, None, None, None, None, 0, None, 1, None, 1, None, None, 0, 0,
                                      None, None, None, 0, None)
     assert rc == 1

@@ -118,3 +118,99 @@ def test_unit_range_partition():
                 lo, hi = D.unit_range(U, G, r)
                 seen.extend(range(lo, hi))
             assert seen == list(range(U))
+
+
+# ---------------------------------------------------------------- run_units + C1 + C2
+class _StubNS:
+    """CPU stand-in with the binding's call signatures (test-only).  Its 'cascade'
+    carries state across chunks (label_t = (bytes_t + carry) mod 3 mod 2), so the
+    result depends on the chunk loop carrying state within a unit and resetting
+    it between units — the logic run_units owns."""
+
+    def noscope_stream_state_init(self, dd):
+        return torch.zeros(1, dtype=torch.int64)
+
+    def noscope_cascade_run(self, dd, arch, w, lo, hi, frames, W, H, state, labeller, user, seg_offset=0,
+                            frame_index_base=0, ws=None, labels=None, scores_out=None, logits_out=None):
+        v = frames.to(torch.int64).sum(dim=1)
+        for i in range(len(v)):
+            state[0] = (v[i] + state[0]) % 3
+            labels[i] = int(state[0] % 2)
+        if scores_out is not None:
+            scores_out.copy_((v % 11).double())
+        if logits_out is not None:
+            logits_out.copy_((v % 7).float() - 3.0)
+
+
+N_UNITS, UNIT_LEN, CHUNK = 6, 23, 5
+
+
+def _units():
+    return [dict(id=i, n_frames=UNIT_LEN, width=4, height=4) for i in range(N_UNITS)]
+
+
+def _make_frames(u, t0, m):
+    rng = np.random.default_rng(1000 * u["id"] + 7)
+    f = rng.integers(0, 256, (UNIT_LEN, 16), dtype=np.uint8)
+    return torch.from_numpy(f[t0:t0 + m].copy())
+
+
+def _truth(u):
+    return (np.random.default_rng(u["id"]).random(UNIT_LEN) < 0.4).astype(np.uint8)
+
+
+def _shard_run(world, rank):
+    """This rank's units -> (labels, per-record histogram over the unit records)."""
+    lo_u, hi_u = D.unit_range(N_UNITS, world, rank)
+    units = _units()[lo_u:hi_u]
+    rec = {}
+    lab = D.run_units(_StubNS(), units, _make_frames, None, None, None, 0.0, 0.0, 0, lambda u: 0,
+                      chunk=CHUNK, device="cpu", records=rec)
+    delta, u = np.array([1.5, 4.5, 8.5]), np.float32([-2.5, 0.0, 2.0])
+
+    def hist_fn(h):
+        for uu, s, z in zip(units, rec["scores"], rec["logits"]):
+            y = _truth(uu)
+            a = O.build_records(s.numpy(), y, 1, 2)
+            h += torch.from_numpy(_hist_np(s.numpy(), z.numpy(), y, a, delta, u))
+
+    def eval_fn(h):
+        T = _tables_from_hist(h.numpy(), len(delta), len(u))
+        return O.sweep_best(T, (1, 10, 1000), 10, 10)
+
+    n_words = (len(delta) + 1) * (2 * len(u) + 1) * 2 + (len(delta) + 1) * 4 + 2
+    best, _ = D.distributed_sweep(hist_fn, eval_fn, n_words, "cpu")
+    return lab, best
+
+
+def _worker_units(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lab, best = _shard_run(world, rank)
+        g = D.gather_labels_to_rank0(lab)
+        q.put((rank, None if g is None else g.numpy().tolist(), best))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_run_units_and_distributed_sweep_are_world_size_invariant(world):
+    """labels (gathered to rank 0) and the sweep's best triple
+    (C1 all-reduce of the local histograms) are identical for G = 1 and G = world."""
+    lab1, best1 = _shard_run(1, 0)                       # single process, no process group
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_units, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=120) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][1] == lab1.numpy().tolist()            # rank 0 holds every unit's labels in order
+    assert all(r[1] is None for r in res[1:])            # a gather, not an all-gather
+    assert all(r[2] == best1 for r in res)               # every rank evaluates the same summed counts
+    # the stub's state carry matters: chunking without carry would change labels
+    assert len(lab1) == N_UNITS * UNIT_LEN

@@ -144,7 +144,7 @@ def test_cnn_zero_and_bias_weights():
     assert np.allclose(1 / (1 + np.exp(-z.cpu().numpy())), 0.75, atol=1e-6)
 
 
-@pytest.mark.parametrize("L,C", [(2, 64), (4, 64), (4, 32)])
+@pytest.mark.parametrize("L,C", [(2, 32), (2, 64), (4, 64), (4, 32)])
 def test_cnn_multi_chunk_sampled(L, C):
     """More frames than one internal chunk: the layer kernels see
     chunk_base > 0 and a ragged last chunk.  Sampled frames from both chunks,
@@ -163,4 +163,42 @@ def test_cnn_multi_chunk_sampled(L, C):
     pick = np.array([0, 1, chunk // 2, chunk - 2, chunk - 1, chunk, chunk + 1, chunk + 108, n - 2, n - 1])
     z_o = O.cnn_logits(hw3(fr[pick], 50, 50), arch, w)
     assert np.abs(z[pick] - z_o).max() <= TOL
+    assert np.isfinite(z).all()
+
+
+@pytest.mark.parametrize("L,C,D", [(2, 32, 64), (2, 32, 256), (2, 64, 64), (4, 32, 256), (4, 64, 256)],
+                         ids=lambda v: str(v))
+def test_cnn_dense_64_and_256(L, C, D):
+    """The paper's dense widths 64 and 256 (Table 2 picks D = 256 for
+    amsterdam and elevator), beyond BASELINE's D in {32, 128}."""
+    nsm = ns()
+    n = 203
+    small, g = _small(n, 12)
+    arch = sg.CnnArch(L, C, D)
+    w = sg.he_normal_weights(arch, 5)
+    z_o = O.cnn_logits(g, arch, w)
+    z = nsm.noscope_specialized_infer(nsm.Arch(L, C, D), nsm.Weights(w), torch.from_numpy(small).cuda())
+    torch.cuda.synchronize()
+    err = np.abs(z.cpu().numpy() - z_o)
+    assert err.max() <= TOL, (arch.name, err.max())
+
+
+def test_cnn_bench_batch_full_parity():
+    """The bench's CNN at its in-cascade batch size: L2C32D32 on 16,384 frames (the
+    webcam hour fires ~16.2k frames per call, ~110 per CTA, so every ring and phase
+    of the fused kernel wraps many times), compared element-wise with the full
+    oracle on every frame."""
+    nsm = ns()
+    n = 16384
+    sc, fr = scene_frames(50, 50, n, seed=21, prevalence=0.5)
+    small = np.zeros((n, 7504), np.uint8)
+    small[:, :7500] = fr[:, :7500]
+    arch = sg.CnnArch(2, 32, 32)
+    w = sg.he_normal_weights(arch, 1)
+    z = nsm.noscope_specialized_infer(nsm.Arch(2, 32, 32), nsm.Weights(w), torch.from_numpy(small).cuda())
+    torch.cuda.synchronize()
+    z = z.cpu().numpy()
+    z_o = O.cnn_logits(hw3(fr, 50, 50), arch, w, batch=1024)
+    err = np.abs(z - z_o)
+    assert err.max() <= TOL, (err.max(), int(np.argmax(err)))
     assert np.isfinite(z).all()

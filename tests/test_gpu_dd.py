@@ -209,3 +209,39 @@ def test_identity_downsample_path(mode, metric, t_skip, k, size, grid):
         pos += c
     assert np.array_equal(disp, d_o)
     assert np.array_equal(score[np.isfinite(s_o)], s_o[np.isfinite(s_o)])
+
+
+@pytest.mark.parametrize("W,H", [(1280, 720), (1170, 1080), (1000, 570), (680, 420), (1000, 530)])
+@pytest.mark.parametrize("mode,metric", [(1, 1), (0, 0)])
+def test_paper_resolutions(W, H, mode, metric):
+    """Every source size of PAPER.md Table 1 -> 50x50: large bands run
+    with fewer worker groups (ds_plan), unaligned rows (1170*3 = 3510 B) through the
+    generic path; small frames, scores and dispositions bit-exact."""
+    nsm = ns()
+    n = 10
+    sc, fr = scene_frames(W, H, n, seed=7, prevalence=0.95)
+    small_o = O.downsample(hw3(fr, W, H), 50, 50)
+    lr = sg.lr_weights(10, 4)
+    ref = O.downsample(sg.background(sc.spec)[None], 50, 50)[0]
+    s_tmp, _ = O.diff_detect(small_o, O.DDConfig(mode=mode, metric=metric, grid=10, t_diff_frames=3,
+                                                 delta_diff=0.0, ref_image=ref, lr_w=lr[0], lr_b=lr[1]))
+    fin = s_tmp[np.isfinite(s_tmp)]
+    delta = float(np.quantile(fin, 0.5))
+    ocfg, g = dd_pair(nsm, mode, metric, k=3, delta=delta, ref=ref, lr=lr)
+    s_o, d_o = O.diff_detect(small_o, ocfg)
+    res = _run(nsm, g, fr, W, H)
+    _compare(res, small_o, s_o, d_o)
+
+
+def test_ssd_overflow_shapes_rejected():
+    """u32 SSDs: out_w*out_h*3*255^2 must stay below 2^32 (53 x 720 would wrap)."""
+    nsm = ns()
+    sc, fr = scene_frames(1280, 720, 2, seed=1)
+    g = nsm.DD(mode=1, metric=0, out_w=53, out_h=720, t_diff_frames=1, delta_diff=0.0)
+    with pytest.raises(nsm.NoScopeError):
+        nsm.noscope_diff_detect(g, torch.from_numpy(fr).cuda(), 1280, 720)
+    g = nsm.DD(mode=1, metric=0, out_w=53, out_h=415, t_diff_frames=1, delta_diff=0.0)   # 53*415*3*65025 < 2^32
+    out = nsm.noscope_diff_detect(g, torch.from_numpy(fr).cuda(), 1280, 720)
+    torch.cuda.synchronize()
+    small_o = O.downsample(hw3(fr, 1280, 720), 415, 53)
+    assert np.array_equal(out["small"].cpu().numpy()[:, :53 * 415 * 3], small_o.reshape(2, -1))

@@ -171,3 +171,66 @@ def test_compact_fired_multi_window(t_skip):
     assert k == len(ref)
     assert np.array_equal(idx[:k].cpu().numpy(), ref)
     assert np.array_equal(d.cpu().numpy(), want)
+
+
+def _best_by_tables(T, timing, fpl, fnl):
+    """Lexicographic argmin of (cost, U, j, -l, h) over feasible l <= h, from the
+    oracle's tables, vectorised over (l, h) per j (O9's objective restated)."""
+    nd, m = T["FPf"].shape
+    t_mse, t_snn, t_full = timing
+    best = None
+    li, hi = np.triu_indices(m)
+    for j in range(nd):
+        fp = int(T["FPnf"][j]) + T["FPf"][j].astype(np.int64)[hi]
+        fn = int(T["FNnf"][j]) + T["FNf"][j].astype(np.int64)[li]
+        U = T["GE"][j].astype(np.int64)[li] - T["GT"][j].astype(np.int64)[hi]
+        ok = (fp <= fpl) & (fn <= fnl)
+        if not ok.any():
+            continue
+        cost = T["checked"] * t_mse + int(T["F"][j]) * t_snn + U * t_full
+        o = np.lexsort((hi[ok], -li[ok], U[ok], cost[ok]))[0]
+        key = (int(cost[ok][o]), int(U[ok][o]), j, -int(li[ok][o]), int(hi[ok][o]))
+        if best is None or key < best:
+            best = key
+    return best
+
+
+@pytest.mark.parametrize("nd,m,n", [(40, 2048, 3000), (2000, 8, 5000)])
+def test_sweep_candidate_limits(nd, m, n):
+    """m = 2048 (the largest accepted candidate count: phase 2's per-delta tables
+    use 164 KB of shared memory) and nd = 2,000 (the d-suffix pass is O(nd*m))."""
+    nsm = ns()
+    s, z, y, a, _, _ = sg.random_sweep_records(n, 77)
+    delta = np.linspace(-7.0, 7.0, nd)                          # distinct, sorted
+    u = np.linspace(-7.0, 7.0, m).astype(np.float32)
+    assert len(np.unique(u)) == m
+    rng = np.random.default_rng(5)
+    hs, hz = rng.random(n) < 0.2, rng.random(n) < 0.2           # exact candidate hits (ties)
+    s[hs] = rng.choice(delta, int(hs.sum()))
+    z[hz] = rng.choice(u, int(hz.sum()))
+    timing = (1, 10, 1000)
+    fpl, fnl = n // 20, n // 20
+    T = O.sweep_tables(s, z, y, a, delta, u)
+    best, code, tabs, _ = _gpu_sweep(nsm, s, z, y, a, delta, u, timing, fpl, fnl, split=2)
+    for k in ("F", "FPnf", "FNnf"):
+        assert np.array_equal(tabs[k], T[k]), k
+    for k in ("FPf", "FNf", "GE", "GT"):
+        assert np.array_equal(tabs[k].reshape(nd, m), T[k]), k
+    key = _best_by_tables(T, timing, fpl, fnl)
+    assert key is not None and code == 0
+    assert (best["cost_ps"], best["uncertain"], best["j"], -best["l"], best["h"]) == key
+
+
+@pytest.mark.parametrize("mode,k,t_skip", [(0, 1, 1), (1, 30, 1), (1, 7, 3), (0, 1, 15), (1, 4, 4)])
+def test_sweep_records_a_matches_oracle(mode, k, t_skip):
+    """The a[] record column (label emitted when not fired) == O.build_records."""
+    nsm = ns()
+    n = 5003
+    rng = np.random.default_rng(k * 31 + t_skip)
+    s = rng.normal(0, 1, n)
+    s[np.arange(n) % t_skip != 0] = -np.inf
+    s[:k][np.arange(min(k, n)) % t_skip == 0] = np.inf if mode == 1 else s[:k][np.arange(min(k, n)) % t_skip == 0]
+    y = (rng.random(n) < 0.3).astype(np.uint8)
+    a = nsm.noscope_sweep_records(torch.from_numpy(s).cuda(), torch.from_numpy(y).cuda(), mode, k, t_skip)
+    torch.cuda.synchronize()
+    assert np.array_equal(a.cpu().numpy(), O.build_records(s, y, mode, k))
