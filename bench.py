@@ -57,8 +57,54 @@ def parse():
     p.add_argument("--no-extras", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-frames", type=int, default=192)
-    p.add_argument("--e2e-frames", type=int, default=8192)
+    p.add_argument("--e2e-frames", type=int, default=13500)
+    p.add_argument("--workload", default="webcam", choices=["webcam", "x"],
+                   help="webcam: BASELINE configs[1] (the metric's config); x: configs[4], "
+                        "8 streams x 24 h sharded over the ranks")
+    p.add_argument("--x-streams", type=int, default=8)
+    p.add_argument("--x-hours", type=int, default=24)
     return p.parse_args()
+
+
+def _free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def maybe_self_launch(args):
+    """`--gpus N` outside torchrun: re-launch this script as N ranks (one process per
+    GPU) under torch.distributed.run on this node; fails if fewer than N GPUs."""
+    if "WORLD_SIZE" in os.environ:
+        if int(os.environ["WORLD_SIZE"]) != args.gpus:
+            sys.exit(f"bench.py: WORLD_SIZE={os.environ['WORLD_SIZE']} but --gpus {args.gpus}")
+        return
+    if args.gpus <= 1:
+        return
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices, {have} visible")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def init_dist(world, device):
+    """One process per GPU over NCCL (NCCL_DEBUG=INFO so the init lines show nranks)."""
+    import torch.distributed as dist
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        dist.init_process_group("nccl", device_id=device)
+
+
+# cost-model timings for the in-step sweep (ps per frame): T_MSE and T_SNN as measured
+# on B200 in round 1 (dd_kernel 14.66 ms / 108k frames; CNN 0.86 ms / 16.2k fired
+# frames), T_full = the paper's YOLOv2 at 80 fps on a P100 (P:162-164)
+SWEEP_TIMING = (135_726, 53_050, 12_500_000_000)
+SWEEP_M = 100
 
 
 def measured_peaks():
@@ -169,13 +215,15 @@ def run_ours(args):
     from paper_1703_02529_b200 import noscope as N
     from synthgen.gpu import truth_labeller_address
 
+    from paper_1703_02529_b200 import dist as D
+    import synthgen as sg
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    if world > 1:   # one process per GPU; bind the NCCL communicator to this rank's device
-        dist.init_process_group("nccl", device_id=device)
+    init_dist(world, device)   # one process per GPU; the NCCL communicator bound to this rank's device
     n = args.frames
     S = setup_gpu(rank, n, device)
     dd, arch, W = S["dd"], S["arch"], S["W"]
@@ -183,23 +231,48 @@ def run_ours(args):
     state = torch.empty(max(1, N.lib().noscope_stream_state_bytes(__import__("ctypes").byref(dd.c()))),
                         dtype=torch.uint8, device=device)
     labels = torch.empty(n, dtype=torch.uint8, device=device)
-    gathered = torch.empty(n * world, dtype=torch.uint8, device=device) if world > 1 else None
+    gathered = torch.empty(n * world, dtype=torch.uint8, device=device) if rank == 0 else None
     lab_fn = truth_labeller_address()
     stream = torch.cuda.current_stream()
     stats = {}
+    # CBO sweep records of the step: s = DD score, z = CNN logit (written for
+    # fired frames; delta candidates are >= the cascade's delta, so every frame fired
+    # under a candidate was fired in the step and has its logit), y = reference label
+    # (stand-in labeller = ground truth), a = label emitted when not fired
+    scores = torch.empty(n, dtype=torch.float64, device=device)
+    logits = torch.zeros(n, dtype=torch.float32, device=device)
+    a_rec = torch.empty(n, dtype=torch.uint8, device=device)
+    truth = S["gs"].truth
+    ul = torch.from_numpy(sg.logit_grid(SWEEP_M)).to(device)
+    hist = torch.zeros(N.sweep_hist_words(SWEEP_M, SWEEP_M), dtype=torch.int64, device=device)
+    sws = N.workspace(N.OP_THRESHOLD_SWEEP, None, None, 0, SWEEP_M, SWEEP_M, device=device)
+    fp_lim = fn_lim = (n * world) // 100                     # FP* = FN* = 1%
+    sweep = {"dl": None, "best": None}
 
     def step(stage_acc=None):
         N.lib().noscope_stream_state_init(__import__("ctypes").byref(dd.c()), N._ptr(state), N._stream())
         stage = [] if stage_acc is not None else None
         out = N.noscope_cascade_run(dd, arch, W, S["lo"], S["hi"], S["frames"], W_SRC, H_SRC, state,
-                                    lab_fn, S["gs"].truth, ws=ws, labels=labels,
+                                    lab_fn, truth, ws=ws, labels=labels, logits_out=logits, scores_out=scores,
                                     want_stats=not stats, stage_ms=stage)
         if "stats" in out:
             stats.update(out["stats"])
         if stage_acc is not None:
             stage_acc.append(stage)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, labels)
+        if sweep["dl"] is None:    # candidates from the first (warm-up) step: 100 quantiles of s >= delta
+            fired_s = scores[scores > dd.delta_diff]
+            q = torch.quantile(fired_s[:: max(1, fired_s.numel() // 100000)], torch.linspace(
+                0, 1, SWEEP_M - 1, dtype=torch.float64, device=device))
+            grid = torch.unique(torch.cat([torch.tensor([dd.delta_diff], dtype=torch.float64, device=device), q]))
+            sweep["dl"] = grid[:SWEEP_M].contiguous()
+        dl = sweep["dl"]
+        N.noscope_sweep_records(scores, truth, 1, K_LAG, 1, a_out=a_rec)
+        hist.zero_()
+        N.noscope_threshold_sweep(1, scores, logits, truth, a_rec, dl, ul, hist)
+        D.allreduce_hist_(hist)                                                   # C1 (NCCL)
+        sweep["best"], _ = N.noscope_threshold_sweep(2, None, None, None, None, dl, ul, hist, SWEEP_TIMING,
+                                                     fp_lim, fn_lim, ws=sws)
+        D.gather_labels_to_rank0(labels, out=gathered)                            # C2 (NCCL gather)
 
     for _ in range(args.warmup):
         step()
@@ -221,10 +294,13 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], device=device)
+    per_rank = [ms]
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+        t = torch.zeros(world, device=device)
+        t[rank] = ms
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        per_rank = [float(v) for v in t.tolist()]
+    ms = max(per_rank)
     ms_step = ms / args.steps
     fps = n * world / (ms_step / 1e3)
     stage = np.mean(np.array(stage_acc), axis=0)   # 7 stages, ms
@@ -275,6 +351,13 @@ def run_ours(args):
             ["dd_kernel", "dd_tail", "compaction", "cnn", "routing", "labeller",
              "labels_state"], stage)},
         "run_stats": stats,
+        "per_rank": [{"rank": r, "ms_per_step": round(v / args.steps, 4),
+                      "fps": round(n / (v / args.steps / 1e3), 1)} for r, v in enumerate(per_rank)],
+        "step": "noscope_cascade_run over the unit (downsample, DD, compaction, CNN, routing, stand-in "
+                "labeller, labels) + sweep records + noscope_threshold_sweep phase 1 + C1 all_reduce of "
+                "the sweep histogram + phase 2 (best triple to host) + C2 gather of the labels to rank 0",
+        "sweep": {k: sweep["best"][k] for k in ("j", "l", "h", "feasible", "cost_ps", "fp", "fn", "fired",
+                                                 "uncertain", "checked", "total")},
         "cnn": {"frames": nf, "tflops": round(cnn_flops / (stage[3] / 1e3) / 1e12, 2) if stage[3] > 0 else None},
         "gpu_launches": int(launches),
     }
@@ -298,6 +381,120 @@ def run_ours(args):
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args, S)
     if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_x(args):
+    """BASELINE configs[4]: S streams x H hours of 640x480 webcam at
+    30 fps, units = (stream, hour) of 108,000 frames (R-19), unit u on rank
+    floor(u*G/U).  Frames are rendered on device in chunks of 8,192 (the decode
+    stand-in, untimed); each chunk goes through noscope_cascade_run with the unit's
+    carried state; the timed work per rank = the sum of its cascade intervals (CUDA
+    events) + the C1 sweep (phase 1 over every unit's records, all_reduce, phase 2)
+    + the C2 label gather to rank 0; value = all frames / max over ranks."""
+    import ctypes
+    import torch
+    import torch.distributed as dist
+    import synthgen as sg
+    from paper_1703_02529_b200 import dist as D
+    from paper_1703_02529_b200 import noscope as N
+    from synthgen.gpu import GpuScene, truth_labeller_address
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    init_dist(world, device)
+    unit_len = args.frames
+    units = [dict(stream=st, hour=h, n_frames=unit_len, width=W_SRC, height=H_SRC)
+             for st in range(args.x_streams) for h in range(args.x_hours)]
+    lo_u, hi_u = D.unit_range(len(units), world, rank)
+    mine = units[lo_u:hi_u]
+    scenes = {}
+    for u in mine:
+        if u["stream"] not in scenes:   # seed 100 + stream (SURVEY 8(d) X); one scene per 24 h stream
+            sc = sg.make_scene(sg.SceneSpec(W_SRC, H_SRC, args.x_hours * unit_len, seed=100 + u["stream"],
+                                            stream=u["stream"]))
+            scenes[u["stream"]] = GpuScene(sc, device=device)
+    chunk = 8192
+    pitch = sg.frame_pitch(W_SRC, H_SRC)
+    buf = torch.empty((chunk, pitch), dtype=torch.uint8, device=device)
+
+    def make_frames(u, t0, m):
+        scenes[u["stream"]].render(buf, u["hour"] * unit_len + t0, m)
+        return buf[:m]
+
+    arch_s, w, (lr_w, lr_b) = make_weights()
+    # the W configuration's thresholds, fixed for every unit (delta at the 85th percentile of
+    # a unit's scores and c_low / c_high at the 30 / 70 % fired-logit quantiles of stream 0, hour 0)
+    S = setup_gpu(0, min(unit_len, 16384), device)
+    dd, arch, Wt, lo, hi = S["dd"], S["arch"], S["W"], S["lo"], S["hi"]
+    del S
+    torch.cuda.empty_cache()
+    ws = N.workspace(N.OP_CASCADE_RUN, dd, arch, chunk, device=device)
+    truth_of = lambda u: scenes[u["stream"]].truth[u["hour"] * unit_len:(u["hour"] + 1) * unit_len]
+    lab_fn = truth_labeller_address()
+    # warm-up: one chunk
+    D.run_units(N, [dict(mine[0], n_frames=chunk)], make_frames, dd, arch, Wt, lo, hi, lab_fn, truth_of,
+                chunk=chunk, ws=ws, device=device)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    timer, rec = [], {}
+    with ClockSampler(local) as clk:
+        labels = D.run_units(N, mine, make_frames, dd, arch, Wt, lo, hi, lab_fn, truth_of, chunk=chunk, ws=ws,
+                             device=device, timer=timer, records=rec)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ul = torch.from_numpy(sg.logit_grid(SWEEP_M)).to(device)
+        s0 = rec["scores"][0]
+        fired_s = s0[s0 > dd.delta_diff]
+        q = torch.quantile(fired_s[:: max(1, fired_s.numel() // 100000)],
+                           torch.linspace(0, 1, SWEEP_M - 1, dtype=torch.float64, device=device))
+        dl = torch.unique(torch.cat([torch.tensor([dd.delta_diff], dtype=torch.float64, device=device), q]))
+        hist = torch.zeros(N.sweep_hist_words(dl.numel(), SWEEP_M), dtype=torch.int64, device=device)
+        a_rec = torch.empty(unit_len, dtype=torch.uint8, device=device)
+        for u, sc_u, z_u in zip(mine, rec["scores"], rec["logits"]):
+            y = truth_of(u)
+            N.noscope_sweep_records(sc_u, y, 1, K_LAG, 1, a_out=a_rec)
+            N.noscope_threshold_sweep(1, sc_u, z_u, y, a_rec, dl, ul, hist)
+        D.allreduce_hist_(hist)                                                            # C1
+        total = len(units) * unit_len
+        best, _ = N.noscope_threshold_sweep(2, None, None, None, None, dl, ul, hist, SWEEP_TIMING,
+                                            total // 100, total // 100)
+        gathered = torch.empty(len(units) * unit_len, dtype=torch.uint8, device=device) if rank == 0 else None
+        D.gather_labels_to_rank0(labels, out=gathered)                                     # C2
+        e1.record()
+        torch.cuda.synchronize()
+    cascade_ms = sum(a.elapsed_time(b) for a, b in timer)
+    ms = cascade_ms + e0.elapsed_time(e1)
+    per_rank = [ms]
+    if world > 1:
+        t = torch.zeros(world, device=device)
+        t[rank] = ms
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        per_rank = [float(v) for v in t.tolist()]
+    tmax = max(per_rank)
+    if rank == 0:
+        line = {"metric": "cascade frames/sec (diff+CNN+routing)", "value": round(total / (tmax / 1e3), 1),
+                "unit": "frames/s", "n_gpus": world, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "u8/int64/f64 (DD), bf16->f32 (CNN)",
+                "data": "synthetic fixed-angle webcam streams rendered on device in 8,192-frame chunks "
+                        "(untimed), random-init CNN weights",
+                "config": {"workload": f"x: {args.x_streams} streams x {args.x_hours} h at 30 fps, 640x480, "
+                                       f"units of {unit_len} frames sharded over {world} GPU(s)",
+                           "frames_total": total, "units": len(units), "chunk": chunk,
+                           "dd": "mode 1 (t-30), blocked 10x10 + LR, t_skip 1", "cnn": "L2C32D32",
+                           "parallelism": f"dp{world} (units by stream and hour)"},
+                "ms_total": round(tmax, 2), "cascade_ms_rank0": round(cascade_ms, 2),
+                "per_rank_ms": [round(v, 2) for v in per_rank],
+                "sweep": {k: best[k] for k in ("j", "l", "h", "feasible", "cost_ps", "fp", "fn", "uncertain")},
+                "labels_positive_frac": round(float(gathered.float().mean().item()), 4) if gathered is not None
+                else None,
+                "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -371,7 +568,7 @@ def run_e2e(args, S, device, world):
     chunk = 1024
     pitch = S["pitch"]
     host = torch.empty((n, pitch), dtype=torch.uint8, pin_memory=True)
-    host.copy_(S["frames"][:n].cpu() if False else S["frames"][:n], non_blocking=False)
+    host.copy_(S["frames"][:n], non_blocking=False)
     lab_host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     dev_buf = [torch.empty((chunk, pitch), dtype=torch.uint8, device=device) for _ in range(2)]
     labels = torch.empty(n, dtype=torch.uint8, device=device)
@@ -415,9 +612,33 @@ def run_e2e(args, S, device, world):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     del host
+    peak = pinned_h2d_peak(device)
+    h2d = n * pitch / ms / 1e6
     return {"value": round(n * world / (ms / 1e3), 1), "unit": "frames/s",
             "h2d_bytes_per_step": n * pitch, "d2h_bytes_per_step": n,
-            "frames_per_step": n, "chunk": chunk, "ms_per_step": round(ms, 3)}
+            "frames_per_step": n, "chunk": chunk, "ms_per_step": round(ms, 3),
+            "h2d_GBps": round(h2d, 1), "pinned_h2d_peak_GBps": peak,
+            "frac_of_h2d_peak": round(h2d / peak, 4) if peak else None}
+
+
+def pinned_h2d_peak(device, nbytes=1 << 30, reps=5):
+    """Measured pinned host -> device copy bandwidth (GB/s, best of reps, CUDA events):
+    the ceiling of the e2e path, whose input crosses PCIe / C2C every step."""
+    import torch
+    host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    dev = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    dev.copy_(host, non_blocking=True)
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dev.copy_(host, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, nbytes / e0.elapsed_time(e1) / 1e6)
+    del host, dev
+    return round(best, 1)
 
 
 def run_extras(device, timing=(1000, 20000, 12_500_000_000)):
@@ -738,49 +959,197 @@ def oracle_sample(S_or_none, frames_n):
     return src, cfg, arch, w, lo, hi, truth
 
 
+def host_cpu():
+    """nproc and the CPU model string of this host (lscpu, else /proc/cpuinfo)."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        model = next((l.split(":", 1)[1].strip() for l in out.splitlines() if l.startswith("Model name")), None)
+    except Exception:
+        pass
+    if model is None:
+        try:
+            model = next((l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")),
+                         None)
+        except Exception:
+            model = None
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+def _pool(fn, jobs):
+    import multiprocessing as mp
+    with mp.get_context("spawn").Pool(min(len(jobs), os.cpu_count() or 1)) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(fn, jobs)
+        return res, time.perf_counter() - t0
+
+
 def cpu_baseline(args, S):
+    """The CPU oracle (oracle/, as it stands) on this host, SURVEY 8(d) "oracle timing":
+    W (the metric's workload) on 1 core over a frame sample and on all cores over one
+    13,500-frame unit; T, G and S legs on 1 core and on all cores.  Each leg states its
+    sample; the main `value` is W on 1 core."""
     import oracle as O
     from threadpoolctl import threadpool_limits
-    src, cfg, arch, w, lo, hi, truth = oracle_sample(S, args.cpu_frames)
+    P = os.cpu_count() or 1
+    delta, lo, hi = S["dd"].delta_diff, S["lo"], S["hi"]
+    src, cfg, arch, w, _, _, truth = oracle_sample(S, args.cpu_frames)
     with threadpool_limits(1):
         t0 = time.perf_counter()
         O.cascade(src, cfg, arch, w, lo, hi, truth)
         dt = time.perf_counter() - t0
     out = {"value": round(len(src) / dt, 3), "unit": "frames/s", "cores": 1, "kind": "oracle",
            "sample": f"{len(src)} consecutive frames (t=50000..) of the webcam unit processed as one "
-                     f"unit by the plain CPU oracle (numpy, 1 thread), {dt:.1f} s",
-           "host_cores_available": os.cpu_count()}
-    # All host cores (SURVEY 8(d) "oracle timing"): one independent unit (stream) per
-    # process, as the GPU shards units; aggregate = frames of all units / slowest unit.
-    import multiprocessing as mp
-    P = os.cpu_count() or 1
-    with mp.get_context("spawn").Pool(P) as pool:
-        res = pool.map(_oracle_unit_job, [(S["dd"].delta_diff, S["lo"], S["hi"], args.cpu_frames, r + 1)
-                                          for r in range(P)])
-    nfr = sum(r[0] for r in res)
-    slow = max(r[1] for r in res)
-    out["all_cores"] = {"value": round(nfr / slow, 3), "cores": P,
-                        "sample": f"{P} processes x {args.cpu_frames} frames, one webcam stream each, "
-                                  f"numpy 1 thread per process; slowest {slow:.1f} s"}
+                     f"unit by the plain CPU oracle (numpy, 1 thread), {dt:.1f} s; the oracle's per-frame "
+                     f"work is position-independent, so the 13,500-frame W unit takes "
+                     f"{13500 * dt / len(src):.0f} s on 1 core (extrapolated)",
+           "host": host_cpu()}
+    # W on all cores: the 13,500-frame unit (SURVEY 8(d) W "1 unit") as P contiguous segments,
+    # each run as its own unit by one single-threaded process
+    unit = 13_500
+    b = np.linspace(0, unit, P + 1).astype(int)
+    res, _ = _pool(_oracle_w_segment, [(delta, lo, hi, int(b[r]), int(b[r + 1])) for r in range(P)])
+    slow = max(res)
+    out["all_cores"] = {"value": round(unit / slow, 3), "cores": P,
+                        "sample": f"one 13,500-frame W unit (frames 0..13499 of stream 0) split into {P} "
+                                  f"contiguous segments, one single-threaded process each (each segment "
+                                  f"starts a unit: its first 30 checked frames are forced fires); time = "
+                                  f"the slowest process's oracle time, {slow:.1f} s (process start and "
+                                  f"input rendering excluded)"}
+    out["legs"] = oracle_legs(P)
     return out
 
 
-def _oracle_unit_job(a):
-    """One process of the all-cores oracle baseline (module-level for spawn)."""
-    delta, lo, hi, frames_n, stream = a
+def _oracle_w_segment(a):
+    delta, lo, hi, t0, t1 = a
     import oracle as O
     import synthgen as sg
     from threadpoolctl import threadpool_limits
-    sc = sg.make_scene(sg.SceneSpec(W_SRC, H_SRC, UNIT, seed=2, stream=stream))
-    fr = sg.render_frames(sc, 50_000, 50_000 + frames_n)
+    sc = sg.make_scene(sg.SceneSpec(W_SRC, H_SRC, UNIT, seed=2, stream=0))
+    fr = sg.render_frames(sc, t0, t1)
     src = fr[:, :W_SRC * H_SRC * 3].reshape(-1, H_SRC, W_SRC, 3)
     arch, w, (lr_w, lr_b) = make_weights()
     cfg = O.DDConfig(mode=1, metric=1, out_w=OUT, out_h=OUT, grid=GRID, t_diff_frames=K_LAG,
                      t_skip_frames=1, delta_diff=delta, lr_w=lr_w, lr_b=lr_b)
     with threadpool_limits(1):
-        t0 = time.perf_counter()
-        O.cascade(src, cfg, arch, w, lo, hi, sc.truth[50_000:50_000 + frames_n])
-        return len(src), time.perf_counter() - t0
+        st = time.perf_counter()
+        O.cascade(src, cfg, arch, w, lo, hi, sc.truth[t0:t1])
+        return time.perf_counter() - st
+
+
+def _tiny_inputs(t0=0, t1=1000):
+    import synthgen as sg
+    sc = sg.make_scene(sg.SceneSpec(50, 50, 1000, seed=1))
+    fr = sg.render_frames(sc, t0, t1)[:, :7500].reshape(-1, 50, 50, 3)
+    return sc, fr
+
+
+def _oracle_t_job(a):
+    """T: tiny cascade (global MSE vs the reference image, delta 20, L2C32D32, -2/+2)."""
+    t0, t1 = a
+    import oracle as O
+    import synthgen as sg
+    from threadpoolctl import threadpool_limits
+    sc, fr = _tiny_inputs(t0, t1)
+    arch = sg.CnnArch(2, 32, 32)
+    w = sg.he_normal_weights(arch, 1)
+    cfg = O.DDConfig(mode=0, metric=0, delta_diff=20.0, ref_image=sg.background(sc.spec))
+    with threadpool_limits(1):
+        st = time.perf_counter()
+        O.cascade(fr, cfg, arch, w, -2.0, 2.0, sc.truth[t0:t1])
+        return time.perf_counter() - st
+
+
+def _oracle_g_job(a):
+    """G: the CNN on frames [f0, f1) of the 65,536-frame grid input, one architecture."""
+    ai, f0, f1 = a
+    import oracle as O
+    import synthgen as sg
+    from threadpoolctl import threadpool_limits
+    arch = sg.ARCH_GRID[ai]
+    sc = sg.make_scene(sg.SceneSpec(50, 50, 65536, seed=3, prevalence=0.15))
+    g = sg.render_frames(sc, f0, f1)[:, :7500].reshape(-1, 50, 50, 3)
+    w = sg.he_normal_weights(arch, 3)
+    with threadpool_limits(1):
+        st = time.perf_counter()
+        O.cnn_logits(g, arch, w)
+        return time.perf_counter() - st
+
+
+def _sweep_records_1m():
+    """The bench's 1M-record sweep instance (config S) and its 100 x 100 candidates."""
+    import synthgen as sg
+    rng = np.random.default_rng(4)
+    M = 1_000_000
+    y = (rng.random(M) < 0.15).astype(np.uint8)
+    s = np.where(rng.random(M) < 0.05, -np.inf, rng.gamma(2.0, 10.0, M) + 40.0 * y)
+    z = (rng.normal(0, 1, M) + 2.5 * y - 1.0).astype(np.float32)
+    a_ = np.where(np.isinf(s), y, 0).astype(np.uint8)
+    return s, z, y, a_, sg.delta_grid(s, 100), sg.logit_grid(100)
+
+
+def _oracle_s_job(a):
+    """S: the oracle's direct per-threshold tables over records [r0, r1)."""
+    r0, r1 = a
+    import oracle as O
+    from threadpoolctl import threadpool_limits
+    s, z, y, a_, dl, ul = _sweep_records_1m()
+    with threadpool_limits(1):
+        st = time.perf_counter()
+        T = O.sweep_tables(s[r0:r1], z[r0:r1], y[r0:r1], a_[r0:r1], dl, ul)
+        return time.perf_counter() - st, T
+
+
+def oracle_legs(P):
+    """T / G / S oracle timings, 1 core and all cores."""
+    import oracle as O
+    import synthgen as sg
+    legs = {}
+    # T: all 1,000 frames
+    t1 = _oracle_t_job((0, 1000))
+    b = np.linspace(0, 1000, P + 1).astype(int)
+    res, _ = _pool(_oracle_t_job, [(int(b[r]), int(b[r + 1])) for r in range(P)])
+    legs["T"] = {"frames": 1000, "one_core_fps": round(1000 / t1, 1), "all_cores_fps": round(1000 / max(res), 1),
+                 "sample": "all 1,000 tiny frames; all cores = mode-0 frames split into P independent "
+                           "segments (exact: mode 0 has no cross-frame state); time = slowest process's "
+                           "oracle time (process start and rendering excluded)"}
+    # G: 1,024 frames per architecture on all cores; 64 per architecture on 1 core
+    flops = sum(cnn_flops_per_frame((a.n_conv, a.base_filters, a.dense)) for a in sg.ARCH_GRID)
+    one = [_oracle_g_job((ai, 0, 64)) for ai in range(len(sg.ARCH_GRID))]
+    per = max(1, P // len(sg.ARCH_GRID))
+    fb = np.linspace(0, 1024, per + 1).astype(int)
+    res, _ = _pool(_oracle_g_job, [(ai, int(fb[k]), int(fb[k + 1])) for ai in range(len(sg.ARCH_GRID))
+                                   for k in range(per)])
+    wall = max(res)
+    legs["G"] = {"one_core": {"frames_per_arch": 64,
+                              "fps_per_arch": {a.name: round(64 / t, 1) for a, t in zip(sg.ARCH_GRID, one)},
+                              "GFLOPs": round(64 * flops / sum(one) / 1e9, 2)},
+                 "all_cores": {"frames_per_arch": 1024, "wall_s": round(wall, 2),
+                               "fps_all_archs": round(1024 * len(sg.ARCH_GRID) / wall, 1),
+                               "GFLOPs": round(1024 * flops / wall / 1e9, 2)},
+                 "sample": "8 archs x 1,024 frames on all cores (frames split per arch into "
+                           f"{per} slices, one single-threaded process each; time = slowest process); "
+                           "64 frames per arch on 1 core"}
+    # S: 1M records, 100 x 100 candidates; 1 core on a 100k-record prefix (the direct
+    # tables are linear in the records) + the full triple search; all cores on all 1M
+    (t_tab, T1), = [_oracle_s_job((0, 100_000))]
+    st = time.perf_counter()
+    O.sweep_best(T1, SWEEP_TIMING, 1000, 1000)
+    t_best = time.perf_counter() - st
+    rb = np.linspace(0, 1_000_000, P + 1).astype(int)
+    res, _ = _pool(_oracle_s_job, [(int(rb[r]), int(rb[r + 1])) for r in range(P)])
+    st = time.perf_counter()
+    T = {k: sum(r[1][k] for r in res) for k in res[0][1]}
+    O.sweep_best(T, SWEEP_TIMING, 10_000, 10_000)
+    wall = max(r[0] for r in res) + time.perf_counter() - st
+    legs["S"] = {"records": 1_000_000, "candidates": [100, 100],
+                 "one_core_s_extrapolated": round(t_tab * 10 + t_best, 2),
+                 "one_core_records_per_s": round(1_000_000 / (t_tab * 10 + t_best), 1),
+                 "all_cores_s": round(wall, 2), "all_cores_records_per_s": round(1_000_000 / wall, 1),
+                 "sample": "1 core: direct per-(j, t) tables over a 100,000-record prefix (x10, tables are "
+                           "linear in the records) + the full 505,000-triple search; all cores: tables of "
+                           "P record shards summed (integer counts) + the search"}
+    return legs
 
 
 def run_reference(args):
@@ -817,4 +1186,8 @@ if __name__ == "__main__":
     if a.impl == "reference":
         run_reference(a)
     else:
-        run_ours(a)
+        maybe_self_launch(a)
+        if a.workload == "x":
+            run_x(a)
+        else:
+            run_ours(a)

@@ -28,7 +28,12 @@ def allreduce_hist_(hist: torch.Tensor) -> torch.Tensor:
     """C1: in-place sum of a uint64-count histogram (stored as int64) over ranks."""
     world, _ = world_rank()
     if world > 1:
-        dist.all_reduce(hist, op=dist.ReduceOp.SUM)
+        if hist.device.type == "cuda" and dist.get_backend() != "nccl":   # gloo: reduce a host copy
+            h = hist.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM)
+            hist.copy_(h)
+        else:
+            dist.all_reduce(hist, op=dist.ReduceOp.SUM)
     return hist
 
 
@@ -64,12 +69,17 @@ def gather_labels_to_rank0(local: torch.Tensor, out: torch.Tensor | None = None)
             out.copy_(local)
             return out
         return local
+    staged = local.device.type == "cuda" and dist.get_backend() != "nccl"   # gloo gathers host tensors
+    src = local.cpu() if staged else local
     if rank == 0:
         out = out if out is not None else torch.empty(world * local.numel(), dtype=local.dtype,
                                                       device=local.device)
-        dist.gather(local, gather_list=list(out.view(world, local.numel())), dst=0)
+        tgt = torch.empty(world * local.numel(), dtype=local.dtype) if staged else out
+        dist.gather(src, gather_list=list(tgt.view(world, local.numel())), dst=0)
+        if staged:
+            out.copy_(tgt)
         return out
-    dist.gather(local, dst=0)
+    dist.gather(src, dst=0)
     return None
 
 
