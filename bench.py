@@ -751,21 +751,28 @@ def run_extras(device, timing=(1000, 20000, 12_500_000_000)):
                       torch.full((), 2, dtype=torch.uint8, device=device),
                       torch.full((), 1, dtype=torch.uint8, device=device))
     nf = int((dsp == 2).sum())
-    ms = _time_ms(lambda: N.noscope_compact_fired(dsp))
+    cws = torch.empty(N.lib().noscope_compact_workspace_bytes(NC), dtype=torch.uint8, device=device)
+    cout = (torch.empty(NC, dtype=torch.int32, device=device), torch.zeros(1, dtype=torch.int64, device=device))
+    ms = _time_ms(lambda: N.noscope_compact_fired(dsp, ws=cws, out=cout))
+    assert int(cout[1].item()) == nf
     byt = NC + 4 * nf                              # disposition read + index write
     out["compaction_2e30"] = {"frames": NC, "fired": nf, "ms": round(ms, 3), "GBps": round(byt / ms / 1e6, 1),
                               "frac_of_hbm": round(byt / ms / 1e6 / hbm, 4),
                               "algorithmic_bytes": byt}
-    del dsp
+    del dsp, cws, cout
     NR = 1 << 28
     zr = torch.randn(NR, device=device, generator=g)
     lo, hi = -0.5, 0.5
     nu = int(((zr >= lo) & (zr <= hi)).sum())
-    ms = _time_ms(lambda: N.noscope_route_logits(lo, hi, zr))
+    rws = torch.empty(N.lib().noscope_route_workspace_bytes(NR), dtype=torch.uint8, device=device)
+    rout = (torch.empty(NR, dtype=torch.uint8, device=device), torch.empty(NR, dtype=torch.int32, device=device),
+            torch.zeros(1, dtype=torch.int64, device=device))
+    ms = _time_ms(lambda: N.noscope_route_logits(lo, hi, zr, ws=rws, out=rout))
+    assert int(rout[2].item()) == nu
     byt = 4 * NR + NR + 4 * nu                     # logits read + route write + uncertain index write
     out["routing_2e28"] = {"logits": NR, "uncertain": nu, "ms": round(ms, 3), "GBps": round(byt / ms / 1e6, 1),
                            "frac_of_hbm": round(byt / ms / 1e6 / hbm, 4), "algorithmic_bytes": byt}
-    del zr
+    del zr, rws, rout
     return out
 
 

@@ -238,11 +238,20 @@ noscope_status noscope_specialized_infer(const noscope_cnn_arch* arch,
                                          float* logits_out, void* ws, size_t ws_bytes,
                                          noscope_stream_t stream);
 
-/* Routing helper: route_out[i] = NEG/POS/UNC of logits[i] for i < *n_dev
- * (or n_max), and the stable list of uncertain positions + count.         */
+/* Routing helper (step H6): route_out[i] = NEG / POS / UNC of
+ * logits[i] (z < c_low -> NEG, z > c_high -> POS, else UNC; R-5) for
+ * i < *n_dev (or n_max), and the stable (ascending) list of uncertain
+ * positions + its count.  logits: device fp32 [n_max]; route_out: device u8
+ * [n_max] (nullable); unc_idx_out: device i32 [n_max]; n_unc_dev: device i64.
+ * ws: device scratch of noscope_route_workspace_bytes(n_max) bytes, 16-byte
+ * aligned.  One persistent launch (classify + bitmask, grid barrier, indices).
+ * Errors: NOSCOPE_INVALID_ARGUMENT for c_low > c_high or null buffers;
+ * NOSCOPE_WORKSPACE_TOO_SMALL.                                              */
+size_t noscope_route_workspace_bytes(int64_t n_max);
 noscope_status noscope_route_logits(noscope_route r, const float* logits, const int64_t* n_dev,
                                     int64_t n_max, uint8_t* route_out, int32_t* unc_idx_out,
-                                    int64_t* n_unc_dev, noscope_stream_t stream);
+                                    int64_t* n_unc_dev, void* ws, size_t ws_bytes,
+                                    noscope_stream_t stream);
 
 /* Stable compaction helper (step H4, "batch input images before
  * passing them to the GPU"): idx_out[0 .. *n_out_dev) = the ascending
@@ -251,12 +260,16 @@ noscope_status noscope_route_logits(noscope_route r, const float* logits, const 
  * NOSCOPE_SKIPPED in place (the t_skip rule; diff_detect applies
  * the same rule before it compacts).
  *  disposition: device u8 [n] (inout); idx_out: device i32 [n];
- *  n_out_dev:   device i64.  Scan scratch comes from the stream-ordered pool.
+ *  n_out_dev:   device i64.
+ *  ws: device scratch of noscope_compact_workspace_bytes(n) bytes (16-byte
+ *  aligned): a 1-bit-per-frame mask plus per-CTA counts.  One persistent
+ *  launch: classify + mask + count, grid barrier, indices from the mask.
  *  Errors: NOSCOPE_INVALID_ARGUMENT for null buffers (n > 0), n < 0, n >= 2^31
- *  or t_skip < 1.                                                            */
+ *  or t_skip < 1; NOSCOPE_WORKSPACE_TOO_SMALL.                               */
+size_t noscope_compact_workspace_bytes(int64_t n);
 noscope_status noscope_compact_fired(uint8_t* disposition, int64_t n, int64_t seg_offset,
                                      int32_t t_skip, int32_t* idx_out, int64_t* n_out_dev,
-                                     noscope_stream_t stream);
+                                     void* ws, size_t ws_bytes, noscope_stream_t stream);
 
 /* The whole cascade on one chunk of one unit:
  * diff_detect -> compaction -> specialized CNN on fired frames -> routing ->

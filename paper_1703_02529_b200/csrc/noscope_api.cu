@@ -263,41 +263,39 @@ noscope_status noscope_specialized_infer(const noscope_cnn_arch* arch,
                     reinterpret_cast<uint32_t*>(wsb), st);
 }
 
+size_t noscope_route_workspace_bytes(int64_t n_max) { return compact_ws_bytes(std::max<int64_t>(n_max, 0)) + 256; }
+
 noscope_status noscope_route_logits(noscope_route r, const float* logits, const int64_t* n_dev,
                                     int64_t n_max, uint8_t* route_out, int32_t* unc_idx_out,
-                                    int64_t* n_unc_dev, noscope_stream_t stream) {
+                                    int64_t* n_unc_dev, void* ws, size_t ws_bytes, noscope_stream_t stream) {
   if (!(r.lo_logit <= r.hi_logit)) return NOSCOPE_INVALID_ARGUMENT;
-  if ((!logits && n_max > 0) || !unc_idx_out || !n_unc_dev || n_max < 0) return NOSCOPE_INVALID_ARGUMENT;
+  if ((!logits && n_max > 0) || !unc_idx_out || !n_unc_dev || n_max < 0 || !ws) return NOSCOPE_INVALID_ARGUMENT;
+  if (!aligned16(ws)) return NOSCOPE_INVALID_ARGUMENT;
+  if (ws_bytes < noscope_route_workspace_bytes(n_max)) return NOSCOPE_WORKSPACE_TOO_SMALL;
   noscope_status s = check_device();
   if (s != NOSCOPE_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
-  // scan scratch: allocated from the stream-ordered pool (small, freed asynchronously)
-  void* scratch = nullptr;
-  size_t bytes = compact_ws_bytes(n_max) + 256;
-  NS_CUDA_TRY(cudaMallocAsync(&scratch, bytes, st));
-  uint32_t* status = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(scratch));
+  uint8_t* b = reinterpret_cast<uint8_t*>(ws);
+  uint32_t* status = reinterpret_cast<uint32_t*>(b);
   NS_CUDA_TRY(cudaMemsetAsync(status, 0, 4, st));
-  s = launch_route(r, logits, n_dev, n_max, nullptr, route_out, nullptr, unc_idx_out, n_unc_dev,
-                   nullptr, nullptr, nullptr, reinterpret_cast<uint8_t*>(scratch) + 256, status, st);
-  cudaFreeAsync(scratch, st);
-  return s;
+  return launch_route(r, logits, n_dev, n_max, nullptr, route_out, nullptr, unc_idx_out, n_unc_dev,
+                      nullptr, nullptr, nullptr, b + 256, status, st);
 }
+
+size_t noscope_compact_workspace_bytes(int64_t n) { return compact_ws_bytes(std::max<int64_t>(n, 0)); }
 
 noscope_status noscope_compact_fired(uint8_t* disposition, int64_t n, int64_t seg_offset,
                                      int32_t t_skip, int32_t* idx_out, int64_t* n_out_dev,
-                                     noscope_stream_t stream) {
-  if (n < 0 || n >= ((int64_t)1 << 31) || t_skip < 1 || seg_offset < 0 || !n_out_dev)
+                                     void* ws, size_t ws_bytes, noscope_stream_t stream) {
+  if (n < 0 || n >= ((int64_t)1 << 31) || t_skip < 1 || seg_offset < 0 || !n_out_dev || !ws)
     return NOSCOPE_INVALID_ARGUMENT;
   if (n > 0 && (!disposition || !idx_out)) return NOSCOPE_INVALID_ARGUMENT;
+  if (!aligned16(ws)) return NOSCOPE_INVALID_ARGUMENT;
+  if (ws_bytes < noscope_compact_workspace_bytes(n)) return NOSCOPE_WORKSPACE_TOO_SMALL;
   noscope_status s = check_device();
   if (s != NOSCOPE_OK) return s;
-  cudaStream_t st = (cudaStream_t)stream;
-  void* scratch = nullptr;
-  NS_CUDA_TRY(cudaMallocAsync(&scratch, compact_ws_bytes(n), st));
-  s = launch_compact_fired(disposition, disposition, nullptr, n, seg_offset, t_skip, idx_out,
-                           n_out_dev, scratch, st);
-  cudaFreeAsync(scratch, st);
-  return s;
+  return launch_compact_fired(disposition, disposition, nullptr, n, seg_offset, t_skip, idx_out,
+                              n_out_dev, ws, (cudaStream_t)stream);
 }
 
 static noscope_status cascade_impl(const noscope_dd_config* dd, const noscope_cnn_arch* arch,

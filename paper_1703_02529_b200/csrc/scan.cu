@@ -1,13 +1,10 @@
 // scan.cu — stream compaction ("batch input images"), routing
 // and per-frame label resolution.
 //
-// Compaction of the FIRED frames is one persistent two-phase launch (count per
-// contiguous range, grid barrier, write) — see compact_fired_kernel.  Routing's
-// compaction of the uncertain frames is a single-pass decoupled look-back scan:
-// tiles of 8192 items are claimed in launch order through an atomic counter,
-// each tile publishes its aggregate then its inclusive prefix in one 64-bit word
-// (flag | count), and successors accumulate predecessors' words walking
-// backwards.  Both outputs are ascending (stable), bit-identical to a serial scan.
+// Compaction of the FIRED frames and of the uncertain logits: one persistent
+// two-phase launch each (classify + bitmask + count per contiguous range, grid
+// barrier, indices from the bitmask) — see compact_fired_kernel / route_kernel.
+// Both outputs are ascending (stable), bit-identical to a serial scan.
 //
 // Label resolution follows the backward pointers of O8 without pointer
 // chasing: among checked frames (tau = p * t_skip) a mode-1 suppression copies
@@ -20,12 +17,6 @@
 
 namespace ns {
 
-constexpr int kScanThreads = 512;
-constexpr int kScanItems = 16;
-constexpr int kScanTile = kScanThreads * kScanItems;
-constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
-constexpr unsigned long long kValMask = (1ull << 62) - 1;
-
 NS_DEV unsigned long long ld_relaxed(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -35,278 +26,241 @@ NS_DEV void st_relaxed(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-struct ScanWs {
-  unsigned long long* status;  // [ntiles]
-  unsigned int* counter;       // tile ticket
+// ------------------------------------------------------------ two-phase bitmask compaction
+// Compaction of the FIRED frames (O5) and of the uncertain logits (O7) as one
+// persistent cooperative launch each, all G CTAs co-resident, CTA c owning the
+// contiguous chunk range [c*C/G, (c+1)*C/G) of 4,096-item warp-chunks:
+//   phase 1: stream the range once (coalesced 16-byte loads, 8 in flight per
+//            lane), classify every item, write a 1-bit-per-item mask (u16 per 16
+//            items) and the side outputs, count the selected items;
+//   grid barrier (arrival counter, acquire spin; co-residency from the launch);
+//   phase 2: offset = the lower ranges' counts; read only the MASK (1/8 byte per
+//            item) and write the ascending indices — each lane owns 128
+//            consecutive items, warp scan + block scan give its output position.
+// DRAM traffic per item = the item + 1/4 byte of mask (write + read) + 4 bytes per
+// selected item: within 1.1x of the algorithmic bytes at 15 % selected.
+constexpr int kMThreads = 512, kMWarps = kMThreads / 32;
+constexpr int kMItems = 16, kMRounds = 4;
+constexpr int kMChunk = 32 * kMItems * kMRounds;   // 2048 items per warp-chunk
+constexpr int kMHalf = kMChunk / 16;               // mask halfwords per chunk
+constexpr int kMLaneWords = kMChunk / 32 / 32;     // phase 2: 32-bit mask words per lane (64 items)
+constexpr int kMMaxCtas = 1024;
+static_assert(NOSCOPE_FIRED == 2, "SWAR compare below tests bytes == 0x02");
+
+struct MaskWs {
+  unsigned* arrive;                // grid-barrier arrivals (zeroed before the launch)
+  unsigned long long* cta_count;   // [kMMaxCtas] selected items per CTA range
+  uint16_t* masks;                 // [nchunks * kMHalf]: bit e of masks[i / 16] = item i selected
 };
 
 size_t compact_ws_bytes(int64_t n) {
-  int64_t tiles = (n + kScanTile - 1) / kScanTile + 1;
-  return (size_t)(tiles * 8 + 64);
+  const int64_t nch = (n + kMChunk - 1) / kMChunk;
+  return 256 + (size_t)kMMaxCtas * 8 + (((size_t)nch * kMHalf * 2 + 255) & ~size_t(255));
 }
-static ScanWs scan_ws_of(void* p, int64_t n) {
-  ScanWs w;
-  w.counter = reinterpret_cast<unsigned int*>(p);
-  w.status = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(p) + 64);
-  (void)n;
-  return w;
+static MaskWs mask_ws_of(void* p) {
+  uint8_t* b = reinterpret_cast<uint8_t*>(p);
+  return MaskWs{reinterpret_cast<unsigned*>(b), reinterpret_cast<unsigned long long*>(b + 256),
+                reinterpret_cast<uint16_t*>(b + 256 + kMMaxCtas * 8)};
 }
-
-// Block-wide exclusive scan of per-thread counts; *total = block sum.
-NS_DEV uint32_t block_excl_scan(uint32_t v, uint32_t* warp_sums, uint32_t* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) warp_sums[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t w = lane < nw ? warp_sums[lane] : 0u;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += y;
-    }
-    if (lane < nw) warp_sums[lane] = w;
-  }
-  __syncthreads();
-  *total = warp_sums[nw - 1];
-  uint32_t pre = warp == 0 ? 0u : warp_sums[warp - 1];
-  return pre + x - v;
-}
-
-// Decoupled look-back: exclusive prefix of this tile.  Warp 0 inspects the 32
-// preceding tiles' status words at once: if one of them holds an inclusive prefix,
-// the nearest such tile ends the walk (sum of the words up to it); otherwise all 32
-// aggregates are added and the window moves 32 tiles back.
-NS_DEV uint64_t tile_lookback(ScanWs ws, int tile, uint32_t agg, uint64_t* s_excl) {
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    uint64_t excl = 0;
-    if (tile == 0) {
-      if (lane == 0) st_relaxed(&ws.status[0], kFlagIncl | agg);
-    } else {
-      if (lane == 0) st_relaxed(&ws.status[tile], kFlagAgg | agg);
-      int p = tile - 1;  // window [p - 31, p]; lane l reads tile p - l
-      while (true) {
-        const int q = p - lane;
-        unsigned long long v = q >= 0 ? ld_relaxed(&ws.status[q]) : kFlagIncl;
-        while (__any_sync(0xffffffffu, (v & ~kValMask) == 0)) {
-          if ((v & ~kValMask) == 0) v = ld_relaxed(&ws.status[q]);
-        }
-        const unsigned incl = __ballot_sync(0xffffffffu, (v & ~kValMask) == kFlagIncl);
-        const int stop = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive tile (or the window)
-        uint64_t x = lane <= stop ? (v & kValMask) : 0ull;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        excl += x;
-        if (incl) break;
-        p -= 32;
-      }
-      if (lane == 0) st_relaxed(&ws.status[tile], kFlagIncl | (excl + agg));
-    }
-    if (lane == 0) *s_excl = excl;
-  }
-  __syncthreads();
-  return *s_excl;
-}
-
-NS_DEV int claim_tile(ScanWs ws, int* s_tile) {
-  if (threadIdx.x == 0) *s_tile = (int)atomicAdd(ws.counter, 1u);
-  __syncthreads();
-  return *s_tile;
-}
-
-// ------------------------------------------------------------ fired frames
-// Tile-local stable write-out: the tile's selected indices are staged in smem in
-// scan order, then stored as one coalesced run at the tile's global offset.
-NS_DEV void store_run(int32_t* out, uint64_t excl, uint32_t total, const int32_t* idx_s) {
-  for (uint32_t k = threadIdx.x; k < total; k += blockDim.x) out[excl + k] = idx_s[k];
-}
-
-// Compaction of the FIRED frames (O5) as one persistent launch in two phases,
-// all G CTAs co-resident, CTA c owning the contiguous tile range
-// [c*T/G, (c+1)*T/G) of 8,192-frame tiles:
-//   phase 1: stream the range, count FIRED frames (and apply the t_skip rewrite:
-//            SKIPPED + score -inf in global memory); publish the range count;
-//   grid barrier (atomic arrival counter, acquire spin);
-//   phase 2: offset = sum of the lower ranges' counts; stream the range again and
-//            write the ascending indices, tile by tile (block scan, indices staged
-//            in smem, one coalesced run per tile).
-// Both phases prefetch kCStages tiles ahead with cp.async.bulk into a smem ring
-// (one mbarrier per stage), so every pass streams at HBM rate; there is no
-// look-back chain (a single-pass decoupled look-back is bound by one L2 round trip
-// per round of G tiles).  At the cascade's chunk sizes phase 2 re-reads from L2.
-// Tail or misaligned tiles are read directly from global memory.
-constexpr int kCThreads = 256, kCItems = 32, kCTile = kCThreads * kCItems, kCStages = 4;
-static_assert(NOSCOPE_FIRED == 2, "SWAR compare below tests bytes == 0x02");
 
 NS_DEV unsigned ld_acquire_gpu(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+NS_DEV uint4 ld_stream16(const void* p) {   // read-once data: do not keep in L1
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
 
-__global__ void __launch_bounds__(kCThreads)
-compact_fired_kernel(uint8_t* disp, double* score, int64_t n, int64_t tau0, int t_skip,
-                     int32_t* idx_out, int64_t* count_out, ScanWs ws, int ntiles, int vec) {
-  extern __shared__ __align__(128) uint8_t csm[];
-  uint8_t* ring = csm;                                            // kCStages x kCTile
-  uint64_t* full = reinterpret_cast<uint64_t*>(csm + kCStages * kCTile);
-  uint32_t* warp_sums = reinterpret_cast<uint32_t*>(full + kCStages);  // [32]
-  uint64_t* s_off = reinterpret_cast<uint64_t*>(warp_sums + 32);
-  int32_t* idx_s = reinterpret_cast<int32_t*>(s_off + 2);         // kCTile staged indices
-  const int tid = threadIdx.x, G = gridDim.x, c = blockIdx.x;
-  const int t0 = (int)(((int64_t)ntiles * c) / G), t1 = (int)(((int64_t)ntiles * (c + 1)) / G);
-  const int nt = t1 - t0;
-  auto bulk_ok = [&](int t) { return vec && (int64_t)(t + 1) * kCTile <= n; };
-  // k-th fill of the ring (k counts over both passes): tile t0 + k % nt into stage k % kCStages
-  auto fill = [&](int k) {
-    const int st = k % kCStages;
-    const int t = t0 + (k < nt ? k : k - nt);
-    if (k < 2 * nt && bulk_ok(t)) {
-      mbar_arrive_expect_tx(&full[st], (uint32_t)kCTile);
-      bulk_g2s(ring + (size_t)st * kCTile, disp + (int64_t)t * kCTile, (uint32_t)kCTile, &full[st]);
-    } else {
-      mbar_arrive(&full[st]);  // keeps the stage's phase count in step
-    }
-  };
-  if (tid == 0) {
-    for (int st = 0; st < kCStages; ++st) mbar_init(&full[st], 1);
-    fence_mbar_init();
-    for (int k = 0; k < kCStages; ++k) fill(k);
-  }
+// Per-warp counts of the warps' contiguous sub-ranges -> publish the CTA's sum,
+// grid barrier, and return this WARP's exclusive output offset (lower CTAs'
+// ranges + lower warps of this CTA).  The last CTA also writes the grand total.
+NS_DEV uint64_t grid_exclusive_offset(MaskWs ws, uint32_t mine, int64_t* total_out) {
+  __shared__ uint32_t wsum[kMWarps];
+  __shared__ uint64_t s_off;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t w = warp_sum(mine);
+  if (lane == 0) wsum[warp] = w;
   __syncthreads();
-  // this thread's 16 frames of the k-th tile of the range: FIRED flags after the t_skip rule
-  auto load_flags = [&](int k, bool rewrite) -> uint32_t {
-    const int st = k % kCStages;
-    mbar_wait(&full[st], (uint32_t)((k / kCStages) & 1));
-    const int t = t0 + (k < nt ? k : k - nt);
-    const int64_t base = (int64_t)t * kCTile + (int64_t)tid * kCItems;
-    uint8_t d[kCItems];
-    if (bulk_ok(t)) {
-      const uint4* vp = reinterpret_cast<const uint4*>(ring + (size_t)st * kCTile + tid * kCItems);
-      const uint4 v0 = vp[0], v1 = vp[1];
-      const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-      if (t_skip == 1) {  // SWAR: FIRED bytes -> 4-bit masks (byte e -> bit e)
-        uint32_t flags = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          flags |= (((__vcmpeq4(w[j], 0x02020202u) & 0x01010101u) * 0x01020408u) >> 24) << (4 * j);
-        return flags;
-      }
-#pragma unroll
-      for (int e = 0; e < kCItems; ++e) d[e] = (uint8_t)(w[e >> 2] >> (8 * (e & 3)));
-    } else {
-#pragma unroll
-      for (int e = 0; e < kCItems; ++e) d[e] = base + e < n ? disp[base + e] : (uint8_t)0;
-    }
-    uint32_t flags = 0;
-    if (t_skip == 1) {
-#pragma unroll
-      for (int e = 0; e < kCItems; ++e)
-        if (d[e] == NOSCOPE_FIRED && base + e < n) flags |= 1u << e;
-    } else {
-      int r = (int)((tau0 + base) % t_skip);  // tau mod t_skip, advanced incrementally
-#pragma unroll
-      for (int e = 0; e < kCItems; ++e) {
-        const int64_t f = base + e;
-        if (f < n) {
-          if (r != 0) {
-            if (rewrite) {
-              disp[f] = NOSCOPE_SKIPPED;
-              if (score) score[f] = __longlong_as_double(0xFFF0000000000000ll);  // -inf
-            }
-          } else if (d[e] == NOSCOPE_FIRED) {
-            flags |= 1u << e;
-          }
-        }
-        if (++r == t_skip) r = 0;
-      }
-    }
-    return flags;
-  };
-
-  // ---- phase 1: count
-  uint32_t mine = 0;
-  for (int k = 0; k < nt; ++k) {
-    mine += __popc(load_flags(k, true));
-    __syncthreads();                    // every thread is done with stage k % kCStages
-    if (tid == 0) fill(k + kCStages);
-  }
-  uint32_t range_total;
-  block_excl_scan(mine, warp_sums, &range_total);
-  if (tid == 0) {
-    st_relaxed(&ws.status[c], (unsigned long long)range_total);
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int i = 0; i < kMWarps; ++i) t += wsum[i];
+    const int c = blockIdx.x, G = gridDim.x;
+    st_relaxed(&ws.cta_count[c], (unsigned long long)t);
     __threadfence();
-    atomicAdd(ws.counter, 1u);
-    while (ld_acquire_gpu(ws.counter) < (unsigned)G) {
+    atomicAdd(ws.arrive, 1u);
+    while (ld_acquire_gpu(ws.arrive) < (unsigned)G) {
     }
     uint64_t off = 0;
-    for (int q = 0; q < c; ++q) off += ld_relaxed(&ws.status[q]);
-    *s_off = off;
-    if (c == G - 1 && count_out) *count_out = (int64_t)(off + range_total);
+    for (int q = 0; q < c; ++q) off += ld_relaxed(&ws.cta_count[q]);
+    s_off = off;
+    if (c == G - 1 && total_out) *total_out = (int64_t)(off + t);
   }
   __syncthreads();
-  uint64_t off = *s_off;
+  uint64_t off = s_off;
+  for (int i = 0; i < warp; ++i) off += wsum[i];
+  return off;
+}
 
-  // ---- phase 2: write the ascending indices
-  for (int k = nt; k < 2 * nt; ++k) {
-    const uint32_t flags = load_flags(k, false);
-    uint32_t total;
-    const uint32_t local = block_excl_scan((uint32_t)__popc(flags), warp_sums, &total);
-    if (tid == 0) fill(k + kCStages);   // block_excl_scan synced: stage free
-    const int64_t base = (int64_t)(t0 + k - nt) * kCTile + (int64_t)tid * kCItems;
-    uint32_t q = local;
-    for (uint32_t f = flags; f; f &= f - 1) idx_s[q++] = (int32_t)(base + __ffs(f) - 1);
-    __syncthreads();
-    if (idx_out) store_run(idx_out, off, total, idx_s);
-    off += total;
-    __syncthreads();                    // idx_s / warp_sums reuse
+// Contiguous chunk sub-range of warp `warp` within the CTA range [ch0, ch1).
+NS_DEV void warp_range(int64_t ch0, int64_t ch1, int warp, int64_t* a, int64_t* b) {
+  const int64_t len = ch1 - ch0;
+  *a = ch0 + len * warp / kMWarps;
+  *b = ch0 + len * (warp + 1) / kMWarps;
+}
+
+// Phase 2: the selected items of this warp's chunks [wa, wb), ascending, from
+// their masks, starting at output position `off`.  Per chunk (2,048 items):
+// lane L owns items 64L .. 64L+63 (one 8-byte mask load, prefetched a chunk
+// ahead), a warp scan gives each selected item its position in the chunk's run;
+// the warp stages the item offsets (u16) in its own shared-memory slice, then
+// writes the run with coalesced stores: emit(item, pos) for k = lane, lane + 32, ..
+constexpr size_t kMStageBytes = (size_t)kMWarps * kMChunk * 2;   // 64 KB dynamic smem (3 CTAs / SM)
+
+template <class Emit>
+NS_DEV void emit_selected(MaskWs ws, int64_t wa, int64_t wb, uint64_t off, uint16_t* stage_all, Emit&& emit) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint16_t* stage = stage_all + (size_t)warp * kMChunk;
+  static_assert(kMLaneWords == 2, "one 8-byte mask load per lane");
+  auto load = [&](int64_t ch) -> uint2 {
+    return ch < wb ? *reinterpret_cast<const uint2*>(ws.masks + (size_t)ch * kMHalf + 4 * lane)
+                   : make_uint2(0, 0);
+  };
+  uint2 nxt = load(wa);
+  for (int64_t ch = wa; ch < wb; ++ch) {
+    const uint2 m = nxt;
+    nxt = load(ch + 1);
+    const uint32_t cnt = __popc(m.x) + __popc(m.y);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+    uint32_t q = incl - cnt;
+    const uint32_t mw[2] = {m.x, m.y};
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      for (uint32_t f = mw[j]; f; f &= f - 1) stage[q++] = (uint16_t)(64 * lane + 32 * j + (__ffs(f) - 1));
+    __syncwarp();
+    const int64_t item0 = ch * kMChunk;
+    for (uint32_t k = lane; k < wtot; k += 32) emit(item0 + stage[k], off + k);
+    __syncwarp();                                           // stage reused next chunk
+    off += wtot;
   }
 }
 
-static size_t compact_smem_bytes() {
-  return (size_t)kCStages * kCTile + kCStages * 8 + 32 * 4 + 16 + (size_t)kCTile * 4;
+__global__ void __launch_bounds__(kMThreads, 3)
+compact_fired_kernel(uint8_t* disp, double* score, int64_t n, int64_t tau0, int t_skip,
+                     int32_t* idx_out, int64_t* count_out, MaskWs ws, int vec) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x, c = blockIdx.x;
+  const int64_t nch = (n + kMChunk - 1) / kMChunk;
+  const int64_t ch0 = nch * c / G, ch1 = nch * (c + 1) / G;
+  // ---- phase 1: FIRED masks (after the t_skip rule) and this warp's count
+  int64_t wa, wb;
+  warp_range(ch0, ch1, warp, &wa, &wb);
+  uint32_t mine = 0;
+  auto fast_ok = [&](int64_t ch) { return vec && t_skip == 1 && (ch + 1) * kMChunk <= n; };
+  auto masks_of = [&](const uint4 (&v)[kMRounds], int64_t ch) {
+    uint16_t* mk = ws.masks + (size_t)ch * kMHalf + lane;
+#pragma unroll
+    for (int r = 0; r < kMRounds; ++r) {   // SWAR: FIRED bytes -> bits (byte e -> bit e)
+      const uint32_t w[4] = {v[r].x, v[r].y, v[r].z, v[r].w};
+      uint32_t m = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        m |= (((__vcmpeq4(w[j], 0x02020202u) & 0x01010101u) * 0x01020408u) >> 24) << (4 * j);
+      mk[r * 32] = (uint16_t)m;
+      mine += __popc(m);
+    }
+  };
+  int64_t ch = wa;
+  for (; ch + 1 < wb && fast_ok(ch + 1); ch += 2) {   // two chunks (8 loads per lane) in flight
+    uint4 v[2][kMRounds];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int r = 0; r < kMRounds; ++r) v[c][r] = ld_stream16(disp + (ch + c) * kMChunk + r * 512 + lane * 16);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) masks_of(v[c], ch + c);
+  }
+  for (; ch < wb; ++ch) {
+    const int64_t base = ch * kMChunk;
+    if (fast_ok(ch)) {
+      uint4 v[kMRounds];
+#pragma unroll
+      for (int r = 0; r < kMRounds; ++r) v[r] = ld_stream16(disp + base + r * 512 + lane * 16);
+      masks_of(v, ch);
+    } else {   // tail, misaligned or t_skip > 1: per item (and the skipped rewrite)
+      uint16_t* mk = ws.masks + (size_t)ch * kMHalf + lane;
+      for (int r = 0; r < kMRounds; ++r) {
+        const int64_t i0 = base + r * 512 + lane * 16;
+        uint32_t m = 0;
+        int ph = t_skip > 1 ? (int)((tau0 + i0) % t_skip) : 0;
+        for (int e = 0; e < kMItems; ++e) {
+          const int64_t f = i0 + e;
+          if (f < n) {
+            if (ph != 0) {
+              disp[f] = NOSCOPE_SKIPPED;
+              if (score) score[f] = __longlong_as_double(0xFFF0000000000000ll);   // -inf
+            } else if (disp[f] == NOSCOPE_FIRED) {
+              m |= 1u << e;
+            }
+          }
+          if (t_skip > 1 && ++ph == t_skip) ph = 0;
+        }
+        mk[r * 32] = (uint16_t)m;
+        mine += __popc(m);
+      }
+    }
+  }
+  const uint64_t off = grid_exclusive_offset(ws, mine, count_out);
+  // ---- phase 2: ascending indices from the masks
+  extern __shared__ __align__(16) uint16_t mstage[];
+  if (idx_out)
+    emit_selected(ws, wa, wb, off, mstage, [&](int64_t i, uint64_t p) { idx_out[p] = (int32_t)i; });
 }
-
-size_t compact_fired_tiles(int64_t n) { return (n + kCTile - 1) / kCTile; }
 
 noscope_status launch_compact_fired(const uint8_t* /*disp_in*/, uint8_t* disp, double* score,
                                     int64_t n, int64_t tau0, int t_skip, int32_t* idx_out,
                                     int64_t* count_out, void* scan_ws, cudaStream_t st) {
-  const int ntiles = (int)compact_fired_tiles(n);
-  if (ntiles == 0) {
+  const int64_t nch = (n + kMChunk - 1) / kMChunk;
+  if (nch == 0) {
     if (count_out) NS_CUDA_TRY(cudaMemsetAsync(count_out, 0, sizeof(int64_t), st));
     return NOSCOPE_OK;
   }
-  NS_CUDA_TRY(cudaMemsetAsync(scan_ws, 0, compact_ws_bytes(n), st));
+  NS_CUDA_TRY(cudaMemsetAsync(scan_ws, 0, 256, st));   // barrier arrivals
   const int vec = (reinterpret_cast<uintptr_t>(disp) & 15) == 0;
-  const size_t smem = compact_smem_bytes();
   static DeviceInt occ;
   int per_sm = occ.get();
   if (per_sm == 0) {
-    NS_CUDA_TRY(cudaFuncSetAttribute(compact_fired_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    NS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compact_fired_kernel, kCThreads, smem));
-    if (per_sm < 1) per_sm = 1;
+    NS_CUDA_TRY(cudaFuncSetAttribute(compact_fired_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kMStageBytes));
+    NS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compact_fired_kernel, kMThreads,
+                                                              kMStageBytes));
+    per_sm = std::max(1, per_sm);
     occ.set(per_sm);
   }
-  int sms = kNumSMs, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // persistent and co-resident (look-back waits only on earlier-claimed tiles)
-  const int grid = std::min(ntiles, per_sm * sms);
-  NS_CUDA_TRY(launch_cooperative(compact_fired_kernel, grid, kCThreads, smem, st, disp, score, n, tau0, t_skip,
-                                 idx_out, count_out, scan_ws_of(scan_ws, n), ntiles, vec));
+  int sms = kNumSMs;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device());
+  // persistent and co-resident (the grid barrier): at most the resident CTA count
+  const int grid = (int)std::min<int64_t>({nch, (int64_t)per_sm * sms, (int64_t)kMMaxCtas});
+  NS_CUDA_TRY(launch_cooperative(compact_fired_kernel, grid, kMThreads, kMStageBytes, st, disp, score, n, tau0, t_skip,
+                                 idx_out, count_out, mask_ws_of(scan_ws), vec));
   NS_LAUNCH_CHECK();
   count_launch();
   return NOSCOPE_OK;
 }
 
 // ------------------------------------------------------------ routing
+// Same two-phase structure over the fired logits (count from the device):
+// phase 1 reads each logit once (float4 loads), writes its route code (compact
+// and/or per frame via frame_idx), counts NEG / POS, marks UNCERTAIN in the mask;
+// phase 2 writes the uncertain frame indices (and per-frame list positions).
 struct RouteArgs {
   float lo, hi;
   const float* logits;
@@ -324,103 +278,93 @@ struct RouteArgs {
   int vec;                   // logits and route_out 16-byte aligned
 };
 
-__global__ void __launch_bounds__(kScanThreads)
-route_kernel(RouteArgs A, ScanWs ws) {
-  __shared__ uint32_t warp_sums[32];
-  __shared__ uint64_t s_excl;
-  __shared__ int s_tile;
-  __shared__ unsigned int s_neg, s_pos;
-  __shared__ int32_t idx_s[kScanTile];
+NS_DEV uint8_t route_code(float z, float lo, float hi) {
+  // NEG iff z < lo, POS iff z > hi, else UNCERTAIN (R-5; NaN -> UNCERTAIN + status)
+  return z < lo ? NOSCOPE_R_NEG : (z > hi ? NOSCOPE_R_POS : NOSCOPE_R_UNC);
+}
+
+__global__ void __launch_bounds__(kMThreads, 2)
+route_kernel(RouteArgs A, MaskWs ws) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x, c = blockIdx.x;
   const int64_t n = A.n_dev ? min(*A.n_dev, A.n_max) : A.n_max;
-  const int ntiles = (int)((n + kScanTile - 1) / kScanTile);
-  const int tile = claim_tile(ws, &s_tile);
-  if (n == 0) {
-    if (tile == 0 && threadIdx.x == 0) *A.n_unc = 0;
-    return;
-  }
-  if (tile >= ntiles) return;
-  if (threadIdx.x == 0) s_neg = s_pos = 0;
-  const int64_t base = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
-  const bool full = A.vec && base + kScanItems <= n;
-  float zv[kScanItems];
-  if (full) {
+  const int64_t nch = (n + kMChunk - 1) / kMChunk;
+  const int64_t ch0 = nch * c / G, ch1 = nch * (c + 1) / G;
+  int64_t wa, wb;
+  warp_range(ch0, ch1, warp, &wa, &wb);
+  uint32_t mine = 0, nneg = 0, npos = 0, nan = 0;
+  for (int64_t ch = wa; ch < wb; ++ch) {
+    const int64_t base = ch * kMChunk;
+    uint16_t* mk = ws.masks + (size_t)ch * kMHalf + lane;
+    const bool fast = A.vec && base + kMChunk <= n;
+#pragma unroll 1
+    for (int r = 0; r < kMRounds; ++r) {
+      const int64_t i0 = base + r * 512 + lane * 16;
+      float z[kMItems];
+      if (fast) {
 #pragma unroll
-    for (int q = 0; q < kScanItems / 4; ++q) {
-      const float4 v = reinterpret_cast<const float4*>(A.logits + base)[q];
-      zv[4 * q] = v.x; zv[4 * q + 1] = v.y; zv[4 * q + 2] = v.z; zv[4 * q + 3] = v.w;
-    }
-  } else {
+        for (int q = 0; q < 4; ++q) {
+          const uint4 v = ld_stream16(A.logits + i0 + 4 * q);
+          z[4 * q] = __uint_as_float(v.x);
+          z[4 * q + 1] = __uint_as_float(v.y);
+          z[4 * q + 2] = __uint_as_float(v.z);
+          z[4 * q + 3] = __uint_as_float(v.w);
+        }
+      } else {
 #pragma unroll
-    for (int e = 0; e < kScanItems; ++e) zv[e] = base + e < n ? A.logits[base + e] : 0.f;
-  }
-  uint32_t flags = 0, cnt = 0, nneg = 0, npos = 0, nan = 0;
-  uint8_t code[kScanItems];
-#pragma unroll
-  for (int e = 0; e < kScanItems; ++e) {
-    const float z = zv[e];
-    const bool in = base + e < n;
-    // NEG iff z < lo, POS iff z > hi, else UNCERTAIN (R-5; NaN -> UNCERTAIN + status)
-    code[e] = z < A.lo ? NOSCOPE_R_NEG : (z > A.hi ? NOSCOPE_R_POS : NOSCOPE_R_UNC);
-    if (in) {
-      nneg += code[e] == NOSCOPE_R_NEG;
-      npos += code[e] == NOSCOPE_R_POS;
-      if (code[e] == NOSCOPE_R_UNC) {
-        flags |= 1u << e;
-        ++cnt;
+        for (int e = 0; e < kMItems; ++e) z[e] = i0 + e < n ? A.logits[i0 + e] : 0.f;
       }
-      nan |= z != z;
+      uint32_t m = 0, w[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int e = 0; e < kMItems; ++e) {
+        const uint32_t code = route_code(z[e], A.lo, A.hi);
+        w[e >> 2] |= code << (8 * (e & 3));
+        if (i0 + e < n) {
+          nneg += code == NOSCOPE_R_NEG;
+          npos += code == NOSCOPE_R_POS;
+          m |= (uint32_t)(code == NOSCOPE_R_UNC) << e;
+          nan |= z[e] != z[e];
+        }
+      }
+      mk[r * 32] = (uint16_t)m;
+      mine += __popc(m);
+      if (A.route_out) {
+        if (fast) {
+          *reinterpret_cast<uint4*>(A.route_out + i0) = make_uint4(w[0], w[1], w[2], w[3]);
+        } else {
+          for (int e = 0; e < kMItems; ++e)
+            if (i0 + e < n) A.route_out[i0 + e] = (uint8_t)(w[e >> 2] >> (8 * (e & 3)));
+        }
+      }
+      if (A.frame_idx) {
+        for (int e = 0; e < kMItems; ++e)
+          if (i0 + e < n) {
+            const int32_t f = A.frame_idx[i0 + e];
+            if (A.route_pf) A.route_pf[f] = (uint8_t)(w[e >> 2] >> (8 * (e & 3)));
+            if (A.logits_pf) A.logits_pf[f] = z[e];
+          }
+      }
     }
   }
   if (nan) atomicOr(A.status, 2u);
-  if (A.route_out) {
-    if (full) {
-      uint32_t w[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        w[q] = code[4 * q] | (code[4 * q + 1] << 8) | (code[4 * q + 2] << 16) | ((uint32_t)code[4 * q + 3] << 24);
-      *reinterpret_cast<uint4*>(A.route_out + base) = make_uint4(w[0], w[1], w[2], w[3]);
-    } else {
-#pragma unroll
-      for (int e = 0; e < kScanItems; ++e)
-        if (base + e < n) A.route_out[base + e] = code[e];
-    }
-  }
-  if (A.frame_idx) {
-#pragma unroll
-    for (int e = 0; e < kScanItems; ++e)
-      if (base + e < n) {
-        const int32_t f = A.frame_idx[base + e];
-        if (A.route_pf) A.route_pf[f] = code[e];
-        if (A.logits_pf) A.logits_pf[f] = zv[e];
-      }
-  }
-  uint32_t total;
-  uint32_t local = block_excl_scan(cnt, warp_sums, &total);
   if (A.counters) {
-    if (nneg) atomicAdd(&s_neg, nneg);
-    if (npos) atomicAdd(&s_pos, npos);
-  }
-  {
-    uint32_t q = local;
-#pragma unroll
-    for (int e = 0; e < kScanItems; ++e)
-      if (flags & (1u << e)) idx_s[q++] = A.frame_idx ? A.frame_idx[base + e] : (int32_t)(base + e);
-  }
-  uint64_t excl = tile_lookback(ws, tile, total, &s_excl);  // ends with __syncthreads
-  if (A.unc_pos_pf) {
-    uint64_t pos = excl + local;
-#pragma unroll
-    for (int e = 0; e < kScanItems; ++e)
-      if (flags & (1u << e)) A.unc_pos_pf[A.frame_idx ? A.frame_idx[base + e] : (int32_t)(base + e)] = (int32_t)pos++;
-  }
-  store_run(A.unc_out, excl, total, idx_s);
-  if (threadIdx.x == 0) {
-    if (A.counters) {
-      atomicAdd(&A.counters[0], (unsigned long long)s_neg);
-      atomicAdd(&A.counters[1], (unsigned long long)s_pos);
+    nneg = warp_sum(nneg);
+    npos = warp_sum(npos);
+    if (lane == 0 && (nneg | npos)) {
+      atomicAdd(&A.counters[0], (unsigned long long)nneg);
+      atomicAdd(&A.counters[1], (unsigned long long)npos);
     }
-    if (tile == ntiles - 1) *A.n_unc = (int64_t)(excl + total);
   }
+  if (nch == 0) {   // no items: the count is still written
+    if (c == 0 && threadIdx.x == 0) *A.n_unc = 0;
+    return;
+  }
+  const uint64_t off = grid_exclusive_offset(ws, mine, A.n_unc);
+  extern __shared__ __align__(16) uint16_t mstage[];
+  emit_selected(ws, wa, wb, off, mstage, [&](int64_t i, uint64_t p) {
+    const int32_t f = A.frame_idx ? A.frame_idx[i] : (int32_t)i;
+    A.unc_out[p] = f;
+    if (A.unc_pos_pf) A.unc_pos_pf[f] = (int32_t)p;
+  });
 }
 
 noscope_status launch_route(noscope_route r, const float* logits, const int64_t* n_dev,
@@ -428,14 +372,25 @@ noscope_status launch_route(noscope_route r, const float* logits, const int64_t*
                             uint8_t* route_pf, int32_t* unc_out, int64_t* n_unc,
                             int32_t* unc_pos_pf, float* logits_pf, uint64_t* counters,
                             void* scan_ws, uint32_t* status, cudaStream_t st) {
-  int ntiles = (int)((n_max + kScanTile - 1) / kScanTile);
-  if (ntiles == 0) ntiles = 1;
-  NS_CUDA_TRY(cudaMemsetAsync(scan_ws, 0, compact_ws_bytes(n_max), st));
+  const int64_t nch = std::max<int64_t>(1, (n_max + kMChunk - 1) / kMChunk);
+  NS_CUDA_TRY(cudaMemsetAsync(scan_ws, 0, 256, st));   // barrier arrivals
   RouteArgs A{r.lo_logit, r.hi_logit, logits, n_dev, n_max, frame_idx, route_out, route_pf,
               unc_out, n_unc, unc_pos_pf, logits_pf,
               reinterpret_cast<unsigned long long*>(counters), status,
               (int)(((reinterpret_cast<uintptr_t>(logits) | reinterpret_cast<uintptr_t>(route_out)) & 15) == 0)};
-  route_kernel<<<ntiles, kScanThreads, 0, st>>>(A, scan_ws_of(scan_ws, n_max));
+  static DeviceInt occ;
+  int per_sm = occ.get();
+  if (per_sm == 0) {
+    NS_CUDA_TRY(cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMStageBytes));
+    NS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, route_kernel, kMThreads, kMStageBytes));
+    per_sm = std::max(1, per_sm);
+    occ.set(per_sm);
+  }
+  int sms = kNumSMs;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device());
+  // n_max bounds the device count: every CTA a grid of this size could need is launched
+  const int grid = (int)std::min<int64_t>({nch, (int64_t)per_sm * sms, (int64_t)kMMaxCtas});
+  NS_CUDA_TRY(launch_cooperative(route_kernel, grid, kMThreads, kMStageBytes, st, A, mask_ws_of(scan_ws)));
   NS_LAUNCH_CHECK();
   count_launch();
   return NOSCOPE_OK;

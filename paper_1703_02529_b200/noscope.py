@@ -133,9 +133,13 @@ def lib():
     L.noscope_specialized_infer.argtypes = [C.POINTER(CnnArchC), C.POINTER(CnnWeightsC), c_p, c_i64,
                                             c_p, c_p, c_i64, c_p, c_p, c_sz, c_p]
     L.noscope_route_logits.restype = c_i32
-    L.noscope_route_logits.argtypes = [Route, c_p, c_p, c_i64, c_p, c_p, c_p, c_p]
+    L.noscope_route_logits.argtypes = [Route, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_sz, c_p]
+    L.noscope_route_workspace_bytes.restype = c_sz
+    L.noscope_route_workspace_bytes.argtypes = [c_i64]
     L.noscope_compact_fired.restype = c_i32
-    L.noscope_compact_fired.argtypes = [c_p, c_i64, c_i64, c_i32, c_p, c_p, c_p]
+    L.noscope_compact_fired.argtypes = [c_p, c_i64, c_i64, c_i32, c_p, c_p, c_p, c_sz, c_p]
+    L.noscope_compact_workspace_bytes.restype = c_sz
+    L.noscope_compact_workspace_bytes.argtypes = [c_i64]
     L.noscope_cascade_run.restype = c_i32
     L.noscope_cascade_run.argtypes = [C.POINTER(DDConfig), C.POINTER(CnnArchC),
                                       C.POINTER(CnnWeightsC), Route, c_p, FramesDesc, c_i64, c_i64,
@@ -317,25 +321,33 @@ def noscope_specialized_infer(arch: Arch, weights: Weights, small: torch.Tensor,
     return out[:n_max]
 
 
-def noscope_route_logits(lo: float, hi: float, logits: torch.Tensor, n_dev=None, stream=None):
+def noscope_route_logits(lo: float, hi: float, logits: torch.Tensor, n_dev=None, ws=None, out=None,
+                         stream=None):
+    """-> (route codes u8 [n], uncertain positions i32, count i64[1]); ws / out reusable."""
     n = logits.numel()
     dev = logits.device
-    route = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
-    unc = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    nunc = torch.zeros(1, dtype=torch.int64, device=dev)
+    if ws is None:
+        ws = torch.empty(lib().noscope_route_workspace_bytes(n), dtype=torch.uint8, device=dev)
+    route, unc, nunc = out if out is not None else (
+        torch.empty(max(n, 1), dtype=torch.uint8, device=dev), torch.empty(max(n, 1), dtype=torch.int32, device=dev),
+        torch.zeros(1, dtype=torch.int64, device=dev))
     _check(lib().noscope_route_logits(Route(lo, hi), _ptr(logits), _ptr(n_dev), n, _ptr(route),
-                                      _ptr(unc), _ptr(nunc), _stream(stream)), "noscope_route_logits")
+                                      _ptr(unc), _ptr(nunc), _ptr(ws), ws.numel(), _stream(stream)),
+           "noscope_route_logits")
     return route[:n], unc, nunc
 
 
-def noscope_compact_fired(disposition: torch.Tensor, seg_offset=0, t_skip=1, stream=None):
-    """Stable list of FIRED positions (disposition u8, rewritten in place for t_skip)."""
+def noscope_compact_fired(disposition: torch.Tensor, seg_offset=0, t_skip=1, ws=None, out=None, stream=None):
+    """Stable list of FIRED positions (disposition u8, rewritten in place for t_skip).
+    -> (indices i32, count i64[1]); ws / out reusable."""
     n = disposition.numel()
     dev = disposition.device
-    idx = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    if ws is None:
+        ws = torch.empty(lib().noscope_compact_workspace_bytes(n), dtype=torch.uint8, device=dev)
+    idx, cnt = out if out is not None else (torch.empty(max(n, 1), dtype=torch.int32, device=dev),
+                                            torch.zeros(1, dtype=torch.int64, device=dev))
     _check(lib().noscope_compact_fired(_ptr(disposition), n, seg_offset, t_skip, _ptr(idx), _ptr(cnt),
-                                       _stream(stream)), "noscope_compact_fired")
+                                       _ptr(ws), ws.numel(), _stream(stream)), "noscope_compact_fired")
     return idx, cnt
 
 

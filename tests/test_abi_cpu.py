@@ -130,12 +130,18 @@ def test_next_row_entry_points_validate_before_device_use(lib):
 def test_compact_fired_validates_before_device_use(lib):
     """noscope_compact_fired (H4 helper) rejects bad arguments on the host."""
     one = ctypes.c_void_p(16)
-    assert lib.noscope_compact_fired(None, 10, 0, 1, one, one, None) == 1        # null dispositions
-    assert lib.noscope_compact_fired(one, 10, 0, 0, one, one, None) == 1         # t_skip < 1
-    assert lib.noscope_compact_fired(one, -1, 0, 1, one, one, None) == 1         # n < 0
-    assert lib.noscope_compact_fired(one, 1 << 31, 0, 1, one, one, None) == 1    # n >= 2^31
-    assert lib.noscope_compact_fired(one, 10, -1, 1, one, one, None) == 1        # seg_offset < 0
-    assert lib.noscope_compact_fired(one, 10, 0, 1, one, None, None) == 1        # null count
+    ws = ctypes.c_void_p(256)
+    big = 1 << 20
+    assert lib.noscope_compact_fired(None, 10, 0, 1, one, one, ws, big, None) == 1        # null dispositions
+    assert lib.noscope_compact_fired(one, 10, 0, 0, one, one, ws, big, None) == 1         # t_skip < 1
+    assert lib.noscope_compact_fired(one, -1, 0, 1, one, one, ws, big, None) == 1         # n < 0
+    assert lib.noscope_compact_fired(one, 1 << 31, 0, 1, one, one, ws, big, None) == 1    # n >= 2^31
+    assert lib.noscope_compact_fired(one, 10, -1, 1, one, one, ws, big, None) == 1        # seg_offset < 0
+    assert lib.noscope_compact_fired(one, 10, 0, 1, one, None, ws, big, None) == 1        # null count
+    assert lib.noscope_compact_fired(one, 10, 0, 1, one, one, None, big, None) == 1       # null workspace
+    need = lib.noscope_compact_workspace_bytes(1 << 20)
+    assert lib.noscope_compact_fired(one, 1 << 20, 0, 1, one, one, ws, need - 1, None) == 3   # too small
+    assert lib.noscope_compact_workspace_bytes(1 << 30) >= (1 << 30) // 8                # 1 bit per frame
 
 
 def test_bench_reference_arm_prints_one_contract_line():

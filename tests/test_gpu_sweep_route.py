@@ -234,3 +234,39 @@ def test_sweep_records_a_matches_oracle(mode, k, t_skip):
     a = nsm.noscope_sweep_records(torch.from_numpy(s).cuda(), torch.from_numpy(y).cuda(), mode, k, t_skip)
     torch.cuda.synchronize()
     assert np.array_equal(a.cpu().numpy(), O.build_records(s, y, mode, k))
+
+
+@pytest.mark.parametrize("p_fired", [0.0, 1.0, 0.5])
+def test_compact_fired_densities_many_ctas(p_fired):
+    """None / all / half fired over 3,000,017 frames (733 warp-chunks: every CTA of
+    the persistent grid owns a range; the all-fired case writes one index per frame)."""
+    nsm = ns()
+    n = 3_000_017
+    g = torch.Generator(device="cuda").manual_seed(3)
+    d = torch.where(torch.rand(n, device="cuda", generator=g) < p_fired,
+                    torch.full((), O.FIRED, dtype=torch.uint8, device="cuda"),
+                    torch.full((), O.SUPPRESSED, dtype=torch.uint8, device="cuda"))
+    idx, cnt = nsm.noscope_compact_fired(d)
+    torch.cuda.synchronize()
+    ref = np.flatnonzero(d.cpu().numpy() == O.FIRED)
+    k = int(cnt.item())
+    assert k == len(ref) and np.array_equal(idx[:k].cpu().numpy(), ref)
+
+
+def test_route_many_ctas_vs_numpy():
+    """2^24 + 13 logits (every CTA of the persistent grid busy, ragged tail) with exact
+    ties at the thresholds; codes and the uncertain list vs the O7 definition in numpy."""
+    nsm = ns()
+    n = (1 << 24) + 13
+    g = torch.Generator(device="cuda").manual_seed(9)
+    z = torch.randn(n, device="cuda", generator=g)
+    z[::1001] = 0.5
+    z[7::997] = -0.25
+    lo, hi = -0.25, 0.5
+    r, unc, nunc = nsm.noscope_route_logits(lo, hi, z)
+    torch.cuda.synchronize()
+    zn = z.cpu().numpy()
+    ro = np.where(zn < np.float32(lo), O.R_NEG, np.where(zn > np.float32(hi), O.R_POS, O.R_UNC)).astype(np.uint8)
+    assert np.array_equal(r.cpu().numpy(), ro)
+    k = int(nunc.item())
+    assert np.array_equal(unc[:k].cpu().numpy(), np.flatnonzero(ro == O.R_UNC))

@@ -22,13 +22,18 @@ for frac in (0.15, 0.5):
     d = torch.where(torch.rand(NC, device="cuda", generator=g) < frac, torch.full((), 2, dtype=torch.uint8, device="cuda"),
                     torch.full((), 1, dtype=torch.uint8, device="cuda"))
     nf = int((d == 2).sum())
-    ms = t_ms(lambda: N.noscope_compact_fired(d))
+    ws = torch.empty(N.lib().noscope_compact_workspace_bytes(NC), dtype=torch.uint8, device="cuda")
+    out = (torch.empty(NC, dtype=torch.int32, device="cuda"), torch.zeros(1, dtype=torch.int64, device="cuda"))
+    ms = t_ms(lambda: N.noscope_compact_fired(d, ws=ws, out=out))
     byt = NC + 4 * nf
     print(f"compaction 2^30 fired {frac}: {ms:.3f} ms  {byt / ms / 1e6:.1f} GB/s")
-    del d
+    del d, ws, out
 NR = 1 << 28
 z = torch.randn(NR, device="cuda", generator=g)
 nu = int(((z >= -0.5) & (z <= 0.5)).sum())
-ms = t_ms(lambda: N.noscope_route_logits(-0.5, 0.5, z))
+ws = torch.empty(N.lib().noscope_route_workspace_bytes(NR), dtype=torch.uint8, device="cuda")
+out = (torch.empty(NR, dtype=torch.uint8, device="cuda"), torch.empty(NR, dtype=torch.int32, device="cuda"),
+       torch.zeros(1, dtype=torch.int64, device="cuda"))
+ms = t_ms(lambda: N.noscope_route_logits(-0.5, 0.5, z, ws=ws, out=out))
 byt = 5 * NR + 4 * nu
 print(f"routing 2^28: {ms:.3f} ms  {byt / ms / 1e6:.1f} GB/s")
