@@ -676,6 +676,21 @@ def run_extras(device, timing=(1000, 20000, 12_500_000_000)):
                         "tflops": round(fl / ms / 1e9, 1), "frac_of_bf16_peak": round(fl / ms / 1e9 / bf16, 4)}
         del ws
     out["cnn_grid_65536"] = grid
+    # the paper's remaining search configurations (C = 16 and D = 64 / 256)
+    extra = {}
+    for a in sg.PAPER_GRID:
+        if a.name in grid:
+            continue
+        w = sg.he_normal_weights(a, 3)
+        A, Wt = N.Arch(a.n_conv, a.base_filters, a.dense), N.Weights(w, device=device)
+        ws = N.workspace(N.OP_SPECIALIZED_INFER, None, A, nG, device=device)
+        logits = torch.empty(nG, dtype=torch.float32, device=device)
+        ms = _time_ms(lambda: N.noscope_specialized_infer(A, Wt, small, ws=ws, logits=logits))
+        fl = cnn_flops_per_frame((a.n_conv, a.base_filters, a.dense)) * nG
+        extra[a.name] = {"ms": round(ms, 3), "fps": round(nG / ms * 1e3, 1), "tflops": round(fl / ms / 1e9, 1),
+                         "frac_of_bf16_peak": round(fl / ms / 1e9 / bf16, 4)}
+        del ws
+    out["cnn_paper_grid_rest_65536"] = extra
     out["tiny_T"] = tiny_config(device)
     out["next_rows"] = next_rows_extras(device, sc, gs, small, nG)
     # configs[3]: sweep over 1M labelled records, 100 x 100 candidates

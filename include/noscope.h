@@ -130,8 +130,10 @@ enum { NOSCOPE_SKIPPED = 0, NOSCOPE_SUPPRESSED = 1, NOSCOPE_FIRED = 2 };
  * ("mean-center the pixel values and change the dynamic range in each color
  * channel to [-1, 1]", reading R-13).  Operands bf16, accumulation
  * fp32 (tensor cores), activations rounded to bf16 after each pool / FC1.
- * Supported: n_conv in {2,4}, base_filters in {32,64}, dense in {32,64,128,256},
- * in_w = in_h = 50.                                                          */
+ * Supported: n_conv in {2,4}, base_filters in {16,32,64} (the text names 32 or
+ * 64, but Table 2 picks C = 16 for coral and night-street, P:1136-1140,
+ * and "24 distinct configurations", = 3 C x 2 L x 4 D), dense in
+ * {32,64,128,256}, in_w = in_h = 50.                                         */
 typedef struct {
   int32_t n_conv, base_filters, dense, in_w, in_h;
   float chan_mean[3];

@@ -263,7 +263,7 @@ static bool make_plan(const noscope_cnn_arch& a, int64_t n_max, CnnPlan* P) {
 bool cnn_arch_supported(const noscope_cnn_arch& a) {
   if (a.in_w != 50 || a.in_h != 50) return false;
   if (a.n_conv != 2 && a.n_conv != 4) return false;
-  if (a.base_filters != 32 && a.base_filters != 64) return false;
+  if (a.base_filters != 16 && a.base_filters != 32 && a.base_filters != 64) return false;
   if (a.dense != 32 && a.dense != 64 && a.dense != 128 && a.dense != 256) return false;
   CnnPlan p;
   return make_plan(a, 128, &p);

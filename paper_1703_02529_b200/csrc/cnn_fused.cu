@@ -5,7 +5,9 @@
 //              planes of conv2 and never touches HBM;
 //   <2, false> base_filters = 64: conv1 only, as two N = 32 halves on the same
 //              TMEM A tile; the pooled 25x25x64 map goes to HBM in the stacked
-//              layout (internal.h) for the generic layer kernel (cnn_gemm.cu).
+//              layout (internal.h) for the generic layer kernel (cnn_gemm.cu);
+//   <1, false, 16> base_filters = 16 (the paper's C = 16 models):
+//              conv1 only as one N = 16 MMA per tile, 25x25x16 map to HBM.
 //
 // Roles (19 warps):
 //   W0      producer    — cp.async.bulk of the u8 input frames (2-deep ring) and
@@ -123,11 +125,12 @@ NS_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "
 // kHalves = conv1 channels / 32 (each half is one N = 32 MMA on the shared A
 // tile); kConv2 = conv2 fused (base_filters = 32) or the conv1 map written to
 // HBM in the stacked layout for the generic layer kernel (base_filters = 64).
-template <int kHalves, bool kConv2>
+template <int kHalves, bool kConv2, int kC1>
 __global__ void __launch_bounds__(fz::kThreads, 1)
 conv12_fused_kernel(FusedArgs A) {
   using namespace fz;
-  constexpr int C1t = C1 * kHalves;
+  static_assert(kC1 == C1 || (kC1 == 16 && !kConv2), "conv2 fusion needs 32 conv1 channels per half");
+  constexpr int C1t = kC1 * kHalves;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int64_t n = min(*A.n_dev, A.n_max);
   const int64_t cnt = min(n - A.chunk_base, A.chunk_len);
@@ -227,7 +230,7 @@ conv12_fused_kernel(FusedArgs A) {
   } else if (warp == 1) {
     // ===================================================== conv1 MMA issuer (A in TMEM)
     if (lane == 0) {
-      constexpr uint32_t id1 = idesc_bf16_f32(128, C1);
+      constexpr uint32_t id1 = idesc_bf16_f32(128, kC1);
       const uint32_t sB1 = smem_u32(smem + oB1);
       mbar_wait(w_full, 0);
       // B1 = [4 kc][C1t][8]: half h = rows 32h.., K chunk kk*2 at kk*2*C1t*16 B
@@ -255,9 +258,9 @@ conv12_fused_kernel(FusedArgs A) {
 #pragma unroll
               for (int q = 0; q < 2; ++q)
                 if (!(NS_EXP & 8))
-                umma_bf16_ts(tmem + kColD1 + (gb * 4 + (int)((u1 + q) & 3)) * C1,
+                umma_bf16_ts(tmem + kColD1 + (gb * 4 + (int)((u1 + q) & 3)) * kC1,
                              tmem + kColA1 + a[q] * kA1Cols + kk * 8,
-                             bd0 + (uint64_t)((kk * 2 * C1t * 16 + h * C1 * 16) >> 4), id1, kk);
+                             bd0 + (uint64_t)((kk * 2 * C1t * 16 + h * kC1 * 16) >> 4), id1, kk);
           }
           umma_commit(&a1_empty[pr]);
           if (((u1 + 1) & 3) == 3)                 // window group complete (all halves)
@@ -421,16 +424,16 @@ conv12_fused_kernel(FusedArgs A) {
           const bool valid = w < kP1 * kP1;
           const int yp = w / kP1, xp = w - kP1 * (w / kP1);
           const int rho = (yp + 1) * kWp + (xp + 1) + 1;
-          const uint32_t tb = tmem + ((uint32_t)lg << 16) + kColD1 + gb * 4 * C1;
+          const uint32_t tb = tmem + ((uint32_t)lg << 16) + kColD1 + gb * 4 * kC1;
 #pragma unroll
-          for (int cb = 0; cb < ((NS_EXP & 64) ? 0 : C1 / 16); ++cb) {
+          for (int cb = 0; cb < ((NS_EXP & 64) ? 0 : kC1 / 16); ++cb) {
             // 2x2 max pool = element-wise max over the window's 4 accumulators
             // (bias already accumulated; max, ReLU and RNE commute: all monotone)
             uint32_t r0[16], r1[16], r2[16], r3[16];
-            tmem_ld16(tb + 0 * C1 + cb * 16, r0);
-            tmem_ld16(tb + 1 * C1 + cb * 16, r1);
-            tmem_ld16(tb + 2 * C1 + cb * 16, r2);
-            tmem_ld16(tb + 3 * C1 + cb * 16, r3);
+            tmem_ld16(tb + 0 * kC1 + cb * 16, r0);
+            tmem_ld16(tb + 1 * kC1 + cb * 16, r1);
+            tmem_ld16(tb + 2 * kC1 + cb * 16, r2);
+            tmem_ld16(tb + 3 * kC1 + cb * 16, r3);
             tmem_ld_wait();
             uint32_t pk[8];
 #pragma unroll
@@ -454,7 +457,7 @@ conv12_fused_kernel(FusedArgs A) {
                 const uint4 z = make_uint4(0, 0, 0, 0);
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
-                  uint4* pl = reinterpret_cast<uint4*>(A.out + (int64_t)(h * 4 + 2 * cb + hh) * A.out_rows * 16);
+                  uint4* pl = reinterpret_cast<uint4*>(A.out + (int64_t)(h * (kC1 / 8) + 2 * cb + hh) * A.out_rows * 16);
                   pl[orow] = hh ? o1 : o0;
                   if (xp == kP1 - 1) pl[orow + 1] = z;          // separator column
                   if (yp == 0) {                                 // separator row above
@@ -562,21 +565,22 @@ conv12_fused_kernel(FusedArgs A) {
 
 size_t conv12_fused_smem() { return (size_t)fz::kSmem; }
 
-template <int kHalves, bool kConv2>
+template <int kHalves, bool kConv2, int kC1>
 static noscope_status launch_variant(const FusedArgs& a, int grid, cudaStream_t st) {
   static DeviceOnce attr;
   if (attr.first())
-    NS_CUDA_TRY(cudaFuncSetAttribute(conv12_fused_kernel<kHalves, kConv2>,
+    NS_CUDA_TRY(cudaFuncSetAttribute(conv12_fused_kernel<kHalves, kConv2, kC1>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, fz::kSmem));
-  conv12_fused_kernel<kHalves, kConv2><<<grid, fz::kThreads, fz::kSmem, st>>>(a);
+  conv12_fused_kernel<kHalves, kConv2, kC1><<<grid, fz::kThreads, fz::kSmem, st>>>(a);
   NS_LAUNCH_CHECK();
   count_launch();
   return NOSCOPE_OK;
 }
 
 noscope_status launch_conv12_fused(const FusedArgs& a, int grid, cudaStream_t st) {
-  if (a.C1 == 32) return launch_variant<1, true>(a, grid, st);
-  if (a.C1 == 64) return launch_variant<2, false>(a, grid, st);
+  if (a.C1 == 32) return launch_variant<1, true, 32>(a, grid, st);
+  if (a.C1 == 64) return launch_variant<2, false, 32>(a, grid, st);
+  if (a.C1 == 16) return launch_variant<1, false, 16>(a, grid, st);
   return NOSCOPE_INVALID_ARGUMENT;
 }
 

@@ -135,7 +135,7 @@ noscope_status launch_labels(const noscope_dd_config& cfg, int64_t tau0, int64_t
 // Specialized CNN.
 // Fused conv1+conv2 (base_filters = 32), cnn_fused.cu.
 struct FusedArgs {
-  int C1;              // conv1 channels: 32 (conv2 fused) or 64 (conv1 only -> stacked map)
+  int C1;              // conv1 channels: 32 (conv2 fused) or 16 / 64 (conv1 only -> stacked map)
   const uint8_t* small;
   int64_t small_pitch;
   const int32_t* idx;

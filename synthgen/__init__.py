@@ -22,12 +22,12 @@ import math
 import numpy as np
 
 from .hashing import (MIX, TAG_BG, TAG_NOISE, hash_key_np, splitmix64_np)
-from .weights import (ARCH_GRID, CnnArch, bf16_bits_to_f32, bf16_round_f32,
+from .weights import (ARCH_GRID, PAPER_GRID, CnnArch, bf16_bits_to_f32, bf16_round_f32,
                       he_normal_weights, zero_weights)
 
 __all__ = [
     "SceneSpec", "Scene", "make_scene", "render_frames", "render_frame",
-    "frame_pitch", "CnnArch", "ARCH_GRID", "he_normal_weights",
+    "frame_pitch", "CnnArch", "ARCH_GRID", "PAPER_GRID", "he_normal_weights",
     "bf16_round_f32", "bf16_bits_to_f32", "zero_weights", "background", "lr_weights", "logit_grid",
     "delta_grid", "random_sweep_records", "hash_key_np", "splitmix64_np",
     "MIX", "TAG_BG", "TAG_NOISE",

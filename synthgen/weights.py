@@ -60,6 +60,9 @@ class CnnArch:
 
 # BASELINE.json configs[2]: 2/4 conv layers x 32/64 filters x 32/128 dense
 ARCH_GRID = [CnnArch(L, C, D) for L, C, D in itertools.product((2, 4), (32, 64), (32, 128))]
+# the paper's model-search grid ("24 distinct configurations";
+# Table 2 P:1136-1140 picks C = 16 for two videos): 2 L x 3 C x 4 D
+PAPER_GRID = [CnnArch(L, C, D) for L, C, D in itertools.product((2, 4), (16, 32, 64), (32, 64, 128, 256))]
 
 
 def bf16_round_f32(x) -> np.ndarray:

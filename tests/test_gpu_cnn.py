@@ -144,7 +144,7 @@ def test_cnn_zero_and_bias_weights():
     assert np.allclose(1 / (1 + np.exp(-z.cpu().numpy())), 0.75, atol=1e-6)
 
 
-@pytest.mark.parametrize("L,C", [(2, 32), (2, 64), (4, 64), (4, 32)])
+@pytest.mark.parametrize("L,C", [(2, 32), (2, 64), (4, 64), (4, 32), (2, 16), (4, 16)])
 def test_cnn_multi_chunk_sampled(L, C):
     """More frames than one internal chunk: the layer kernels see
     chunk_base > 0 and a ragged last chunk.  Sampled frames from both chunks,
@@ -202,3 +202,20 @@ def test_cnn_bench_batch_full_parity():
     err = np.abs(z - z_o)
     assert err.max() <= TOL, (err.max(), int(np.argmax(err)))
     assert np.isfinite(z).all()
+
+
+@pytest.mark.parametrize("arch", [a for a in sg.PAPER_GRID if a.base_filters == 16], ids=lambda a: a.name)
+def test_cnn_base_filters_16(arch):
+    """C = 16 (Table 2's choice for coral and night-street): the paper's
+    24-configuration grid = {2, 4} layers x {16, 32, 64} filters x
+    {32, 64, 128, 256} dense; the C = 16 rows against the oracle."""
+    nsm = ns()
+    n = 203
+    small, g = _small(n, 13)
+    w = sg.he_normal_weights(arch, 6)
+    z_o = O.cnn_logits(g, arch, w)
+    A = nsm.Arch(arch.n_conv, arch.base_filters, arch.dense)
+    z = nsm.noscope_specialized_infer(A, nsm.Weights(w), torch.from_numpy(small).cuda())
+    torch.cuda.synchronize()
+    err = np.abs(z.cpu().numpy() - z_o)
+    assert err.max() <= TOL, (arch.name, err.max())

@@ -89,7 +89,8 @@ def _torch_forward(small, arch, w):
     return z.to(torch.float32).numpy()
 
 
-@pytest.mark.parametrize("arch", sg.ARCH_GRID, ids=lambda a: a.name)
+@pytest.mark.parametrize("arch", sg.ARCH_GRID + [sg.CnnArch(2, 16, 32), sg.CnnArch(4, 16, 256),
+                                                 sg.CnnArch(2, 16, 64)], ids=lambda a: a.name)
 def test_oracle_vs_torch_fp64(arch):
     w = sg.he_normal_weights(arch, 5)
     sc = sg.make_scene(sg.SceneSpec(50, 50, 60, seed=9, prevalence=0.5))

@@ -48,3 +48,19 @@ o = N.noscope_cascade_run(dd, N.Arch(2, 32, 32), Wt, -0.5, 0.5, fr, 50, 50, st, 
                           want_stats=True)
 torch.cuda.synchronize()
 print("cascade", o["stats"])
+# every CNN variant (fused C = 32, conv1-only C = 16 / 64 + generic layers, FC) on a few frames
+for L, C, D in [(2, 32, 32), (4, 64, 128), (2, 16, 256), (4, 16, 64)]:
+    a = sg.CnnArch(L, C, D)
+    zc = N.noscope_specialized_infer(N.Arch(L, C, D), N.Weights(sg.he_normal_weights(a, 2)), fr[:130])
+    torch.cuda.synchronize()
+    print("cnn", a.name, float(zc.abs().max()))
+# threshold sweep (all phases) and the LR fit
+s, zz, y, a_, delta, uu = sg.random_sweep_records(3000, 2, n_delta=12, m=10)
+T = lambda x, dt: torch.from_numpy(np.ascontiguousarray(x, dtype=dt)).cuda()
+hist = torch.zeros(N.sweep_hist_words(len(delta), len(uu)), dtype=torch.int64, device="cuda")
+best, code = N.noscope_threshold_sweep(3, T(s, np.float64), T(zz, np.float32), T(y, np.uint8), T(a_, np.uint8),
+                                       T(delta, np.float64), T(uu, np.float32), hist, (1, 10, 1000), 30, 30)
+print("sweep", best["j"], best["l"], best["h"], code)
+F = torch.rand((500, 8), dtype=torch.float64, device="cuda")
+t = (F[:, 0] + 0.3 * torch.rand(500, dtype=torch.float64, device="cuda") > 0.6).to(torch.uint8)
+print("lr", N.noscope_lr_fit(F, t))
