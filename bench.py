@@ -860,7 +860,7 @@ def next_rows_extras(device, sc, gs, small, n):
     import torch
     import synthgen as sg
     from paper_1703_02529_b200 import noscope as N
-    hbm = measured_peaks()[0]
+    hbm, bf16 = measured_peaks()[:2]
     out = {}
     y = gs.truth[:n].contiguous()
     neg = int((y == 0).sum())
@@ -911,8 +911,10 @@ def next_rows_extras(device, sc, gs, small, n):
     ms = _time_ms(lambda: N.noscope_cbo_search([(d0, dg), (d1, dg)], cnns, fr, 50, 50, ym, u, 5, 12_500_000,
                                                m // 100, m // 100), reps=2)
     out["cbo_search"] = {"eval_frames": m, "dd_configs": 2, "cnns": 2, "ms_incl_sync": round(ms, 2)}
-    # NEXT #4: specialized-CNN training, L2C32D32, 8,192 frames x 2 epochs, batch 64;
-    # GEMMs are fp32 SGEMM on CUDA cores: peak = 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz
+    # NEXT #4: specialized-CNN training, L2C32D32, 8,192 frames x 2 epochs, batch 64; the
+    # GEMMs run on the tcgen05 tensor cores in 3xTF32 (three tf32 products per fp32
+    # product): tensor rate = 3 x the algorithmic FLOP rate, against the tf32 dense peak
+    # (the measured bf16 peak x the nominal tf32/bf16 ratio 0.5, B200_PROFILING.md)
     arch = sg.CnnArch(2, 32, 32)
     A = N.Arch(2, 32, 32)
     nt, ep = 8192, 2
@@ -927,10 +929,11 @@ def next_rows_extras(device, sc, gs, small, n):
     fwd = cnn_flops_per_frame((2, 32, 32))
     conv1 = 2 * 2500 * 27 * 32
     train_flops = (3 * fwd - conv1) * nt * run + fwd * 1024 * run     # fwd + dW + dX (no dX for conv1), + val
-    peak32 = 148 * 128 * 2 * 1.965   # GFLOP/s
+    tf32_peak = bf16 * 0.5   # TFLOP/s
     out["cnn_train"] = {"arch": "L2C32D32", "frames": nt, "epochs": run, "batch": 64, "s": round(dt, 3),
                         "frames_per_s": round(nt * run / dt, 1), "tflops": round(train_flops / dt / 1e12, 2),
-                        "frac_of_fp32_alu_peak": round(train_flops / dt / 1e9 / peak32, 4),
+                        "tensor_tflops_3xtf32": round(3 * train_flops / dt / 1e12, 2),
+                        "frac_of_tf32_peak": round(3 * train_flops / dt / 1e12 / tf32_peak, 4),
                         "history": [[round(a, 5), round(b, 5)] for a, b in hist]}
     # live-stream latency: one 30-frame chunk (1 s of 30 fps video) per call, direct
     # vs replayed from a CUDA graph captured once (the chunk pipeline has no host sync)

@@ -22,9 +22,9 @@
  *    (any CUDA allocation visible to the current device, e.g. the PyTorch
  *    caching allocator); *_host pointers are host memory.  The caller owns
  *    every buffer; the library never allocates or frees device memory and
- *    holds no global state beyond per-device caches of kernel attributes and
- *    (noscope_cnn_train only) one cuBLAS handle per host thread, so calls on
- *    different streams with distinct workspaces/states are independent.
+ *    holds no global state beyond per-device caches of kernel attributes, so
+ *    calls on different streams with distinct workspaces/states are
+ *    independent.
  *  - Work is enqueued asynchronously on `stream` (a cudaStream_t; 0 = legacy
  *    default stream).  Exceptions: noscope_threshold_sweep with phase 2/3 and
  *    any call given a non-null *_host output synchronise `stream` once to copy
@@ -498,9 +498,10 @@ noscope_status noscope_eval_labels(const uint8_t* pred, const uint8_t* ref, int6
  *   for each conv layer l: w [Cout][3][3][Cin], b [Cout]; then fc1 w [D][K]
  *   ((h, w, c) feature order), fc1 b [D], fc2 w [D], fc2 b [1].
  * history_host: host double [2 * epochs] (train loss, val loss per epoch run);
- * epochs_run_host: host.  Convolutions and dense layers run as cuBLAS SGEMMs on
- * explicit im2col rows (plain library GEMMs); everything else in this
- * library's kernels.  Synchronous (one host sync per epoch).                 */
+ * epochs_run_host: host.  Convolutions and dense layers run as GEMMs on
+ * explicit im2col rows on the tcgen05 tensor cores at fp32 accuracy (3xTF32);
+ * everything else in this library's kernels.  Synchronous (one host sync per
+ * epoch).                                                                    */
 typedef struct {
   int32_t batch, epochs;   /* mini-batch size; maximum epochs (the paper's 1-5) */
   float lr, rho, eps;
@@ -517,6 +518,19 @@ noscope_status noscope_cnn_train(const noscope_cnn_arch* arch, const noscope_tra
  * sizes the buffers as for noscope_specialized_infer).  Asynchronous.         */
 noscope_status noscope_cnn_params_to_weights(const noscope_cnn_arch* arch, const float* params,
                                              const noscope_cnn_weights* weights_out, noscope_stream_t stream);
+
+/* Test hooks (not part of the cascade contract).
+ * noscope_debug_cnn_layout: internal CNN activation offsets (layer-level tests).
+ * noscope_debug_tc_gemm: the training path's fp32-accurate tcgen05 GEMM
+ * (3xTF32 split: x = tf32(x) + (x - tf32(x)), three tensor-core products
+ * accumulated in fp32) on caller buffers: C[m*ldc + n] = sum_k A[m*sam + k*sak]
+ * * B[n*sbn + k*sbk], all device fp32; part = split-K scratch of
+ * noscope_debug_tc_gemm_part_floats(M, N, K) floats (nullable when 0).      */
+int32_t noscope_debug_cnn_layout(const noscope_cnn_arch* arch, int64_t n_max, int64_t* out);
+size_t noscope_debug_tc_gemm_part_floats(int32_t M, int32_t N, int64_t K);
+int32_t noscope_debug_tc_gemm(const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbn, int64_t sbk,
+                              float* C, int64_t ldc, int32_t M, int32_t N, int64_t K, float* part,
+                              noscope_stream_t stream);
 
 /* Reads and clears the device status word in a workspace (synchronises). */
 noscope_status noscope_check(void* ws, noscope_stream_t stream);

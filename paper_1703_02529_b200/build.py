@@ -21,7 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 
-LIB_SOURCES = ["noscope_api.cu", "dd.cu", "scan.cu", "sweep.cu", "cnn.cu", "cnn_fused.cu", "cnn_gemm.cu", "cnn_tile.cu", "fit.cu", "cbo.cu", "train.cu"]
+LIB_SOURCES = ["noscope_api.cu", "dd.cu", "scan.cu", "sweep.cu", "cnn.cu", "cnn_fused.cu", "cnn_gemm.cu", "cnn_tile.cu", "fit.cu", "cbo.cu", "train.cu", "gemm_tc.cu"]
 LIB_HEADERS = ["common.cuh", "internal.h"]
 
 
@@ -53,7 +53,7 @@ def build_noscope():
     csrc = os.path.join(PKG, "csrc")
     srcs = [os.path.join(csrc, s) for s in LIB_SOURCES]
     deps = [os.path.join(csrc, h) for h in LIB_HEADERS] + [os.path.join(ROOT, "include", "noscope.h")]
-    return _build(os.path.join(PKG, "libnoscope.so"), srcs, deps, extra=("-lcublas",))
+    return _build(os.path.join(PKG, "libnoscope.so"), srcs, deps)
 
 
 def build_synthgen():

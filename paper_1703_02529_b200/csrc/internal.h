@@ -105,6 +105,27 @@ noscope_status launch_diff_detect(const noscope_dd_config& cfg, const uint8_t* f
                                   uint8_t* state, uint8_t* small, int64_t small_pitch,
                                   double* score, uint8_t* disp, uint32_t* status,
                                   unsigned* flags, cudaStream_t st, Prof* prof = nullptr);
+// fp32-accurate tcgen05 GEMM (gemm_tc.cu, 3xTF32): C[m][n] = sum_k A(m,k) B(k,n)
+// with A(m,k) = A[m*sam + k*sak], B(k,n) = B[n*sbn + k*sbk]; `part` = split-K
+// scratch of tc_gemm_part_floats(M, N, K) floats (nullable when that is 0).
+struct TcGemmArgs {
+  const float* A;
+  int64_t sam, sak;
+  const float* B;
+  int64_t sbn, sbk;
+  float* C;
+  int64_t ldc;
+  int M, N;
+  int64_t K;
+  int a_m_fast, b_n_fast;   // load order: along m / n (unit stride) instead of k
+  int ksplit;
+  int64_t kper;
+  float* part;
+};
+size_t tc_gemm_part_floats(int M, int N, int64_t K);
+noscope_status tc_gemm(const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbn, int64_t sbk, float* C,
+                       int64_t ldc, int M, int N, int64_t K, float* part, cudaStream_t st);
+
 // Whether dd_kernel's band ring (>= 2 stages of one output row's source rows per
 // worker group, at least one group) fits shared memory for this source size.
 bool dd_frames_fit(const noscope_dd_config& cfg, const noscope_frames_desc& desc);

@@ -722,4 +722,20 @@ int32_t noscope_debug_cnn_layout(const noscope_cnn_arch* arch, int64_t n_max, in
   return 0;
 }
 
+// Test/debug helper: the training path's fp32-accurate tcgen05 GEMM (gemm_tc.cu)
+// on caller buffers, C[m*ldc + n] = sum_k A[m*sam + k*sak] * B[n*sbn + k*sbk]
+// (device fp32); part: device scratch of noscope_debug_tc_gemm_part_floats(M, N,
+// K) floats (nullable when 0).  Asynchronous.
+size_t noscope_debug_tc_gemm_part_floats(int32_t M, int32_t N, int64_t K) {
+  return ns::tc_gemm_part_floats(M, N, K);
+}
+int32_t noscope_debug_tc_gemm(const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbn, int64_t sbk,
+                              float* C, int64_t ldc, int32_t M, int32_t N, int64_t K, float* part,
+                              noscope_stream_t stream) {
+  if (!A || !B || !C || M < 0 || N < 0 || K < 0) return NOSCOPE_INVALID_ARGUMENT;
+  noscope_status s = check_device();
+  if (s != NOSCOPE_OK) return s;
+  return ns::tc_gemm(A, sam, sak, B, sbn, sbk, C, ldc, M, N, K, part, (cudaStream_t)stream);
+}
+
 }  // extern "C"

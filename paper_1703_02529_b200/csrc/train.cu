@@ -4,15 +4,14 @@
 // bf16 rounding (input = the inference normalisation), mean binary cross-entropy
 // on the logit, RMSprop, max-pool gradient to the first maximum of each window.
 //
-// Every convolution and dense layer is a plain GEMM on explicit im2col rows
-// (cuBLAS SGEMM: forward Y = cols W^T, weight gradient dW = dY^T cols, input
-// gradient dcols = dY W); the custom kernels here do the rest: normalisation +
-// gather, im2col / col2im (gather form, no atomics), bias + ReLU + 2x2 max pool
-// with argmax, the unpool/ReLU mask, the dense-head elementwise steps, the loss
-// and RMSprop; bias gradients are cuBLAS GEMVs against a ones vector.  No
-// atomics anywhere, so a run is reproducible.
-#include <cublas_v2.h>
-
+// Every convolution and dense layer is a GEMM on explicit im2col rows, run on
+// the tcgen05 tensor cores at fp32 accuracy (gemm_tc.cu, 3xTF32: forward
+// Y = cols W^T, weight gradient dW = dY^T cols, input gradient dcols = dY W, bias
+// gradients = dY^T 1); the kernels here do the rest: normalisation + gather,
+// im2col / col2im (gather form, no atomics), bias + ReLU + 2x2 max pool with
+// argmax, the unpool/ReLU mask, the dense-head elementwise steps, the loss and
+// RMSprop.  No atomics anywhere (split-K partials are summed in a fixed order),
+// so a run is reproducible.
 #include <cmath>
 #include <vector>
 
@@ -23,6 +22,11 @@ namespace ns {
 
 namespace {
 constexpr int kT = 256;
+#define NS_TRY(expr)                          \
+  do {                                        \
+    noscope_status _s = (expr);               \
+    if (_s != NOSCOPE_OK) return _s;          \
+  } while (0)
 
 inline int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + kT - 1) / kT, 16 * kNumSMs)); }
 
@@ -244,18 +248,14 @@ TPlan make_tplan(const noscope_cnn_arch& a) {
   return p;
 }
 
-// Row-major GEMM on cuBLAS (column-major): C[M][N] = op(A) op(B), op(A) M x K.
-bool g_gemm_ok = true;   // sticky per call of launch_cnn_train (host-side, single thread)
-void sgemm_rm(cublasHandle_t h, bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B,
-              int ldb, float* C, int ldc, float beta = 0.0f) {
-  const float one = 1.0f;
-  if (cublasSgemm(h, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, N, M, K, &one, B, ldb, A,
-                  lda, &beta, C, ldc) != CUBLAS_STATUS_SUCCESS)
-    g_gemm_ok = false;
+// Row-major C[M][N] = op(A) op(B), op(A) M x K (transposes are strides, not copies).
+noscope_status gemm_rm(bool ta, bool tb, int M, int N, int64_t K, const float* A, int64_t lda, const float* B,
+                       int64_t ldb, float* C, int64_t ldc, float* part, cudaStream_t st) {
+  return tc_gemm(A, ta ? 1 : lda, ta ? lda : 1, B, tb ? ldb : 1, tb ? 1 : ldb, C, ldc, M, N, K, part, st);
 }
 
 struct TWs {
-  float *G, *V, *best, *x[5], *a[4], *cols, *dcols, *dx, *dxb, *h1, *dz, *dh1, *ones;
+  float *G, *V, *best, *x[5], *a[4], *cols, *dcols, *dx, *dxb, *h1, *dz, *dh1, *ones, *part;
   uint8_t* arg[4];
   int32_t* idx_tmp;
   double* loss;
@@ -293,21 +293,36 @@ TWs carve_t(const TPlan& p, int B, void* base) {
   w.dz = (float*)take((size_t)B * 4);
   w.dh1 = (float*)take((size_t)B * p.D * 4);
   w.ones = (float*)take((size_t)B * p.lay[0].H * p.lay[0].W * 4);
+  // split-K scratch of the largest GEMM of a step (the weight gradients)
+  size_t part = 0;
+  auto need = [&](int M, int N, int64_t K) { part = std::max(part, tc_gemm_part_floats(M, N, K)); };
+  for (int l = 0; l < p.L; ++l) {
+    const TLayer& t = p.lay[l];
+    const int64_t rows = (int64_t)B * t.H * t.W;
+    need((int)rows, t.cout, 9 * t.cin);
+    need(t.cout, 9 * t.cin, rows);
+    need((int)rows, 9 * t.cin, t.cout);
+    need(t.cout, 1, rows);
+  }
+  need(B, p.D, p.K);
+  need(p.D, p.K, B);
+  need(B, p.K, p.D);
+  need(p.D, 1, B);
+  w.part = (float*)take(std::max<size_t>(part, 1) * 4);
   w.loss = (double*)take(8);
   w.total = off;
   return w;
 }
 
-// column sums of a row-major [rows][C] matrix = (column-major C x rows) * ones
-void colsum(cublasHandle_t h, const float* m, int64_t rows, int C, float* out, const float* ones) {
-  const float one = 1.0f, zero = 0.0f;
-  if (cublasSgemv(h, CUBLAS_OP_N, C, (int)rows, &one, m, C, ones, 1, &zero, out, 1) != CUBLAS_STATUS_SUCCESS)
-    g_gemm_ok = false;
+// column sums of a row-major [rows][C] matrix: out[c] = sum_r m[r][c] * 1 (a GEMM with N = 1)
+noscope_status colsum(const float* m, int64_t rows, int C, float* out, const float* ones, float* part,
+                      cudaStream_t st) {
+  return tc_gemm(m, 1, C, ones, 0, 1, out, 1, C, 1, rows, part, st);
 }
 
 // Forward on B frames (idx on device); leaves activations for the backward pass,
 // adds the batch's summed loss to *w.loss; dz if want_grad.
-noscope_status forward(cublasHandle_t h, const TPlan& p, const noscope_cnn_arch& a, const float* P, TWs& w,
+noscope_status forward(const TPlan& p, const noscope_cnn_arch& a, const float* P, TWs& w,
                        const uint8_t* small, int64_t pitch, const uint8_t* labels, const int32_t* idx, int B,
                        int want_grad, cudaStream_t st) {
   norm_gather_kernel<<<grid_for((int64_t)B * 7500), kT, 0, st>>>(small, pitch, idx, B, a.chan_mean[0],
@@ -317,25 +332,25 @@ noscope_status forward(cublasHandle_t h, const TPlan& p, const noscope_cnn_arch&
     const int64_t rows = (int64_t)B * t.H * t.W;
     im2col_kernel<<<grid_for(rows * 9 * (t.cin % 4 ? 1 : t.cin / 4)), kT, 0, st>>>(w.x[l], B, t.H, t.W, t.cin,
                                                                                  w.cols);
-    sgemm_rm(h, false, true, (int)rows, t.cout, 9 * t.cin, w.cols, 9 * t.cin, P + t.w_off, 9 * t.cin, w.a[l],
-             t.cout);
+    NS_TRY(gemm_rm(false, true, (int)rows, t.cout, 9 * t.cin, w.cols, 9 * t.cin, P + t.w_off, 9 * t.cin, w.a[l],
+                   t.cout, w.part, st));
     bias_relu_pool_kernel<<<grid_for((int64_t)B * (t.H / 2) * (t.W / 2) * t.cout), kT, 0, st>>>(
         w.a[l], P + t.b_off, B, t.H, t.W, t.cout, w.x[l + 1], w.arg[l]);
   }
-  sgemm_rm(h, false, true, B, p.D, p.K, w.x[p.L], p.K, P + p.fc1_w, p.K, w.h1, p.D);
+  NS_TRY(gemm_rm(false, true, B, p.D, p.K, w.x[p.L], p.K, P + p.fc1_w, p.K, w.h1, p.D, w.part, st));
   bias_relu_kernel<<<grid_for((int64_t)B * p.D), kT, 0, st>>>(w.h1, P + p.fc1_b, B, p.D);
   head_kernel<<<1, kT, 0, st>>>(w.h1, P + p.fc2_w, P + p.fc2_b, labels, idx, B, p.D, w.dz, w.loss, want_grad);
   NS_LAUNCH_CHECK();
-  return g_gemm_ok ? NOSCOPE_OK : NOSCOPE_CUDA;
+  return NOSCOPE_OK;
 }
 
-noscope_status backward(cublasHandle_t h, const TPlan& p, const float* P, TWs& w, int B, cudaStream_t st) {
+noscope_status backward(const TPlan& p, const float* P, TWs& w, int B, cudaStream_t st) {
   float* G = w.G;
   head_grad_kernel<<<1, kT, 0, st>>>(w.h1, P + p.fc2_w, w.dz, B, p.D, G + p.fc2_w, G + p.fc2_b, w.dh1);
-  sgemm_rm(h, true, false, p.D, p.K, B, w.dh1, p.D, w.x[p.L], p.K, G + p.fc1_w, p.K);
-  colsum(h, w.dh1, B, p.D, G + p.fc1_b, w.ones);
+  NS_TRY(gemm_rm(true, false, p.D, p.K, B, w.dh1, p.D, w.x[p.L], p.K, G + p.fc1_w, p.K, w.part, st));
+  NS_TRY(colsum(w.dh1, B, p.D, G + p.fc1_b, w.ones, w.part, st));
   float* dpool = w.dx;   // gradient w.r.t. the current pooled map
-  sgemm_rm(h, false, false, B, p.K, p.D, w.dh1, p.D, P + p.fc1_w, p.K, dpool, p.K);
+  NS_TRY(gemm_rm(false, false, B, p.K, p.D, w.dh1, p.D, P + p.fc1_w, p.K, dpool, p.K, w.part, st));
   for (int l = p.L - 1; l >= 0; --l) {
     const TLayer& t = p.lay[l];
     const int64_t rows = (int64_t)B * t.H * t.W;
@@ -344,19 +359,19 @@ noscope_status backward(cublasHandle_t h, const TPlan& p, const float* P, TWs& w
     // the forward im2col of this layer was overwritten by later layers: rebuild it
     im2col_kernel<<<grid_for(rows * 9 * (t.cin % 4 ? 1 : t.cin / 4)), kT, 0, st>>>(w.x[l], B, t.H, t.W, t.cin,
                                                                                  w.cols);
-    sgemm_rm(h, true, false, t.cout, 9 * t.cin, (int)rows, w.a[l], t.cout, w.cols, 9 * t.cin, G + t.w_off,
-             9 * t.cin);
-    colsum(h, w.a[l], rows, t.cout, G + t.b_off, w.ones);
+    NS_TRY(gemm_rm(true, false, t.cout, 9 * t.cin, rows, w.a[l], t.cout, w.cols, 9 * t.cin, G + t.w_off,
+                   9 * t.cin, w.part, st));
+    NS_TRY(colsum(w.a[l], rows, t.cout, G + t.b_off, w.ones, w.part, st));
     if (l > 0) {
-      sgemm_rm(h, false, false, (int)rows, 9 * t.cin, t.cout, w.a[l], t.cout, P + t.w_off, 9 * t.cin, w.dcols,
-               9 * t.cin);
+      NS_TRY(gemm_rm(false, false, (int)rows, 9 * t.cin, t.cout, w.a[l], t.cout, P + t.w_off, 9 * t.cin, w.dcols,
+                     9 * t.cin, w.part, st));
       float* out = (dpool == w.dx) ? w.dxb : w.dx;
       col2im_kernel<<<grid_for(rows * t.cin), kT, 0, st>>>(w.dcols, B, t.H, t.W, t.cin, out);
       dpool = out;
     }
   }
   NS_LAUNCH_CHECK();
-  return g_gemm_ok ? NOSCOPE_OK : NOSCOPE_CUDA;
+  return NOSCOPE_OK;
 }
 }  // namespace
 
@@ -373,13 +388,6 @@ noscope_status launch_cnn_train(const noscope_cnn_arch& a, const noscope_train_c
                                 int32_t* epochs_run, void* ws, cudaStream_t st) {
   const TPlan p = make_tplan(a);
   TWs w = carve_t(p, cfg.batch, ws);
-  // one cuBLAS handle per host thread, created on first use and kept (creation
-  // and cuBLAS's lazy kernel loading cost far more than a training epoch)
-  static thread_local cublasHandle_t h = nullptr;
-  if (!h && cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) { h = nullptr; return NOSCOPE_CUDA; }
-  g_gemm_ok = true;
-  cublasSetStream(h, st);
-  cublasSetMathMode(h, CUBLAS_PEDANTIC_MATH);   // fp32 throughout (no TF32)
   noscope_status s = NOSCOPE_OK;
   auto fail = [&](noscope_status e) { return e; };
   NS_CUDA_TRY(cudaMemsetAsync(w.V, 0, p.nparams * 4, st));
@@ -395,8 +403,8 @@ noscope_status launch_cnn_train(const noscope_cnn_arch& a, const noscope_train_c
     for (int64_t s0 = 0; s0 < n_train; s0 += cfg.batch) {
       const int B = (int)std::min<int64_t>(cfg.batch, n_train - s0);
       const int32_t* idx = perms + (int64_t)e * n_train + s0;
-      if ((s = forward(h, p, a, P, w, small, pitch, labels, idx, B, 1, st)) != NOSCOPE_OK) return fail(s);
-      if ((s = backward(h, p, P, w, B, st)) != NOSCOPE_OK) return fail(s);
+      if ((s = forward(p, a, P, w, small, pitch, labels, idx, B, 1, st)) != NOSCOPE_OK) return fail(s);
+      if ((s = backward(p, P, w, B, st)) != NOSCOPE_OK) return fail(s);
       rmsprop_kernel<<<grid_for(p.nparams), kT, 0, st>>>(P, w.G, w.V, p.nparams, cfg.lr, cfg.rho, cfg.eps);
     }
     double tr = 0.0, va = 0.0;
@@ -405,7 +413,7 @@ noscope_status launch_cnn_train(const noscope_cnn_arch& a, const noscope_train_c
     NS_CUDA_TRY(cudaMemsetAsync(w.loss, 0, 8, st));
     for (int64_t s0 = 0; s0 < n_val; s0 += cfg.batch) {
       const int B = (int)std::min<int64_t>(cfg.batch, n_val - s0);
-      if ((s = forward(h, p, a, P, w, small, pitch, labels, val_idx + s0, B, 0, st)) != NOSCOPE_OK) return fail(s);
+      if ((s = forward(p, a, P, w, small, pitch, labels, val_idx + s0, B, 0, st)) != NOSCOPE_OK) return fail(s);
     }
     NS_CUDA_TRY(cudaMemcpyAsync(&va, w.loss, 8, cudaMemcpyDeviceToHost, st));
     NS_CUDA_TRY(cudaStreamSynchronize(st));

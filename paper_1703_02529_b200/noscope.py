@@ -182,6 +182,11 @@ def lib():
                                     c_p, c_i64, C.POINTER(C.c_double), C.POINTER(c_i32), c_p, c_sz, c_p]
     L.noscope_cnn_params_to_weights.restype = c_i32
     L.noscope_cnn_params_to_weights.argtypes = [C.POINTER(CnnArchC), c_p, C.POINTER(CnnWeightsC), c_p]
+    L.noscope_debug_tc_gemm_part_floats.restype = c_sz
+    L.noscope_debug_tc_gemm_part_floats.argtypes = [c_i32, c_i32, c_i64]
+    L.noscope_debug_tc_gemm.restype = c_i32
+    L.noscope_debug_tc_gemm.argtypes = [c_p, c_i64, c_i64, c_p, c_i64, c_i64, c_p, c_i64, c_i32, c_i32, c_i64, c_p,
+                                        c_p]
     L.noscope_debug_cnn_layout.restype = c_i32
     L.noscope_debug_cnn_layout.argtypes = [C.POINTER(CnnArchC), c_i64, C.POINTER(c_i64)]
     _lib = L
@@ -559,6 +564,16 @@ def noscope_cnn_params_to_weights(arch: Arch, params: torch.Tensor, weights: "We
 
 def noscope_check(ws, stream=None):
     return lib().noscope_check(_ptr(ws), _stream(stream))
+
+
+def debug_tc_gemm(A: torch.Tensor, sam, sak, B: torch.Tensor, sbn, sbk, M, N, K, stream=None):
+    """C [M, N] fp32 = sum_k A[m*sam + k*sak] * B[n*sbn + k*sbk] on the tcgen05 3xTF32 GEMM."""
+    C = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    nf = lib().noscope_debug_tc_gemm_part_floats(M, N, K)
+    part = torch.empty(max(nf, 1), dtype=torch.float32, device=A.device) if nf else None
+    _check(lib().noscope_debug_tc_gemm(_ptr(A), sam, sak, _ptr(B), sbn, sbk, _ptr(C), N, M, N, K, _ptr(part),
+                                       _stream(stream)), "noscope_debug_tc_gemm")
+    return C
 
 
 def debug_cnn_layout(arch: Arch, n_max: int):
