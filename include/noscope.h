@@ -329,7 +329,11 @@ uint64_t noscope_launch_count(void);
  * phase 1 ACCUMULATES the local records into `hist` (caller zeroes it first;
  * size noscope_sweep_hist_words(n_delta, m) uint64); the caller may sum `hist`
  * across GPUs (e.g. ncclAllReduce) before phase 2, which evaluates it.
- * phase 3 = 1 then 2.                                                        */
+ * phase 3 = 1 then 2.  phase | NOSCOPE_SWEEP_ASYNC: phase 2 enqueues the copy
+ * of the best triple into best_host (page-locked memory) without synchronising
+ * `stream`; the result is valid once the stream's work completes and the call
+ * returns NOSCOPE_OK (read best_host->feasible for feasibility).            */
+enum { NOSCOPE_SWEEP_ASYNC = 4 };
 typedef struct { uint64_t t_mse_ps, t_snn_ps, t_full_ps; } noscope_timing;
 typedef struct {
   int32_t j, l, h, feasible;

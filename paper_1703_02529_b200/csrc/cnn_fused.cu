@@ -23,11 +23,12 @@
 //                         window the 4 members' im2col rows from one 4x4 cell
 //                         neighbourhood, stored into TMEM with tcgen05.st (no
 //                         shared-memory traffic for A)
-//   W7-W14  epilogue 1  — two 4-warp groups on alternate (window group, half):
-//                         element-wise max of the window's 4 member accumulators
+//   W7-      epilogue 1  — element-wise max of the window's 4 member accumulators
 //                         -> ReLU -> bf16 -> conv2 operand planes (double-buffered
-//                         per frame) or the stacked map in HBM
-//   W15-W18 epilogue 2  — TMEM (bias accumulated by an extra K step) -> ReLU -> bf16
+//                         per frame; W7-W10, one group) or the stacked map in HBM
+//                         (W7-W14, two groups on alternate (window group, half))
+//   W11-W18  epilogue 2  — (conv2 fused) two 4-warp groups on alternate conv2 tiles:
+//                         TMEM (bias accumulated by an extra K step) -> ReLU -> bf16
 //                         -> 2x2 max by shuffles ->
 //                         FC feature tiles (L = 2) or the stacked layer-3 map (L = 4)
 // conv2 M tile = 16 conv rows x 8 conv columns: 16 core-matrix groups of 8
@@ -80,7 +81,11 @@ constexpr int kK2 = 9 * C1 / 16;        // 18 K16 steps for conv2
 constexpr int kPlaneRows = kHp * kWp + 1;  // rho = q + 1, q in [-1, 729)
 constexpr int kPlaneBytes = kPlaneRows * 16;  // 11,680
 constexpr int kActBytes = (C1 / 8) * kPlaneBytes;  // 46,720
-constexpr int wBuild0 = 3, wEp1_0 = 7, wEp2_0 = 15;
+constexpr int wBuild0 = 3, wEp1_0 = 7;
+// epilogue split: with conv2 fused, 4 warps of epilogue 1 (one group) and 8 of
+// epilogue 2 (two groups on alternate conv2 tiles: the pooling shuffles are the
+// longest per-frame chain); conv1 only, 8 warps of epilogue 1 (two groups)
+template <bool kConv2> constexpr int wEp2_of() { return kConv2 ? 11 : 15; }
 // smem offsets (bytes)
 constexpr int oB1 = 0;                                   // conv1 weights [4][32][8]
 constexpr int oB2 = oB1 + (kK1 / 8) * kC1Max * 16;       // conv2 weights [36][64][8]
@@ -131,6 +136,8 @@ conv12_fused_kernel(FusedArgs A) {
   using namespace fz;
   static_assert(kC1 == C1 || (kC1 == 16 && !kConv2), "conv2 fusion needs 32 conv1 channels per half");
   constexpr int C1t = kC1 * kHalves;
+  constexpr int wEp2_0 = wEp2_of<kConv2>();
+  constexpr int kEp1Groups = (wEp2_0 - wEp1_0) / 4;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int64_t n = min(*A.n_dev, A.n_max);
   const int64_t cnt = min(n - A.chunk_base, A.chunk_len);
@@ -156,7 +163,7 @@ conv12_fused_kernel(FusedArgs A) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(&in_full[s], 1);
       mbar_init(&in_empty[s], 128);
-      mbar_init(&act_full[s], 256);
+      mbar_init(&act_full[s], 32 * (wEp2_of<kConv2>() - wEp1_0));
       mbar_init(&act_empty[s], 1);
     }
     for (int s = 0; s < kA1Stages; ++s) {
@@ -417,7 +424,7 @@ conv12_fused_kernel(FusedArgs A) {
       for (int G = 0; G < kG1; ++G) {
         for (int h = 0; h < kHalves; ++h, ++ugh) {
           const int gb = (int)(ugh % kNG1);
-          if (gb != grp) continue;
+          if (kEp1Groups > 1 && gb != grp) continue;
           mbar_wait(&t1_full[gb], (uint32_t)((ugh / kNG1) & 1));
           tc_fence_after();
           const int w = G * 128 + row;
@@ -480,7 +487,8 @@ conv12_fused_kernel(FusedArgs A) {
   } else if (kConv2) {
     // ===================================================== epilogue 2
     const int lg = (warp & 3) * 32;
-    const int et = tid - wEp2_0 * 32;  // 0..127
+    const int et = tid - wEp2_0 * 32;  // 0..255
+    const int grp2 = et >> 7;          // tiles t with t % 2 == grp2
     // lane -> conv position inside the tile: 4 conv rows x 8 conv columns per warp
     const int rl = (warp & 3) * 4 + (lane >> 3), cl = lane & 7;
     const bool pool_lane = ((lane & 1) == 0) && (((lane >> 3) & 1) == 0);
@@ -488,7 +496,7 @@ conv12_fused_kernel(FusedArgs A) {
     // 13, 169 rows per frame, 14 leading guard rows
     constexpr int kHpool = 12, kWqo = 13, kPo = 13 * 13, kGo = 14;
     if (!A.to_features && blockIdx.x == 0) {  // zero the leading / trailing guards
-      for (int e = et; e < (C2 / 8) * (kGo + kWqo); e += 128) {
+      for (int e = et; e < (C2 / 8) * (kGo + kWqo); e += 256) {
         const int c = e / (kGo + kWqo), k = e % (kGo + kWqo);
         const int64_t row = k < kGo ? k : kGo + cnt * kPo + (k - kGo);
         *reinterpret_cast<uint4*>(A.out + ((int64_t)c * A.out_rows + row) * 16) = make_uint4(0, 0, 0, 0);
@@ -496,7 +504,7 @@ conv12_fused_kernel(FusedArgs A) {
     }
     for (int64_t it = 0; it < my_frames; ++it) {
       const int64_t i = blockIdx.x + it * gridDim.x;  // chunk-relative frame
-      for (int t = 0; t < kT2; ++t) {
+      for (int t = grp2; t < kT2; t += 2) {             // this group's tiles
         const int b = t % kNB2;                          // kT2 = 2 * kNB2
         mbar_wait(&t2_full[b], (uint32_t)((t / kNB2) & 1));
         tc_fence_after();

@@ -437,6 +437,8 @@ noscope_status noscope_threshold_sweep(int32_t phase, const double* s, const flo
                                        const noscope_sweep_tables* tables,
                                        noscope_sweep_best* best_host, void* ws, size_t ws_bytes,
                                        noscope_stream_t stream) {
+  const bool async_best = (phase & NOSCOPE_SWEEP_ASYNC) != 0;
+  phase &= 3;
   if (phase < 1 || phase > 3) return NOSCOPE_INVALID_ARGUMENT;
   if (nd < 1 || m < 1 || m > 2048 || nd > 65535) return NOSCOPE_INVALID_ARGUMENT;
   if (!hist || !delta || !u || !ws) return NOSCOPE_INVALID_ARGUMENT;
@@ -449,7 +451,7 @@ noscope_status noscope_threshold_sweep(int32_t phase, const double* s, const flo
   noscope_timing t0{0, 0, 0};
   bool infeasible = false;
   st = launch_sweep(phase, s, z, y, a, n, delta, nd, u, m, hist, timing ? *timing : t0, fp_limit,
-                    fn_limit, tables, best_host, ws, (cudaStream_t)stream, &infeasible);
+                    fn_limit, tables, best_host, ws, (cudaStream_t)stream, async_best ? nullptr : &infeasible);
   if (st != NOSCOPE_OK) return st;
   return infeasible ? NOSCOPE_INFEASIBLE : NOSCOPE_OK;
 }

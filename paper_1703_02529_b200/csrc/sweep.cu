@@ -433,8 +433,10 @@ noscope_status launch_sweep(int32_t phase, const double* s, const float* z, cons
     if (best_host) {
       NS_CUDA_TRY(cudaMemcpyAsync(best_host, best_dev, sizeof(noscope_sweep_best),
                                   cudaMemcpyDeviceToHost, st));
-      NS_CUDA_TRY(cudaStreamSynchronize(st));
-      if (infeasible) *infeasible = best_host->feasible == 0;
+      if (infeasible) {   // synchronous form: the caller gets the result and the status now
+        NS_CUDA_TRY(cudaStreamSynchronize(st));
+        *infeasible = best_host->feasible == 0;
+      }
     }
   }
   return NOSCOPE_OK;

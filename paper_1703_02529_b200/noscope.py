@@ -402,15 +402,20 @@ def sweep_hist_words(n_delta, m):
 
 
 def noscope_threshold_sweep(phase, s, z, y, a, delta, u, hist, timing=(0, 0, 0), fp_limit=0,
-                            fn_limit=0, tables=None, ws=None, stream=None):
+                            fn_limit=0, tables=None, ws=None, stream=None, best_out=None):
     """phase 1: accumulate records into hist (uint64 tensor; viewed as int64 here);
-    phase 2: evaluate hist -> (best dict, status); phase 3 both."""
+    phase 2: evaluate hist -> (best dict, status); phase 3 both.
+    best_out: a SweepBest in page-locked memory (pinned_sweep_best()) -> phase 2 is
+    asynchronous (NOSCOPE_SWEEP_ASYNC); returns (best_out, 0) and best_out is valid
+    after the stream synchronises (sweep_best_dict(best_out))."""
     nd, m = delta.numel(), u.numel()
     dev = delta.device
     if ws is None:
         ws = workspace(OP_THRESHOLD_SWEEP, None, None, 0, nd, m, device=dev)
     n = 0 if s is None else s.numel()
-    best = SweepBest()
+    best = best_out if best_out is not None else SweepBest()
+    if best_out is not None and phase & 2:
+        phase |= 4
     tab = None
     if tables is not None:
         tab = SweepTables(*[tables[k].data_ptr() for k in ("F", "FPnf", "FNnf", "FPf", "FNf", "GE", "GT")])
@@ -424,7 +429,21 @@ def noscope_threshold_sweep(phase, s, z, y, a, delta, u, hist, timing=(0, 0, 0),
         raise NoScopeError(code, "noscope_threshold_sweep")
     if not phase & 2:
         return None, code
-    return {f: getattr(best, f) for f, _ in SweepBest._fields_}, code
+    if best_out is not None:
+        return best_out, code
+    return sweep_best_dict(best), code
+
+
+def sweep_best_dict(best):
+    return {f: getattr(best, f) for f, _ in SweepBest._fields_}
+
+
+def pinned_sweep_best():
+    """A SweepBest living in page-locked host memory (target of an asynchronous phase 2)."""
+    buf = torch.empty(C.sizeof(SweepBest), dtype=torch.uint8, pin_memory=True)
+    best = SweepBest.from_address(buf.data_ptr())
+    best._buf = buf    # keep the pinned storage alive
+    return best
 
 
 def noscope_sweep_records(s: torch.Tensor, y: torch.Tensor, mode: int, k: int, t_skip: int = 1, a_out=None,

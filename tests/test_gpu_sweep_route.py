@@ -270,3 +270,21 @@ def test_route_many_ctas_vs_numpy():
     assert np.array_equal(r.cpu().numpy(), ro)
     k = int(nunc.item())
     assert np.array_equal(unc[:k].cpu().numpy(), np.flatnonzero(ro == O.R_UNC))
+
+
+def test_sweep_async_phase2_matches_sync():
+    """NOSCOPE_SWEEP_ASYNC: phase 2 copies the best triple into page-locked memory
+    without synchronising; after the stream completes it equals the synchronous result."""
+    nsm = ns()
+    s, z, y, a, delta, u = sg.random_sweep_records(5000, 11, n_delta=20, m=16)
+    T = lambda x, dt: torch.from_numpy(np.ascontiguousarray(x, dtype=dt)).cuda()
+    args = (T(s, np.float64), T(z, np.float32), T(y, np.uint8), T(a, np.uint8), T(delta, np.float64),
+            T(u, np.float32))
+    words = nsm.sweep_hist_words(len(delta), len(u))
+    h1 = torch.zeros(words, dtype=torch.int64, device="cuda")
+    best_sync, code = nsm.noscope_threshold_sweep(3, *args, h1, (1, 10, 1000), 200, 200)
+    h2 = torch.zeros(words, dtype=torch.int64, device="cuda")
+    out = nsm.pinned_sweep_best()
+    r, code2 = nsm.noscope_threshold_sweep(3, *args, h2, (1, 10, 1000), 200, 200, best_out=out)
+    torch.cuda.synchronize()
+    assert code2 == 0 and nsm.sweep_best_dict(out) == best_sync
