@@ -729,9 +729,14 @@ def run_extras(device, timing=(1000, 20000, 12_500_000_000)):
                        "records_per_s": round(M / wall, 1), "hist_GBps": round(M * 14 / h_ms / 1e6, 1),
                        "best": {k: best[k] for k in ("j", "l", "h", "feasible", "cost_ps", "uncertain")}}
     # Scale point: 1e9 records generated on device, histogram
-    # phase timed.  Its bound is the shared-memory atomic rate, not HBM: one
-    # scattered ATOMS per record (+1 when a != y) at 2 cycles/lane/SM
-    # (B300_MICROARCH.md "ATOMS spread-addr"), reported as atomic_floor_ms.
+    # phase timed.  Its bound is the shared memory, not HBM: per record two binary
+    # searches over the candidate grids (scattered smem loads) and ~1.14 scattered
+    # smem atomics.  Ceilings measured on B200 (tools/smem_atomic_bw.cu,
+    # profiles/r02/smem_atomic_bw.txt): 5.28 random-address u32 atomics and 4.7
+    # random loads per clock per SM; ncu counts 0.967 shared-memory wavefronts per
+    # record for this kernel (profiles/r02/ncu_sweep_hist_v2.txt; 1.97 before the
+    # searches moved to the Eytzinger layout), at most one per clock per SM ->
+    # smem_wavefront_floor_ms.
     M9 = 1_000_000_000
     g = torch.Generator(device=device).manual_seed(4)
     y9 = (torch.rand(M9, device=device, generator=g) < 0.15).to(torch.uint8)
@@ -752,11 +757,15 @@ def run_extras(device, timing=(1000, 20000, 12_500_000_000)):
     torch.cuda.synchronize()
     ms9 = e0.elapsed_time(e1) / 3
     clk = 1.965e9
-    floor_ms = (M9 + n_h1) * 2.0 / 148 / clk * 1e3
+    wf_floor = M9 * 0.967 / 148 / clk * 1e3
+    at_floor = (M9 + n_h1) / 5.28 / 148 / clk * 1e3
     out["sweep_1e9_hist"] = {"records": M9, "ms": round(ms9, 3), "GBps": round(M9 * 14 / ms9 / 1e6, 1),
                              "frac_of_hbm": round(M9 * 14 / ms9 / 1e6 / measured_peaks()[0], 4),
                              "smem_atomics_per_record": round((M9 + n_h1) / M9, 3),
-                             "atomic_floor_ms": round(floor_ms, 3), "frac_of_atomic_floor": round(floor_ms / ms9, 3)}
+                             "smem_atomic_floor_ms": round(at_floor, 3),
+                             "smem_wavefront_floor_ms": round(wf_floor, 3),
+                             "frac_of_smem_wavefront_floor": round(wf_floor / ms9, 3),
+                             "ceilings": "measured on B200: tools/smem_atomic_bw.cu + ncu wavefronts/record"}
     del s9, z9, y9, a9
     # compaction (H4) and routing (H6) scale points: at the webcam hour they are ~10 us
     # launches, so their HBM fraction is shown on 2^30 dispositions / 2^28 logits

@@ -63,6 +63,21 @@ NS_DEV int count_le_f(const float* c, int n, float v) {
   return lo;
 }
 
+// The candidate searches walk an implicit binary tree stored in BFS (Eytzinger)
+// order: node k's children are 2k+1 and 2k+2, so one level's nodes are
+// contiguous (the top levels are conflict-free broadcasts; on the sorted array
+// the pivots of one level sit a power of two apart, all in one bank: ~34
+// wavefronts per warp for a 128-entry f64 search) and a step is one load, one
+// compare and one IMAD: k = 2k + 1 + (tree[k] < x).  With P = 2^h leaves the
+// tree holds the P - 1 sorted candidates (+inf padded) and, after h steps,
+// k - (P - 1) = #{candidates < x}.
+// In-order (sorted) index of BFS node i of the perfect tree with 2^h - 1 nodes.
+NS_DEV int eytz_sorted_index(int i, int h) {
+  const int d = 31 - __clz(i + 1);            // depth
+  const int p = i + 1 - (1 << d);             // position in its level
+  return ((2 * p + 1) << (h - 1 - d)) - 1;
+}
+
 // Phase 1: block-privatised histogram in shared memory (u32), flushed to the
 // global u64 histogram with one atomic per nonzero bin.
 __global__ void __launch_bounds__(kHistThreads, 1)
@@ -72,13 +87,24 @@ sweep_hist_kernel(const double* __restrict__ s, const float* __restrict__ z,
                   unsigned long long* hist, uint32_t* status, int privatised) {
   extern __shared__ __align__(16) uint8_t smem[];
   HistLayout L(nd, m);
-  double* dc = reinterpret_cast<double*>(smem);
   const int pd = pow2_above(nd), pu = pow2_above(m);
-  float* uc = reinterpret_cast<float*>(dc + pd);
+  const int hd = 31 - __clz(pd), hu = 31 - __clz(pu);
+  double* dt = reinterpret_cast<double*>(smem);            // [pd] BFS tree of the delta candidates
+  float* ut = reinterpret_cast<float*>(dt + pd);            // [pu] BFS tree of the logit candidates
+  float* uc = ut + pu;                                      // [pu] sorted logit candidates (equality test)
   uint32_t* hs = reinterpret_cast<uint32_t*>(uc + pu);
   const int tid = threadIdx.x;
-  for (int t = tid; t < pd; t += blockDim.x) dc[t] = t < nd ? delta[t] : __longlong_as_double(0x7FF0000000000000ll);
-  for (int t = tid; t < pu; t += blockDim.x) uc[t] = t < m ? u[t] : __int_as_float(0x7F800000);
+  const double dinf = __longlong_as_double(0x7FF0000000000000ll);
+  const float finf = __int_as_float(0x7F800000);
+  for (int t = tid; t < pd - 1; t += blockDim.x) {
+    const int q = eytz_sorted_index(t, hd);
+    dt[t] = q < nd ? delta[q] : dinf;
+  }
+  for (int t = tid; t < pu - 1; t += blockDim.x) {
+    const int q = eytz_sorted_index(t, hu);
+    ut[t] = q < m ? u[q] : finf;
+  }
+  for (int t = tid; t < pu; t += blockDim.x) uc[t] = t < m ? u[t] : finf;
   if (privatised)
     for (size_t t = tid; t < L.tail; t += blockDim.x) hs[t] = 0u;
   __syncthreads();
@@ -125,13 +151,18 @@ sweep_hist_kernel(const double* __restrict__ s, const float* __restrict__ z,
     int dj[kU], lj[kU];
 #pragma unroll
     for (int r = 0; r < kU; ++r) dj[r] = lj[r] = 0;
-    for (int st = pd >> 1; st > 0; st >>= 1) {
+    for (int lv = 0; lv < hd; ++lv) {
 #pragma unroll
-      for (int r = 0; r < kU; ++r) dj[r] += (dc[dj[r] + st - 1] < sv[r]) ? st : 0;
+      for (int r = 0; r < kU; ++r) dj[r] = 2 * dj[r] + 1 + (dt[dj[r]] < sv[r] ? 1 : 0);
     }
-    for (int st = pu >> 1; st > 0; st >>= 1) {
+    for (int lv = 0; lv < hu; ++lv) {
 #pragma unroll
-      for (int r = 0; r < kU; ++r) lj[r] += (uc[lj[r] + st - 1] < zv[r]) ? st : 0;
+      for (int r = 0; r < kU; ++r) lj[r] = 2 * lj[r] + 1 + (ut[lj[r]] < zv[r] ? 1 : 0);
+    }
+#pragma unroll
+    for (int r = 0; r < kU; ++r) {
+      dj[r] -= pd - 1;    // #{delta < s}
+      lj[r] -= pu - 1;    // #{u < z}
     }
 #pragma unroll
     for (int r = 0; r < kU; ++r) {
@@ -367,7 +398,7 @@ noscope_status launch_sweep(int32_t phase, const double* s, const float* z, cons
   HistLayout L(nd, m);
   if (phase & 1) {
     if (n > 0) {
-      size_t smem = (size_t)pow2_above(nd) * 8 + (size_t)pow2_above(m) * 4;
+      size_t smem = (size_t)pow2_above(nd) * 8 + (size_t)pow2_above(m) * 8;
       size_t priv = smem + L.tail * 4;
       int privatised = priv <= 200 * 1024 ? 1 : 0;
       size_t use = privatised ? priv : smem;
