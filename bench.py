@@ -94,7 +94,7 @@ def maybe_self_launch(args):
 def init_dist(world, device):
     """One process per GPU over NCCL (NCCL_DEBUG=INFO so the init lines show nranks)."""
     import torch.distributed as dist
-    if world > 1:
+    if world > 1 or "WORLD_SIZE" in os.environ:   # under torchrun: NCCL even for one rank
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=device)
@@ -277,7 +277,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
     torch.cuda.synchronize()
     stage_acc = []
@@ -290,12 +290,12 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
     launches = N.launch_count() - l0 + args.steps      # + the stand-in labeller kernel per step
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     per_rank = [ms]
-    if world > 1:
+    if dist.is_initialized():
         t = torch.zeros(world, device=device)
         t[rank] = ms
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
@@ -382,7 +382,7 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline(args, S)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
@@ -441,7 +441,7 @@ def run_x(args):
     D.run_units(N, [dict(mine[0], n_frames=chunk)], make_frames, dd, arch, Wt, lo, hi, lab_fn, truth_of,
                 chunk=chunk, ws=ws, device=device)
     torch.cuda.synchronize()
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
     timer, rec = [], {}
     with ClockSampler(local) as clk:
@@ -472,7 +472,7 @@ def run_x(args):
     cascade_ms = sum(a.elapsed_time(b) for a, b in timer)
     ms = cascade_ms + e0.elapsed_time(e1)
     per_rank = [ms]
-    if world > 1:
+    if dist.is_initialized():
         t = torch.zeros(world, device=device)
         t[rank] = ms
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
@@ -496,7 +496,7 @@ def run_x(args):
                 else None,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -25,9 +25,9 @@ def world_rank():
 
 
 def allreduce_hist_(hist: torch.Tensor) -> torch.Tensor:
-    """C1: in-place sum of a uint64-count histogram (stored as int64) over ranks."""
-    world, _ = world_rank()
-    if world > 1:
+    """C1: in-place sum of a uint64-count histogram (stored as int64) over ranks
+    (a collective whenever a process group exists, also with one rank)."""
+    if dist.is_available() and dist.is_initialized():
         if hist.device.type == "cuda" and dist.get_backend() != "nccl":   # gloo: reduce a host copy
             h = hist.cpu()
             dist.all_reduce(h, op=dist.ReduceOp.SUM)
@@ -64,7 +64,7 @@ def gather_labels_to_rank0(local: torch.Tensor, out: torch.Tensor | None = None)
     Every rank passes an equal-length track; rank 0 returns the concatenation in
     rank order (written into `out` [world * n] if given), other ranks None."""
     world, rank = world_rank()
-    if world == 1:
+    if not (dist.is_available() and dist.is_initialized()):
         if out is not None:
             out.copy_(local)
             return out
