@@ -96,7 +96,8 @@ def init_dist(world, device):
     import torch.distributed as dist
     if world > 1 or "WORLD_SIZE" in os.environ:   # under torchrun: NCCL even for one rank
         os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        # NCCL logs to stdout by default: keep stdout for the one JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=device)
 
 
@@ -389,7 +390,7 @@ def run_ours(args):
 def run_x(args):
     """BASELINE configs[4]: S streams x H hours of 640x480 webcam at
     30 fps, units = (stream, hour) of 108,000 frames (R-19), unit u on rank
-    floor(u*G/U).  Frames are rendered on device in chunks of 8,192 (the decode
+    floor(u*G/U).  Frames are rendered on device in chunks of 27,000 (the decode
     stand-in, untimed); each chunk goes through noscope_cascade_run with the unit's
     carried state; the timed work per rank = the sum of its cascade intervals (CUDA
     events) + the C1 sweep (phase 1 over every unit's records, all_reduce, phase 2)
@@ -419,7 +420,7 @@ def run_x(args):
             sc = sg.make_scene(sg.SceneSpec(W_SRC, H_SRC, args.x_hours * unit_len, seed=100 + u["stream"],
                                             stream=u["stream"]))
             scenes[u["stream"]] = GpuScene(sc, device=device)
-    chunk = 8192
+    chunk = 27_000          # 4 chunks per one-hour unit (24.9 GB of frames per chunk)
     pitch = sg.frame_pitch(W_SRC, H_SRC)
     buf = torch.empty((chunk, pitch), dtype=torch.uint8, device=device)
 
@@ -437,9 +438,22 @@ def run_x(args):
     ws = N.workspace(N.OP_CASCADE_RUN, dd, arch, chunk, device=device)
     truth_of = lambda u: scenes[u["stream"]].truth[u["hour"] * unit_len:(u["hour"] + 1) * unit_len]
     lab_fn = truth_labeller_address()
-    # warm-up: one chunk
+    # warm-up: one chunk (its scores also fix the sweep's delta candidates: 100
+    # quantiles of the fired scores, as in the webcam line)
+    rec0 = {}
     D.run_units(N, [dict(mine[0], n_frames=chunk)], make_frames, dd, arch, Wt, lo, hi, lab_fn, truth_of,
-                chunk=chunk, ws=ws, device=device)
+                chunk=chunk, ws=ws, device=device, records=rec0)
+    s0 = rec0["scores"][0]
+    fired_s = s0[s0 > dd.delta_diff]
+    q = torch.quantile(fired_s, torch.linspace(0, 1, SWEEP_M - 1, dtype=torch.float64, device=device))
+    dl = torch.unique(torch.cat([torch.tensor([dd.delta_diff], dtype=torch.float64, device=device), q]))
+    ul = torch.from_numpy(sg.logit_grid(SWEEP_M)).to(device)
+    hist = torch.zeros(N.sweep_hist_words(dl.numel(), SWEEP_M), dtype=torch.int64, device=device)
+    sws = N.workspace(N.OP_THRESHOLD_SWEEP, None, None, 0, dl.numel(), SWEEP_M, device=device)
+    a_rec = torch.empty(unit_len, dtype=torch.uint8, device=device)
+    best = N.pinned_sweep_best()
+    total = len(units) * unit_len
+    gathered = torch.empty(total, dtype=torch.uint8, device=device) if rank == 0 else None
     torch.cuda.synchronize()
     if dist.is_initialized():
         dist.barrier()
@@ -449,26 +463,17 @@ def run_x(args):
                              device=device, timer=timer, records=rec)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        ul = torch.from_numpy(sg.logit_grid(SWEEP_M)).to(device)
-        s0 = rec["scores"][0]
-        fired_s = s0[s0 > dd.delta_diff]
-        q = torch.quantile(fired_s[:: max(1, fired_s.numel() // 100000)],
-                           torch.linspace(0, 1, SWEEP_M - 1, dtype=torch.float64, device=device))
-        dl = torch.unique(torch.cat([torch.tensor([dd.delta_diff], dtype=torch.float64, device=device), q]))
-        hist = torch.zeros(N.sweep_hist_words(dl.numel(), SWEEP_M), dtype=torch.int64, device=device)
-        a_rec = torch.empty(unit_len, dtype=torch.uint8, device=device)
         for u, sc_u, z_u in zip(mine, rec["scores"], rec["logits"]):
             y = truth_of(u)
             N.noscope_sweep_records(sc_u, y, 1, K_LAG, 1, a_out=a_rec)
             N.noscope_threshold_sweep(1, sc_u, z_u, y, a_rec, dl, ul, hist)
         D.allreduce_hist_(hist)                                                            # C1
-        total = len(units) * unit_len
-        best, _ = N.noscope_threshold_sweep(2, None, None, None, None, dl, ul, hist, SWEEP_TIMING,
-                                            total // 100, total // 100)
-        gathered = torch.empty(len(units) * unit_len, dtype=torch.uint8, device=device) if rank == 0 else None
+        N.noscope_threshold_sweep(2, None, None, None, None, dl, ul, hist, SWEEP_TIMING, total // 100,
+                                  total // 100, ws=sws, best_out=best)
         D.gather_labels_to_rank0(labels, out=gathered)                                     # C2
         e1.record()
         torch.cuda.synchronize()
+    best = N.sweep_best_dict(best)
     cascade_ms = sum(a.elapsed_time(b) for a, b in timer)
     ms = cascade_ms + e0.elapsed_time(e1)
     per_rank = [ms]
@@ -482,7 +487,7 @@ def run_x(args):
         line = {"metric": "cascade frames/sec (diff+CNN+routing)", "value": round(total / (tmax / 1e3), 1),
                 "unit": "frames/s", "n_gpus": world, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "u8/int64/f64 (DD), bf16->f32 (CNN)",
-                "data": "synthetic fixed-angle webcam streams rendered on device in 8,192-frame chunks "
+                "data": "synthetic fixed-angle webcam streams rendered on device in 27,000-frame chunks "
                         "(untimed), random-init CNN weights",
                 "config": {"workload": f"x: {args.x_streams} streams x {args.x_hours} h at 30 fps, 640x480, "
                                        f"units of {unit_len} frames sharded over {world} GPU(s)",

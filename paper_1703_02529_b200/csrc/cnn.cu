@@ -218,7 +218,7 @@ static bool make_plan(const noscope_cnn_arch& a, int64_t n_max, CnnPlan* P) {
   p.L = a.n_conv;
   p.C = a.base_filters;
   p.D = a.dense;
-  p.fused = p.C == 32;
+  p.fused = p.C == 32 || p.C == 16;
   p.first_g = p.fused ? 2 : 1;
   p.chunk = std::min<int64_t>(kCnnChunk, std::max<int64_t>(128, (n_max + 127) / 128 * 128));
   size_t off = 256;  // status words etc. live before the CNN region (caller offset)

@@ -6,8 +6,9 @@
 //   <2, false> base_filters = 64: conv1 only, as two N = 32 halves on the same
 //              TMEM A tile; the pooled 25x25x64 map goes to HBM in the stacked
 //              layout (internal.h) for the generic layer kernel (cnn_gemm.cu);
-//   <1, false, 16> base_filters = 16 (the paper's C = 16 models):
-//              conv1 only as one N = 16 MMA per tile, 25x25x16 map to HBM.
+//   <1, true, 16> base_filters = 16 (the paper's C = 16 models):
+//              conv1 (one N = 16 MMA per tile) + conv2 (16 -> 32, N = 32) fused
+//              like the C = 32 variant.
 //
 // Roles (19 warps):
 //   W0      producer    — cp.async.bulk of the u8 input frames (2-deep ring) and
@@ -134,8 +135,14 @@ template <int kHalves, bool kConv2, int kC1>
 __global__ void __launch_bounds__(fz::kThreads, 1)
 conv12_fused_kernel(FusedArgs A) {
   using namespace fz;
-  static_assert(kC1 == C1 || (kC1 == 16 && !kConv2), "conv2 fusion needs 32 conv1 channels per half");
+  static_assert(kC1 == C1 || kC1 == 16, "conv1 halves of 32 or 16 channels");
+  static_assert(!kConv2 || kHalves == 1, "conv2 fusion reads one conv1 half");
   constexpr int C1t = kC1 * kHalves;
+  // conv2 (fused variants): kC1 -> kC2 = 2 kC1 channels ("filter doubling"); the
+  // shared-memory regions are sized for the widest variant (32 -> 64)
+  constexpr int kC2 = 2 * kC1;
+  constexpr int kK2v = 9 * kC1 / 16;    // K16 steps: 9 taps x (kC1 / 16)
+  constexpr int kSpt = kC1 / 16;        // K16 steps per tap
   constexpr int wEp2_0 = wEp2_of<kConv2>();
   constexpr int kEp1Groups = (wEp2_0 - wEp1_0) / 4;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -200,9 +207,9 @@ conv12_fused_kernel(FusedArgs A) {
     for (int e = tid; e < 2 * 128 * 4; e += blockDim.x)
       ones[e] = (e < 128 * 4 && (e & 3) == 0) ? 0x3F803F80u : 0u;   // row r: K0 = K1 = 1.0
     uint32_t* b2b = reinterpret_cast<uint32_t*>(smem + oB2b);
-    for (int e = tid; e < 2 * C2 * 4; e += blockDim.x) {
+    for (int e = tid; e < 2 * kC2 * 4; e += blockDim.x) {
       uint32_t v = 0;
-      if (e < C2 * 4 && (e & 3) == 0) {
+      if (e < kC2 * 4 && (e & 3) == 0) {
         const float b = A.b2[e >> 2];
         const __nv_bfloat16 hi = __float2bfloat16_rn(b);
         const __nv_bfloat16 lo = __float2bfloat16_rn(b - __bfloat162float(hi));
@@ -222,9 +229,9 @@ conv12_fused_kernel(FusedArgs A) {
   if (warp == 0) {
     // ===================================================== producer
     if (lane == 0) {
-      mbar_arrive_expect_tx(w_full, (kK1 / 8) * C1t * 16 + (kConv2 ? 9 * (C1 / 8) * C2 * 16 : 0));
+      mbar_arrive_expect_tx(w_full, (kK1 / 8) * C1t * 16 + (kConv2 ? 9 * (kC1 / 8) * kC2 * 16 : 0));
       bulk_g2s(smem + oB1, A.w1, (kK1 / 8) * C1t * 16, w_full);
-      if (kConv2) bulk_g2s(smem + oB2, A.w2, 9 * (C1 / 8) * C2 * 16, w_full);
+      if (kConv2) bulk_g2s(smem + oB2, A.w2, 9 * (kC1 / 8) * kC2 * 16, w_full);
       for (int64_t it = 0; it < my_frames; ++it) {
         const int s = (int)(it & 1);
         if (it >= 2) mbar_wait(&in_empty[s], (uint32_t)(((it >> 1) - 1) & 1));
@@ -278,10 +285,10 @@ conv12_fused_kernel(FusedArgs A) {
   } else if (warp == 2) {
     // ===================================================== conv2 MMA issuer
     if (kConv2 && lane == 0) {
-      constexpr uint32_t id2 = idesc_bf16_f32(128, C2);
+      constexpr uint32_t id2 = idesc_bf16_f32(128, kC2);
       const uint32_t sB2 = smem_u32(smem + oB2), sAct = smem_u32(smem + oAct);
       const uint64_t dOnes = sdesc(smem_u32(smem + oOnes), 128 * 16, 128);
-      const uint64_t dBias = sdesc(smem_u32(smem + oB2b), C2 * 16, 128);
+      const uint64_t dBias = sdesc(smem_u32(smem + oB2b), kC2 * 16, 128);
       mbar_wait(w_full, 0);
       for (int64_t it = 0; it < my_frames; ++it) {
         const int pb = (int)(it & 1);
@@ -306,14 +313,14 @@ conv12_fused_kernel(FusedArgs A) {
           // 16 groups of 8 pixels, one image row apart: SBO = Wp * 16 bytes
           const uint64_t ad0 = sdesc(abase + (uint32_t)(q0[0] + 1) * 16, kPlaneBytes, kWp * 16);
           const uint64_t ad1 = sdesc(abase + (uint32_t)(q0[1] + 1) * 16, kPlaneBytes, kWp * 16);
-          const uint64_t bd0 = sdesc(sB2, C2 * 16, 128);
-          const uint32_t d0 = tmem + kColD2 + b[0] * C2, d1 = tmem + kColD2 + b[1] * C2;
+          const uint64_t bd0 = sdesc(sB2, kC2 * 16, 128);
+          const uint32_t d0 = tmem + kColD2 + b[0] * kC2, d1 = tmem + kColD2 + b[1] * kC2;
 #pragma unroll
-          for (int ks = 0; ks < kK2; ++ks) {
-            const int tap = ks >> 1, cg = (ks & 1) * 2;  // 4 channel groups per tap, 2 per step
+          for (int ks = 0; ks < kK2v; ++ks) {
+            const int tap = ks / kSpt, cg = (ks % kSpt) * 2;  // kC1/8 channel groups per tap, 2 per step
             const int shift = (tap / 3 - 1) * kWp + (tap % 3 - 1);
             const uint64_t aoff = (uint64_t)((cg * kPlaneBytes + shift * 16) >> 4);
-            const uint64_t bd = bd0 + (uint64_t)(((tap * 4 + cg) * C2 * 16) >> 4);
+            const uint64_t bd = bd0 + (uint64_t)(((tap * (kC1 / 8) + cg) * kC2 * 16) >> 4);
             if (NS_EXP & 16) continue;
             umma_bf16(d0, ad0 + aoff, bd, id2, ks > 0 ? 1u : 0u);
             umma_bf16(d1, ad1 + aoff, bd, id2, ks > 0 ? 1u : 0u);
@@ -496,7 +503,7 @@ conv12_fused_kernel(FusedArgs A) {
     // 13, 169 rows per frame, 14 leading guard rows
     constexpr int kHpool = 12, kWqo = 13, kPo = 13 * 13, kGo = 14;
     if (!A.to_features && blockIdx.x == 0) {  // zero the leading / trailing guards
-      for (int e = et; e < (C2 / 8) * (kGo + kWqo); e += 256) {
+      for (int e = et; e < (kC2 / 8) * (kGo + kWqo); e += 256) {
         const int c = e / (kGo + kWqo), k = e % (kGo + kWqo);
         const int64_t row = k < kGo ? k : kGo + cnt * kPo + (k - kGo);
         *reinterpret_cast<uint4*>(A.out + ((int64_t)c * A.out_rows + row) * 16) = make_uint4(0, 0, 0, 0);
@@ -513,15 +520,15 @@ conv12_fused_kernel(FusedArgs A) {
         // the second y block re-computes conv rows 8..15: only rows >= 16 are new
         const bool keep = pool_lane && yc < 24 && (yb == 0 || yc >= 16);
         const int yp = yc >> 1, xp = xc >> 1;
-        // All 64 accumulator columns -> packed bf16x2 registers first (two 32-column
+        // All kC2 accumulator columns -> packed bf16x2 registers first (32-column
         // loads, one wait each), then release the TMEM buffer to the conv2 issuer
         // before the shuffles and global stores.
-        uint32_t pk[32];
+        uint32_t pk[kC2 / 2];
 #pragma unroll
-        for (int hg = 0; hg < ((NS_EXP & 32) ? 0 : 2); ++hg) {
+        for (int hg = 0; hg < ((NS_EXP & 32) ? 0 : kC2 / 32); ++hg) {
           uint32_t r[32];
-          tmem_ld16(tmem + ((uint32_t)lg << 16) + kColD2 + b * C2 + hg * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
-          tmem_ld16(tmem + ((uint32_t)lg << 16) + kColD2 + b * C2 + hg * 32 + 16,
+          tmem_ld16(tmem + ((uint32_t)lg << 16) + kColD2 + b * kC2 + hg * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
+          tmem_ld16(tmem + ((uint32_t)lg << 16) + kColD2 + b * kC2 + hg * 32 + 16,
                     *reinterpret_cast<uint32_t(*)[16]>(r + 16));
           tmem_ld_wait();
 #pragma unroll
@@ -531,7 +538,7 @@ conv12_fused_kernel(FusedArgs A) {
         tc_fence_before();
         mbar_arrive(&t2_empty[b]);
 #pragma unroll
-        for (int g = 0; g < ((NS_EXP & 32) ? 0 : C2 / 16); ++g) {
+        for (int g = 0; g < ((NS_EXP & 32) ? 0 : kC2 / 16); ++g) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             uint32_t v = pk[g * 8 + j];
@@ -544,7 +551,7 @@ conv12_fused_kernel(FusedArgs A) {
             const uint4 o1 = make_uint4(pk[g * 8 + 4], pk[g * 8 + 5], pk[g * 8 + 6], pk[g * 8 + 7]);
             const int cgo = g * 2;
             if (A.to_features) {
-              const int64_t kc = ((int64_t)(yp * kHpool + xp) * C2) / 8 + cgo;
+              const int64_t kc = ((int64_t)(yp * kHpool + xp) * kC2) / 8 + cgo;
               uint8_t* dst = A.out + (i / 128) * ((int64_t)A.K_feat * 256) + kc * 2048 + (i % 128) * 16;
               *reinterpret_cast<uint4*>(dst) = o0;
               *reinterpret_cast<uint4*>(dst + 2048) = o1;
@@ -588,7 +595,7 @@ static noscope_status launch_variant(const FusedArgs& a, int grid, cudaStream_t 
 noscope_status launch_conv12_fused(const FusedArgs& a, int grid, cudaStream_t st) {
   if (a.C1 == 32) return launch_variant<1, true, 32>(a, grid, st);
   if (a.C1 == 64) return launch_variant<2, false, 32>(a, grid, st);
-  if (a.C1 == 16) return launch_variant<1, false, 16>(a, grid, st);
+  if (a.C1 == 16) return launch_variant<1, true, 16>(a, grid, st);
   return NOSCOPE_INVALID_ARGUMENT;
 }
 

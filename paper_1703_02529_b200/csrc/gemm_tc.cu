@@ -82,33 +82,50 @@ gemm3xtf32_kernel(TcGemmArgs G) {
   const int nchunks = (int)((k1 - k0 + kBK - 1) / kBK);
   for (int it = 0; it < nchunks; ++it) {
     const int s = it & 1;
-    if (it >= 2) mbar_wait(&done[s], (uint32_t)(((it >> 1) - 1) & 1));   // stage s free again
     uint8_t* st = sm + s * S::kStage;
     float* ahi = reinterpret_cast<float*>(st);
     float* alo = reinterpret_cast<float*>(st + S::kA);
     float* bhi = reinterpret_cast<float*>(st + 2 * S::kA);
     float* blo = reinterpret_cast<float*>(st + 2 * S::kA + S::kB);
     const int64_t kb = k0 + (int64_t)it * kBK;
-    // A chunk: 128 rows x 32 k (element order along the unit stride for coalescing)
-    for (int e = tid; e < kBM * kBK; e += kGT) {
+    // all of this thread's global loads first (memory-level parallelism), coalesced
+    // along whichever stride is 1; then the tf32 split and the canonical-layout stores
+    constexpr int kPA = kBM * kBK / kGT, kPB = BN * kBK / kGT;
+    float va[kPA], vb[kPB];
+#pragma unroll
+    for (int i = 0; i < kPA; ++i) {
+      const int e = tid + i * kGT;
       const int r = G.a_m_fast ? (e % kBM) : (e / kBK), k = G.a_m_fast ? (e / kBM) : (e % kBK);
       const int m = m0 + r;
       const int64_t kk = kb + k;
-      const float x = (m < G.M && kk < k1) ? G.A[(int64_t)m * G.sam + kk * G.sak] : 0.0f;
-      const float hi = tf32_rna(x);
-      const uint32_t o = kmaj_off(r, k, kBM) >> 2;
-      ahi[o] = hi;
-      alo[o] = x - hi;
+      va[i] = (m < G.M && kk < k1) ? __ldg(G.A + (int64_t)m * G.sam + kk * G.sak) : 0.0f;
     }
-    for (int e = tid; e < BN * kBK; e += kGT) {
+#pragma unroll
+    for (int i = 0; i < kPB; ++i) {
+      const int e = tid + i * kGT;
       const int r = G.b_n_fast ? (e % BN) : (e / kBK), k = G.b_n_fast ? (e / BN) : (e % kBK);
       const int n = n0 + r;
       const int64_t kk = kb + k;
-      const float x = (n < G.N && kk < k1) ? G.B[(int64_t)n * G.sbn + kk * G.sbk] : 0.0f;
-      const float hi = tf32_rna(x);
+      vb[i] = (n < G.N && kk < k1) ? __ldg(G.B + (int64_t)n * G.sbn + kk * G.sbk) : 0.0f;
+    }
+    if (it >= 2) mbar_wait(&done[s], (uint32_t)(((it >> 1) - 1) & 1));   // stage s free again
+#pragma unroll
+    for (int i = 0; i < kPA; ++i) {
+      const int e = tid + i * kGT;
+      const int r = G.a_m_fast ? (e % kBM) : (e / kBK), k = G.a_m_fast ? (e / kBM) : (e % kBK);
+      const float hi = tf32_rna(va[i]);
+      const uint32_t o = kmaj_off(r, k, kBM) >> 2;
+      ahi[o] = hi;
+      alo[o] = va[i] - hi;
+    }
+#pragma unroll
+    for (int i = 0; i < kPB; ++i) {
+      const int e = tid + i * kGT;
+      const int r = G.b_n_fast ? (e % BN) : (e / kBK), k = G.b_n_fast ? (e / BN) : (e % kBK);
+      const float hi = tf32_rna(vb[i]);
       const uint32_t o = kmaj_off(r, k, BN) >> 2;
       bhi[o] = hi;
-      blo[o] = x - hi;
+      blo[o] = vb[i] - hi;
     }
     fence_proxy_async_smem();   // generic-proxy stores -> tensor-core reads
     tc_fence_before();
@@ -161,13 +178,21 @@ gemm3xtf32_kernel(TcGemmArgs G) {
   if (warp == 0) tmem_dealloc_rt(tmem, BN);
 }
 
+// C = sum of the split-K partials: one warp per output element, lanes take the
+// splits z = lane, lane + 32, ... and a fixed shuffle tree combines them
+// (deterministic: the same order every run).
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, int ksplit, int M, int N, float* __restrict__ C,
                                      int64_t ldc) {
   const int64_t total = (int64_t)M * N;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t e = w0; e < total; e += nw) {
     float s = 0.0f;
-    for (int z = 0; z < ksplit; ++z) s += part[(int64_t)z * total + e];   // split order: deterministic
-    C[(e / N) * ldc + e % N] = s;
+    for (int z = lane; z < ksplit; z += 32) s += part[(int64_t)z * total + e];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) C[(e / N) * ldc + e % N] = s;
   }
 }
 
@@ -216,8 +241,8 @@ noscope_status tc_gemm(const float* A, int64_t sam, int64_t sak, const float* B,
   noscope_status s = BN == 32 ? launch_bn<32>(g, st) : (BN == 64 ? launch_bn<64>(g, st) : launch_bn<128>(g, st));
   if (s != NOSCOPE_OK || ks == 1) return s;
   const int64_t total = (int64_t)M * N;
-  splitk_reduce_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 8 * kNumSMs), 256, 0, st>>>(part, ks, M, N, C,
-                                                                                                   ldc);
+  splitk_reduce_kernel<<<(int)std::min<int64_t>((total * 32 + 255) / 256, 16 * kNumSMs), 256, 0, st>>>(part, ks, M,
+                                                                                                     N, C, ldc);
   NS_LAUNCH_CHECK();
   count_launch();
   return NOSCOPE_OK;
