@@ -7,22 +7,23 @@
 // a_hi b_hi + a_hi b_lo + a_lo b_hi in fp32 (the a_lo b_lo term is below fp32
 // rounding), which keeps the result at fp32 accuracy (R-25: training runs in fp32).
 //
-// CTA tile 128 x BN (BN in {32, 64, 128}), K in chunks of 32: 128 threads load and
-// split a chunk of A and B (coalesced along whichever stride is 1) into the
-// canonical no-swizzle K-major shared-memory layout (core matrix = 8 rows x 4
-// tf32), one elected thread issues 4 K-steps x 3 tcgen05.mma.kind::tf32 into the
-// TMEM accumulator, double-buffered against the next chunk's loads (mbarrier per
-// stage).  Split-K over blockIdx.z writes fp32 partials that a second kernel sums
-// in split order (deterministic, no atomics).
+// CTA tile 128 x BN (BN in {32, 64, 128}), K in stages of 32 (16 for BN = 128): 256
+// threads load a stage of A and B (all loads in flight before any store), split it
+// and store it into the canonical no-swizzle K-major shared-memory layout (core
+// matrix = 8 rows x 4 tf32; a warp fills one core matrix per store, bank-conflict
+// free); one elected thread issues the K-steps x 3 tcgen05.mma.kind::tf32 into the
+// TMEM accumulator, double-buffered against the next stage's loads (mbarrier per
+// stage); the epilogue stages each warp's 32 x 16 block through shared memory so the
+// global stores are row segments.  Split-K over blockIdx.z writes fp32 partials that
+// a second kernel sums in a fixed order (deterministic, no atomics).
 #include "common.cuh"
 #include "internal.h"
 
 namespace ns {
 
 namespace {
-constexpr int kGT = 128;           // threads per CTA
-constexpr int kBM = 128, kBK = 32;
-constexpr int kKSteps = kBK / 8;   // tf32 MMA K = 8
+constexpr int kGT = 256;           // threads per CTA (8 warps: loads / splits / stores)
+constexpr int kBM = 128, kBK = 32;   // kBK: host-side chunk granularity (split-K ranges)
 
 // Instruction descriptor: kind::tf32, A/B tf32, D fp32, both K-major.
 __host__ __device__ constexpr uint32_t idesc_tf32_f32(int M, int N) {
@@ -44,16 +45,15 @@ NS_DEV float tf32_rna(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
-// byte offset of element (row r, k) in a K-major canonical tile of `rows` rows x 32 k:
-// core matrix (8-row group g, 4-element K chunk c) at ((c * rows/8) + g) * 128
-NS_DEV uint32_t kmaj_off(int r, int k, int rows) {
-  return (uint32_t)((((k >> 2) * (rows >> 3) + (r >> 3)) << 7) + ((r & 7) << 4) + ((k & 3) << 2));
-}
+// K-major canonical tile of `rows` rows x 32 k: core matrix (8-row group g, 4-element K
+// chunk c) at byte ((c * rows/8) + g) * 128; element (r, k) at + (r % 8) * 16 + (k % 4) * 4
 
 template <int BN>
 struct GemmSmem {
-  static constexpr int kA = kBM * kBK * 4;   // 16 KB per split half
-  static constexpr int kB = BN * kBK * 4;
+  static constexpr int BK = BN == 128 ? 16 : 32;   // K per stage (BN = 128: 2 CTAs / SM)
+  static constexpr int kKSteps = BK / 8;           // tf32 MMA K = 8
+  static constexpr int kA = kBM * BK * 4;
+  static constexpr int kB = BN * BK * 4;
   static constexpr int kStage = 2 * kA + 2 * kB;   // hi + lo of A and B
   static constexpr int kBytes = 2 * kStage + 64;
 };
@@ -79,7 +79,7 @@ gemm3xtf32_kernel(TcGemmArgs G) {
   tc_fence_after();
   const uint32_t tmem = *tslot;
   constexpr uint32_t idesc = idesc_tf32_f32(kBM, BN);
-  const int nchunks = (int)((k1 - k0 + kBK - 1) / kBK);
+  const int nchunks = (int)((k1 - k0 + S::BK - 1) / S::BK);
   for (int it = 0; it < nchunks; ++it) {
     const int s = it & 1;
     uint8_t* st = sm + s * S::kStage;
@@ -87,23 +87,27 @@ gemm3xtf32_kernel(TcGemmArgs G) {
     float* alo = reinterpret_cast<float*>(st + S::kA);
     float* bhi = reinterpret_cast<float*>(st + 2 * S::kA);
     float* blo = reinterpret_cast<float*>(st + 2 * S::kA + S::kB);
-    const int64_t kb = k0 + (int64_t)it * kBK;
-    // all of this thread's global loads first (memory-level parallelism), coalesced
-    // along whichever stride is 1; then the tf32 split and the canonical-layout stores
-    constexpr int kPA = kBM * kBK / kGT, kPB = BN * kBK / kGT;
+    const int64_t kb = k0 + (int64_t)it * S::BK;
+    // All of this thread's global loads first (memory-level parallelism), then the tf32
+    // split and the stores.  A warp fills one core matrix (8 rows x 4 k = 128 B) per
+    // step: lane -> (row 8g + lane/4, k 4c + lane%4), core matrix cm = c * rows/8 + g
+    // at byte cm * 128, so the shared-memory stores are 32 consecutive words (no bank
+    // conflicts) and the global loads are 8 segments of 16 B (rows) or 4 of 32 B (k).
+    constexpr int kPA = kBM * S::BK / kGT, kPB = BN * S::BK / kGT;
+    const int lane = tid & 31, wq = tid >> 5;
     float va[kPA], vb[kPB];
 #pragma unroll
     for (int i = 0; i < kPA; ++i) {
-      const int e = tid + i * kGT;
-      const int r = G.a_m_fast ? (e % kBM) : (e / kBK), k = G.a_m_fast ? (e / kBM) : (e % kBK);
+      const int cm = wq + i * (kGT / 32);
+      const int r = 8 * (cm % (kBM / 8)) + (lane >> 2), k = 4 * (cm / (kBM / 8)) + (lane & 3);
       const int m = m0 + r;
       const int64_t kk = kb + k;
       va[i] = (m < G.M && kk < k1) ? __ldg(G.A + (int64_t)m * G.sam + kk * G.sak) : 0.0f;
     }
 #pragma unroll
     for (int i = 0; i < kPB; ++i) {
-      const int e = tid + i * kGT;
-      const int r = G.b_n_fast ? (e % BN) : (e / kBK), k = G.b_n_fast ? (e / BN) : (e % kBK);
+      const int cm = wq + i * (kGT / 32);
+      const int r = 8 * (cm % (BN / 8)) + (lane >> 2), k = 4 * (cm / (BN / 8)) + (lane & 3);
       const int n = n0 + r;
       const int64_t kk = kb + k;
       vb[i] = (n < G.N && kk < k1) ? __ldg(G.B + (int64_t)n * G.sbn + kk * G.sbk) : 0.0f;
@@ -111,19 +115,15 @@ gemm3xtf32_kernel(TcGemmArgs G) {
     if (it >= 2) mbar_wait(&done[s], (uint32_t)(((it >> 1) - 1) & 1));   // stage s free again
 #pragma unroll
     for (int i = 0; i < kPA; ++i) {
-      const int e = tid + i * kGT;
-      const int r = G.a_m_fast ? (e % kBM) : (e / kBK), k = G.a_m_fast ? (e / kBM) : (e % kBK);
+      const int o = (wq + i * (kGT / 32)) * 32 + lane;   // float index = cm * 32 + lane
       const float hi = tf32_rna(va[i]);
-      const uint32_t o = kmaj_off(r, k, kBM) >> 2;
       ahi[o] = hi;
       alo[o] = va[i] - hi;
     }
 #pragma unroll
     for (int i = 0; i < kPB; ++i) {
-      const int e = tid + i * kGT;
-      const int r = G.b_n_fast ? (e % BN) : (e / kBK), k = G.b_n_fast ? (e / BN) : (e % kBK);
+      const int o = (wq + i * (kGT / 32)) * 32 + lane;
       const float hi = tf32_rna(vb[i]);
-      const uint32_t o = kmaj_off(r, k, BN) >> 2;
       bhi[o] = hi;
       blo[o] = vb[i] - hi;
     }
@@ -136,7 +136,7 @@ gemm3xtf32_kernel(TcGemmArgs G) {
       // K-major canonical: LBO = next 4-element K chunk = rows/8 core matrices, SBO = 128 B
       const uint32_t lboA = (kBM / 8) * 128, lboB = (BN / 8) * 128;
 #pragma unroll
-      for (int ks = 0; ks < kKSteps; ++ks) {
+      for (int ks = 0; ks < S::kKSteps; ++ks) {
         const uint32_t oa = (uint32_t)(2 * ks) * lboA, ob = (uint32_t)(2 * ks) * lboB;
         const uint64_t dah = sdesc(sa + oa, lboA, 128), dal = sdesc(sal + oa, lboA, 128);
         const uint64_t dbh = sdesc(sb + ob, lboB, 128), dbl = sdesc(sbl + ob, lboB, 128);
@@ -151,27 +151,38 @@ gemm3xtf32_kernel(TcGemmArgs G) {
   // drain: the last commit covers every earlier MMA
   if (nchunks > 0) mbar_wait(&done[(nchunks - 1) & 1], (uint32_t)(((nchunks - 1) >> 1) & 1));
   tc_fence_after();
-  const int row = warp * 32 + (tid & 31);
-  const int m = m0 + row;
+  // epilogue: warp w reads TMEM lanes 32 (w % 4) .. + 31 (its lane quarter), warps
+  // w and w + 4 split the accumulator columns
+  const int quarter = warp & 3, half = warp >> 2;
   float* out = G.part ? G.part + (int64_t)blockIdx.z * G.M * G.N : G.C;
   const int64_t ldo = G.part ? G.N : G.ldc;
+  constexpr int kColsPerHalf = BN / 2;
+  // stores staged per warp through shared memory (the stage buffers are free now):
+  // 32 rows x 16 columns written by row, read back two rows per instruction so a
+  // warp's global stores are two contiguous 64-byte row segments
+  __syncthreads();
+  float* stage = reinterpret_cast<float*>(sm) + warp * (32 * 17);
+  const int lane = tid & 31;
 #pragma unroll 1
-  for (int c = 0; c < BN; c += 16) {
+  for (int c = half * kColsPerHalf; c < (half + 1) * kColsPerHalf; c += 16) {
     uint32_t r[16];
     if (nchunks > 0) {
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c, r);
+      tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + c, r);
       tmem_ld_wait();
     } else {
 #pragma unroll
       for (int j = 0; j < 16; ++j) r[j] = 0u;
     }
-    if (m < G.M) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int n = n0 + c + j;
-        if (n < G.N) out[(int64_t)m * ldo + n] = __uint_as_float(r[j]);
-      }
+    for (int j = 0; j < 16; ++j) stage[lane * 17 + j] = __uint_as_float(r[j]);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int rr = 2 * i + (lane >> 4), cc = lane & 15;
+      const int mm = m0 + quarter * 32 + rr, n = n0 + c + cc;
+      if (mm < G.M && n < G.N) out[(int64_t)mm * ldo + n] = stage[rr * 17 + cc];
     }
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
@@ -219,16 +230,10 @@ size_t tc_gemm_part_floats(int M, int N, int64_t K) {
   return ks > 1 ? (size_t)ks * M * N : 0;
 }
 
-noscope_status tc_gemm(const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbn, int64_t sbk, float* C,
-                       int64_t ldc, int M, int N, int64_t K, float* part, cudaStream_t st) {
+static noscope_status run_gemm(TcGemmArgs g, float* part, cudaStream_t st) {
+  const int M = g.M, N = g.N;
+  const int64_t K = g.K;
   if (M <= 0 || N <= 0) return NOSCOPE_OK;
-  TcGemmArgs g{};
-  g.A = A; g.sam = sam; g.sak = sak;
-  g.B = B; g.sbn = sbn; g.sbk = sbk;
-  g.C = C; g.ldc = ldc;
-  g.M = M; g.N = N; g.K = K;
-  g.a_m_fast = sam == 1 && sak != 1;
-  g.b_n_fast = sbn == 1 && sbk != 1;
   const int BN = N <= 32 ? 32 : (N <= 64 ? 64 : 128);
   const int64_t tiles = (int64_t)((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   const int64_t chunks = (K + kBK - 1) / kBK;
@@ -241,11 +246,21 @@ noscope_status tc_gemm(const float* A, int64_t sam, int64_t sak, const float* B,
   noscope_status s = BN == 32 ? launch_bn<32>(g, st) : (BN == 64 ? launch_bn<64>(g, st) : launch_bn<128>(g, st));
   if (s != NOSCOPE_OK || ks == 1) return s;
   const int64_t total = (int64_t)M * N;
-  splitk_reduce_kernel<<<(int)std::min<int64_t>((total * 32 + 255) / 256, 16 * kNumSMs), 256, 0, st>>>(part, ks, M,
-                                                                                                     N, C, ldc);
+  splitk_reduce_kernel<<<(int)std::min<int64_t>((total * 32 + 255) / 256, 16 * kNumSMs), 256, 0, st>>>(
+      part, ks, M, N, g.C, g.ldc);
   NS_LAUNCH_CHECK();
   count_launch();
   return NOSCOPE_OK;
+}
+
+noscope_status tc_gemm(const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbn, int64_t sbk, float* C,
+                       int64_t ldc, int M, int N, int64_t K, float* part, cudaStream_t st) {
+  TcGemmArgs g{};
+  g.A = A; g.sam = sam; g.sak = sak;
+  g.B = B; g.sbn = sbn; g.sbk = sbk;
+  g.C = C; g.ldc = ldc;
+  g.M = M; g.N = N; g.K = K;
+  return run_gemm(g, part, st);
 }
 
 }  // namespace ns

@@ -117,7 +117,6 @@ struct TcGemmArgs {
   int64_t ldc;
   int M, N;
   int64_t K;
-  int a_m_fast, b_n_fast;   // load order: along m / n (unit stride) instead of k
   int ksplit;
   int64_t kper;
   float* part;
