@@ -828,6 +828,7 @@ noscope_status launch_diff_detect(const noscope_dd_config& cfg, const uint8_t* f
     int sms = kNumSMs, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (const char* e = std::getenv("NOSCOPE_DD_SMS")) sms = std::max(1, std::min(sms, std::atoi(e)));  // experiments
     // all CTAs co-resident (deferred scoring waits on earlier CTAs' flags)
     const int grid = (int)std::min<int64_t>(frames_needed, (int64_t)std::min(per_sm, cps) * sms);
     if (cfg.mode == 1) NS_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)grid * 4, st));
