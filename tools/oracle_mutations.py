@@ -64,6 +64,22 @@ MUTATIONS = {
     "N1_lr_sign_error": ("delta = -np.linalg.solve(", "delta = np.linalg.solve("),
     "N1_lr_unscale_bias": ("return w / sd, v[d] - float(np.sum(w * mu / sd))", "return w / sd, v[d]"),
     "N1_ref_round_down": ("return ((2 * S + m) // (2 * m)).astype(np.uint8)", "return (S // m).astype(np.uint8)"),
+    "N1_ref_uses_positives": ("neg = np.asarray(labels) == 0", "neg = np.asarray(labels) != 0"),
+    "N1_features_wrong_anchor": ("out[i] = blocked_mse(small[i], small[i - k], grid)",
+                                 "out[i] = blocked_mse(small[i], small[i - k + 1], grid)"),
+    "N1_sample_std": ("sd = F.std(axis=0)\n    sd = np.where(sd > 0, sd, 1.0)\n    X = (F - mu) / sd",
+                      "sd = F.std(axis=0, ddof=1)\n    sd = np.where(sd > 0, sd, 1.0)\n    X = (F - mu) / sd"),
+    # O9 record builder and tables
+    "O9_records_mode1_no_lag": ("a[i] = 0 if (mode == 0 or i < k) else y[i - k]", "a[i] = 0 if (mode == 0 or i < k) else y[i]"),
+    "O9_records_skip_current": ("a[i] = y[last_checked]", "a[i] = y[i]"),
+    "O9_FPnf_wrong_cell": ('T["FPnf"][j] = (nf & (a == 1) & (y == 0)).sum()', 'T["FPnf"][j] = (nf & (a == 0) & (y == 1)).sum()'),
+    "O9_fired_non_strict": ("fired = s > delta[j]", "fired = s >= delta[j]"),
+    "O9_tiebreak_min_low": ("key = (c, U, j, -l, h)", "key = (c, U, j, l, h)"),
+    # N3 evaluation
+    "N3_window_strict": ("return float((per >= agree_min).sum()) / nw", "return float((per > agree_min).sum()) / nw"),
+    "N3_speedup_drops_snn": ('+ (c["fired"] * t_snn if "cnn" in stages else 0)', '+ 0'),
+    # N4 training: best epoch on ties / by training loss
+    "N4_best_by_train_loss": ("if val < best_val:", "if tot / len(perm) < best_val:"),
 }
 
 
