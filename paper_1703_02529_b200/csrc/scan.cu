@@ -11,7 +11,8 @@
 // checked frame p - K, K = ceil(k / t_skip) (the checked frame that frame
 // tau - k copies), so labels are a "last resolved value" scan inside each of
 // the K residue classes; skipped frames copy their period's checked frame.
-// Two launches: per-(class, segment) summaries, then apply with carries.
+// Three launches, a warp per (class, 32-element segment) with the lanes on the
+// elements: per-segment summaries, per-class carries (a warp per class), apply.
 #include "common.cuh"
 #include "internal.h"
 
@@ -431,19 +432,50 @@ NS_DEV uint8_t hist_label(const LabArgs& A, int64_t tau) {
   return A.lab_hist ? A.lab_hist[tau % A.lh] : 0;
 }
 
+// One warp per (class r, segment s) of 32 checked elements, lane = element: the
+// element values are read in one instruction, and "copy the predecessor" (kNone)
+// is resolved by a warp scan of the last defined value.
+NS_DEV uint8_t warp_last_defined(uint8_t v, int lane, bool inclusive) {
+  // returns, per lane, the value of the nearest lane <= lane (inclusive) or < lane
+  // (exclusive) whose v != kNone, else kNone
+  const unsigned def = __ballot_sync(0xffffffffu, v != kNone);
+  const unsigned upto = inclusive ? (lane == 31 ? 0xffffffffu : ((1u << (lane + 1)) - 1)) : ((1u << lane) - 1);
+  const unsigned m = def & upto;
+  const int src = m ? 31 - __clz(m) : 0;
+  const uint8_t w = (uint8_t)__shfl_sync(0xffffffffu, (int)v, src);
+  return m ? w : kNone;
+}
+
 __global__ void labels_summary_kernel(LabArgs A) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (int64_t)A.K * A.nseg) return;
-  const int r = (int)(t / A.nseg), s = (int)(t % A.nseg);
-  uint8_t last = kNone;
-  for (int jj = 0; jj < kSeg; ++jj) {
-    const int64_t e = (int64_t)(s * kSeg + jj) * A.K + r;
-    if (e >= A.nc) break;
-    const int64_t f = (A.p_first + e) * A.t_skip - A.tau0;
-    const uint8_t v = checked_value(A, f);
-    if (v != kNone) last = v;
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wg >= (int64_t)A.K * A.nseg) return;
+  const int r = (int)(wg / A.nseg), s = (int)(wg % A.nseg);
+  const int64_t e = (int64_t)(s * kSeg + lane) * A.K + r;
+  uint8_t v = kNone;
+  if (e < A.nc) v = checked_value(A, (A.p_first + e) * A.t_skip - A.tau0);
+  const uint8_t last = warp_last_defined(v, 31, true);   // lane 31's inclusive view = the segment's last value
+  if (lane == 0) A.summary[wg] = last;
+}
+
+// carry into segment s of class r = the last defined summary of segments < s (one
+// warp per class walks its segments 32 at a time), else the class head's
+// predecessor from the label history; stored after the summaries.
+__global__ void labels_carry_kernel(LabArgs A) {
+  const int r = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= A.K) return;
+  uint8_t* carry = A.summary + (int64_t)A.K * A.nseg;
+  uint8_t run = kNone;
+  for (int s0 = 0; s0 < A.nseg; s0 += 32) {
+    const int s = s0 + lane;
+    const uint8_t v = s < A.nseg ? A.summary[(int64_t)r * A.nseg + s] : kNone;
+    uint8_t c = warp_last_defined(v, lane, false);    // segments s0 .. s-1
+    if (c == kNone) c = run;
+    if (s < A.nseg) carry[(int64_t)r * A.nseg + s] = c;
+    const uint8_t tail = warp_last_defined(v, 31, true);
+    if (tail != kNone) run = tail;
   }
-  A.summary[t] = last;
 }
 
 __global__ void labels_apply_kernel(LabArgs A) {
@@ -456,36 +488,36 @@ __global__ void labels_apply_kernel(LabArgs A) {
       if (A.route_out) A.route_out[tau - A.tau0] = NOSCOPE_R_SKIP;
     }
   }
-  if (t >= (int64_t)A.K * A.nseg) return;
-  const int r = (int)(t / A.nseg), s = (int)(t % A.nseg);
+  const int64_t wg = t >> 5;
+  const int lane = (int)(t & 31);
+  if (wg >= (int64_t)A.K * A.nseg) return;
+  const int r = (int)(wg / A.nseg), s = (int)(wg % A.nseg);
   uint8_t carry = kNone;
   if (A.mode == 1) {
-    for (int ss = s - 1; ss >= 0 && carry == kNone; --ss) carry = A.summary[(int64_t)r * A.nseg + ss];
+    carry = A.summary[(int64_t)A.K * A.nseg + wg];
     if (carry == kNone) {
       const int64_t p_pred = A.p_first + r - A.K;  // predecessor of the class head
       carry = p_pred >= 0 ? hist_label(A, p_pred * A.t_skip) : 0;
     }
   }
-  for (int jj = 0; jj < kSeg; ++jj) {
-    const int64_t e = (int64_t)(s * kSeg + jj) * A.K + r;
-    if (e >= A.nc) break;
-    const int64_t tau = (A.p_first + e) * A.t_skip;
-    const int64_t f = tau - A.tau0;
-    uint8_t v = checked_value(A, f);
-    const uint8_t d = A.disp[f];
-    if (v == kNone) v = carry;
-    carry = v;
-    A.labels[f] = v;
-    if (A.route_out)
-      A.route_out[f] = d == NOSCOPE_FIRED ? A.route_pf[f] : (uint8_t)NOSCOPE_R_SUPP;
-    for (int q = 1; q < A.t_skip && f + q < A.n; ++q) {
-      A.labels[f + q] = v;
-      if (A.route_out) A.route_out[f + q] = NOSCOPE_R_SKIP;
-    }
+  const int64_t e = (int64_t)(s * kSeg + lane) * A.K + r;
+  const bool in = e < A.nc;
+  const int64_t tau = (A.p_first + e) * A.t_skip;
+  const int64_t f = tau - A.tau0;
+  uint8_t v = in ? checked_value(A, f) : kNone;
+  const uint8_t prev = warp_last_defined(v, lane, true);   // suppressed elements copy the last defined one
+  if (!in) return;
+  v = prev != kNone ? prev : carry;
+  const uint8_t d = A.disp[f];
+  A.labels[f] = v;
+  if (A.route_out) A.route_out[f] = d == NOSCOPE_FIRED ? A.route_pf[f] : (uint8_t)NOSCOPE_R_SUPP;
+  for (int q = 1; q < A.t_skip && f + q < A.n; ++q) {
+    A.labels[f + q] = v;
+    if (A.route_out) A.route_out[f + q] = NOSCOPE_R_SKIP;
   }
 }
 
-size_t labels_ws_bytes(int64_t n) { return (size_t)(n / kSeg + 4096); }
+size_t labels_ws_bytes(int64_t n) { return (size_t)(2 * (n / kSeg + 4096)); }   // summaries + carries
 
 noscope_status launch_labels(const noscope_dd_config& cfg, int64_t tau0, int64_t n,
                              const uint8_t* disp, const uint8_t* route_pf,
@@ -513,12 +545,14 @@ noscope_status launch_labels(const noscope_dd_config& cfg, int64_t tau0, int64_t
   A.labels = labels;
   A.route_out = route_out;
   A.summary = reinterpret_cast<uint8_t*>(lws);
-  const int64_t threads = (int64_t)A.K * A.nseg;
-  const int blocks = (int)std::max<int64_t>(1, (threads + 255) / 256);
-  if (cfg.mode == 1 && threads > 0) {
+  const int64_t warps = (int64_t)A.K * A.nseg;
+  const int blocks = (int)std::max<int64_t>(1, (warps * 32 + 255) / 256);
+  if (cfg.mode == 1 && warps > 0) {
     labels_summary_kernel<<<blocks, 256, 0, st>>>(A);
     NS_LAUNCH_CHECK();
-    count_launch();
+    labels_carry_kernel<<<(int)((A.K * 32 + 255) / 256), 256, 0, st>>>(A);
+    NS_LAUNCH_CHECK();
+    count_launch(2);
   }
   labels_apply_kernel<<<blocks, 256, 0, st>>>(A);
   NS_LAUNCH_CHECK();

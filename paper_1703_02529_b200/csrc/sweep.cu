@@ -202,7 +202,7 @@ sweep_hist_kernel(const double* __restrict__ s, const float* __restrict__ z,
 }
 
 // Phase 2a: per-delta tables.
-// sweep_dsuffix_kernel: one thread per histogram column, one pass over d —
+// sweep_dsuffix_kernel: one warp per histogram column, one pass over d —
 //   G[d][b][y] = sum_{d' >= d} H2[d'][b][y]   (fired under delta_j  <=>  d > j)
 //   Pn[d][c]   = sum_{d' <= d} H1[d'][c]      (c = (a=1,y=0), (a=0,y=1); not fired <=> d <= j)
 struct Tables {
@@ -211,21 +211,37 @@ struct Tables {
 
 __global__ void sweep_dsuffix_kernel(const unsigned long long* __restrict__ hist, int nd, int m,
                                      unsigned long long* __restrict__ G, unsigned long long* __restrict__ Pn) {
+  // one warp per column; the d axis in slices of 32 (lane = d), scanned with shuffles
   HistLayout L(nd, m);
   const int cols = 2 * L.B;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
   if (c < cols) {
-    unsigned long long acc = 0;
-    for (int d = nd; d >= 0; --d) {
-      acc += hist[L.h2 + (size_t)d * cols + c];
-      G[(size_t)d * cols + c] = acc;
+    unsigned long long carry = 0;   // sum over the d already done (above this slice)
+    for (int top = nd; top >= 0; top -= 32) {
+      const int d = top - lane;     // lane 0 = largest d of the slice
+      unsigned long long v = d >= 0 ? hist[L.h2 + (size_t)d * cols + c] : 0ull;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {      // inclusive scan towards smaller d
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      if (d >= 0) G[(size_t)d * cols + c] = carry + v;
+      carry += __shfl_sync(0xffffffffu, v, 31);
     }
   } else if (c < cols + 2) {
     const int w = c == cols ? 1 * 2 + 0 : 0 * 2 + 1;   // (a, y) = (1, 0) FP, (0, 1) FN
-    unsigned long long acc = 0;
-    for (int d = 0; d <= nd; ++d) {
-      acc += hist[L.h1 + (size_t)d * 4 + w];
-      Pn[(size_t)d * 2 + (c - cols)] = acc;
+    unsigned long long carry = 0;
+    for (int d0 = 0; d0 <= nd; d0 += 32) {
+      const int d = d0 + lane;
+      unsigned long long v = d <= nd ? hist[L.h1 + (size_t)d * 4 + w] : 0ull;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      if (d <= nd) Pn[(size_t)d * 2 + (c - cols)] = carry + v;
+      carry += __shfl_sync(0xffffffffu, v, 31);
     }
   }
 }
@@ -351,13 +367,28 @@ __global__ void sweep_final_kernel(const EvalOut* blocks, int nblocks, Tables T,
                                    const double* delta, const float* u,
                                    unsigned long long t_mse, unsigned long long t_snn,
                                    unsigned long long t_full, noscope_sweep_best* out) {
-  if (threadIdx.x != 0) return;
+  // 256 threads stride over the block results, then a shared-memory tree (the
+  // key order is total, so the reduction order does not change the result)
+  __shared__ Cand sf[256], si[256];
   HistLayout L(nd, m);
   Cand bf{0, 0, 0, 0, 0, 0, 0}, bi{0, 0, 0, 0, 0, 0, 0};
-  for (int b = 0; b < nblocks; ++b) {
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
     if (cand_less(blocks[b].feas, bf)) bf = blocks[b].feas;
     if (cand_less(blocks[b].infeas, bi)) bi = blocks[b].infeas;
   }
+  sf[threadIdx.x] = bf;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      if (cand_less(sf[threadIdx.x + o], sf[threadIdx.x])) sf[threadIdx.x] = sf[threadIdx.x + o];
+      if (cand_less(si[threadIdx.x + o], si[threadIdx.x])) si[threadIdx.x] = si[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  bf = sf[0];
+  bi = si[0];
   const bool feasible = bf.valid != 0;
   const Cand c = feasible ? bf : bi;
   noscope_sweep_best r{};
@@ -447,7 +478,7 @@ noscope_status launch_sweep(int32_t phase, const double* s, const float* z, cons
     p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
     noscope_sweep_best* best_dev = reinterpret_cast<noscope_sweep_best*>(p);
     const int cols = 2 * L.B + 2;
-    sweep_dsuffix_kernel<<<(cols + 255) / 256, 256, 0, st>>>(hist, nd, m, G, Pn);
+    sweep_dsuffix_kernel<<<(cols * 32 + 255) / 256, 256, 0, st>>>(hist, nd, m, G, Pn);
     NS_LAUNCH_CHECK();
     const size_t smem = (size_t)(5 * L.B + 2) * 8;   // up to 164 KB at m = 2048
     NS_CUDA_TRY(cudaFuncSetAttribute(sweep_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -458,7 +489,7 @@ noscope_status launch_sweep(int32_t phase, const double* s, const float* z, cons
     sweep_eval_kernel<<<nblocks, 256, 0, st>>>(T, hist, nd, m, tm.t_mse_ps, tm.t_snn_ps,
                                                tm.t_full_ps, fp_limit, fn_limit, bo);
     NS_LAUNCH_CHECK();
-    sweep_final_kernel<<<1, 32, 0, st>>>(bo, nblocks, T, hist, nd, m, delta, u, tm.t_mse_ps,
+    sweep_final_kernel<<<1, 256, 0, st>>>(bo, nblocks, T, hist, nd, m, delta, u, tm.t_mse_ps,
                                          tm.t_snn_ps, tm.t_full_ps, best_dev);
     NS_LAUNCH_CHECK();
     if (best_host) {
