@@ -95,10 +95,22 @@ def init_dist(world, device):
     """One process per GPU over NCCL (NCCL_DEBUG=INFO so the init lines show nranks)."""
     import torch.distributed as dist
     if world > 1 or "WORLD_SIZE" in os.environ:   # under torchrun: NCCL even for one rank
+        import torch
         os.environ.setdefault("NCCL_DEBUG", "INFO")
-        # NCCL logs to stdout by default: keep stdout for the one JSON line
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
-        dist.init_process_group("nccl", device_id=device)
+        # NCCL prints its banner and logs to stdout: create the communicator (one warm-up
+        # all-reduce) with fd 1 pointed at stderr, so stdout carries only the JSON line
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=device)
+            t = torch.ones(1, device=device)
+            dist.all_reduce(t)
+            torch.cuda.synchronize()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
 
 
 # cost-model timings for the in-step sweep (ps per frame): T_MSE and T_SNN as measured

@@ -685,7 +685,11 @@ __global__ void dd_state_update_kernel(const uint8_t* small, int64_t small_pitch
     const int64_t tau = tau0 + f;
     const uint8_t* src = small + f * small_pitch;
     uint8_t* dst = ring + (tau % k) * ring_pitch;
-    for (int t = threadIdx.x; t < small_bytes; t += blockDim.x) dst[t] = src[t];
+    // both pitches are multiples of 16 (16-byte vectors; the tail of the last vector
+    // is the pitch padding on both sides)
+    const int nv = (small_bytes + 15) / 16;
+    for (int t = threadIdx.x; t < nv; t += blockDim.x)
+      reinterpret_cast<uint4*>(dst)[t] = reinterpret_cast<const uint4*>(src)[t];
   }
   if (labels && blockIdx.x == 0) {
     const int64_t lf = n - lh > 0 ? n - lh : 0;
