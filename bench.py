@@ -96,7 +96,10 @@ def init_dist(world, device):
     import torch.distributed as dist
     if world > 1 or "WORLD_SIZE" in os.environ:   # under torchrun: NCCL even for one rank
         import torch
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        # torch pre-sets NCCL_DEBUG=VERSION; INFO (init subsystem) so the log shows nranks
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("", "VERSION", "WARN"):
+            os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         # NCCL prints its banner and logs to stdout: create the communicator (one warm-up
         # all-reduce) with fd 1 pointed at stderr, so stdout carries only the JSON line
         sys.stdout.flush()
