@@ -91,6 +91,27 @@ def maybe_self_launch(args):
     sys.exit(subprocess.call(cmd))
 
 
+class _StdoutToStderr:
+    """fd 1 -> stderr while NCCL creates / destroys communicators (it logs to stdout)."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *a):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
+def destroy_dist():
+    import torch.distributed as dist
+    if dist.is_initialized():
+        with _StdoutToStderr():
+            dist.destroy_process_group()
+
+
 def init_dist(world, device):
     """One process per GPU over NCCL (NCCL_DEBUG=INFO so the init lines show nranks)."""
     import torch.distributed as dist
@@ -100,20 +121,14 @@ def init_dist(world, device):
         if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("", "VERSION", "WARN"):
             os.environ["NCCL_DEBUG"] = "INFO"
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         # NCCL prints its banner and logs to stdout: create the communicator (one warm-up
         # all-reduce) with fd 1 pointed at stderr, so stdout carries only the JSON line
-        sys.stdout.flush()
-        saved = os.dup(1)
-        os.dup2(2, 1)
-        try:
+        with _StdoutToStderr():
             dist.init_process_group("nccl", device_id=device)
             t = torch.ones(1, device=device)
             dist.all_reduce(t)
             torch.cuda.synchronize()
-        finally:
-            sys.stdout.flush()
-            os.dup2(saved, 1)
-            os.close(saved)
 
 
 # cost-model timings for the in-step sweep (ps per frame): T_MSE and T_SNN as measured
@@ -398,8 +413,7 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline(args, S)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if dist.is_initialized():
-        dist.destroy_process_group()
+    destroy_dist()
 
 
 def run_x(args):
@@ -516,8 +530,7 @@ def run_x(args):
                 else None,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
-    if dist.is_initialized():
-        dist.destroy_process_group()
+    destroy_dist()
 
 
 def run_tskip(S, device, t_skip, steps=5):
