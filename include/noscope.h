@@ -285,7 +285,12 @@ noscope_status noscope_compact_fired(uint8_t* disposition, int64_t n, int64_t se
  *  codes (nullable); logits_out: device fp32 [n_frames] (nullable; written
  *  for fired frames only); scores_out: device fp64 [n_frames] (nullable).
  *  stream_state is required (init once per unit).  stats_host (nullable)
- *  triggers one synchronisation to copy counts back.                        */
+ *  triggers one synchronisation to copy counts back.  n_frames = 0 is a no-op
+ *  (frames / labels_out may then be null; stats are all zero).
+ *  Errors: NOSCOPE_INVALID_ARGUMENT for null required buffers, c_low > c_high,
+ *  unaligned buffers; NOSCOPE_SHAPE as noscope_diff_detect, or a CNN input size
+ *  that differs from the DD's out_w x out_h; NOSCOPE_WORKSPACE_TOO_SMALL;
+ *  NOSCOPE_LABELLER if the callback returns nonzero.                         */
 noscope_status noscope_cascade_run(const noscope_dd_config* dd, const noscope_cnn_arch* arch,
                                    const noscope_cnn_weights* weights, noscope_route route,
                                    const uint8_t* frames, noscope_frames_desc desc,

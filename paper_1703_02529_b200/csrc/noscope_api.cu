@@ -312,8 +312,8 @@ static noscope_status cascade_impl(const noscope_dd_config* dd, const noscope_cn
   if ((s = validate_arch(arch, weights)) != NOSCOPE_OK) return s;
   if (dd->out_w != arch->in_w || dd->out_h != arch->in_h) return NOSCOPE_SHAPE;
   if (!(route.lo_logit <= route.hi_logit)) return NOSCOPE_INVALID_ARGUMENT;
-  if (!frames || !labels_out || !state || !labeller || !ws || n < 0 || seg_offset < 0)
-    return NOSCOPE_INVALID_ARGUMENT;
+  if ((n > 0 && (!frames || !labels_out)) || !state || !labeller || !ws || n < 0 || seg_offset < 0)
+    return NOSCOPE_INVALID_ARGUMENT;   // frames / labels may be null for an empty chunk
   if (!aligned16(frames) || !aligned16(ws) || !aligned16(state)) return NOSCOPE_INVALID_ARGUMENT;
   CascadeWs w = cascade_ws(dd, arch, n);
   if (ws_bytes < w.total) return NOSCOPE_WORKSPACE_TOO_SMALL;
