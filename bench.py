@@ -708,6 +708,14 @@ def run_extras(device, timing=(1000, 20000, 12_500_000_000)):
         grid[a.name] = {"ms": round(ms, 3), "fps": round(nG / ms * 1e3, 1),
                         "tflops": round(fl / ms / 1e9, 1), "frac_of_bf16_peak": round(fl / ms / 1e9 / bf16, 4)}
         del ws
+    # ncu tensor-pipe activity of the same calls (captured once per kernel change by
+    # tools/gpu_cnn_tensor.sh; a profiler cannot run inside the timed bench)
+    tpath = os.path.join(ROOT, "profiles", "r02", "cnn_tensor_pipe.json")
+    if os.path.exists(tpath):
+        tp = json.load(open(tpath))["archs"]
+        for name, rec in grid.items():
+            if name in tp:
+                rec["ncu_tensor_pipe_active_pct"] = tp[name]["tensor_pipe_active_pct"]
     out["cnn_grid_65536"] = grid
     # the paper's remaining search configurations (C = 16 and D = 64 / 256)
     extra = {}
