@@ -264,21 +264,50 @@ __global__ void sweep_prefix_kernel(const unsigned long long* __restrict__ G,
     fh1[b] = g[2 * b + 1];
   }
   __syncthreads();
-  if (tid == 0) {
-    S0[L.B] = 0;
-    SA[L.B] = 0;
-    for (int b = L.B - 1; b >= 0; --b) {
-      S0[b] = S0[b + 1] + fh0[b];
-      SA[b] = SA[b + 1] + fh0[b] + fh1[b];
+  // suffix sums of fh0 and fh0 + fh1 and the prefix sum of fh1 over b, by warp 0:
+  // 32 lanes per slice with shuffle scans, a carry between slices (B <= 4097)
+  if (tid < 32) {
+    const int lane = tid;
+    unsigned long long c0 = 0, cA = 0;
+    for (int top = L.B - 1; top >= 0; top -= 32) {
+      const int b = top - lane;
+      unsigned long long v0 = b >= 0 ? fh0[b] : 0ull, vA = b >= 0 ? fh0[b] + fh1[b] : 0ull;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y0 = __shfl_up_sync(0xffffffffu, v0, o);
+        const unsigned long long yA = __shfl_up_sync(0xffffffffu, vA, o);
+        if (lane >= o) {
+          v0 += y0;
+          vA += yA;
+        }
+      }
+      if (b >= 0) {
+        S0[b] = c0 + v0;
+        SA[b] = cA + vA;
+      }
+      c0 += __shfl_sync(0xffffffffu, v0, 31);
+      cA += __shfl_sync(0xffffffffu, vA, 31);
     }
-    unsigned long long p = 0;
-    for (int b = 0; b < L.B; ++b) {
-      p += fh1[b];
-      P1[b] = p;
+    unsigned long long c1 = 0;
+    for (int b0 = 0; b0 < L.B; b0 += 32) {
+      const int b = b0 + lane;
+      unsigned long long v1 = b < L.B ? fh1[b] : 0ull;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y1 = __shfl_up_sync(0xffffffffu, v1, o);
+        if (lane >= o) v1 += y1;
+      }
+      if (b < L.B) P1[b] = c1 + v1;
+      c1 += __shfl_sync(0xffffffffu, v1, 31);
     }
-    T.F[j] = SA[0];
-    T.FPnf[j] = Pn[(size_t)j * 2 + 0];
-    T.FNnf[j] = Pn[(size_t)j * 2 + 1];
+    __syncwarp();   // SA[0] was written by another lane
+    if (lane == 0) {
+      S0[L.B] = 0;
+      SA[L.B] = 0;
+      T.F[j] = SA[0];
+      T.FPnf[j] = Pn[(size_t)j * 2 + 0];
+      T.FNnf[j] = Pn[(size_t)j * 2 + 1];
+    }
   }
   __syncthreads();
   for (int t = tid; t < m; t += blockDim.x) {
@@ -310,25 +339,36 @@ struct EvalOut {
   Cand feas, infeas;
 };
 
+// One CTA per (j, slice of 256 l values): the j row of FPf and GT (m entries each)
+// staged in shared memory, each thread scans h = l .. m-1 from there.
 __global__ void __launch_bounds__(256)
 sweep_eval_kernel(Tables T, const unsigned long long* hist, int nd, int m,
                   unsigned long long t_mse, unsigned long long t_snn,
                   unsigned long long t_full, unsigned long long fp_lim,
                   unsigned long long fn_lim, EvalOut* block_out) {
+  extern __shared__ __align__(16) uint8_t esm[];
+  unsigned long long* fpf = reinterpret_cast<unsigned long long*>(esm);   // [m]
+  unsigned long long* gt = fpf + m;                                        // [m]
   __shared__ Cand sf[256], si[256];
   HistLayout L(nd, m);
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lslices = (m + 255) / 256;
+  const int j = blockIdx.x / lslices, l = (blockIdx.x % lslices) * 256 + threadIdx.x;
+  for (int h = threadIdx.x; h < m; h += blockDim.x) {
+    fpf[h] = T.FPf[(size_t)j * m + h];
+    gt[h] = T.GT[(size_t)j * m + h];
+  }
+  __syncthreads();
   Cand bf{0, 0, 0, 0, 0, 0, 0}, bi{0, 0, 0, 0, 0, 0, 0};
-  if (t < (int64_t)nd * m) {
-    const int j = (int)(t / m), l = (int)(t % m);
+  if (l < m) {
     const unsigned long long checked = hist[L.tail];
     const unsigned long long F = T.F[j];
+    const unsigned long long fpnf = T.FPnf[j];
     const unsigned long long fn = T.FNnf[j] + T.FNf[(size_t)j * m + l];
     const unsigned long long ge = T.GE[(size_t)j * m + l];
     const unsigned long long base_cost = checked * t_mse + F * t_snn;
     for (int h = l; h < m; ++h) {
-      const unsigned long long fp = T.FPnf[j] + T.FPf[(size_t)j * m + h];
-      const unsigned long long U = ge - T.GT[(size_t)j * m + h];
+      const unsigned long long fp = fpnf + fpf[h];
+      const unsigned long long U = ge - gt[h];
       const unsigned long long cost = base_cost + U * t_full;
       Cand c;
       c.j = j;
@@ -414,7 +454,7 @@ __global__ void sweep_final_kernel(const EvalOut* blocks, int nblocks, Tables T,
 size_t sweep_ws_bytes(int32_t nd, int32_t m) {
   size_t tabs = (size_t)nd * 3 + (size_t)nd * m * 4;
   size_t suffix = (size_t)(nd + 1) * (2 * (2 * (size_t)m + 1)) + (size_t)(nd + 1) * 2;
-  size_t blocks = ((size_t)nd * m + 255) / 256;
+  size_t blocks = (size_t)nd * ((m + 255) / 256);
   return 256 + (tabs + suffix) * 8 + blocks * sizeof(EvalOut) + sizeof(noscope_sweep_best) + 256;
 }
 
@@ -472,7 +512,7 @@ noscope_status launch_sweep(int32_t phase, const double* s, const float* z, cons
     }
     unsigned long long* G = take((size_t)(nd + 1) * 2 * L.B);
     unsigned long long* Pn = take((size_t)(nd + 1) * 2);
-    const int nblocks = (int)(((int64_t)nd * m + 255) / 256);
+    const int nblocks = nd * ((m + 255) / 256);   // one CTA per (j, 256-wide slice of l)
     EvalOut* bo = reinterpret_cast<EvalOut*>(p);
     p += (size_t)nblocks * sizeof(EvalOut);
     p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
@@ -486,8 +526,10 @@ noscope_status launch_sweep(int32_t phase, const double* s, const float* z, cons
     sweep_prefix_kernel<<<nd, 256, smem, st>>>(G, Pn, nd, m, T);
     NS_LAUNCH_CHECK();
     count_launch(4);
-    sweep_eval_kernel<<<nblocks, 256, 0, st>>>(T, hist, nd, m, tm.t_mse_ps, tm.t_snn_ps,
-                                               tm.t_full_ps, fp_limit, fn_limit, bo);
+    NS_CUDA_TRY(cudaFuncSetAttribute(sweep_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)((size_t)m * 16)));
+    sweep_eval_kernel<<<nblocks, 256, (size_t)m * 16, st>>>(T, hist, nd, m, tm.t_mse_ps, tm.t_snn_ps,
+                                                             tm.t_full_ps, fp_limit, fn_limit, bo);
     NS_LAUNCH_CHECK();
     sweep_final_kernel<<<1, 256, 0, st>>>(bo, nblocks, T, hist, nd, m, delta, u, tm.t_mse_ps,
                                          tm.t_snn_ps, tm.t_full_ps, best_dev);
