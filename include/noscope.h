@@ -290,7 +290,15 @@ noscope_status noscope_compact_fired(uint8_t* disposition, int64_t n, int64_t se
  *  Errors: NOSCOPE_INVALID_ARGUMENT for null required buffers, c_low > c_high,
  *  unaligned buffers; NOSCOPE_SHAPE as noscope_diff_detect, or a CNN input size
  *  that differs from the DD's out_w x out_h; NOSCOPE_WORKSPACE_TOO_SMALL;
- *  NOSCOPE_LABELLER if the callback returns nonzero.                         */
+ *  NOSCOPE_LABELLER if the callback returns nonzero.
+ *  Schedule: serial (DD, compaction, CNN, routing, labels).  NOSCOPE_OVERLAP=1 in
+ *  the environment (read per call, also by noscope_workspace_bytes, which then
+ *  sizes for it) selects an overlapped schedule for chunks of >= 8,192 frames with
+ *  an L = 2, C in {16, 32} CNN on source frames larger than the output: the conv
+ *  kernel runs on a few SMs beside the DD, consuming fired frames as the DD
+ *  publishes them.  Results are bit-identical; it is not faster on B200
+ *  (DESIGN.md §9), so it is off by default.  It falls back to the serial schedule
+ *  under stream capture or when the workspace was sized without it.           */
 noscope_status noscope_cascade_run(const noscope_dd_config* dd, const noscope_cnn_arch* arch,
                                    const noscope_cnn_weights* weights, noscope_route route,
                                    const uint8_t* frames, noscope_frames_desc desc,

@@ -13,6 +13,8 @@
 //   + FC2.
 // FC: features (h, w, c) in the canonical A layout [tile][K/8][128][8] ->
 //   tcgen05 GEMM with N = dense, epilogue bias+ReLU+bf16, FC2 dot + bias.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -54,6 +56,8 @@ struct FcArgs {
   int ksplit;            // K split across CTAs (fixed per K: results do not depend on n)
   float* part;           // [tiles][ksplit][128][D] fp32 partial sums (ksplit > 1)
   unsigned* counters;    // [tiles] arrival counters, zero between uses
+  const int32_t* fq;     // queue mode: row p is queue slot p, frame fq[p] ...
+  const int32_t* pos_pf; // ... whose logit goes to logits[pos_pf[frame]] (null: index mode)
 };
 constexpr int kFcKChunk = 64;
 
@@ -190,7 +194,7 @@ fc_kernel(FcArgs A) {
   }
   z += A.b2[0];
   const int64_t row = tile * 128 + tid;
-  if (row < cnt) A.logits[A.chunk_base + row] = z;
+  if (row < cnt) A.logits[A.fq ? (int64_t)A.pos_pf[A.fq[row]] : A.chunk_base + row] = z;
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc_rt(tmem, A.tmem_cols);
@@ -213,14 +217,16 @@ struct CnnPlan {
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-static bool make_plan(const noscope_cnn_arch& a, int64_t n_max, CnnPlan* P) {
+// whole: one chunk of n_max frames (queue mode: features of every queue slot)
+static bool make_plan(const noscope_cnn_arch& a, int64_t n_max, CnnPlan* P, bool whole = false) {
   CnnPlan p{};
   p.L = a.n_conv;
   p.C = a.base_filters;
   p.D = a.dense;
   p.fused = p.C == 32 || p.C == 16;
   p.first_g = p.fused ? 2 : 1;
-  p.chunk = std::min<int64_t>(kCnnChunk, std::max<int64_t>(128, (n_max + 127) / 128 * 128));
+  p.chunk = std::max<int64_t>(128, (n_max + 127) / 128 * 128);
+  if (!whole) p.chunk = std::min<int64_t>(kCnnChunk, p.chunk);
   size_t off = 256;  // status words etc. live before the CNN region (caller offset)
   p.w1_off = off;
   off = align_up(off + (size_t)p.C * 32 * 2, 256);
@@ -335,6 +341,84 @@ __global__ void pack_multi_kernel(PackJobs J) {
 }
 
 
+static noscope_status pack_weights(const CnnPlan& P, const noscope_cnn_weights& w, uint8_t* ws,
+                                   cudaStream_t st) {
+  PackJobs J{};
+  auto job = [&](const uint16_t* wsrc, int rows, int Kreal, int Kpad, int pn, uint8_t* out) {
+    J.j[J.n++] = PackJob{wsrc, reinterpret_cast<uint16_t*>(out), rows, Kreal, Kpad, pn,
+                         (int64_t)rows * Kpad};
+  };
+  job(w.conv_w[0], P.C, 27, 32, P.C, ws + P.w1_off);  // + bias in K 27/28
+  if (P.fused) job(w.conv_w[1], 2 * P.C, 9 * P.C, 9 * P.C, 2 * P.C, ws + P.w2_off);
+  job(w.fc1_w, P.D, P.K, P.K, P.D, ws + P.fc_off);
+  J.bias1 = w.conv_b[0];
+  int64_t total = 0;
+  for (int q = 0; q < J.n; ++q) total += J.j[q].total;
+  const int grid = (int)std::min<int64_t>((total + 255) / 256, 4 * kNumSMs);
+  pack_multi_kernel<<<grid, 256, 0, st>>>(J);
+  NS_LAUNCH_CHECK();
+  count_launch();
+  for (int l = P.first_g; l < P.L; ++l) {
+    noscope_status s = pack_convg(w.conv_w[l], P.g[l], ws + P.gw_off[l], st);
+    if (s != NOSCOPE_OK) return s;
+  }
+  return NOSCOPE_OK;
+}
+
+static FusedArgs fused_args(const CnnPlan& P, const noscope_cnn_arch& a, const noscope_cnn_weights& w,
+                            const uint8_t* small, int64_t small_pitch, uint8_t* ws) {
+  FusedArgs fa{};
+  fa.C1 = P.C;
+  fa.small = small;
+  fa.small_pitch = small_pitch;
+  fa.w1 = ws + P.w1_off;
+  fa.w2 = P.fused ? ws + P.w2_off : nullptr;
+  fa.b1 = w.conv_b[0];
+  fa.b2 = P.fused ? w.conv_b[1] : nullptr;
+  fa.mean[0] = a.chan_mean[0];
+  fa.mean[1] = a.chan_mean[1];
+  fa.mean[2] = a.chan_mean[2];
+  fa.to_features = (P.fused && P.L == 2) ? 1 : 0;
+  fa.out = fa.to_features ? ws + P.feat_off : ws + P.in_off[P.first_g];
+  fa.K_feat = P.K;
+  fa.out_rows = fa.to_features ? 0 : P.g[P.first_g].R;
+  return fa;
+}
+
+static noscope_status launch_fc(const CnnPlan& P, const noscope_cnn_weights& w, uint8_t* ws,
+                                const int64_t* n_dev, int64_t n_max, int64_t base, int64_t len,
+                                float* logits, const int32_t* fq, const int32_t* pos_pf,
+                                cudaStream_t st) {
+  static DeviceOnce attr;
+  if (attr.first())
+    NS_CUDA_TRY(cudaFuncSetAttribute(fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  FcArgs f{};
+  f.feat = ws + P.feat_off;
+  f.K = P.K;
+  f.D = P.D;
+  f.wpack = ws + P.fc_off;
+  f.b1 = w.fc1_b;
+  f.w2 = w.fc2_w;
+  f.b2 = w.fc2_b;
+  f.logits = logits;
+  f.n_dev = n_dev;
+  f.n_max = n_max;
+  f.chunk_base = base;
+  f.chunk_len = len;
+  f.tmem_cols = tmem_cols_host(2 * P.D);
+  f.ksplit = fc_ksplit(P.K);
+  f.part = reinterpret_cast<float*>(ws + P.part_off);
+  f.counters = reinterpret_cast<unsigned*>(ws + P.cnt_off);
+  f.fq = fq;
+  f.pos_pf = pos_pf;
+  const size_t fsm = (size_t)kBStages * (128 * kFcKChunk * 2 + P.D * kFcKChunk * 2) +
+                     (2 * kBStages + 1) * 8 + 32 + 1024;
+  fc_kernel<<<(int)((len + 127) / 128) * f.ksplit, kCnnThreads, fsm, st>>>(f);
+  NS_LAUNCH_CHECK();
+  count_launch();
+  return NOSCOPE_OK;
+}
+
 noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& w,
                           const uint8_t* small, int64_t small_pitch, const int32_t* idx,
                           const int64_t* n_dev, int64_t n_max, float* logits, void* ws_v,
@@ -344,57 +428,19 @@ noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& 
   if (!make_plan(a, n_max, &P)) return NOSCOPE_INVALID_ARGUMENT;
   if (n_max <= 0) return NOSCOPE_OK;
   uint8_t* ws = reinterpret_cast<uint8_t*>(ws_v);
-  // pack weights into the canonical UMMA layouts
-  {
-    PackJobs J{};
-    auto job = [&](const uint16_t* wsrc, int rows, int Kreal, int Kpad, int pn, uint8_t* out) {
-      J.j[J.n++] = PackJob{wsrc, reinterpret_cast<uint16_t*>(out), rows, Kreal, Kpad, pn,
-                           (int64_t)rows * Kpad};
-    };
-    job(w.conv_w[0], P.C, 27, 32, P.C, ws + P.w1_off);  // + bias in K 27/28
-    if (P.fused) job(w.conv_w[1], 2 * P.C, 9 * P.C, 9 * P.C, 2 * P.C, ws + P.w2_off);
-    job(w.fc1_w, P.D, P.K, P.K, P.D, ws + P.fc_off);
-    J.bias1 = w.conv_b[0];
-    int64_t total = 0;
-    for (int q = 0; q < J.n; ++q) total += J.j[q].total;
-    const int grid = (int)std::min<int64_t>((total + 255) / 256, 4 * kNumSMs);
-    pack_multi_kernel<<<grid, 256, 0, st>>>(J);
-    NS_LAUNCH_CHECK();
-    count_launch();
-  }
-  for (int l = P.first_g; l < P.L; ++l) {
-    noscope_status s = pack_convg(w.conv_w[l], P.g[l], ws + P.gw_off[l], st);
-    if (s != NOSCOPE_OK) return s;
-  }
-
-  static DeviceOnce attr;
-  if (attr.first())
-    NS_CUDA_TRY(cudaFuncSetAttribute(fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  noscope_status s = pack_weights(P, w, ws, st);   // canonical UMMA layouts
+  if (s != NOSCOPE_OK) return s;
   if (fc_ksplit(P.K) > 1)   // FC split-K arrival counters start at zero (reset by their last CTA)
     NS_CUDA_TRY(cudaMemsetAsync(ws + P.cnt_off, 0, (size_t)(P.chunk / 128) * 4, st));
   for (int64_t base = 0; base < n_max; base += P.chunk) {
     const int64_t len = std::min<int64_t>(P.chunk, n_max - base);
-    FusedArgs fa{};
-    fa.C1 = P.C;
-    fa.small = small;
-    fa.small_pitch = small_pitch;
+    FusedArgs fa = fused_args(P, a, w, small, small_pitch, ws);
     fa.idx = idx;
     fa.n_dev = n_dev;
     fa.n_max = n_max;
     fa.chunk_base = base;
     fa.chunk_len = len;
-    fa.w1 = ws + P.w1_off;
-    fa.w2 = P.fused ? ws + P.w2_off : nullptr;
-    fa.b1 = w.conv_b[0];
-    fa.b2 = P.fused ? w.conv_b[1] : nullptr;
-    fa.mean[0] = a.chan_mean[0];
-    fa.mean[1] = a.chan_mean[1];
-    fa.mean[2] = a.chan_mean[2];
-    fa.to_features = (P.fused && P.L == 2) ? 1 : 0;
-    fa.out = fa.to_features ? ws + P.feat_off : ws + P.in_off[P.first_g];
-    fa.K_feat = P.K;
-    fa.out_rows = fa.to_features ? 0 : P.g[P.first_g].R;
-    noscope_status s = launch_conv12_fused(fa, (int)std::min<int64_t>(len, kNumSMs), st);
+    s = launch_conv12_fused(fa, (int)std::min<int64_t>(len, kNumSMs), st);
     if (s != NOSCOPE_OK) return s;
     for (int l = P.first_g; l < P.L; ++l) {
       ConvGArgs c{};
@@ -410,33 +456,62 @@ noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& 
       c.n_max = n_max;
       c.chunk_base = base;
       c.chunk_len = len;
-      noscope_status s = c.g.tiled ? launch_convt(c, st) : launch_convg(c, st);
+      s = c.g.tiled ? launch_convt(c, st) : launch_convg(c, st);
       if (s != NOSCOPE_OK) return s;
     }
-    FcArgs f{};
-    f.feat = ws + P.feat_off;
-    f.K = P.K;
-    f.D = P.D;
-    f.wpack = ws + P.fc_off;
-    f.b1 = w.fc1_b;
-    f.w2 = w.fc2_w;
-    f.b2 = w.fc2_b;
-    f.logits = logits;
-    f.n_dev = n_dev;
-    f.n_max = n_max;
-    f.chunk_base = base;
-    f.chunk_len = len;
-    f.tmem_cols = tmem_cols_host(2 * P.D);
-    f.ksplit = fc_ksplit(P.K);
-    f.part = reinterpret_cast<float*>(ws + P.part_off);
-    f.counters = reinterpret_cast<unsigned*>(ws + P.cnt_off);
-    const size_t fsm = (size_t)kBStages * (128 * kFcKChunk * 2 + P.D * kFcKChunk * 2) +
-                       (2 * kBStages + 1) * 8 + 32 + 1024;
-    fc_kernel<<<(int)((len + 127) / 128) * f.ksplit, kCnnThreads, fsm, st>>>(f);
-    NS_LAUNCH_CHECK();
-    count_launch();
+    s = launch_fc(P, w, ws, n_dev, n_max, base, len, logits, nullptr, nullptr, st);
+    if (s != NOSCOPE_OK) return s;
   }
   return NOSCOPE_OK;
+}
+
+// ----------------------------------------------------------- queue mode
+bool cnn_queue_supported(const noscope_cnn_arch& a) {
+  return cnn_arch_supported(a) && (a.base_filters == 32 || a.base_filters == 16) && a.n_conv == 2;
+}
+
+size_t cnn_queue_ws_bytes(const noscope_cnn_arch& a, int64_t n_max) {
+  CnnPlan p;
+  if (!cnn_queue_supported(a) || !make_plan(a, n_max, &p, true)) return 0;
+  return p.total;
+}
+
+noscope_status cnn_queue_pack(const noscope_cnn_arch& a, const noscope_cnn_weights& w,
+                              int64_t n_max, void* ws_v, cudaStream_t st) {
+  CnnPlan P;
+  if (!cnn_queue_supported(a) || !make_plan(a, n_max, &P, true)) return NOSCOPE_INVALID_ARGUMENT;
+  uint8_t* ws = reinterpret_cast<uint8_t*>(ws_v);
+  noscope_status s = pack_weights(P, w, ws, st);
+  if (s != NOSCOPE_OK) return s;
+  if (fc_ksplit(P.K) > 1)
+    NS_CUDA_TRY(cudaMemsetAsync(ws + P.cnt_off, 0, (size_t)(P.chunk / 128) * 4, st));
+  return NOSCOPE_OK;
+}
+
+noscope_status cnn_queue_conv(const noscope_cnn_arch& a, const noscope_cnn_weights& w,
+                              const uint8_t* small, int64_t small_pitch, const FiredQueue& fq,
+                              int qmode, int grid, int64_t n_max, void* ws_v, cudaStream_t st) {
+  CnnPlan P;
+  if (!cnn_queue_supported(a) || !make_plan(a, n_max, &P, true)) return NOSCOPE_INVALID_ARGUMENT;
+  if (grid <= 0) return NOSCOPE_OK;
+  uint8_t* ws = reinterpret_cast<uint8_t*>(ws_v);
+  FusedArgs fa = fused_args(P, a, w, small, small_pitch, ws);
+  fa.n_max = n_max;
+  fa.chunk_len = P.chunk;
+  fa.qmode = qmode;
+  fa.fq = fq;
+  return launch_conv12_fused(fa, grid, st);
+}
+
+noscope_status cnn_queue_fc(const noscope_cnn_arch& a, const noscope_cnn_weights& w,
+                            const FiredQueue& fq, int64_t n_max, const int32_t* pos_pf,
+                            float* logits, void* ws_v, cudaStream_t st) {
+  CnnPlan P;
+  if (!cnn_queue_supported(a) || !make_plan(a, n_max, &P, true)) return NOSCOPE_INVALID_ARGUMENT;
+  if (n_max <= 0) return NOSCOPE_OK;
+  return launch_fc(P, w, reinterpret_cast<uint8_t*>(ws_v),
+                   reinterpret_cast<const int64_t*>(fq.count), n_max, 0, n_max, logits, fq.q,
+                   pos_pf, st);
 }
 
 }  // namespace ns

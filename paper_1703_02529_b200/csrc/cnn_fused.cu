@@ -38,6 +38,16 @@
 // MMAs on one accumulator serialise on the D read-modify-write (measured in
 // tools/umma_bench.cu), so both issuers interleave the K steps of two tiles with
 // independent accumulators (4 TMEM buffers each).
+//
+// Queue mode (A.qmode != 0, conv2-fused variants writing FC features; the
+// overlapped cascade): the producer claims frames one at a time from the
+// FiredQueue dd_kernel is filling (fq_claim below) and writes the claimed slot into
+// a shared-memory ring (pos[it % 16]).  When it runs out it writes -1 there; every
+// role reads pos[it % 16] after the first barrier wait of frame `it` and, on -1,
+// forwards the stop along its usual hand-off (after the same "empty" wait it would
+// do before producing, so no mbarrier phase is completed twice) and leaves.  The
+// features of slot p go to FC row p; a frame's arithmetic does not depend on which
+// CTA or slot it lands in, so the logits are bit-identical to index mode.
 #include "common.cuh"
 #include "internal.h"
 
@@ -98,7 +108,9 @@ constexpr int oLut = oX + 2 * kXPlane * 8;               // bf16 LUT [3][256]
 // B = [bf16(b), bf16(b - bf16(b))] per output channel (~2^-17 relative)
 constexpr int oOnes = oLut + 3 * 256 * 2;                // [2][128][8] bf16
 constexpr int oB2b = oOnes + 2 * 128 * 16;               // [2][64][8] bf16
-constexpr int oBar = oB2b + 2 * C2 * 16;
+constexpr int oPos = oB2b + 2 * C2 * 16;                 // queue mode: slot of frame it (ring)
+constexpr int kPosRing = 16;     // > the frames between the producer and epilogue 2 (<= 7)
+constexpr int oBar = oPos + kPosRing * 8;
 constexpr int kNumBars = 2 + 2 + 2 * kA1Stages + 2 * kNG1 + 2 + 2 + 2 * kNB2 + 1;
 constexpr int kSmem = oBar + kNumBars * 8 + 16;
 }  // namespace fz
@@ -128,6 +140,38 @@ NS_DEV void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
 }
 NS_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// Queue-mode claim of the next slot (producer thread), or -1 when there is none.
+//   qmode 2 (tail, after dd_kernel in stream order): count is final;
+//   qmode 1 (side, concurrent with dd_kernel): claim a reserved slot (claim < count)
+//   by CAS while dd_kernel runs; stop once every dd_kernel CTA is done (the tail
+//   launch takes the rest) or after a 30 s guard (the tail still covers every slot).
+NS_DEV int64_t fq_claim(const FusedArgs& A, uint64_t t_start) {
+  const FiredQueue& Q = A.fq;
+  if (A.qmode == 2) {
+    const unsigned long long p = atomicAdd(Q.claim, 1ull);
+    return p < ld_acquire_u64(Q.count) ? (int64_t)p : -1;
+  }
+  for (;;) {
+    if (ld_acquire_u32(Q.done) >= (unsigned)Q.producers) return -1;
+    const unsigned long long c = ld_relaxed_u64(Q.claim);
+    if (c < ld_relaxed_u64(Q.count)) {
+      if (atomicCAS(Q.claim, c, c + 1ull) == c) return (int64_t)c;
+      continue;
+    }
+    if (globaltimer_ns() - t_start > 30000000000ull) return -1;
+    __nanosleep(256);
+  }
+}
+// The frame index of a claimed slot (published by dd_kernel's release store right
+// after the reservation), ordered before the bulk copy that reads the frame.
+NS_DEV int64_t fq_frame(const FusedArgs& A, int64_t p) {
+  int32_t f;
+  while ((f = ld_acquire_s32(A.fq.q + p)) < 0) {
+  }
+  fence_proxy_async_global();
+  return f;
+}
+
 // kHalves = conv1 channels / 32 (each half is one N = 32 MMA on the shared A
 // tile); kConv2 = conv2 fused (base_filters = 32) or the conv1 map written to
 // HBM in the stacked layout for the generic layer kernel (base_filters = 64).
@@ -146,10 +190,24 @@ conv12_fused_kernel(FusedArgs A) {
   constexpr int wEp2_0 = wEp2_of<kConv2>();
   constexpr int kEp1Groups = (wEp2_0 - wEp1_0) / 4;
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int64_t n = min(*A.n_dev, A.n_max);
-  const int64_t cnt = min(n - A.chunk_base, A.chunk_len);
-  if (cnt <= 0 || blockIdx.x >= cnt) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool qm = kConv2 && A.qmode != 0;   // queue mode (host: conv2-fused + features only)
+  volatile int64_t* pos = reinterpret_cast<volatile int64_t*>(smem + oPos);
+  int64_t cnt = 0;
+  uint64_t t_start = 0;
+  if (qm) {  // claim the first frame before any setup: CTAs without work leave at once
+    if (tid == 0) {
+      t_start = globaltimer_ns();
+      pos[0] = fq_claim(A, t_start);
+    }
+    __syncthreads();
+    if (pos[0] < 0) return;
+    cnt = A.chunk_len;
+  } else {
+    const int64_t n = min(*A.n_dev, A.n_max);
+    cnt = min(n - A.chunk_base, A.chunk_len);
+    if (cnt <= 0 || blockIdx.x >= cnt) return;
+  }
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + oBar);
   uint64_t* in_full = bars + 0;                 // [2]
@@ -224,7 +282,8 @@ conv12_fused_kernel(FusedArgs A) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int64_t my_frames = (cnt - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  // queue mode: unbounded, every role leaves on the -1 slot
+  const int64_t my_frames = qm ? INT64_MAX : (cnt - blockIdx.x + gridDim.x - 1) / gridDim.x;
 
   if (warp == 0) {
     // ===================================================== producer
@@ -235,8 +294,19 @@ conv12_fused_kernel(FusedArgs A) {
       for (int64_t it = 0; it < my_frames; ++it) {
         const int s = (int)(it & 1);
         if (it >= 2) mbar_wait(&in_empty[s], (uint32_t)(((it >> 1) - 1) & 1));
-        const int64_t g = A.chunk_base + blockIdx.x + it * gridDim.x;
-        const int64_t f = A.idx ? (int64_t)A.idx[g] : g;
+        int64_t f;
+        if (qm) {
+          const int64_t p = it == 0 ? pos[0] : fq_claim(A, t_start);
+          pos[it % kPosRing] = p;
+          if (p < 0) {                       // no more frames: stop token to the builders
+            mbar_arrive(&in_full[s]);
+            break;
+          }
+          f = fq_frame(A, p);
+        } else {
+          const int64_t g = A.chunk_base + blockIdx.x + it * gridDim.x;
+          f = A.idx ? (int64_t)A.idx[g] : g;
+        }
         mbar_arrive_expect_tx(&in_full[s], kInBytes);
         bulk_g2s(smem + oIn + s * kInBytes, A.small + f * A.small_pitch, kInBytes, &in_full[s]);
       }
@@ -251,6 +321,7 @@ conv12_fused_kernel(FusedArgs A) {
       const uint64_t bd0 = sdesc(sB1, C1t * 16, 128);
       uint64_t u1 = 0;  // global conv1 tile sequence; window group = u1 / 4, member = u1 % 4
       for (int64_t it = 0; it < my_frames; ++it) {
+        bool stop = false;
         for (int t = 0; t < kT1; t += 2, u1 += 2) {
           const uint64_t ug = u1 >> 2;           // global window-group sequence
           // A1 slots come in pairs (slot 2p, 2p+1 = window members of one pair),
@@ -258,6 +329,14 @@ conv12_fused_kernel(FusedArgs A) {
           const int pr = (int)((u1 >> 1) & 1);
           const int a[2] = {2 * pr, 2 * pr + 1};
           mbar_wait(&a1_full[pr], (uint32_t)((u1 >> 2) & 1));
+          if (qm && t == 0 && pos[it % kPosRing] < 0) {   // stop: forward to epilogue 1
+            const uint64_t ugh = ug * kHalves;
+            const int gb = (int)(ugh % kNG1);
+            if (ugh >= kNG1) mbar_wait(&t1_empty[gb], (uint32_t)(((ugh / kNG1) - 1) & 1));
+            mbar_arrive(&t1_full[gb]);
+            stop = true;
+            break;
+          }
           tc_fence_after();
 #pragma unroll
           for (int h = 0; h < kHalves; ++h) {
@@ -280,6 +359,7 @@ conv12_fused_kernel(FusedArgs A) {
           if (((u1 + 1) & 3) == 3)                 // window group complete (all halves)
             for (int h = 0; h < kHalves; ++h) umma_commit(&t1_full[(int)((ug * kHalves + h) % kNG1)]);
         }
+        if (stop) break;
       }
     }
   } else if (warp == 2) {
@@ -293,6 +373,13 @@ conv12_fused_kernel(FusedArgs A) {
       for (int64_t it = 0; it < my_frames; ++it) {
         const int pb = (int)(it & 1);
         mbar_wait(&act_full[pb], (uint32_t)((it >> 1) & 1));
+        if (qm && pos[it % kPosRing] < 0) {   // stop: forward to both epilogue-2 groups
+          for (int q = 0; q < 2; ++q) {       // their first tiles t = q use buffers q
+            if (it > 0) mbar_wait(&t2_empty[q], 1u);
+            mbar_arrive(&t2_full[q]);
+          }
+          break;
+        }
         for (int t = 0; t < kT2; t += 2) {
           int b[2], q0[2];
           // kT2 = 2 * kNB2: tile t of any frame uses buffer t % 3 with phase
@@ -340,6 +427,11 @@ conv12_fused_kernel(FusedArgs A) {
     for (int64_t it = 0; it < my_frames; ++it) {
       const int s = (int)(it & 1);
       mbar_wait(&in_full[s], (uint32_t)((it >> 1) & 1));
+      if (qm && pos[it % kPosRing] < 0) {   // stop: forward to the conv1 issuer (pair 0)
+        if (u1 >= kA1Stages) mbar_wait(&a1_empty[0], (uint32_t)(((u1 >> 2) - 1) & 1));
+        mbar_arrive(&a1_full[0]);
+        break;
+      }
       nbar_sync(1, 128);  // previous frame's rows are all built: X may be overwritten
       const uint8_t* in = smem + oIn + s * kInBytes;
       for (int p = bt; p < ((NS_EXP & 2) ? 0 : kIn * kIn); p += 128) {
@@ -428,11 +520,17 @@ conv12_fused_kernel(FusedArgs A) {
       if (kConv2 && it >= 2) mbar_wait(&act_empty[pb], (uint32_t)(((it >> 1) - 1) & 1));
       uint8_t* planes = smem + oAct + pb * kActBytes;
       const int64_t i = blockIdx.x + it * gridDim.x;  // chunk-relative frame
-      for (int G = 0; G < kG1; ++G) {
+      bool stop = false;
+      for (int G = 0; G < kG1 && !stop; ++G) {
         for (int h = 0; h < kHalves; ++h, ++ugh) {
           const int gb = (int)(ugh % kNG1);
           if (kEp1Groups > 1 && gb != grp) continue;
           mbar_wait(&t1_full[gb], (uint32_t)((ugh / kNG1) & 1));
+          if (qm && G == 0 && pos[it % kPosRing] < 0) {   // stop: forward to the conv2 issuer
+            mbar_arrive(&act_full[pb]);                    // (act_empty waited above)
+            stop = true;
+            break;
+          }
           tc_fence_after();
           const int w = G * 128 + row;
           const bool valid = w < kP1 * kP1;
@@ -486,6 +584,7 @@ conv12_fused_kernel(FusedArgs A) {
           mbar_arrive(&t1_empty[gb]);
         }
       }
+      if (stop) break;
       if (kConv2) {
         fence_proxy_async_smem();  // planes written by threads -> read by the tensor core
         mbar_arrive(&act_full[pb]);
@@ -510,10 +609,18 @@ conv12_fused_kernel(FusedArgs A) {
       }
     }
     for (int64_t it = 0; it < my_frames; ++it) {
-      const int64_t i = blockIdx.x + it * gridDim.x;  // chunk-relative frame
+      int64_t i = blockIdx.x + it * gridDim.x;  // chunk-relative frame (queue mode: slot)
+      bool stop = false;
       for (int t = grp2; t < kT2; t += 2) {             // this group's tiles
         const int b = t % kNB2;                          // kT2 = 2 * kNB2
         mbar_wait(&t2_full[b], (uint32_t)((t / kNB2) & 1));
+        if (qm && t == grp2) {
+          i = pos[it % kPosRing];
+          if (i < 0) {
+            stop = true;
+            break;
+          }
+        }
         tc_fence_after();
         const int yb = (t / 3) * 8, xb = (t % 3) * 8;
         const int yc = yb + rl, xc = xb + cl;                 // conv output position
@@ -572,6 +679,7 @@ conv12_fused_kernel(FusedArgs A) {
           }
         }
       }
+      if (stop) break;
     }
   }
   __syncthreads();

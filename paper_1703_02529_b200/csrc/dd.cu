@@ -62,14 +62,6 @@ NS_DEV void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 NS_DEV void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-NS_DEV unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-NS_DEV void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 struct DsArgs {
   const uint8_t* frames;
@@ -96,6 +88,7 @@ struct DsArgs {
   int cs_stride;    // u16 words of column sums per worker warp (multiple of 8)
   // dynamic smem byte offsets (host-planned, ds_plan)
   int off_ref, off_blkn, off_blk, off_wlr, off_cs, off_stages;
+  FiredQueue fq;    // fq.q != null: append fired frames (overlapped cascade)
 };
 
 struct BandInfo {   // per output row i
@@ -167,6 +160,20 @@ NS_DEV FrameCtx frame_ctx(const DsArgs& A, int64_t m, int64_t tau_first) {
   return c;
 }
 
+// Append fired frame f to the queue (scorer lane 0).  The frame's small image was
+// written by this CTA's worker warps before they arrived on its frame barrier, which
+// this thread has waited on: the fence + release store publish it at gpu scope.
+NS_DEV void fq_push(const DsArgs& A, int64_t f) {
+  if (!A.fq.q) return;
+  const unsigned long long p = atomicAdd(A.fq.count, 1ull);
+  st_release_s32(A.fq.q + p, (int32_t)f);   // release: cumulative over the observed writes
+}
+// Every entry of this CTA is published (scorer lane 0, after its last push).
+NS_DEV void fq_finish(const DsArgs& A) {
+  if (!A.fq.q) return;
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.fq.done) : "memory");
+}
+
 // Score of one frame from its per-block SSDs (one warp): O3, fixed order.
 NS_DEV void score_frame(const DsArgs& A, uint32_t* blk, const uint32_t* blkn,
                         const double* wlr, double* pk, int64_t f, int lane) {
@@ -176,6 +183,7 @@ NS_DEV void score_frame(const DsArgs& A, uint32_t* blk, const uint32_t* blkn,
       blk[0] = 0u;
       A.score[f] = sc;
       A.disp[f] = sc > A.delta ? NOSCOPE_FIRED : NOSCOPE_SUPPRESSED;
+      if (sc > A.delta) fq_push(A, f);
     }
   } else {
     const int gg = A.grid * A.grid;
@@ -190,6 +198,7 @@ NS_DEV void score_frame(const DsArgs& A, uint32_t* blk, const uint32_t* blkn,
       if (z != z) atomicOr(A.status, 1u);
       A.score[f] = z;
       A.disp[f] = z > A.delta ? NOSCOPE_FIRED : NOSCOPE_SUPPRESSED;
+      if (z > A.delta) fq_push(A, f);
     }
   }
   __syncwarp();
@@ -368,6 +377,7 @@ dd_kernel(DsArgs A) {
       } else if (c.forced && lane == 0) {
         A.score[c.f] = __longlong_as_double(0x7FF0000000000000ll);  // +inf
         A.disp[c.f] = NOSCOPE_FIRED;
+        fq_push(A, c.f);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bfree[lm & 1]);
@@ -491,7 +501,10 @@ dd_kernel(DsArgs A) {
   }
 
   // ---- publish completion, then score deferred frames (mode 1 only)
-  if (A.mode != 1) return;
+  if (A.mode != 1) {
+    if (warp == 1 && lane == 0) fq_finish(A);
+    return;
+  }
   const int nthr = blockDim.x - 32;  // every warp but the producer
   const int et = tid - 32;
   bar_sync(kBarEnd, nthr);
@@ -553,6 +566,7 @@ dd_kernel(DsArgs A) {
     if (warp == 1) score_frame(A, blk, blkn, wlr, pk, ff, lane);
     bar_sync(kBarEnd, nthr);
   }
+  if (warp == 1 && lane == 0) fq_finish(A);
 }
 
 // ------------------------------------------------- identity downsample (out == source)
@@ -747,6 +761,11 @@ static size_t ds_plan(DsArgs& A, int ctas_per_sm) {
   return b + (size_t)A.ng * A.nsg * A.stage_bytes;
 }
 
+bool dd_uses_band_kernel(const noscope_dd_config& cfg, const noscope_frames_desc& desc) {
+  const int grid = cfg.metric == 1 ? cfg.grid : 1;
+  return !(desc.width == cfg.out_w && desc.height == cfg.out_h && grid <= kMaxGrid);
+}
+
 bool dd_frames_fit(const noscope_dd_config& cfg, const noscope_frames_desc& desc) {
   if (desc.width == cfg.out_w && desc.height == cfg.out_h) return true;   // identity kernel, no bands
   DsArgs A{};
@@ -768,7 +787,7 @@ noscope_status launch_diff_detect(const noscope_dd_config& cfg, const uint8_t* f
                                   const noscope_frames_desc& desc, int64_t n, int64_t tau0,
                                   uint8_t* state, uint8_t* small, int64_t small_pitch,
                                   double* score, uint8_t* disp, uint32_t* status, unsigned* flags,
-                                  cudaStream_t st, Prof* prof) {
+                                  cudaStream_t st, Prof* prof, FiredQueue* fq, int reserve_sms) {
   DsArgs A{};
   A.frames = frames;
   A.frame_pitch = desc.frame_pitch;
@@ -812,6 +831,7 @@ noscope_status launch_diff_detect(const noscope_dd_config& cfg, const uint8_t* f
   if (A.fast && A.rlo == 9 && A.W / A.out_w == 12 && A.RB == 1920) kern = dd_kernel<9, 12, 120>;
   const int64_t frames_needed = A.need.m1 - A.need.m0;
   if (A.W == A.out_w && A.H == A.out_h && A.grid <= kMaxGrid) {  // O1 is the identity
+    if (fq) return NOSCOPE_INVALID_ARGUMENT;   // no fired-frame queue on this path
     if (frames_needed > 0) {
       const int grid = (int)std::min<int64_t>(frames_needed, (int64_t)kNumSMs * 8);
       dd_identity_kernel<<<grid, kIdThreads, 0, st>>>(A);
@@ -833,8 +853,13 @@ noscope_status launch_diff_detect(const noscope_dd_config& cfg, const uint8_t* f
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (const char* e = std::getenv("NOSCOPE_DD_SMS")) sms = std::max(1, std::min(sms, std::atoi(e)));  // experiments
+    sms = std::max(1, sms - std::max(0, reserve_sms));
     // all CTAs co-resident (deferred scoring waits on earlier CTAs' flags)
     const int grid = (int)std::min<int64_t>(frames_needed, (int64_t)std::min(per_sm, cps) * sms);
+    if (fq) {
+      fq->producers = grid;
+      A.fq = *fq;
+    }
     if (cfg.mode == 1) NS_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)grid * 4, st));
     NS_CUDA_TRY(launch_cooperative(kern, grid, threads, smem, st, A));  // deferred anchors wait on earlier CTAs
     NS_LAUNCH_CHECK();

@@ -100,11 +100,29 @@ inline int state_label_len(const noscope_dd_config& c) {
 }
 
 // ---- launchers (all asynchronous on `st`)
+// Fired-frame queue of the overlapped cascade (noscope_api.cu): dd_kernel's scorer
+// appends every frame it fires (reserve a slot with an atomic, then publish the frame
+// index with a release store after its small frame is written); the queue-mode CNN
+// (cnn_fused.cu) claims slots and reads the frames while the DD is still streaming.
+struct FiredQueue {
+  int32_t* q;                   // [n] frame indices (call-relative), -1 until published
+  unsigned long long* count;    // slots reserved by dd_kernel
+  unsigned long long* claim;    // slots claimed by CNN CTAs
+  unsigned* done;               // dd_kernel CTAs finished (all entries published)
+  int producers;                // dd_kernel grid size (0 until launched)
+};
+constexpr size_t kFqHeaderBytes = 256;   // count @0, claim @8, done @16
+// fq (nullable): also append fired frames to the queue (dd_kernel path only; the
+// identity kernel does not produce a queue: fq->producers stays 0).  reserve_sms:
+// SMs left free for a concurrently running kernel.
 noscope_status launch_diff_detect(const noscope_dd_config& cfg, const uint8_t* frames,
                                   const noscope_frames_desc& desc, int64_t n, int64_t tau0,
                                   uint8_t* state, uint8_t* small, int64_t small_pitch,
                                   double* score, uint8_t* disp, uint32_t* status,
-                                  unsigned* flags, cudaStream_t st, Prof* prof = nullptr);
+                                  unsigned* flags, cudaStream_t st, Prof* prof = nullptr,
+                                  FiredQueue* fq = nullptr, int reserve_sms = 0);
+// Would launch_diff_detect use the band-pipeline dd_kernel (and so feed a queue)?
+bool dd_uses_band_kernel(const noscope_dd_config& cfg, const noscope_frames_desc& desc);
 // fp32-accurate tcgen05 GEMM (gemm_tc.cu, 3xTF32): C[m][n] = sum_k A(m,k) B(k,n)
 // with A(m,k) = A[m*sam + k*sak], B(k,n) = B[n*sbn + k*sbk]; `part` = split-K
 // scratch of tc_gemm_part_floats(M, N, K) floats (nullable when that is 0).
@@ -135,9 +153,11 @@ noscope_status launch_state_update(const noscope_dd_config& cfg, const uint8_t* 
 
 // Stable compaction of fired frames (+ fills skipped frames' disposition/score).
 size_t compact_ws_bytes(int64_t n);
+// pos_pf (nullable): per-frame position in idx_out, written for the selected frames.
 noscope_status launch_compact_fired(const uint8_t* disp_in, uint8_t* disp, double* score,
                                     int64_t n, int64_t tau0, int t_skip, int32_t* idx_out,
-                                    int64_t* count_out, void* scan_ws, cudaStream_t st);
+                                    int64_t* count_out, void* scan_ws, cudaStream_t st,
+                                    int32_t* pos_pf = nullptr);
 // Routing of compacted logits + compaction of uncertain ones.
 noscope_status launch_route(noscope_route r, const float* logits, const int64_t* n_dev,
                             int64_t n_max, const int32_t* frame_idx, uint8_t* route_out,
@@ -170,6 +190,13 @@ struct FusedArgs {
   uint8_t* out;
   int K_feat;          // feature length (to_features)
   int64_t out_rows;    // rows per channel-group plane of the stacked map (!to_features)
+  // queue mode (conv2-fused variants writing FC features): frames are claimed from a
+  // FiredQueue instead of idx/n_dev; the features of queue slot p go to row p.
+  //   qmode 1 ("side"): runs beside dd_kernel, claims published slots until every
+  //           dd_kernel CTA is done, then stops (the rest is left to qmode 2);
+  //   qmode 2 ("tail"): launched after dd_kernel, claims every remaining slot.
+  int qmode;           // 0 = index mode
+  FiredQueue fq;
 };
 size_t conv12_fused_smem();
 
@@ -218,6 +245,20 @@ noscope_status launch_cnn(const noscope_cnn_arch& a, const noscope_cnn_weights& 
                           const uint8_t* small, int64_t small_pitch, const int32_t* idx,
                           const int64_t* n_dev, int64_t n_max, float* logits, void* ws,
                           uint32_t* status, cudaStream_t st);
+// Queue mode of the specialized CNN (the overlapped cascade, noscope_api.cu): archs
+// whose conv1+conv2 kernel writes the FC features (conv2 fused, L = 2).  The
+// workspace holds the features of up to n_max queue slots (no 32,768-frame chunks).
+bool cnn_queue_supported(const noscope_cnn_arch& a);
+size_t cnn_queue_ws_bytes(const noscope_cnn_arch& a, int64_t n_max);
+noscope_status cnn_queue_pack(const noscope_cnn_arch& a, const noscope_cnn_weights& w,
+                              int64_t n_max, void* ws, cudaStream_t st);
+noscope_status cnn_queue_conv(const noscope_cnn_arch& a, const noscope_cnn_weights& w,
+                              const uint8_t* small, int64_t small_pitch, const FiredQueue& fq,
+                              int qmode, int grid, int64_t n_max, void* ws, cudaStream_t st);
+// FC over queue slots [0, *fq.count): logit of slot p -> logits[pos_pf[fq.q[p]]].
+noscope_status cnn_queue_fc(const noscope_cnn_arch& a, const noscope_cnn_weights& w,
+                            const FiredQueue& fq, int64_t n_max, const int32_t* pos_pf,
+                            float* logits, void* ws, cudaStream_t st);
 
 // DD fitting (fit.cu).
 size_t fit_ws_bytes(int64_t n, int32_t d, int64_t small_bytes);

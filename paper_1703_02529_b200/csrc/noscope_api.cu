@@ -2,6 +2,8 @@
 // workspace carving and launch sequencing.  No torch types cross this boundary.
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
+#include <algorithm>
 
 #include "common.cuh"
 #include "internal.h"
@@ -90,12 +92,31 @@ DDWs dd_ws(int64_t n) {
   return w;
 }
 
+// Overlapped cascade (cascade_front_overlapped; opt-in, NOSCOPE_OVERLAP=1): for calls
+// of at least kOverlapMinFrames frames whose CNN has a queue mode, the conv1+conv2
+// kernel runs on kSideSms SMs beside dd_kernel (which leaves them free), consuming
+// the fired frames as dd_kernel publishes them; what is left when the DD ends runs
+// on the whole GPU.  Results are identical to the serial schedule; it is not the
+// default because on B200 it is not faster: with the side SMs computing, dd_kernel
+// (power-capped, HBM-bound) slows by as much as the CNN time it hides.
+constexpr int64_t kOverlapMinFrames = 8192;
+constexpr int kSideSms = 8;
+bool overlap_requested() {
+  const char* e = std::getenv("NOSCOPE_OVERLAP");
+  return e && e[0] == '1';
+}
+bool overlap_sized(const noscope_cnn_arch* a, int64_t n) {
+  return a && n >= kOverlapMinFrames && cnn_queue_supported(*a) && overlap_requested();
+}
+
 struct CascadeWs {
   size_t status, scan, small, score, disp, idx, nfired, logits, route_pf, unc, nunc, unc_pos,
-      answers, counters, lab, flags, cnn, total;
+      answers, counters, lab, flags, fq_head, fq, pos_pf, cnn, total;
   int64_t small_pitch;
 };
-CascadeWs cascade_ws(const noscope_dd_config* dd, const noscope_cnn_arch* a, int64_t n) {
+// ovl: with the overlapped schedule's buffers (queue, per-frame positions, features of
+// every queue slot)
+CascadeWs cascade_ws(const noscope_dd_config* dd, const noscope_cnn_arch* a, int64_t n, bool ovl) {
   CascadeWs w{};
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -120,8 +141,11 @@ CascadeWs cascade_ws(const noscope_dd_config* dd, const noscope_cnn_arch* a, int
   w.counters = take(64);
   w.lab = take(labels_ws_bytes(n));
   w.flags = take(dd_flags_bytes());
+  w.fq_head = take(ovl ? kFqHeaderBytes : 0);
+  w.fq = take(ovl ? (size_t)n * 4 : 0);
+  w.pos_pf = take(ovl ? (size_t)n * 4 : 0);
   w.cnn = off;
-  off += a ? cnn_ws_bytes(*a, n) : 0;
+  off += a ? std::max(cnn_ws_bytes(*a, n), ovl ? cnn_queue_ws_bytes(*a, n) : (size_t)0) : 0;
   w.total = align256(off);
   return w;
 }
@@ -179,7 +203,7 @@ size_t noscope_workspace_bytes(noscope_op op, const noscope_dd_config* dd,
     case NOSCOPE_OP_CASCADE_RUN:
       if (!arch || !dd || validate_dd(dd, false) != NOSCOPE_OK || !cnn_arch_supported(*arch))
         return 0;
-      return cascade_ws(dd, arch, n).total;
+      return cascade_ws(dd, arch, n, overlap_sized(arch, n)).total;
     case NOSCOPE_OP_THRESHOLD_SWEEP:
       if (nd < 1 || m < 1) return 0;
       return sweep_ws_bytes(nd, m);
@@ -298,6 +322,93 @@ noscope_status noscope_compact_fired(uint8_t* disposition, int64_t n, int64_t se
                               n_out_dev, ws, (cudaStream_t)stream);
 }
 
+// Overlap for this call?  Requested (NOSCOPE_OVERLAP=1), large, on the band-pipeline
+// DD with a queue-mode CNN, outside stream capture (the side stream is created per
+// call) and with a workspace sized for it (queried while the request was set).
+static bool use_overlap(const noscope_dd_config* dd, const noscope_cnn_arch* arch,
+                        const noscope_frames_desc& desc, int64_t n, cudaStream_t st) {
+  if (!overlap_sized(arch, n) || !dd_uses_band_kernel(*dd, desc)) return false;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+  return true;
+}
+
+static int side_sms() {
+  int v = kSideSms;
+  if (const char* e = std::getenv("NOSCOPE_SIDE_SMS")) v = std::max(0, std::min(32, std::atoi(e)));  // 0: no side kernel (A/B)
+  return v;
+}
+
+// DD -> compaction -> CNN logits (compacted order) with the conv1+conv2 kernel
+// overlapped with the DD:
+//   main: fork | dd_kernel on (SMs - side) CTAs, appending fired frames to the queue
+//   side:      | conv kernel, qmode 1, on `side` CTAs: claims published slots
+//   main: conv kernel, qmode 2, whole GPU: the slots left when the DD ended
+//         -> compaction (+ per-frame position) -> join side -> FC: slot p's logit to
+//         logits[pos_pf[q[p]]], i.e. the same compacted order as the serial schedule.
+static noscope_status cascade_front_overlapped(
+    const noscope_dd_config* dd, const noscope_cnn_arch* arch, const noscope_cnn_weights* weights,
+    const uint8_t* frames, const noscope_frames_desc& desc, int64_t n, int64_t seg_offset,
+    uint8_t* st8, uint8_t* small, int64_t small_pitch, double* score, uint8_t* disp,
+    uint32_t* status, int32_t* idx, int64_t* nfired, float* logits, uint8_t* b,
+    const CascadeWs& w, cudaStream_t st, Prof* prof) {
+  FiredQueue fq{};
+  fq.q = reinterpret_cast<int32_t*>(b + w.fq);
+  fq.count = reinterpret_cast<unsigned long long*>(b + w.fq_head);
+  fq.claim = fq.count + 1;
+  fq.done = reinterpret_cast<unsigned*>(fq.count + 2);
+  int32_t* pos_pf = reinterpret_cast<int32_t*>(b + w.pos_pf);
+  void* cws = b + w.cnn;
+  NS_CUDA_TRY(cudaMemsetAsync(fq.count, 0, kFqHeaderBytes, st));
+  NS_CUDA_TRY(cudaMemsetAsync(fq.q, 0xFF, (size_t)n * 4, st));   // -1: not yet published
+  noscope_status s = cnn_queue_pack(*arch, *weights, n, cws, st);
+  if (s != NOSCOPE_OK) return s;
+  const int side = side_sms();
+  cudaStream_t ss = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  auto cleanup = [&]() {
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (ss) cudaStreamDestroy(ss);   // released once its work completes
+  };
+  auto fail = [&](noscope_status e) {
+    cleanup();
+    return e;
+  };
+  if (cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventRecord(fork, st) != cudaSuccess)
+    return fail(NOSCOPE_CUDA);
+  s = launch_diff_detect(*dd, frames, desc, n, seg_offset, seg_offset > 0 ? st8 : nullptr, small,
+                         small_pitch, score, disp, status, reinterpret_cast<unsigned*>(b + w.flags),
+                         st, prof, &fq, side);  // e1
+  if (s != NOSCOPE_OK) return fail(s);
+  // the side kernel only after dd_kernel is enqueued (it waits for fq.producers CTAs)
+  const bool side_on = fq.producers > 0 && side > 0;
+  if (side_on) {
+    if (cudaStreamWaitEvent(ss, fork, 0) != cudaSuccess) return fail(NOSCOPE_CUDA);
+    s = cnn_queue_conv(*arch, *weights, small, small_pitch, fq, 1, side, n, cws, ss);
+    if (s != NOSCOPE_OK) return fail(s);
+    if (cudaEventRecord(join, ss) != cudaSuccess) return fail(NOSCOPE_CUDA);
+  }
+  int sms = kNumSMs;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device());
+  s = cnn_queue_conv(*arch, *weights, small, small_pitch, fq, 2, sms, n, cws, st);
+  if (s != NOSCOPE_OK) return fail(s);
+  prof_mark(prof, st);  // e2
+  s = launch_compact_fired(disp, disp, score, n, seg_offset, dd->t_skip_frames, idx, nfired,
+                           b + w.scan, st, pos_pf);
+  if (s != NOSCOPE_OK) return fail(s);
+  prof_mark(prof, st);  // e3
+  if (side_on && cudaStreamWaitEvent(st, join, 0) != cudaSuccess) return fail(NOSCOPE_CUDA);
+  s = cnn_queue_fc(*arch, *weights, fq, n, pos_pf, logits, cws, st);
+  if (s != NOSCOPE_OK) return fail(s);
+  prof_mark(prof, st);  // e4
+  cleanup();
+  return NOSCOPE_OK;
+}
+
 static noscope_status cascade_impl(const noscope_dd_config* dd, const noscope_cnn_arch* arch,
                                    const noscope_cnn_weights* weights, noscope_route route,
                                    const uint8_t* frames, noscope_frames_desc desc, int64_t n,
@@ -315,7 +426,12 @@ static noscope_status cascade_impl(const noscope_dd_config* dd, const noscope_cn
   if ((n > 0 && (!frames || !labels_out)) || !state || !labeller || !ws || n < 0 || seg_offset < 0)
     return NOSCOPE_INVALID_ARGUMENT;   // frames / labels may be null for an empty chunk
   if (!aligned16(frames) || !aligned16(ws) || !aligned16(state)) return NOSCOPE_INVALID_ARGUMENT;
-  CascadeWs w = cascade_ws(dd, arch, n);
+  bool ovl = use_overlap(dd, arch, desc, n, (cudaStream_t)stream);
+  CascadeWs w = cascade_ws(dd, arch, n, ovl);
+  if (ovl && ws_bytes < w.total) {   // workspace sized for the serial schedule
+    ovl = false;
+    w = cascade_ws(dd, arch, n, false);
+  }
   if (ws_bytes < w.total) return NOSCOPE_WORKSPACE_TOO_SMALL;
   if ((s = check_device()) != NOSCOPE_OK) return s;
   if (n == 0) {
@@ -341,6 +457,12 @@ static noscope_status cascade_impl(const noscope_dd_config* dd, const noscope_cn
 
   NS_CUDA_TRY(cudaMemsetAsync(counters, 0, 64, st));
   prof_mark(prof, st);  // e0
+  if (ovl) {
+    s = cascade_front_overlapped(dd, arch, weights, frames, desc, n, seg_offset, st8, small,
+                                 w.small_pitch, score, disp, status, idx, nfired, logits, b, w, st,
+                                 prof);  // e1 .. e4
+    if (s != NOSCOPE_OK) return s;
+  } else {
   s = launch_diff_detect(*dd, frames, desc, n, seg_offset, seg_offset > 0 ? st8 : nullptr, small,
                          w.small_pitch, score, disp, status, reinterpret_cast<unsigned*>(b + w.flags),
                          st, prof);  // e1 after the fused downsample + score kernel
@@ -354,6 +476,7 @@ static noscope_status cascade_impl(const noscope_dd_config* dd, const noscope_cn
                  st);
   if (s != NOSCOPE_OK) return s;
   prof_mark(prof, st);  // e4
+  }
   s = launch_route(route, logits, nfired, n, idx, nullptr, route_pf, unc, nunc, unc_pos, logits_out,
                    counters, b + w.scan, status, st);
   if (s != NOSCOPE_OK) return s;

@@ -157,7 +157,7 @@ NS_DEV void emit_selected(MaskWs ws, int64_t wa, int64_t wb, uint64_t off, uint1
 
 __global__ void __launch_bounds__(kMThreads, 3)
 compact_fired_kernel(uint8_t* disp, double* score, int64_t n, int64_t tau0, int t_skip,
-                     int32_t* idx_out, int64_t* count_out, MaskWs ws, int vec) {
+                     int32_t* idx_out, int64_t* count_out, MaskWs ws, int vec, int32_t* pos_pf) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x, c = blockIdx.x;
   const int64_t nch = (n + kMChunk - 1) / kMChunk;
   const int64_t ch0 = nch * c / G, ch1 = nch * (c + 1) / G;
@@ -223,12 +223,16 @@ compact_fired_kernel(uint8_t* disp, double* score, int64_t n, int64_t tau0, int 
   // ---- phase 2: ascending indices from the masks
   extern __shared__ __align__(16) uint16_t mstage[];
   if (idx_out)
-    emit_selected(ws, wa, wb, off, mstage, [&](int64_t i, uint64_t p) { idx_out[p] = (int32_t)i; });
+    emit_selected(ws, wa, wb, off, mstage, [&](int64_t i, uint64_t p) {
+      idx_out[p] = (int32_t)i;
+      if (pos_pf) pos_pf[i] = (int32_t)p;
+    });
 }
 
 noscope_status launch_compact_fired(const uint8_t* /*disp_in*/, uint8_t* disp, double* score,
                                     int64_t n, int64_t tau0, int t_skip, int32_t* idx_out,
-                                    int64_t* count_out, void* scan_ws, cudaStream_t st) {
+                                    int64_t* count_out, void* scan_ws, cudaStream_t st,
+                                    int32_t* pos_pf) {
   const int64_t nch = (n + kMChunk - 1) / kMChunk;
   if (nch == 0) {
     if (count_out) NS_CUDA_TRY(cudaMemsetAsync(count_out, 0, sizeof(int64_t), st));
@@ -251,7 +255,7 @@ noscope_status launch_compact_fired(const uint8_t* /*disp_in*/, uint8_t* disp, d
   // persistent and co-resident (the grid barrier): at most the resident CTA count
   const int grid = (int)std::min<int64_t>({nch, (int64_t)per_sm * sms, (int64_t)kMMaxCtas});
   NS_CUDA_TRY(launch_cooperative(compact_fired_kernel, grid, kMThreads, kMStageBytes, st, disp, score, n, tau0, t_skip,
-                                 idx_out, count_out, mask_ws_of(scan_ws), vec));
+                                 idx_out, count_out, mask_ws_of(scan_ws), vec, pos_pf));
   NS_LAUNCH_CHECK();
   count_launch();
   return NOSCOPE_OK;
