@@ -13,6 +13,7 @@
 // RMSprop.  No atomics anywhere (split-K partials are summed in a fixed order),
 // so a run is reproducible.
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -255,7 +256,7 @@ noscope_status gemm_rm(bool ta, bool tb, int M, int N, int64_t K, const float* A
 }
 
 struct TWs {
-  float *G, *V, *best, *x[5], *a[4], *cols, *dcols, *dx, *dxb, *h1, *dz, *dh1, *ones, *part;
+  float *G, *V, *best, *x[5], *a[4], *cols[4], *dcols, *dx, *dxb, *h1, *dz, *dh1, *ones, *part;
   uint8_t* arg[4];
   int32_t* idx_tmp;
   double* loss;
@@ -280,12 +281,13 @@ TWs carve_t(const TPlan& p, int B, void* base) {
     w.x[l] = (float*)take((size_t)B * t.H * t.W * t.cin * 4);
     w.a[l] = (float*)take((size_t)B * t.H * t.W * t.cout * 4);
     w.arg[l] = take((size_t)B * (t.H / 2) * (t.W / 2) * t.cout);
+    // each layer keeps its forward im2col rows for the weight gradient
+    w.cols[l] = (float*)take((size_t)B * t.H * t.W * 9 * t.cin * 4);
     cols = std::max(cols, (size_t)B * t.H * t.W * 9 * t.cin);
     xmax = std::max(xmax, (size_t)B * t.H * t.W * t.cin);
     xmax = std::max(xmax, (size_t)B * (t.H / 2) * (t.W / 2) * t.cout);
   }
   w.x[p.L] = (float*)take((size_t)B * p.K * 4);
-  w.cols = (float*)take(cols * 4);
   w.dcols = (float*)take(cols * 4);
   w.dx = (float*)take(xmax * 4);
   w.dxb = (float*)take(xmax * 4);
@@ -310,6 +312,7 @@ TWs carve_t(const TPlan& p, int B, void* base) {
   need(p.D, 1, B);
   w.part = (float*)take(std::max<size_t>(part, 1) * 4);
   w.loss = (double*)take(8);
+  w.idx_tmp = (int32_t*)take((size_t)B * 4);   // the captured step's batch indices
   w.total = off;
   return w;
 }
@@ -331,8 +334,8 @@ noscope_status forward(const TPlan& p, const noscope_cnn_arch& a, const float* P
     const TLayer& t = p.lay[l];
     const int64_t rows = (int64_t)B * t.H * t.W;
     im2col_kernel<<<grid_for(rows * 9 * (t.cin % 4 ? 1 : t.cin / 4)), kT, 0, st>>>(w.x[l], B, t.H, t.W, t.cin,
-                                                                                 w.cols);
-    NS_TRY(gemm_rm(false, true, (int)rows, t.cout, 9 * t.cin, w.cols, 9 * t.cin, P + t.w_off, 9 * t.cin, w.a[l],
+                                                                                 w.cols[l]);
+    NS_TRY(gemm_rm(false, true, (int)rows, t.cout, 9 * t.cin, w.cols[l], 9 * t.cin, P + t.w_off, 9 * t.cin, w.a[l],
                    t.cout, w.part, st));
     bias_relu_pool_kernel<<<grid_for((int64_t)B * (t.H / 2) * (t.W / 2) * t.cout), kT, 0, st>>>(
         w.a[l], P + t.b_off, B, t.H, t.W, t.cout, w.x[l + 1], w.arg[l]);
@@ -356,10 +359,8 @@ noscope_status backward(const TPlan& p, const float* P, TWs& w, int B, cudaStrea
     const int64_t rows = (int64_t)B * t.H * t.W;
     unpool_relu_kernel<<<grid_for((int64_t)B * (t.H / 2) * (t.W / 2) * t.cout), kT, 0, st>>>(
         w.a[l], dpool, w.arg[l], B, t.H, t.W, t.cout);
-    // the forward im2col of this layer was overwritten by later layers: rebuild it
-    im2col_kernel<<<grid_for(rows * 9 * (t.cin % 4 ? 1 : t.cin / 4)), kT, 0, st>>>(w.x[l], B, t.H, t.W, t.cin,
-                                                                                 w.cols);
-    NS_TRY(gemm_rm(true, false, t.cout, 9 * t.cin, rows, w.a[l], t.cout, w.cols, 9 * t.cin, G + t.w_off,
+    // dW = dY^T cols, on this layer's forward im2col rows
+    NS_TRY(gemm_rm(true, false, t.cout, 9 * t.cin, rows, w.a[l], t.cout, w.cols[l], 9 * t.cin, G + t.w_off,
                    9 * t.cin, w.part, st));
     NS_TRY(colsum(w.a[l], rows, t.cout, G + t.b_off, w.ones, w.part, st));
     if (l > 0) {
@@ -389,34 +390,84 @@ noscope_status launch_cnn_train(const noscope_cnn_arch& a, const noscope_train_c
   const TPlan p = make_tplan(a);
   TWs w = carve_t(p, cfg.batch, ws);
   noscope_status s = NOSCOPE_OK;
-  auto fail = [&](noscope_status e) { return e; };
-  NS_CUDA_TRY(cudaMemsetAsync(w.V, 0, p.nparams * 4, st));
+  // Full mini-batches replay one captured CUDA graph of the whole step (forward,
+  // backward, RMSprop: ~40 dependent launches) with the batch's indices copied into
+  // a fixed buffer first; the first batch (which also sets the kernels' attributes)
+  // and a partial last batch run as plain launches.  Same kernels, same order: the
+  // results are identical.  NOSCOPE_TRAIN_GRAPH=0 disables it (A/B).
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cs = nullptr;
+  bool use_graph = true;
+  if (const char* e = std::getenv("NOSCOPE_TRAIN_GRAPH")) use_graph = e[0] != '0';
+  {
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cst) != cudaSuccess || cst != cudaStreamCaptureStatusNone) use_graph = false;
+  }
+  auto release = [&]() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (cs) cudaStreamDestroy(cs);
+    gexec = nullptr;
+    cs = nullptr;
+  };
+  auto fail = [&](noscope_status e) {
+    release();
+    return e;
+  };
+  auto step = [&](const int32_t* idx, int B, cudaStream_t s1) -> noscope_status {
+    noscope_status r = forward(p, a, P, w, small, pitch, labels, idx, B, 1, s1);
+    if (r != NOSCOPE_OK) return r;
+    if ((r = backward(p, P, w, B, s1)) != NOSCOPE_OK) return r;
+    rmsprop_kernel<<<grid_for(p.nparams), kT, 0, s1>>>(P, w.G, w.V, p.nparams, cfg.lr, cfg.rho, cfg.eps);
+    NS_LAUNCH_CHECK();
+    return NOSCOPE_OK;
+  };
+#define NS_TRAIN_TRY(expr)                                   \
+  do {                                                       \
+    if ((expr) != cudaSuccess) return fail(NOSCOPE_CUDA);    \
+  } while (0)
+  auto capture = [&]() -> noscope_status {
+    cudaGraph_t g = nullptr;
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return NOSCOPE_CUDA;
+    if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return NOSCOPE_CUDA;
+    noscope_status r = step(w.idx_tmp, cfg.batch, cs);
+    const cudaError_t ec = cudaStreamEndCapture(cs, &g);
+    if (r != NOSCOPE_OK) return r;
+    if (ec != cudaSuccess || !g) return NOSCOPE_CUDA;
+    const cudaError_t ei = cudaGraphInstantiate(&gexec, g, 0);
+    cudaGraphDestroy(g);
+    return ei == cudaSuccess ? NOSCOPE_OK : NOSCOPE_CUDA;
+  };
+  NS_TRAIN_TRY(cudaMemsetAsync(w.V, 0, p.nparams * 4, st));
   {
     const int64_t nr = (int64_t)cfg.batch * p.lay[0].H * p.lay[0].W;
     fill_kernel<<<grid_for(nr), kT, 0, st>>>(w.ones, nr, 1.0f);
   }
-  NS_CUDA_TRY(cudaMemcpyAsync(w.best, P, p.nparams * 4, cudaMemcpyDeviceToDevice, st));
+  NS_TRAIN_TRY(cudaMemcpyAsync(w.best, P, p.nparams * 4, cudaMemcpyDeviceToDevice, st));
   double best_val = INFINITY, prev_tr = INFINITY;
   int run = 0;
   for (int e = 0; e < cfg.epochs; ++e) {
-    NS_CUDA_TRY(cudaMemsetAsync(w.loss, 0, 8, st));
+    NS_TRAIN_TRY(cudaMemsetAsync(w.loss, 0, 8, st));
     for (int64_t s0 = 0; s0 < n_train; s0 += cfg.batch) {
       const int B = (int)std::min<int64_t>(cfg.batch, n_train - s0);
       const int32_t* idx = perms + (int64_t)e * n_train + s0;
-      if ((s = forward(p, a, P, w, small, pitch, labels, idx, B, 1, st)) != NOSCOPE_OK) return fail(s);
-      if ((s = backward(p, P, w, B, st)) != NOSCOPE_OK) return fail(s);
-      rmsprop_kernel<<<grid_for(p.nparams), kT, 0, st>>>(P, w.G, w.V, p.nparams, cfg.lr, cfg.rho, cfg.eps);
+      if (use_graph && B == cfg.batch && (e > 0 || s0 > 0)) {
+        if (!gexec && (s = capture()) != NOSCOPE_OK) return fail(s);
+        NS_TRAIN_TRY(cudaMemcpyAsync(w.idx_tmp, idx, (size_t)B * 4, cudaMemcpyDeviceToDevice, st));
+        if (cudaGraphLaunch(gexec, st) != cudaSuccess) return fail(NOSCOPE_CUDA);
+        continue;
+      }
+      if ((s = step(idx, B, st)) != NOSCOPE_OK) return fail(s);
     }
     double tr = 0.0, va = 0.0;
-    NS_CUDA_TRY(cudaMemcpyAsync(&tr, w.loss, 8, cudaMemcpyDeviceToHost, st));
-    NS_CUDA_TRY(cudaStreamSynchronize(st));
-    NS_CUDA_TRY(cudaMemsetAsync(w.loss, 0, 8, st));
+    NS_TRAIN_TRY(cudaMemcpyAsync(&tr, w.loss, 8, cudaMemcpyDeviceToHost, st));
+    NS_TRAIN_TRY(cudaStreamSynchronize(st));
+    NS_TRAIN_TRY(cudaMemsetAsync(w.loss, 0, 8, st));
     for (int64_t s0 = 0; s0 < n_val; s0 += cfg.batch) {
       const int B = (int)std::min<int64_t>(cfg.batch, n_val - s0);
       if ((s = forward(p, a, P, w, small, pitch, labels, val_idx + s0, B, 0, st)) != NOSCOPE_OK) return fail(s);
     }
-    NS_CUDA_TRY(cudaMemcpyAsync(&va, w.loss, 8, cudaMemcpyDeviceToHost, st));
-    NS_CUDA_TRY(cudaStreamSynchronize(st));
+    NS_TRAIN_TRY(cudaMemcpyAsync(&va, w.loss, 8, cudaMemcpyDeviceToHost, st));
+    NS_TRAIN_TRY(cudaStreamSynchronize(st));
     tr /= (double)n_train;
     va /= (double)std::max<int64_t>(n_val, 1);
     hist[2 * e] = tr;
@@ -427,16 +478,18 @@ noscope_status launch_cnn_train(const noscope_cnn_arch& a, const noscope_train_c
     // increases")
     if (va < best_val) {
       best_val = va;
-      NS_CUDA_TRY(cudaMemcpyAsync(w.best, P, p.nparams * 4, cudaMemcpyDeviceToDevice, st));
+      NS_TRAIN_TRY(cudaMemcpyAsync(w.best, P, p.nparams * 4, cudaMemcpyDeviceToDevice, st));
     }
     if (e > 0 && tr > prev_tr) break;
     prev_tr = tr;
   }
-  NS_CUDA_TRY(cudaMemcpyAsync(P, w.best, p.nparams * 4, cudaMemcpyDeviceToDevice, st));
-  NS_CUDA_TRY(cudaStreamSynchronize(st));
+  NS_TRAIN_TRY(cudaMemcpyAsync(P, w.best, p.nparams * 4, cudaMemcpyDeviceToDevice, st));
+  NS_TRAIN_TRY(cudaStreamSynchronize(st));
+  release();
   *epochs_run = run;
   return NOSCOPE_OK;
 }
+#undef NS_TRAIN_TRY
 
 noscope_status launch_params_to_weights(const noscope_cnn_arch& a, const float* P, const noscope_cnn_weights& wt,
                                         cudaStream_t st) {

@@ -130,3 +130,30 @@ def test_params_to_weights_rounding():
     exp = p[:n0].to(torch.bfloat16).view(torch.int16)
     assert torch.equal(out.conv_w[0].view(-1), exp)
     assert torch.equal(out.conv_b[0], p[n0:n0 + 32])
+
+
+@pytest.mark.parametrize("L,n_train,batch", [(2, 200, 32), (4, 96, 16)])
+def test_graph_replay_equals_plain_launches(L, n_train, batch, monkeypatch):
+    """Full mini-batches after the first replay one captured CUDA graph of the step
+    (train.cu); the same kernels in the same order, so the parameters and loss
+    histories are bit-identical to plain launches (NOSCOPE_TRAIN_GRAPH=0) — with a
+    partial last batch (200 = 6 x 32 + 8) that runs outside the graph."""
+    nsm = ns()
+    n = n_train + 32
+    small, g, y = _data(n, 11)
+    arch = sg.CnnArch(L, 32, 32)
+    A = nsm.Arch(L, 32, 32)
+    w = sg.he_normal_weights(arch, 12)
+    rng = np.random.default_rng(3)
+    perms = torch.from_numpy(np.stack([rng.permutation(n_train) for _ in range(3)]).astype(np.int32)).cuda()
+    val = torch.arange(n_train, n, dtype=torch.int32, device="cuda")
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("NOSCOPE_TRAIN_GRAPH", mode)
+        p = nsm.params_from_weight_dict(A, w)
+        hist, run = nsm.noscope_cnn_train(A, p, torch.from_numpy(small).cuda(), torch.from_numpy(y).cuda(),
+                                          perms, val, batch=batch, lr=1e-3)
+        out[mode] = (p.cpu().numpy(), hist, run)
+    assert out["0"][2] == out["1"][2]
+    assert out["0"][1] == out["1"][1]
+    assert np.array_equal(out["0"][0].view(np.uint32), out["1"][0].view(np.uint32))
