@@ -54,7 +54,21 @@
 #ifndef NS_EXP
 #define NS_EXP 0  // timing experiments only (tools/exp_fused.sh); 0 in the product
 // bits: 1 no conv2-plane stores, 2 no image build, 4 no im2col loads, 8 no conv1 MMAs,
-// 16 no conv2 MMAs, 32 no epilogue-2 work, 64 no epilogue-1 work, 128 no tcgen05.wait::st
+// 16 no conv2 MMAs, 32 no epilogue-2 work, 64 no epilogue-1 work, 128 no tcgen05.wait::st,
+// 256 per-role wait-time accounting (clock64 around every barrier wait, printed per role)
+#endif
+#if NS_EXP & 256
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+#define NS_TW(k, stmt)                 \
+  do {                                 \
+    const long long _t0 = clock64();   \
+    stmt;                              \
+    twait[k] += clock64() - _t0;       \
+  } while (0)
+#else
+#define NS_TW(k, stmt) stmt
 #endif
 
 namespace ns {
@@ -66,10 +80,17 @@ constexpr int kC1Max = 64;        // conv1 channels of the widest variant (2 hal
 constexpr int kIn = 50, kInP = 52, kP1 = 25;
 // The zero-haloed bf16 image is stored column-polyphase: X[x & 1][y][x >> 1]
 // (8-byte cells).  im2col lanes are consecutive pool windows (x stride 2), so a
-// tap's loads are consecutive cells of one parity plane; the 40-cell row stride
-// (320 B = 64 mod 128) keeps a half-warp that wraps to the next row conflict-free.
-constexpr int kXs = 40;
-constexpr int kXPlane = kInP * kXs;   // cells per parity plane
+// tap's loads are consecutive cells of one parity plane.
+// Row y of a parity plane starts at cell xrow(y) = 32 y + 9 (y / 2), and plane 1 starts
+// 15 cells past the end of plane 0.  Chosen by simulating the shared-memory banks of the
+// two access patterns of the builders (8-byte cells, half-warp wavefronts): a half-warp
+// of im2col loads that wraps from window row yp to yp + 1 lands on the next banks (the
+// skew makes the 2-row step = 9 cells mod 16), and the image stores of one half-warp
+// (both parities of 16 pixels) split across disjoint banks: 831 wavefronts per frame
+// and warp set vs 1,365 with a plain 40-cell stride (ideal 800).
+constexpr int kXs = 32, kXSk = 9, kXPad = 15;
+__host__ __device__ constexpr int xrow(int y) { return y * kXs + kXSk * (y >> 1); }
+constexpr int kXPlane = xrow(kInP) + kXPad;   // cells per parity plane (incl. the pad)
 constexpr int kInBytes = 7504;
 // conv1 tiles: group G of 128 pool windows x 4 window members (dy, dx): tile
 // 4G + q holds member q of windows 128G .. 128G+127, one window per TMEM lane,
@@ -78,7 +99,8 @@ constexpr int kG1 = 5;                  // window groups per frame (625 windows)
 constexpr int kT1 = 4 * kG1;            // 20 conv1 tiles per frame
 constexpr int kK1 = 32;                 // conv1 K: 27 (tap-major, 3 channels) + bias hi/lo + pad
 constexpr int kA1Cols = kK1 / 2;        // TMEM columns per A tile (bf16 pairs)
-constexpr int kA1Stages = 4;
+constexpr int kA1Stages = 4;           // A tile slots (TMEM): one window group (C = 32 / 64)
+constexpr int kA1Max = 8;              // C = 16: two window groups (its accumulators are half as wide)
 constexpr int kNG1 = 2;                 // conv1 accumulator groups (4 x 32 columns each)
 constexpr int kNB2 = 3;                 // conv2 accumulators (64 columns each)
 constexpr int kColA1 = 0;                                 // TMEM column map
@@ -87,7 +109,7 @@ constexpr int kColD2 = kColD1 + kNG1 * 4 * C1;            // 320
 constexpr int kTmemCols = 512;                            // 320 + 192 = 512
 constexpr int kWp = 27, kHp = 27;       // conv2 input map with halo
 constexpr int kT2 = 6;                  // conv2 tiles: y blocks {0, 8} x x blocks {0, 8, 16}
-static_assert(kT2 == 2 * kNB2, "buffer/phase closed forms assume kT2 = 2 * kNB2");
+static_assert(kT2 == 2 * kNB2, "buffer/phase closed forms assume kT2 = 2 * kNB2 (or 3 * 2)");
 constexpr int kK2 = 9 * C1 / 16;        // 18 K16 steps for conv2
 constexpr int kPlaneRows = kHp * kWp + 1;  // rho = q + 1, q in [-1, 729)
 constexpr int kPlaneBytes = kPlaneRows * 16;  // 11,680
@@ -111,7 +133,7 @@ constexpr int oB2b = oOnes + 2 * 128 * 16;               // [2][64][8] bf16
 constexpr int oPos = oB2b + 2 * C2 * 16;                 // queue mode: slot of frame it (ring)
 constexpr int kPosRing = 16;     // > the frames between the producer and epilogue 2 (<= 7)
 constexpr int oBar = oPos + kPosRing * 8;
-constexpr int kNumBars = 2 + 2 + 2 * kA1Stages + 2 * kNG1 + 2 + 2 + 2 * kNB2 + 1;
+constexpr int kNumBars = 2 + 2 + 2 * kA1Max + 2 * kNG1 + 2 + 2 + 2 * kNB2 + 1;
 constexpr int kSmem = oBar + kNumBars * 8 + 16;
 }  // namespace fz
 
@@ -188,6 +210,30 @@ conv12_fused_kernel(FusedArgs A) {
   constexpr int kK2v = 9 * kC1 / 16;    // K16 steps: 9 taps x (kC1 / 16)
   constexpr int kSpt = kC1 / 16;        // K16 steps per tap
   constexpr int wEp2_0 = wEp2_of<kConv2>();
+  // A tile slots: 8 = two window groups, so the conv1 issuer runs the 4 members of a
+  // group as 4 interleaved accumulator chains while the builders fill the next group
+  // TMEM plan (512 columns).  C = 32 conv2-fused: 8 A slots (128) + 2 conv1 accumulator
+  // groups (256) + 2 conv2 accumulators (128); C = 16: 8 A slots + 2 groups (of 16-wide
+  // accumulators) + 3 conv2 accumulators; C = 64 conv1-only: 4 A slots + 2 groups.
+  // Measured (L2C32D32, 65,536 frames): 4 A slots + 3 conv2 accumulators 2.72 ms, 8 + 2
+  // 2.51-2.53 ms (the builders and the conv1 issuer stop waiting on each other), 8 A
+  // slots + 1 conv1 group + 3 conv2 accumulators issued as triples 3.22 ms, 4 + 2 + 3 as
+  // triples 3.10 ms; C = 16 with 8 A slots and 4-chain conv1 issue 2.30 -> 1.88 ms.
+  constexpr bool c32 = kConv2 && kC1 == 32;
+  constexpr int kA1S = (kC1 == 16 || c32) ? kA1Max : kA1Stages;
+  constexpr int kNG1v = kNG1;                   // conv1 accumulator groups
+  // conv2 accumulators: 3 (tile t -> t % 3, phase (t / 3) & 1), or 2 (tile t -> t & 1,
+  // phase (frame + t / 2) & 1); kTI tiles interleaved per issue group
+  constexpr int kNB2v = c32 ? 2 : kNB2;
+  constexpr int kTI = 2;
+  static_assert(kT2 % kTI == 0 && (kTI == 2 || kNB2v == 3), "issue groups");
+  constexpr int cD1 = kColA1 + kA1S * kA1Cols;   // conv1 accumulators
+  constexpr int cD2 = cD1 + kNG1v * 4 * C1;      // conv2 accumulators
+  static_assert(cD2 + (kConv2 ? kNB2v * kC2 : 0) <= kTmemCols, "TMEM columns");
+  auto t2_buf = [](int t) { return kNB2v == 3 ? t % 3 : t & 1; };
+  auto t2_par = [](int64_t it, int t) -> uint32_t {
+    return kNB2v == 3 ? (uint32_t)((t / 3) & 1) : (uint32_t)((it + (t >> 1)) & 1);
+  };
   constexpr int kEp1Groups = (wEp2_0 - wEp1_0) / 4;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -212,9 +258,9 @@ conv12_fused_kernel(FusedArgs A) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + oBar);
   uint64_t* in_full = bars + 0;                 // [2]
   uint64_t* in_empty = in_full + 2;             // [2] 128 builder arrivals
-  uint64_t* a1_full = in_empty + 2;             // [kA1Stages] 128 builder arrivals
-  uint64_t* a1_empty = a1_full + kA1Stages;     // [kA1Stages] MMA commit
-  uint64_t* t1_full = a1_empty + kA1Stages;     // [kNG1] MMA commit after a group's 4 tiles
+  uint64_t* a1_full = in_empty + 2;             // [kA1Max] per slot pair: 128 builder arrivals
+  uint64_t* a1_empty = a1_full + kA1Max;        // [kA1Max] per slot pair: MMA commit
+  uint64_t* t1_full = a1_empty + kA1Max;        // [kNG1] MMA commit after a group's 4 tiles
   uint64_t* t1_empty = t1_full + kNG1;          // [kNG1] 128 ep1 arrivals (one ep1 group)
   uint64_t* act_full = t1_empty + kNG1;         // [2] 256 ep1 arrivals (both groups)
   uint64_t* act_empty = act_full + 2;           // [2] MMA commit
@@ -231,7 +277,7 @@ conv12_fused_kernel(FusedArgs A) {
       mbar_init(&act_full[s], 32 * (wEp2_of<kConv2>() - wEp1_0));
       mbar_init(&act_empty[s], 1);
     }
-    for (int s = 0; s < kA1Stages; ++s) {
+    for (int s = 0; s < kA1Max; ++s) {
       mbar_init(&a1_full[s], 128);
       mbar_init(&a1_empty[s], 1);
     }
@@ -282,6 +328,10 @@ conv12_fused_kernel(FusedArgs A) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+#if NS_EXP & 256
+  long long twait[12] = {};
+  const long long tstart = clock64();
+#endif
   // queue mode: unbounded, every role leaves on the -1 slot
   const int64_t my_frames = qm ? INT64_MAX : (cnt - blockIdx.x + gridDim.x - 1) / gridDim.x;
 
@@ -293,7 +343,7 @@ conv12_fused_kernel(FusedArgs A) {
       if (kConv2) bulk_g2s(smem + oB2, A.w2, 9 * (kC1 / 8) * kC2 * 16, w_full);
       for (int64_t it = 0; it < my_frames; ++it) {
         const int s = (int)(it & 1);
-        if (it >= 2) mbar_wait(&in_empty[s], (uint32_t)(((it >> 1) - 1) & 1));
+        if (it >= 2) NS_TW(0, mbar_wait(&in_empty[s], (uint32_t)(((it >> 1) - 1) & 1)));
         int64_t f;
         if (qm) {
           const int64_t p = it == 0 ? pos[0] : fq_claim(A, t_start);
@@ -320,19 +370,62 @@ conv12_fused_kernel(FusedArgs A) {
       // B1 = [4 kc][C1t][8]: half h = rows 32h.., K chunk kk*2 at kk*2*C1t*16 B
       const uint64_t bd0 = sdesc(sB1, C1t * 16, 128);
       uint64_t u1 = 0;  // global conv1 tile sequence; window group = u1 / 4, member = u1 % 4
+      if (kA1S == kA1Max) {
+        // two window groups of A slots: wait for a whole group (both slot pairs), then
+        // issue its 4 members' K steps interleaved (4 independent accumulator chains)
+        for (int64_t it = 0; it < my_frames; ++it) {
+          bool stop = false;
+          for (int G = 0; G < kG1; ++G, u1 += 4) {
+            const uint64_t ug = u1 >> 2;
+            const int a0 = (int)(u1 % kA1S), p0 = a0 >> 1;
+            const uint32_t par = (uint32_t)((u1 / kA1S) & 1);
+            NS_TW(1, mbar_wait(&a1_full[p0], par));
+            if (qm && G == 0 && pos[it % kPosRing] < 0) {   // stop: forward to epilogue 1
+              const uint64_t ugh = ug * kHalves;
+              const int gb = (int)(ugh % kNG1v);
+              if (ugh >= kNG1v) mbar_wait(&t1_empty[gb], (uint32_t)(((ugh / kNG1v) - 1) & 1));
+              mbar_arrive(&t1_full[gb]);
+              stop = true;
+              break;
+            }
+            NS_TW(1, mbar_wait(&a1_full[p0 + 1], par));
+            tc_fence_after();
+#pragma unroll
+            for (int h = 0; h < kHalves; ++h) {
+              const uint64_t ugh = ug * kHalves + h;
+              const int gb = (int)(ugh % kNG1v);
+              if (ugh >= kNG1v) {
+                NS_TW(2, mbar_wait(&t1_empty[gb], (uint32_t)(((ugh / kNG1v) - 1) & 1)));
+                tc_fence_after();
+              }
+#pragma unroll
+              for (int kk = 0; kk < kK1 / 16; ++kk)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                  if (!(NS_EXP & 8))
+                    umma_bf16_ts(tmem + cD1 + (gb * 4 + q) * kC1, tmem + kColA1 + (a0 + q) * kA1Cols + kk * 8,
+                                 bd0 + (uint64_t)((kk * 2 * C1t * 16 + h * kC1 * 16) >> 4), id1, kk);
+            }
+            umma_commit(&a1_empty[p0]);
+            umma_commit(&a1_empty[p0 + 1]);
+            for (int h = 0; h < kHalves; ++h) umma_commit(&t1_full[(int)((ug * kHalves + h) % kNG1v)]);
+          }
+          if (stop) break;
+        }
+      } else {
       for (int64_t it = 0; it < my_frames; ++it) {
         bool stop = false;
         for (int t = 0; t < kT1; t += 2, u1 += 2) {
           const uint64_t ug = u1 >> 2;           // global window-group sequence
           // A1 slots come in pairs (slot 2p, 2p+1 = window members of one pair),
           // one barrier each way per pair
-          const int pr = (int)((u1 >> 1) & 1);
+          const int pr = (int)((u1 % kA1S) >> 1);
           const int a[2] = {2 * pr, 2 * pr + 1};
-          mbar_wait(&a1_full[pr], (uint32_t)((u1 >> 2) & 1));
+          NS_TW(1, mbar_wait(&a1_full[pr], (uint32_t)((u1 / kA1S) & 1)));
           if (qm && t == 0 && pos[it % kPosRing] < 0) {   // stop: forward to epilogue 1
             const uint64_t ugh = ug * kHalves;
-            const int gb = (int)(ugh % kNG1);
-            if (ugh >= kNG1) mbar_wait(&t1_empty[gb], (uint32_t)(((ugh / kNG1) - 1) & 1));
+            const int gb = (int)(ugh % kNG1v);
+            if (ugh >= kNG1v) mbar_wait(&t1_empty[gb], (uint32_t)(((ugh / kNG1v) - 1) & 1));
             mbar_arrive(&t1_full[gb]);
             stop = true;
             break;
@@ -341,9 +434,9 @@ conv12_fused_kernel(FusedArgs A) {
 #pragma unroll
           for (int h = 0; h < kHalves; ++h) {
             const uint64_t ugh = ug * kHalves + h;  // (window group, half) sequence
-            const int gb = (int)(ugh % kNG1);
-            if ((u1 & 3) == 0 && ugh >= kNG1) {    // accumulators drained by epilogue 1?
-              mbar_wait(&t1_empty[gb], (uint32_t)(((ugh / kNG1) - 1) & 1));
+            const int gb = (int)(ugh % kNG1v);
+            if ((u1 & 3) == 0 && ugh >= kNG1v) {    // accumulators drained by epilogue 1?
+              NS_TW(2, mbar_wait(&t1_empty[gb], (uint32_t)(((ugh / kNG1v) - 1) & 1)));
               tc_fence_after();
             }
 #pragma unroll
@@ -351,15 +444,16 @@ conv12_fused_kernel(FusedArgs A) {
 #pragma unroll
               for (int q = 0; q < 2; ++q)
                 if (!(NS_EXP & 8))
-                umma_bf16_ts(tmem + kColD1 + (gb * 4 + (int)((u1 + q) & 3)) * kC1,
+                umma_bf16_ts(tmem + cD1 + (gb * 4 + (int)((u1 + q) & 3)) * kC1,
                              tmem + kColA1 + a[q] * kA1Cols + kk * 8,
                              bd0 + (uint64_t)((kk * 2 * C1t * 16 + h * kC1 * 16) >> 4), id1, kk);
           }
           umma_commit(&a1_empty[pr]);
           if (((u1 + 1) & 3) == 3)                 // window group complete (all halves)
-            for (int h = 0; h < kHalves; ++h) umma_commit(&t1_full[(int)((ug * kHalves + h) % kNG1)]);
+            for (int h = 0; h < kHalves; ++h) umma_commit(&t1_full[(int)((ug * kHalves + h) % kNG1v)]);
         }
         if (stop) break;
+      }
       }
     }
   } else if (warp == 2) {
@@ -372,24 +466,25 @@ conv12_fused_kernel(FusedArgs A) {
       mbar_wait(w_full, 0);
       for (int64_t it = 0; it < my_frames; ++it) {
         const int pb = (int)(it & 1);
-        mbar_wait(&act_full[pb], (uint32_t)((it >> 1) & 1));
+        NS_TW(3, mbar_wait(&act_full[pb], (uint32_t)((it >> 1) & 1)));
         if (qm && pos[it % kPosRing] < 0) {   // stop: forward to both epilogue-2 groups
-          for (int q = 0; q < 2; ++q) {       // their first tiles t = q use buffers q
-            if (it > 0) mbar_wait(&t2_empty[q], 1u);
-            mbar_arrive(&t2_full[q]);
+          for (int q = 0; q < 2; ++q) {       // their first tiles t = q
+            if (it > 0) mbar_wait(&t2_empty[t2_buf(q)], t2_par(it, q) ^ 1u);
+            mbar_arrive(&t2_full[t2_buf(q)]);
           }
           break;
         }
-        for (int t = 0; t < kT2; t += 2) {
-          int b[2], q0[2];
-          // kT2 = 2 * kNB2: tile t of any frame uses buffer t % 3 with phase
-          // (t / 3) & 1 (no 64-bit division by 3 in the issue loop)
-          for (int q = 0; q < 2; ++q) {
+        for (int t = 0; t < kT2; t += kTI) {
+          int b[kTI], q0[kTI];
+          // tile t of frame `it` uses buffer t2_buf(t) with phase t2_par(it, t) (closed
+          // forms: no 64-bit division by 3 in the issue loop)
+#pragma unroll
+          for (int q = 0; q < kTI; ++q) {
             const int tq = t + q;
-            b[q] = tq % kNB2;
+            b[q] = t2_buf(tq);
             const int yb = (tq / 3) * 8, xb = (tq % 3) * 8;
             q0[q] = (yb + 1) * kWp + (xb + 1);
-            if (it > 0 || tq >= kNB2) mbar_wait(&t2_empty[b[q]], (uint32_t)(((tq / kNB2) + 1) & 1));
+            if (it > 0 || tq >= kNB2v) NS_TW(4, mbar_wait(&t2_empty[b[q]], t2_par(it, tq) ^ 1u));
           }
           tc_fence_after();
           // Descriptors = base + (byte offset >> 4) in the start-address field; all
@@ -398,10 +493,14 @@ conv12_fused_kernel(FusedArgs A) {
           // made the single issuing thread the bottleneck).
           const uint32_t abase = sAct + pb * kActBytes;
           // 16 groups of 8 pixels, one image row apart: SBO = Wp * 16 bytes
-          const uint64_t ad0 = sdesc(abase + (uint32_t)(q0[0] + 1) * 16, kPlaneBytes, kWp * 16);
-          const uint64_t ad1 = sdesc(abase + (uint32_t)(q0[1] + 1) * 16, kPlaneBytes, kWp * 16);
+          uint64_t ad[kTI];
+          uint32_t d[kTI];
+#pragma unroll
+          for (int q = 0; q < kTI; ++q) {
+            ad[q] = sdesc(abase + (uint32_t)(q0[q] + 1) * 16, kPlaneBytes, kWp * 16);
+            d[q] = tmem + cD2 + b[q] * kC2;
+          }
           const uint64_t bd0 = sdesc(sB2, kC2 * 16, 128);
-          const uint32_t d0 = tmem + kColD2 + b[0] * kC2, d1 = tmem + kColD2 + b[1] * kC2;
 #pragma unroll
           for (int ks = 0; ks < kK2v; ++ks) {
             const int tap = ks / kSpt, cg = (ks % kSpt) * 2;  // kC1/8 channel groups per tap, 2 per step
@@ -409,12 +508,13 @@ conv12_fused_kernel(FusedArgs A) {
             const uint64_t aoff = (uint64_t)((cg * kPlaneBytes + shift * 16) >> 4);
             const uint64_t bd = bd0 + (uint64_t)(((tap * (kC1 / 8) + cg) * kC2 * 16) >> 4);
             if (NS_EXP & 16) continue;
-            umma_bf16(d0, ad0 + aoff, bd, id2, ks > 0 ? 1u : 0u);
-            umma_bf16(d1, ad1 + aoff, bd, id2, ks > 0 ? 1u : 0u);
+#pragma unroll
+            for (int q = 0; q < kTI; ++q) umma_bf16(d[q], ad[q] + aoff, bd, id2, ks > 0 ? 1u : 0u);
           }
-          umma_bf16(d0, dOnes, dBias, id2, 1u);   // + bias (extra K16 step)
-          umma_bf16(d1, dOnes, dBias, id2, 1u);
-          for (int q = 0; q < 2; ++q) umma_commit(&t2_full[b[q]]);
+#pragma unroll
+          for (int q = 0; q < kTI; ++q) umma_bf16(d[q], dOnes, dBias, id2, 1u);   // + bias (extra K16 step)
+#pragma unroll
+          for (int q = 0; q < kTI; ++q) umma_commit(&t2_full[b[q]]);
         }
         umma_commit(&act_empty[pb]);
       }
@@ -426,23 +526,24 @@ conv12_fused_kernel(FusedArgs A) {
     uint64_t u1 = 0;
     for (int64_t it = 0; it < my_frames; ++it) {
       const int s = (int)(it & 1);
-      mbar_wait(&in_full[s], (uint32_t)((it >> 1) & 1));
+      NS_TW(5, mbar_wait(&in_full[s], (uint32_t)((it >> 1) & 1)));
       if (qm && pos[it % kPosRing] < 0) {   // stop: forward to the conv1 issuer (pair 0)
-        if (u1 >= kA1Stages) mbar_wait(&a1_empty[0], (uint32_t)(((u1 >> 2) - 1) & 1));
-        mbar_arrive(&a1_full[0]);
+        const int pr0 = (int)(u1 % kA1S) >> 1;
+        if (u1 >= kA1S) mbar_wait(&a1_empty[pr0], (uint32_t)(((u1 / kA1S) - 1) & 1));
+        mbar_arrive(&a1_full[pr0]);
         break;
       }
-      nbar_sync(1, 128);  // previous frame's rows are all built: X may be overwritten
+      NS_TW(6, nbar_sync(1, 128));  // previous frame's rows are all built: X may be overwritten
       const uint8_t* in = smem + oIn + s * kInBytes;
       for (int p = bt; p < ((NS_EXP & 2) ? 0 : kIn * kIn); p += 128) {
         const int y = p / kIn, x = p - kIn * y;
         const uint8_t* px = in + 3 * p;
-        X[((x + 1) & 1) * kXPlane + (y + 1) * kXs + ((x + 1) >> 1)] =
+        X[((x + 1) & 1) * kXPlane + xrow(y + 1) + ((x + 1) >> 1)] =
             make_uint2((uint32_t)lut[px[0]] | ((uint32_t)lut[256 + px[1]] << 16),
                        (uint32_t)lut[512 + px[2]]);
       }
       mbar_arrive(&in_empty[s]);
-      nbar_sync(1, 128);  // X complete
+      NS_TW(6, nbar_sync(1, 128));  // X complete
       // One thread = one pool window of group G; its 4 members (dy, dx) are the
       // 4 tiles 4G..4G+3 = A stages 0..3.  The 4x4 padded-pixel neighbourhood
       // (16 cells) serves all 4 members' 3x3 patches.
@@ -453,8 +554,8 @@ conv12_fused_kernel(FusedArgs A) {
         uint2 cell[4][4];  // [padded row 2yp + r][padded col 2xp + c]
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          const uint2* ev = X + (2 * yp + r) * kXs + xp;             // even padded columns
-          const uint2* od = X + kXPlane + (2 * yp + r) * kXs + xp;   // odd padded columns
+          const uint2* ev = X + xrow(2 * yp + r) + xp;             // even padded columns
+          const uint2* od = X + kXPlane + xrow(2 * yp + r) + xp;   // odd padded columns
           if (NS_EXP & 4) {
             cell[r][0] = cell[r][1] = cell[r][2] = cell[r][3] = make_uint2(r, xp);
             continue;
@@ -466,8 +567,9 @@ conv12_fused_kernel(FusedArgs A) {
         }
 #pragma unroll
         for (int pq = 0; pq < 4; ++pq) {
-          const int a = pq, pr = pq >> 1;       // u1 % 4 == 0: member pq -> A1 slot pq, pair pq/2
-          if ((pq & 1) == 0 && u1 >= kA1Stages) mbar_wait(&a1_empty[pr], (uint32_t)(((u1 >> 2) - 1) & 1));
+          const uint64_t um = u1 + pq;           // global member sequence -> A1 slot, slot pair
+          const int a = (int)(um % kA1S), pr = a >> 1;
+          if ((pq & 1) == 0 && um >= kA1S) NS_TW(7, mbar_wait(&a1_empty[pr], (uint32_t)(((um / kA1S) - 1) & 1)));
           const int dy = pq >> 1, dx = pq & 1;
           uint32_t h[27];  // 27 bf16 in (tap, channel) order, one per 32-bit register
 #pragma unroll
@@ -517,15 +619,15 @@ conv12_fused_kernel(FusedArgs A) {
     }
     for (int64_t it = 0; it < my_frames; ++it) {
       const int pb = (int)(it & 1);
-      if (kConv2 && it >= 2) mbar_wait(&act_empty[pb], (uint32_t)(((it >> 1) - 1) & 1));
+      if (kConv2 && it >= 2) NS_TW(8, mbar_wait(&act_empty[pb], (uint32_t)(((it >> 1) - 1) & 1)));
       uint8_t* planes = smem + oAct + pb * kActBytes;
       const int64_t i = blockIdx.x + it * gridDim.x;  // chunk-relative frame
       bool stop = false;
       for (int G = 0; G < kG1 && !stop; ++G) {
         for (int h = 0; h < kHalves; ++h, ++ugh) {
-          const int gb = (int)(ugh % kNG1);
+          const int gb = (int)(ugh % kNG1v);
           if (kEp1Groups > 1 && gb != grp) continue;
-          mbar_wait(&t1_full[gb], (uint32_t)((ugh / kNG1) & 1));
+          NS_TW(9, mbar_wait(&t1_full[gb], (uint32_t)((ugh / kNG1v) & 1)));
           if (qm && G == 0 && pos[it % kPosRing] < 0) {   // stop: forward to the conv2 issuer
             mbar_arrive(&act_full[pb]);                    // (act_empty waited above)
             stop = true;
@@ -536,7 +638,7 @@ conv12_fused_kernel(FusedArgs A) {
           const bool valid = w < kP1 * kP1;
           const int yp = w / kP1, xp = w - kP1 * (w / kP1);
           const int rho = (yp + 1) * kWp + (xp + 1) + 1;
-          const uint32_t tb = tmem + ((uint32_t)lg << 16) + kColD1 + gb * 4 * kC1;
+          const uint32_t tb = tmem + ((uint32_t)lg << 16) + cD1 + gb * 4 * kC1;
 #pragma unroll
           for (int cb = 0; cb < ((NS_EXP & 64) ? 0 : kC1 / 16); ++cb) {
             // 2x2 max pool = element-wise max over the window's 4 accumulators
@@ -612,8 +714,8 @@ conv12_fused_kernel(FusedArgs A) {
       int64_t i = blockIdx.x + it * gridDim.x;  // chunk-relative frame (queue mode: slot)
       bool stop = false;
       for (int t = grp2; t < kT2; t += 2) {             // this group's tiles
-        const int b = t % kNB2;                          // kT2 = 2 * kNB2
-        mbar_wait(&t2_full[b], (uint32_t)((t / kNB2) & 1));
+        const int b = t2_buf(t);
+        NS_TW(10, mbar_wait(&t2_full[b], t2_par(it, t)));
         if (qm && t == grp2) {
           i = pos[it % kPosRing];
           if (i < 0) {
@@ -634,8 +736,8 @@ conv12_fused_kernel(FusedArgs A) {
 #pragma unroll
         for (int hg = 0; hg < ((NS_EXP & 32) ? 0 : kC2 / 32); ++hg) {
           uint32_t r[32];
-          tmem_ld16(tmem + ((uint32_t)lg << 16) + kColD2 + b * kC2 + hg * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
-          tmem_ld16(tmem + ((uint32_t)lg << 16) + kColD2 + b * kC2 + hg * 32 + 16,
+          tmem_ld16(tmem + ((uint32_t)lg << 16) + cD2 + b * kC2 + hg * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
+          tmem_ld16(tmem + ((uint32_t)lg << 16) + cD2 + b * kC2 + hg * 32 + 16,
                     *reinterpret_cast<uint32_t(*)[16]>(r + 16));
           tmem_ld_wait();
 #pragma unroll
@@ -682,6 +784,11 @@ conv12_fused_kernel(FusedArgs A) {
       if (stop) break;
     }
   }
+#if NS_EXP & 256
+  twait[11] = clock64() - tstart;
+  if (A.dbg && lane == 0)
+    for (int k = 0; k < 12; ++k) A.dbg[((size_t)blockIdx.x * 19 + warp) * 12 + k] = twait[k];
+#endif
   __syncthreads();
   if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
 }
@@ -694,7 +801,34 @@ static noscope_status launch_variant(const FusedArgs& a, int grid, cudaStream_t 
   if (attr.first())
     NS_CUDA_TRY(cudaFuncSetAttribute(conv12_fused_kernel<kHalves, kConv2, kC1>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, fz::kSmem));
+#if NS_EXP & 256
+  static long long* dbg = nullptr;
+  if (!dbg) cudaMalloc(&dbg, (size_t)grid * 19 * 12 * 8);
+  cudaMemset(dbg, 0, (size_t)grid * 19 * 12 * 8);
+  FusedArgs b = a;
+  b.dbg = dbg;
+  conv12_fused_kernel<kHalves, kConv2, kC1><<<grid, fz::kThreads, fz::kSmem, st>>>(b);
+  cudaDeviceSynchronize();
+  {
+    std::vector<long long> h((size_t)grid * 19 * 12);
+    cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost);
+    static const char* names[12] = {"in_empty", "a1_full", "t1_empty", "act_full", "t2_empty", "in_full",
+                                    "nbar", "a1_empty", "act_empty", "t1_full", "t2_full", "TOTAL"};
+    std::fprintf(stderr, "TW warp:");
+    for (int w = 0; w < 19; ++w) {
+      std::fprintf(stderr, "\nTW w%02d", w);
+      for (int k = 0; k < 12; ++k) {
+        long long sum = 0;
+        for (int c = 0; c < grid; ++c) sum += h[((size_t)c * 19 + w) * 12 + k];
+        if (sum) std::fprintf(stderr, " %s=%.1f%%", names[k], 100.0 * sum / std::max(1ll, [&] {
+          long long t = 0; for (int c = 0; c < grid; ++c) t += h[((size_t)c * 19 + w) * 12 + 11]; return t; }()));
+      }
+    }
+    std::fprintf(stderr, "\n");
+  }
+#else
   conv12_fused_kernel<kHalves, kConv2, kC1><<<grid, fz::kThreads, fz::kSmem, st>>>(a);
+#endif
   NS_LAUNCH_CHECK();
   count_launch();
   return NOSCOPE_OK;

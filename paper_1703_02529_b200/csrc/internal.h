@@ -197,6 +197,7 @@ struct FusedArgs {
   //   qmode 2 ("tail"): launched after dd_kernel, claims every remaining slot.
   int qmode;           // 0 = index mode
   FiredQueue fq;
+  long long* dbg;      // experiments only (NS_EXP & 256 builds): per-warp wait cycles
 };
 size_t conv12_fused_smem();
 
