@@ -99,14 +99,11 @@ constexpr int kG1 = 5;                  // window groups per frame (625 windows)
 constexpr int kT1 = 4 * kG1;            // 20 conv1 tiles per frame
 constexpr int kK1 = 32;                 // conv1 K: 27 (tap-major, 3 channels) + bias hi/lo + pad
 constexpr int kA1Cols = kK1 / 2;        // TMEM columns per A tile (bf16 pairs)
-constexpr int kA1Stages = 4;           // A tile slots (TMEM): one window group (C = 32 / 64)
-constexpr int kA1Max = 8;              // C = 16: two window groups (its accumulators are half as wide)
+constexpr int kA1Max = 8;              // A tile slots (TMEM): two window groups
 constexpr int kNG1 = 2;                 // conv1 accumulator groups (4 x 32 columns each)
 constexpr int kNB2 = 3;                 // conv2 accumulators (64 columns each)
 constexpr int kColA1 = 0;                                 // TMEM column map
-constexpr int kColD1 = kColA1 + kA1Stages * kA1Cols;      // 64
-constexpr int kColD2 = kColD1 + kNG1 * 4 * C1;            // 320
-constexpr int kTmemCols = 512;                            // 320 + 192 = 512
+constexpr int kTmemCols = 512;                            // per-variant plans: see the kernel
 constexpr int kWp = 27, kHp = 27;       // conv2 input map with halo
 constexpr int kT2 = 6;                  // conv2 tiles: y blocks {0, 8} x x blocks {0, 8, 16}
 static_assert(kT2 == 2 * kNB2, "buffer/phase closed forms assume kT2 = 2 * kNB2 (or 3 * 2)");
@@ -133,7 +130,8 @@ constexpr int oB2b = oOnes + 2 * 128 * 16;               // [2][64][8] bf16
 constexpr int oPos = oB2b + 2 * C2 * 16;                 // queue mode: slot of frame it (ring)
 constexpr int kPosRing = 16;     // > the frames between the producer and epilogue 2 (<= 7)
 constexpr int oBar = oPos + kPosRing * 8;
-constexpr int kNumBars = 2 + 2 + 2 * kA1Max + 2 * kNG1 + 2 + 2 + 2 * kNB2 + 1;
+constexpr int kNG1Max = 3;              // C = 64 conv1-only: 3 accumulator groups
+constexpr int kNumBars = 2 + 2 + 2 * kA1Max + 2 * kNG1Max + 2 + 2 + 2 * kNB2 + 1;
 constexpr int kSmem = oBar + kNumBars * 8 + 16;
 }  // namespace fz
 
@@ -214,14 +212,18 @@ conv12_fused_kernel(FusedArgs A) {
   // group as 4 interleaved accumulator chains while the builders fill the next group
   // TMEM plan (512 columns).  C = 32 conv2-fused: 8 A slots (128) + 2 conv1 accumulator
   // groups (256) + 2 conv2 accumulators (128); C = 16: 8 A slots + 2 groups (of 16-wide
-  // accumulators) + 3 conv2 accumulators; C = 64 conv1-only: 4 A slots + 2 groups.
+  // accumulators) + 3 conv2 accumulators; C = 64 conv1-only: 8 A slots + 3 groups of
+  // (window group, half) accumulators (384): L2C64D32 9.18 -> 8.32-8.43 ms (4 slots + 2
+  // groups -> 8 + 2 -> 8 + 3; both halves' chains interleaved measured no better).
   // Measured (L2C32D32, 65,536 frames): 4 A slots + 3 conv2 accumulators 2.72 ms, 8 + 2
   // 2.51-2.53 ms (the builders and the conv1 issuer stop waiting on each other), 8 A
   // slots + 1 conv1 group + 3 conv2 accumulators issued as triples 3.22 ms, 4 + 2 + 3 as
   // triples 3.10 ms; C = 16 with 8 A slots and 4-chain conv1 issue 2.30 -> 1.88 ms.
   constexpr bool c32 = kConv2 && kC1 == 32;
-  constexpr int kA1S = (kC1 == 16 || c32) ? kA1Max : kA1Stages;
-  constexpr int kNG1v = kNG1;                   // conv1 accumulator groups
+  constexpr int kA1S = kA1Max;
+  // conv1 accumulator groups ((window group, half) units in flight): 3 for the C = 64
+  // conv1-only variant (its 8 A slots + 3 x 128 accumulator columns = 512)
+  constexpr int kNG1v = (!kConv2 && kA1S == kA1Max) ? kNG1Max : kNG1;
   // conv2 accumulators: 3 (tile t -> t % 3, phase (t / 3) & 1), or 2 (tile t -> t & 1,
   // phase (frame + t / 2) & 1); kTI tiles interleaved per issue group
   constexpr int kNB2v = c32 ? 2 : kNB2;
@@ -260,9 +262,9 @@ conv12_fused_kernel(FusedArgs A) {
   uint64_t* in_empty = in_full + 2;             // [2] 128 builder arrivals
   uint64_t* a1_full = in_empty + 2;             // [kA1Max] per slot pair: 128 builder arrivals
   uint64_t* a1_empty = a1_full + kA1Max;        // [kA1Max] per slot pair: MMA commit
-  uint64_t* t1_full = a1_empty + kA1Max;        // [kNG1] MMA commit after a group's 4 tiles
-  uint64_t* t1_empty = t1_full + kNG1;          // [kNG1] 128 ep1 arrivals (one ep1 group)
-  uint64_t* act_full = t1_empty + kNG1;         // [2] 256 ep1 arrivals (both groups)
+  uint64_t* t1_full = a1_empty + kA1Max;        // [kNG1Max] MMA commit after a group's 4 tiles
+  uint64_t* t1_empty = t1_full + kNG1Max;       // [kNG1Max] 128 ep1 arrivals (one ep1 group)
+  uint64_t* act_full = t1_empty + kNG1Max;      // [2] 256 ep1 arrivals (both groups)
   uint64_t* act_empty = act_full + 2;           // [2] MMA commit
   uint64_t* t2_full = act_empty + 2;            // [kNB2] MMA commit
   uint64_t* t2_empty = t2_full + kNB2;          // [kNB2] 128 ep2 arrivals
@@ -281,7 +283,7 @@ conv12_fused_kernel(FusedArgs A) {
       mbar_init(&a1_full[s], 128);
       mbar_init(&a1_empty[s], 1);
     }
-    for (int s = 0; s < kNG1; ++s) {
+    for (int s = 0; s < kNG1Max; ++s) {
       mbar_init(&t1_full[s], 1);
       mbar_init(&t1_empty[s], 128);
     }
@@ -370,59 +372,16 @@ conv12_fused_kernel(FusedArgs A) {
       // B1 = [4 kc][C1t][8]: half h = rows 32h.., K chunk kk*2 at kk*2*C1t*16 B
       const uint64_t bd0 = sdesc(sB1, C1t * 16, 128);
       uint64_t u1 = 0;  // global conv1 tile sequence; window group = u1 / 4, member = u1 % 4
-      if (kA1S == kA1Max) {
-        // two window groups of A slots: wait for a whole group (both slot pairs), then
-        // issue its 4 members' K steps interleaved (4 independent accumulator chains)
-        for (int64_t it = 0; it < my_frames; ++it) {
-          bool stop = false;
-          for (int G = 0; G < kG1; ++G, u1 += 4) {
-            const uint64_t ug = u1 >> 2;
-            const int a0 = (int)(u1 % kA1S), p0 = a0 >> 1;
-            const uint32_t par = (uint32_t)((u1 / kA1S) & 1);
-            NS_TW(1, mbar_wait(&a1_full[p0], par));
-            if (qm && G == 0 && pos[it % kPosRing] < 0) {   // stop: forward to epilogue 1
-              const uint64_t ugh = ug * kHalves;
-              const int gb = (int)(ugh % kNG1v);
-              if (ugh >= kNG1v) mbar_wait(&t1_empty[gb], (uint32_t)(((ugh / kNG1v) - 1) & 1));
-              mbar_arrive(&t1_full[gb]);
-              stop = true;
-              break;
-            }
-            NS_TW(1, mbar_wait(&a1_full[p0 + 1], par));
-            tc_fence_after();
-#pragma unroll
-            for (int h = 0; h < kHalves; ++h) {
-              const uint64_t ugh = ug * kHalves + h;
-              const int gb = (int)(ugh % kNG1v);
-              if (ugh >= kNG1v) {
-                NS_TW(2, mbar_wait(&t1_empty[gb], (uint32_t)(((ugh / kNG1v) - 1) & 1)));
-                tc_fence_after();
-              }
-#pragma unroll
-              for (int kk = 0; kk < kK1 / 16; ++kk)
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                  if (!(NS_EXP & 8))
-                    umma_bf16_ts(tmem + cD1 + (gb * 4 + q) * kC1, tmem + kColA1 + (a0 + q) * kA1Cols + kk * 8,
-                                 bd0 + (uint64_t)((kk * 2 * C1t * 16 + h * kC1 * 16) >> 4), id1, kk);
-            }
-            umma_commit(&a1_empty[p0]);
-            umma_commit(&a1_empty[p0 + 1]);
-            for (int h = 0; h < kHalves; ++h) umma_commit(&t1_full[(int)((ug * kHalves + h) % kNG1v)]);
-          }
-          if (stop) break;
-        }
-      } else {
+      // two window groups of A slots: wait for a whole group (both slot pairs), then
+      // issue its 4 members' K steps interleaved (4 independent accumulator chains)
       for (int64_t it = 0; it < my_frames; ++it) {
         bool stop = false;
-        for (int t = 0; t < kT1; t += 2, u1 += 2) {
-          const uint64_t ug = u1 >> 2;           // global window-group sequence
-          // A1 slots come in pairs (slot 2p, 2p+1 = window members of one pair),
-          // one barrier each way per pair
-          const int pr = (int)((u1 % kA1S) >> 1);
-          const int a[2] = {2 * pr, 2 * pr + 1};
-          NS_TW(1, mbar_wait(&a1_full[pr], (uint32_t)((u1 / kA1S) & 1)));
-          if (qm && t == 0 && pos[it % kPosRing] < 0) {   // stop: forward to epilogue 1
+        for (int G = 0; G < kG1; ++G, u1 += 4) {
+          const uint64_t ug = u1 >> 2;
+          const int a0 = (int)(u1 % kA1S), p0 = a0 >> 1;
+          const uint32_t par = (uint32_t)((u1 / kA1S) & 1);
+          NS_TW(1, mbar_wait(&a1_full[p0], par));
+          if (qm && G == 0 && pos[it % kPosRing] < 0) {   // stop: forward to epilogue 1
             const uint64_t ugh = ug * kHalves;
             const int gb = (int)(ugh % kNG1v);
             if (ugh >= kNG1v) mbar_wait(&t1_empty[gb], (uint32_t)(((ugh / kNG1v) - 1) & 1));
@@ -430,30 +389,29 @@ conv12_fused_kernel(FusedArgs A) {
             stop = true;
             break;
           }
+          NS_TW(1, mbar_wait(&a1_full[p0 + 1], par));
           tc_fence_after();
 #pragma unroll
           for (int h = 0; h < kHalves; ++h) {
-            const uint64_t ugh = ug * kHalves + h;  // (window group, half) sequence
+            const uint64_t ugh = ug * kHalves + h;
             const int gb = (int)(ugh % kNG1v);
-            if ((u1 & 3) == 0 && ugh >= kNG1v) {    // accumulators drained by epilogue 1?
+            if (ugh >= kNG1v) {
               NS_TW(2, mbar_wait(&t1_empty[gb], (uint32_t)(((ugh / kNG1v) - 1) & 1)));
               tc_fence_after();
             }
 #pragma unroll
             for (int kk = 0; kk < kK1 / 16; ++kk)
 #pragma unroll
-              for (int q = 0; q < 2; ++q)
+              for (int q = 0; q < 4; ++q)
                 if (!(NS_EXP & 8))
-                umma_bf16_ts(tmem + cD1 + (gb * 4 + (int)((u1 + q) & 3)) * kC1,
-                             tmem + kColA1 + a[q] * kA1Cols + kk * 8,
-                             bd0 + (uint64_t)((kk * 2 * C1t * 16 + h * kC1 * 16) >> 4), id1, kk);
+                  umma_bf16_ts(tmem + cD1 + (gb * 4 + q) * kC1, tmem + kColA1 + (a0 + q) * kA1Cols + kk * 8,
+                               bd0 + (uint64_t)((kk * 2 * C1t * 16 + h * kC1 * 16) >> 4), id1, kk);
           }
-          umma_commit(&a1_empty[pr]);
-          if (((u1 + 1) & 3) == 3)                 // window group complete (all halves)
-            for (int h = 0; h < kHalves; ++h) umma_commit(&t1_full[(int)((ug * kHalves + h) % kNG1v)]);
+          umma_commit(&a1_empty[p0]);
+          umma_commit(&a1_empty[p0 + 1]);
+          for (int h = 0; h < kHalves; ++h) umma_commit(&t1_full[(int)((ug * kHalves + h) % kNG1v)]);
         }
         if (stop) break;
-      }
       }
     }
   } else if (warp == 2) {
@@ -626,7 +584,7 @@ conv12_fused_kernel(FusedArgs A) {
       for (int G = 0; G < kG1 && !stop; ++G) {
         for (int h = 0; h < kHalves; ++h, ++ugh) {
           const int gb = (int)(ugh % kNG1v);
-          if (kEp1Groups > 1 && gb != grp) continue;
+          if (kEp1Groups > 1 && (int)(ugh % kEp1Groups) != grp) continue;   // alternate units
           NS_TW(9, mbar_wait(&t1_full[gb], (uint32_t)((ugh / kNG1v) & 1)));
           if (qm && G == 0 && pos[it % kPosRing] < 0) {   // stop: forward to the conv2 issuer
             mbar_arrive(&act_full[pb]);                    // (act_empty waited above)
