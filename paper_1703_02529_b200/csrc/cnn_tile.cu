@@ -18,6 +18,23 @@
 #include "common.cuh"
 #include "internal.h"
 
+#ifndef NS_EXP
+#define NS_EXP 0   // 256: per-role wait-time accounting (timing experiments only)
+#endif
+#if NS_EXP & 256
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+#define NS_TT(k, stmt)                 \
+  do {                                 \
+    const long long _t0 = clock64();   \
+    stmt;                              \
+    twait[k] += clock64() - _t0;       \
+  } while (0)
+#else
+#define NS_TT(k, stmt) stmt
+#endif
+
 namespace ns {
 
 namespace gt {
@@ -116,6 +133,10 @@ convt_kernel(ConvGArgs A) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+#if NS_EXP & 256
+  long long twait[8] = {};
+  const long long tstart = clock64();
+#endif
 
   if (warp == 10) {
     // ============================================== A producer
@@ -125,7 +146,7 @@ convt_kernel(ConvGArgs A) {
         const int64_t u = blockIdx.x + it * gridDim.x;
         const int64_t r0 = (int64_t)G + 16 * u * Wq - 1;   // image row 16u, column -1
         for (int cp = 0; cp < ncgp; ++cp) {
-          if (fill >= (uint32_t)g.nA) mbar_wait(&a_empty[st], ph ^ 1);
+          if (fill >= (uint32_t)g.nA) NS_TT(0, mbar_wait(&a_empty[st], ph ^ 1));
           else ++fill;
           mbar_arrive_expect_tx(&a_full[st], astage);
           for (int h = 0; h < 2; ++h)
@@ -142,7 +163,7 @@ convt_kernel(ConvGArgs A) {
       uint32_t st = 0, ph = 0, fill = 0;
       for (int64_t it = 0; it < my_units; ++it)
         for (int s = 0; s < g.steps; s += 3) {
-          if (fill >= (uint32_t)g.bstages) mbar_wait(&b_empty[st], ph ^ 1);
+          if (fill >= (uint32_t)g.bstages) NS_TT(1, mbar_wait(&b_empty[st], ph ^ 1));
           else ++fill;
           mbar_arrive_expect_tx(&b_full[st], bbytes);
           bulk_g2s(smem + g.oB + (size_t)st * bbytes, A.wpack + (size_t)s * (bbytes / 3), bbytes, &b_full[st]);
@@ -166,16 +187,16 @@ convt_kernel(ConvGArgs A) {
         uint32_t col[3];
         for (int x = 0; x < XB; ++x) {
           const uint32_t t = tseq + x, sl = t % gt::kSlots;
-          if (t >= (uint32_t)gt::kSlots) mbar_wait(&t_empty[sl], ((t / gt::kSlots) - 1) & 1u);
+          if (t >= (uint32_t)gt::kSlots) NS_TT(2, mbar_wait(&t_empty[sl], ((t / gt::kSlots) - 1) & 1u));
           col[x] = tmem + sl * 128;
         }
         tc_fence_after();
         for (int cp = 0; cp < ncgp; ++cp) {
-          mbar_wait(&a_full[ast], aph);
+          NS_TT(3, mbar_wait(&a_full[ast], aph));
           const uint64_t ac = ad0 + (uint64_t)(ast * astep);
 #pragma unroll
           for (int ky = 0; ky < 3; ++ky) {          // B stage = taps (ky, 0..2)
-            mbar_wait(&b_full[bst], bph);
+            NS_TT(4, mbar_wait(&b_full[bst], bph));
             tc_fence_after();
             const uint64_t bs = bd0 + (uint64_t)(bst * bstage);
 #pragma unroll
@@ -222,7 +243,7 @@ convt_kernel(ConvGArgs A) {
       for (int x = 0; x < XB; ++x, ++tseq) {
         if ((int)(tseq & 1) != eg) continue;
         const uint32_t sl = tseq % gt::kSlots;
-        mbar_wait(&t_full[sl], (tseq / gt::kSlots) & 1u);
+        NS_TT(5, mbar_wait(&t_full[sl], (tseq / gt::kSlots) & 1u));
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(lq * 32) << 16) + sl * 128;
         uint32_t pk[64];
@@ -275,6 +296,11 @@ convt_kernel(ConvGArgs A) {
     }
   }
   __syncthreads();
+#if NS_EXP & 256
+  twait[7] = clock64() - tstart;
+  if (A.dbg && lane == 0)
+    for (int k = 0; k < 8; ++k) A.dbg[((size_t)blockIdx.x * 11 + warp) * 8 + k] = twait[k];
+#endif
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
@@ -285,7 +311,33 @@ noscope_status launch_convt(const ConvGArgs& a, cudaStream_t st) {
   const ConvGGeom& g = a.g;
   const int64_t umax = (a.chunk_len * (g.H + 1) + 15) / 16;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(umax, kNumSMs));
+#if NS_EXP & 256
+  static long long* dbg = nullptr;
+  if (!dbg) cudaMalloc(&dbg, (size_t)grid * 11 * 8 * 8);
+  cudaMemset(dbg, 0, (size_t)grid * 11 * 8 * 8);
+  ConvGArgs b = a;
+  b.dbg = dbg;
+  convt_kernel<<<grid, gt::kThreads, g.smem, st>>>(b);
+  cudaDeviceSynchronize();
+  {
+    std::vector<long long> h((size_t)grid * 11 * 8);
+    cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost);
+    static const char* nm[8] = {"a_empty", "b_empty", "t_empty", "a_full", "b_full", "t_full", "-", "TOTAL"};
+    for (int w = 0; w < 11; ++w) {
+      long long tot = 0;
+      for (int c = 0; c < grid; ++c) tot += h[((size_t)c * 11 + w) * 8 + 7];
+      std::fprintf(stderr, "TT w%02d", w);
+      for (int k = 0; k < 7; ++k) {
+        long long sm = 0;
+        for (int c = 0; c < grid; ++c) sm += h[((size_t)c * 11 + w) * 8 + k];
+        if (sm) std::fprintf(stderr, " %s=%.1f%%", nm[k], 100.0 * sm / std::max(1ll, tot));
+      }
+      std::fprintf(stderr, "\n");
+    }
+  }
+#else
   convt_kernel<<<grid, gt::kThreads, g.smem, st>>>(a);
+#endif
   NS_LAUNCH_CHECK();
   count_launch();
   return NOSCOPE_OK;

@@ -235,6 +235,7 @@ struct ConvGArgs {
   int K_feat;
   const int64_t* n_dev;
   int64_t n_max, chunk_base, chunk_len;
+  long long* dbg;          // experiments only (NS_EXP & 256 builds)
 };
 noscope_status launch_convg(const ConvGArgs& a, cudaStream_t st);
 bool make_convt_geom(int cin, int cout, int H, int64_t chunk, ConvGGeom* g);

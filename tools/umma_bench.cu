@@ -115,8 +115,14 @@ void run() {
 }
 
 int main() {
-  run<128, 3, false, 416, 0, 16, 128, 0>(); run<128, 3, false, 416, 0, 16, 128, 1>();
-  run<128, 3, false, 416, 0, 16, 128, 3>(); run<128, 2, false, 128, 0, 16, 128, 1>();
-  run<256, 2, false, 128, 0, 16, 128, 1>(); run<64, 2, false, 432, 0, 16, 128, 1>();
+  // aligned vs unaligned A start (16-B shifts per K step) at the conv SBOs: convt (N = 128,
+  // 3 accumulators, SBO = 26 px * 16 B) and the fused conv2 (N = 64, 2 accumulators, SBO = 27 px)
+  run<128, 3, false, 416, 0, 0, 128, 0>(); run<128, 3, false, 416, 0, 16, 128, 0>();
+  run<128, 3, false, 512, 0, 0, 128, 0>(); run<128, 3, false, 128, 0, 0, 128, 0>();
+  run<128, 4, false, 128, 0, 0, 128, 0>();
+  run<64, 2, false, 432, 0, 0, 128, 0>(); run<64, 2, false, 432, 0, 16, 128, 0>();
+  run<64, 2, false, 512, 0, 0, 128, 0>(); run<64, 2, false, 128, 0, 0, 128, 0>();
+  run<64, 4, false, 128, 0, 0, 128, 0>();
+  run<128, 3, true>(); run<64, 2, true>();
   return 0;
 }
