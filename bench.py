@@ -841,17 +841,21 @@ def run_extras(device, timing=(1000, 20000, 12_500_000_000)):
     return out
 
 
-def _time_ms(fn, reps=3):
+def _time_ms(fn, reps=3, rounds=5):
+    """Median over `rounds` of the mean time of `reps` back-to-back calls (after one warm-up)."""
     import torch
     fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        fn()
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps
+    ts = []
+    for _ in range(rounds):
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / reps)
+    return float(np.median(ts))
 
 
 def tiny_config(device):

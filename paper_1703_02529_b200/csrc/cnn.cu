@@ -23,6 +23,10 @@ namespace ns {
 constexpr int kCnnThreads = 128;
 constexpr int kBStages = 4;
 constexpr int64_t kCnnChunk = 32768;  // frames per internal chunk (workspace bound)
+// L = 2 with conv2 fused: the only chunk-sized buffers are the FC features (K x 2 B per
+// frame), so one chunk covers a whole webcam hour (no empty per-chunk launches when the
+// device count is far below n_max)
+constexpr int64_t kCnnChunkFusedL2 = 262144;
 
 NS_DEV uint16_t f2bf(float v) {
   __nv_bfloat16 h = __float2bfloat16_rn(v);
@@ -226,7 +230,7 @@ static bool make_plan(const noscope_cnn_arch& a, int64_t n_max, CnnPlan* P, bool
   p.fused = p.C == 32 || p.C == 16;
   p.first_g = p.fused ? 2 : 1;
   p.chunk = std::max<int64_t>(128, (n_max + 127) / 128 * 128);
-  if (!whole) p.chunk = std::min<int64_t>(kCnnChunk, p.chunk);
+  if (!whole) p.chunk = std::min<int64_t>(p.fused && p.L == 2 ? kCnnChunkFusedL2 : kCnnChunk, p.chunk);
   size_t off = 256;  // status words etc. live before the CNN region (caller offset)
   p.w1_off = off;
   off = align_up(off + (size_t)p.C * 32 * 2, 256);

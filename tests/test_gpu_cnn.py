@@ -150,18 +150,22 @@ def test_cnn_multi_chunk_sampled(L, C):
     chunk_base > 0 and a ragged last chunk.  Sampled frames from both chunks,
     including the chunk boundary, against the oracle."""
     nsm = ns()
+    from synthgen.gpu import GpuScene
     chunk = nsm.debug_cnn_layout(nsm.Arch(L, C, 32), 1 << 20)[18]      # internal chunk size
     n = chunk + 301
-    sc, fr = scene_frames(50, 50, n, seed=19, prevalence=0.4)
-    small = np.zeros((n, 7504), np.uint8)
-    small[:, :7500] = fr[:, :7500]
+    sc = sg.make_scene(sg.SceneSpec(50, 50, n, seed=19, prevalence=0.4))
+    small = torch.empty((n, 7504), dtype=torch.uint8, device="cuda")   # rendered on device
+    GpuScene(sc).render(small, 0, n)
     arch = sg.CnnArch(L, C, 32)
     w = sg.he_normal_weights(arch, 8)
-    z = nsm.noscope_specialized_infer(nsm.Arch(L, C, 32), nsm.Weights(w), torch.from_numpy(small).cuda())
+    z = nsm.noscope_specialized_infer(nsm.Arch(L, C, 32), nsm.Weights(w), small)
     torch.cuda.synchronize()
     z = z.cpu().numpy()
     pick = np.array([0, 1, chunk // 2, chunk - 2, chunk - 1, chunk, chunk + 1, chunk + 108, n - 2, n - 1])
-    z_o = O.cnn_logits(hw3(fr[pick], 50, 50), arch, w)
+    bg = sg.background(sc.spec)
+    g = np.stack([sg.render_frame(sc, int(t), bg) for t in pick])
+    assert np.array_equal(small[torch.from_numpy(pick).cuda(), :7500].cpu().numpy(), g.reshape(len(pick), -1))
+    z_o = O.cnn_logits(g, arch, w)
     assert np.abs(z[pick] - z_o).max() <= TOL
     assert np.isfinite(z).all()
 
