@@ -36,8 +36,9 @@
 // consecutive pixels at a stride of one image row (SBO = Wp*16 B), so a warp's
 // 32 TMEM lanes hold a 4x8 pixel block and the 2x2 pool is two shuffles.
 // MMAs on one accumulator serialise on the D read-modify-write (measured in
-// tools/umma_bench.cu), so both issuers interleave the K steps of two tiles with
-// independent accumulators (4 TMEM buffers each).
+// tools/umma_bench.cu), so the issuers interleave independent accumulators: conv1
+// the 4 members of a window group (8 TMEM A slots = two groups, so the builders
+// fill one while the other is multiplied), conv2 two tiles at a time.
 //
 // Queue mode (A.qmode != 0, conv2-fused variants writing FC features; the
 // overlapped cascade): the producer claims frames one at a time from the
