@@ -20,7 +20,15 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   return d;
 }
 
-template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0, int OFF = 0, int M = 128, int CE = 0>
+NS_DEV void umma_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; "
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }" ::"r"(d),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0, int OFF = 0, int M = 128, int CE = 0, int TS = 0>
 __global__ void __launch_bounds__(512, 1) mma_loop(int iters, int ksteps, long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* A = smem;                      // 128 rows x 128 B per 4 K-steps (sw) / 4 KB per step
@@ -69,7 +77,8 @@ __global__ void __launch_bounds__(512, 1) mma_loop(int iters, int ksteps, long l
             ad = sdesc(a0 + (k & 1) * 16 * (SBO / 16) + (OFF ? (k & 7) * OFF : 0), 11680, SBO);
             bd = sdesc(b0 + (k & 7) * N * 32, N * 16, 128);
           }
-          umma_bf16(tmem + acc * N, ad, bd, idesc, (it | k) ? 1u : 0u);
+          if (TS) umma_ts(tmem + acc * N, tmem + 256 + (k & 7) * 8, bd, idesc, (it | k) ? 1u : 0u);
+          else umma_bf16(tmem + acc * N, ad, bd, idesc, (it | k) ? 1u : 0u);
         }
         if (CE && (k % CE) == CE - 1) umma_commit(&bar2);   // per-step completion tracking
       }
@@ -84,21 +93,21 @@ __global__ void __launch_bounds__(512, 1) mma_loop(int iters, int ksteps, long l
   if (threadIdx.x < 32) tmem_dealloc<512>(tmem);
 }
 
-template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0, int OFF = 0, int M = 128, int CE = 0>
+template <int N, int NACC, bool SW, int SBO = 128, int HAMMER = 0, int OFF = 0, int M = 128, int CE = 0, int TS = 0>
 void run() {
   const int iters = 500, ksteps = 8;
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
   size_t smem = 32768 + 8 * 256 * 32 + 2048;
-  cudaFuncSetAttribute(mma_loop<N, NACC, SW, SBO, HAMMER, OFF, M, CE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  mma_loop<N, NACC, SW, SBO, HAMMER, OFF, M, CE><<<148, 512, smem>>>(iters, ksteps, d);
+  cudaFuncSetAttribute(mma_loop<N, NACC, SW, SBO, HAMMER, OFF, M, CE, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  mma_loop<N, NACC, SW, SBO, HAMMER, OFF, M, CE, TS><<<148, 512, smem>>>(iters, ksteps, d);
   cudaError_t err = cudaDeviceSynchronize();
   if (err != cudaSuccess) { printf("N=%d acc=%d sw=%d: %s\n", N, NACC, (int)SW, cudaGetErrorString(err)); fflush(stdout); return; }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  mma_loop<N, NACC, SW, SBO, HAMMER, OFF, M, CE><<<148, 512, smem>>>(iters, ksteps, d);
+  mma_loop<N, NACC, SW, SBO, HAMMER, OFF, M, CE, TS><<<148, 512, smem>>>(iters, ksteps, d);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
@@ -107,7 +116,7 @@ void run() {
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double mmas = (double)iters * ksteps * NACC;
   double flops = mmas * 2.0 * M * N * 16 * 148;
-  printf("CE=%d M=%3d H=%d OFF=%3d SBO=%3d N=%3d acc=%d %s: %6.2f cycles/MMA (floor %3d), %7.1f TFLOP/s  %s\n", CE, M, HAMMER, OFF, SBO, N, NACC,
+  printf("%s CE=%d M=%3d H=%d OFF=%3d SBO=%3d N=%3d acc=%d %s: %6.2f cycles/MMA (floor %3d), %7.1f TFLOP/s  %s\n", TS ? "TS" : "SS", CE, M, HAMMER, OFF, SBO, N, NACC,
          SW ? "SW128" : "none ", (double)h[0] / mmas, M * N / 256, flops / (ms * 1e-3) / 1e12,
          cudaGetErrorString(cudaGetLastError()));
   fflush(stdout);
@@ -115,14 +124,11 @@ void run() {
 }
 
 int main() {
-  // aligned vs unaligned A start (16-B shifts per K step) at the conv SBOs: convt (N = 128,
-  // 3 accumulators, SBO = 26 px * 16 B) and the fused conv2 (N = 64, 2 accumulators, SBO = 27 px)
-  run<128, 3, false, 416, 0, 0, 128, 0>(); run<128, 3, false, 416, 0, 16, 128, 0>();
-  run<128, 3, false, 512, 0, 0, 128, 0>(); run<128, 3, false, 128, 0, 0, 128, 0>();
-  run<128, 4, false, 128, 0, 0, 128, 0>();
-  run<64, 2, false, 432, 0, 0, 128, 0>(); run<64, 2, false, 432, 0, 16, 128, 0>();
-  run<64, 2, false, 512, 0, 0, 128, 0>(); run<64, 2, false, 128, 0, 0, 128, 0>();
-  run<64, 4, false, 128, 0, 0, 128, 0>();
-  run<128, 3, true>(); run<64, 2, true>();
+  // A from TMEM (TS mode, conv1 of the fused kernel) vs smem (SS), N = 16 / 32 / 64
+  run<32, 4, false, 128, 0, 0, 128, 0, 1>(); run<32, 4, false, 128, 0, 0, 128, 0, 0>();
+  run<32, 2, false, 128, 0, 0, 128, 0, 1>(); run<32, 8, false, 128, 0, 0, 128, 0, 1>();
+  run<16, 4, false, 128, 0, 0, 128, 0, 1>(); run<16, 4, false, 128, 0, 0, 128, 0, 0>();
+  run<64, 4, false, 128, 0, 0, 128, 0, 1>(); run<64, 2, false, 128, 0, 0, 128, 0, 1>();
+  run<128, 2, false, 128, 0, 0, 128, 0, 1>();
   return 0;
 }
