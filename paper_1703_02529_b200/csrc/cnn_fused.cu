@@ -215,7 +215,9 @@ conv12_fused_kernel(FusedArgs A) {
   // groups (256) + 2 conv2 accumulators (128); C = 16: 8 A slots + 2 groups (of 16-wide
   // accumulators) + 3 conv2 accumulators; C = 64 conv1-only: 8 A slots + 3 groups of
   // (window group, half) accumulators (384): L2C64D32 9.18 -> 8.32-8.43 ms (4 slots + 2
-  // groups -> 8 + 2 -> 8 + 3; both halves' chains interleaved measured no better).
+  // groups -> 8 + 2 -> 8 + 3; both halves' chains interleaved measured no better), then
+  // "wide" (one N = 64 MMA per member and K step, A slots in shared memory, 2 groups of
+  // 4 x 64 accumulator columns = all of TMEM): 8.05-8.11 ms, builder-bound.
   // Measured (L2C32D32, 65,536 frames): 4 A slots + 3 conv2 accumulators 2.72 ms, 8 + 2
   // 2.51-2.53 ms (the builders and the conv1 issuer stop waiting on each other), 8 A
   // slots + 1 conv1 group + 3 conv2 accumulators issued as triples 3.22 ms, 4 + 2 + 3 as
@@ -224,14 +226,26 @@ conv12_fused_kernel(FusedArgs A) {
   constexpr int kA1S = kA1Max;
   // conv1 accumulator groups ((window group, half) units in flight): 3 for the C = 64
   // conv1-only variant (its 8 A slots + 3 x 128 accumulator columns = 512)
-  constexpr int kNG1v = (!kConv2 && kA1S == kA1Max) ? kNG1Max : kNG1;
+  // C = 64 conv1-only, "wide": one N = 64 MMA per (member, K step) instead of two N = 32
+  // halves (an M128 x K16 MMA costs ~50-60 cycles for any N <= 64: tools/umma_bench.cu);
+  // its 4 x 64-column member accumulators leave TMEM for one group, drained by both
+  // epilogue-1 groups (one channel half each)
+  constexpr bool kWide = !kConv2 && kHalves == 2;
+  // wide: the A slots live in SHARED memory (the conv2 operand region, unused without
+  // conv2; SS-mode MMAs cost the same as TS-mode ones) so that TMEM holds two groups of
+  // 4 x 64-column accumulators and conv1 overlaps the epilogue's drain
+  constexpr bool kASmem = kWide;
+  constexpr int kASlotBytes = 128 * kK1 * 2;     // one A slot: 128 rows x 32 K bf16 (K-major)
+  static_assert(!kASmem || kA1Max * kASlotBytes <= 2 * kActBytes, "A slots in the conv2 planes");
+  constexpr int kNG1v = kWide ? (kASmem ? 2 : 1) : ((!kConv2 && kA1S == kA1Max) ? kNG1Max : kNG1);
+  constexpr int kMemCols = kWide ? C1t : kC1;     // TMEM columns per member accumulator
   // conv2 accumulators: 3 (tile t -> t % 3, phase (t / 3) & 1), or 2 (tile t -> t & 1,
   // phase (frame + t / 2) & 1); kTI tiles interleaved per issue group
   constexpr int kNB2v = c32 ? 2 : kNB2;
   constexpr int kTI = 2;
   static_assert(kT2 % kTI == 0 && (kTI == 2 || kNB2v == 3), "issue groups");
-  constexpr int cD1 = kColA1 + kA1S * kA1Cols;   // conv1 accumulators
-  constexpr int cD2 = cD1 + kNG1v * 4 * C1;      // conv2 accumulators
+  constexpr int cD1 = kASmem ? 0 : kColA1 + kA1S * kA1Cols;   // conv1 accumulators
+  constexpr int cD2 = cD1 + kNG1v * 4 * (kWide ? C1t : C1);   // conv2 accumulators
   static_assert(cD2 + (kConv2 ? kNB2v * kC2 : 0) <= kTmemCols, "TMEM columns");
   auto t2_buf = [](int t) { return kNB2v == 3 ? t % 3 : t & 1; };
   auto t2_par = [](int64_t it, int t) -> uint32_t {
@@ -286,7 +300,7 @@ conv12_fused_kernel(FusedArgs A) {
     }
     for (int s = 0; s < kNG1Max; ++s) {
       mbar_init(&t1_full[s], 1);
-      mbar_init(&t1_empty[s], 128);
+      mbar_init(&t1_empty[s], kWide ? 256 : 128);
     }
     for (int s = 0; s < kNB2; ++s) {
       mbar_init(&t2_full[s], 1);
@@ -392,6 +406,31 @@ conv12_fused_kernel(FusedArgs A) {
           }
           NS_TW(1, mbar_wait(&a1_full[p0 + 1], par));
           tc_fence_after();
+          if (kWide) {   // both channel halves in one N = 64 MMA per (member, K step)
+            constexpr uint32_t idw = idesc_bf16_f32(128, C1t);
+            const int gbw = (int)(ug % kNG1v);
+            if (ug >= (uint64_t)kNG1v) {
+              NS_TW(2, mbar_wait(&t1_empty[gbw], (uint32_t)(((ug / kNG1v) - 1) & 1)));
+              tc_fence_after();
+            }
+            const uint32_t sA = smem_u32(smem + oAct);
+#pragma unroll
+            for (int kk = 0; kk < kK1 / 16; ++kk)
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (!(NS_EXP & 8)) {
+                  const uint32_t d = tmem + cD1 + (gbw * 4 + q) * kMemCols;
+                  const uint64_t bd = bd0 + (uint64_t)((kk * 2 * C1t * 16) >> 4);
+                  if (kASmem)   // K-major canonical slot: K chunks 2048 B apart, 8-row groups 128 B
+                    umma_bf16(d, sdesc(sA + (a0 + q) * kASlotBytes + kk * 2 * 2048, 2048, 128), bd, idw, kk);
+                  else
+                    umma_bf16_ts(d, tmem + kColA1 + (a0 + q) * kA1Cols + kk * 8, bd, idw, kk);
+                }
+            umma_commit(&a1_empty[p0]);
+            umma_commit(&a1_empty[p0 + 1]);
+            umma_commit(&t1_full[gbw]);
+            continue;
+          }
 #pragma unroll
           for (int h = 0; h < kHalves; ++h) {
             const uint64_t ugh = ug * kHalves + h;
@@ -549,12 +588,23 @@ conv12_fused_kernel(FusedArgs A) {
           v[13] = valid ? (h[26] | (0x3F80u << 16)) : 0u;
           v[14] = valid ? 0x3F80u : 0u;
           v[15] = 0;
-          tc_fence_after();
-          tmem_st16(tmem + ((uint32_t)lg << 16) + kColA1 + a * kA1Cols, v);
-          if (pq & 1) {                        // pair complete: publish both members
-            if (!(NS_EXP & 128)) tmem_st_wait();
-            tc_fence_before();
-            mbar_arrive(&a1_full[pr]);
+          if (kASmem) {   // row bt of slot a: K chunk c (8 bf16) at c * 2048 + (bt / 8) * 128 + (bt % 8) * 16
+            uint8_t* slot = smem + oAct + a * kASlotBytes + (bt >> 3) * 128 + (bt & 7) * 16;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              *reinterpret_cast<uint4*>(slot + c * 2048) = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+            if (pq & 1) {                      // pair complete: publish both members
+              fence_proxy_async_smem();        // generic stores -> tensor-core reads
+              mbar_arrive(&a1_full[pr]);
+            }
+          } else {
+            tc_fence_after();
+            tmem_st16(tmem + ((uint32_t)lg << 16) + kColA1 + a * kA1Cols, v);
+            if (pq & 1) {                      // pair complete: publish both members
+              if (!(NS_EXP & 128)) tmem_st_wait();
+              tc_fence_before();
+              mbar_arrive(&a1_full[pr]);
+            }
           }
         }
       }
@@ -584,9 +634,12 @@ conv12_fused_kernel(FusedArgs A) {
       bool stop = false;
       for (int G = 0; G < kG1 && !stop; ++G) {
         for (int h = 0; h < kHalves; ++h, ++ugh) {
-          const int gb = (int)(ugh % kNG1v);
-          if (kEp1Groups > 1 && (int)(ugh % kEp1Groups) != grp) continue;   // alternate units
-          NS_TW(9, mbar_wait(&t1_full[gb], (uint32_t)((ugh / kNG1v) & 1)));
+          // wide: every window group's single accumulator group, channel half h = grp;
+          // otherwise alternate (window group, half) units
+          const uint64_t ugw = (uint64_t)it * kG1 + G;
+          const int gb = kWide ? (int)(ugw % kNG1v) : (int)(ugh % kNG1v);
+          if (kWide ? h != grp : (kEp1Groups > 1 && (int)(ugh % kEp1Groups) != grp)) continue;
+          NS_TW(9, mbar_wait(&t1_full[gb], kWide ? (uint32_t)((ugw / kNG1v) & 1) : (uint32_t)((ugh / kNG1v) & 1)));
           if (qm && G == 0 && pos[it % kPosRing] < 0) {   // stop: forward to the conv2 issuer
             mbar_arrive(&act_full[pb]);                    // (act_empty waited above)
             stop = true;
@@ -597,16 +650,16 @@ conv12_fused_kernel(FusedArgs A) {
           const bool valid = w < kP1 * kP1;
           const int yp = w / kP1, xp = w - kP1 * (w / kP1);
           const int rho = (yp + 1) * kWp + (xp + 1) + 1;
-          const uint32_t tb = tmem + ((uint32_t)lg << 16) + cD1 + gb * 4 * kC1;
+          const uint32_t tb = tmem + ((uint32_t)lg << 16) + cD1 + gb * 4 * kMemCols + (kWide ? h * kC1 : 0);
 #pragma unroll
           for (int cb = 0; cb < ((NS_EXP & 64) ? 0 : kC1 / 16); ++cb) {
             // 2x2 max pool = element-wise max over the window's 4 accumulators
             // (bias already accumulated; max, ReLU and RNE commute: all monotone)
             uint32_t r0[16], r1[16], r2[16], r3[16];
-            tmem_ld16(tb + 0 * kC1 + cb * 16, r0);
-            tmem_ld16(tb + 1 * kC1 + cb * 16, r1);
-            tmem_ld16(tb + 2 * kC1 + cb * 16, r2);
-            tmem_ld16(tb + 3 * kC1 + cb * 16, r3);
+            tmem_ld16(tb + 0 * kMemCols + cb * 16, r0);
+            tmem_ld16(tb + 1 * kMemCols + cb * 16, r1);
+            tmem_ld16(tb + 2 * kMemCols + cb * 16, r2);
+            tmem_ld16(tb + 3 * kMemCols + cb * 16, r3);
             tmem_ld_wait();
             uint32_t pk[8];
 #pragma unroll
