@@ -24,7 +24,11 @@
  *    every buffer; the library never allocates or frees device memory and
  *    holds no global state beyond per-device caches of kernel attributes, so
  *    calls on different streams with distinct workspaces/states are
- *    independent.
+ *    independent.  Two calls create short-lived CUDA objects of their own:
+ *    noscope_cnn_train captures and replays a CUDA graph of one training step
+ *    on a private stream, and the opt-in overlapped schedule of
+ *    noscope_cascade_run (NOSCOPE_OVERLAP=1) uses a private side stream and two
+ *    events; all are destroyed before the call returns.
  *  - Work is enqueued asynchronously on `stream` (a cudaStream_t; 0 = legacy
  *    default stream).  Exceptions: noscope_threshold_sweep with phase 2/3 and
  *    any call given a non-null *_host output synchronise `stream` once to copy
