@@ -479,23 +479,31 @@ def run_x(args):
     ul = torch.from_numpy(sg.logit_grid(SWEEP_M)).to(device)
     hist = torch.zeros(N.sweep_hist_words(dl.numel(), SWEEP_M), dtype=torch.int64, device=device)
     sws = N.workspace(N.OP_THRESHOLD_SWEEP, None, None, 0, dl.numel(), SWEEP_M, device=device)
-    a_rec = torch.empty(unit_len, dtype=torch.uint8, device=device)
     best = N.pinned_sweep_best()
     total = len(units) * unit_len
     gathered = torch.empty(total, dtype=torch.uint8, device=device) if rank == 0 else None
+    # this rank's records, all units back to back: one record-builder and one phase-1 call
+    # cover every unit (a unit's first K_LAG frames are forced fires, s = +inf, fired for
+    # every delta candidate, so the label they would inherit across the unit boundary only
+    # lands in the H1 row d = n_delta, which phase 2 never reads: every count the sweep
+    # reads, and so the best triple, equals the per-unit calls)
+    n_mine = sum(u["n_frames"] for u in mine)
+    s_all = torch.empty(n_mine, dtype=torch.float64, device=device)
+    z_all = torch.zeros(n_mine, dtype=torch.float32, device=device)
+    y_all = torch.cat([truth_of(u) for u in mine]) if mine else torch.empty(0, dtype=torch.uint8, device=device)
+    a_all = torch.empty(max(n_mine, 1), dtype=torch.uint8, device=device)
     torch.cuda.synchronize()
     if dist.is_initialized():
         dist.barrier()
-    timer, rec = [], {}
+    timer, rec = [], {"flat": (s_all, z_all)}
     with ClockSampler(local) as clk:
         labels = D.run_units(N, mine, make_frames, dd, arch, Wt, lo, hi, lab_fn, truth_of, chunk=chunk, ws=ws,
                              device=device, timer=timer, records=rec)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for u, sc_u, z_u in zip(mine, rec["scores"], rec["logits"]):
-            y = truth_of(u)
-            N.noscope_sweep_records(sc_u, y, 1, K_LAG, 1, a_out=a_rec)
-            N.noscope_threshold_sweep(1, sc_u, z_u, y, a_rec, dl, ul, hist)
+        if n_mine:
+            N.noscope_sweep_records(s_all, y_all, 1, K_LAG, 1, a_out=a_all[:n_mine])
+            N.noscope_threshold_sweep(1, s_all, z_all, y_all, a_all[:n_mine], dl, ul, hist)
         D.allreduce_hist_(hist)                                                            # C1
         N.noscope_threshold_sweep(2, None, None, None, None, dl, ul, hist, SWEEP_TIMING, total // 100,
                                   total // 100, ws=sws, best_out=best)

@@ -118,16 +118,22 @@ def run_units(nsm, units, make_frames, dd, arch, weights, lo, hi, labeller, labe
     decode stand-in; called outside the timed intervals).  timer: optional list;
     a (start, end) CUDA event pair is appended around every cascade call, so the
     caller can sum the cascade time without the generation.  records: optional
-    dict of per-unit lists that receives each unit's scores / logits (device)."""
+    dict of per-unit lists that receives each unit's scores / logits (device); if it
+    holds "flat" = (scores, logits) tensors of all units' frames, the per-unit records
+    are consecutive slices of those (one sweep call can then cover every unit)."""
     outs = []
+    off = 0
     for u in units:
         n = u["n_frames"]
         state = nsm.noscope_stream_state_init(dd)
         labels = torch.empty(n, dtype=torch.uint8, device=device)
         scores = logits = None
-        if records is not None:
+        if records is not None and "flat" in records:
+            scores, logits = records["flat"][0][off:off + n], records["flat"][1][off:off + n]
+        elif records is not None:
             scores = torch.empty(n, dtype=torch.float64, device=device)
             logits = torch.zeros(n, dtype=torch.float32, device=device)
+        off += n
         for t0 in range(0, n, chunk):
             m = min(chunk, n - t0)
             frames = make_frames(u, t0, m)
