@@ -18,7 +18,8 @@
 //                         N = 32 per half); owns the TMEM allocation
 //   W2      conv2 MMA   — one thread issues the shifted-window conv2 tiles
 //                         (A and B from shared memory, K = 9 x 32, N = 64)
-//   W3-W6   builders    — normalisation through a 3x256 table of the
+//   W3-W6   builders    — (C = 16 and C = 64: a second set on W15-W18, the sets
+//                         alternating window groups) normalisation through a 3x256 table of the
 //                         exact fp32 formula into a
 //                         zero-haloed column-polyphase bf16 image, then per pool
 //                         window the 4 members' im2col rows from one 4x4 cell
@@ -252,6 +253,15 @@ conv12_fused_kernel(FusedArgs A) {
     return kNB2v == 3 ? (uint32_t)((t / 3) & 1) : (uint32_t)((it + (t >> 1)) & 1);
   };
   constexpr int kEp1Groups = (wEp2_0 - wEp1_0) / 4;
+  // Builder sets: C = 16 and C = 64 (builder-bound after the 8-slot change) take a second
+  // set of 4 builder warps (W15-W18: idle without conv2 / the second epilogue-2 group for
+  // C = 16, whose N = 32 conv2 tiles one group drains); the sets alternate window groups
+  // (global group parity) and split the image build.
+  // (measured: L2C16D32 1.88 -> 1.67 ms, L2C64D32 8.04-8.08 -> 7.86-8.03 ms per 65,536 frames)
+  constexpr int kBSets = (kC1 == 16 || !kConv2) ? 2 : 1;
+  constexpr int wB2_0 = 15;
+  constexpr int wEp2_end = kBSets == 2 ? wB2_0 : 19;
+  constexpr int kEp2Groups = (wEp2_end - wEp2_0) / 4;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool qm = kConv2 && A.qmode != 0;   // queue mode (host: conv2-fused + features only)
@@ -290,7 +300,7 @@ conv12_fused_kernel(FusedArgs A) {
   if (tid == 0) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(&in_full[s], 1);
-      mbar_init(&in_empty[s], 128);
+      mbar_init(&in_empty[s], 128 * kBSets);
       mbar_init(&act_full[s], 32 * (wEp2_of<kConv2>() - wEp1_0));
       mbar_init(&act_empty[s], 1);
     }
@@ -517,23 +527,26 @@ conv12_fused_kernel(FusedArgs A) {
         umma_commit(&act_empty[pb]);
       }
     }
-  } else if (warp < wEp1_0) {
+  } else if (warp < wEp1_0 || (kBSets == 2 && warp >= wB2_0)) {
     // ===================================================== builders
     const int lg = (warp & 3) * 32;
     const int bt = lg + lane;  // im2col row = TMEM lane
+    const int bset = (kBSets == 2 && warp >= wB2_0) ? 1 : 0;
     uint64_t u1 = 0;
     for (int64_t it = 0; it < my_frames; ++it) {
       const int s = (int)(it & 1);
       NS_TW(5, mbar_wait(&in_full[s], (uint32_t)((it >> 1) & 1)));
       if (qm && pos[it % kPosRing] < 0) {   // stop: forward to the conv1 issuer (pair 0)
-        const int pr0 = (int)(u1 % kA1S) >> 1;
-        if (u1 >= kA1S) mbar_wait(&a1_empty[pr0], (uint32_t)(((u1 / kA1S) - 1) & 1));
-        mbar_arrive(&a1_full[pr0]);
+        if (((u1 >> 2) & (kBSets - 1)) == (uint64_t)bset) {   // the set that builds that group
+          const int pr0 = (int)(u1 % kA1S) >> 1;
+          if (u1 >= kA1S) mbar_wait(&a1_empty[pr0], (uint32_t)(((u1 / kA1S) - 1) & 1));
+          mbar_arrive(&a1_full[pr0]);
+        }
         break;
       }
-      NS_TW(6, nbar_sync(1, 128));  // previous frame's rows are all built: X may be overwritten
+      NS_TW(6, nbar_sync(1, 128 * kBSets));  // previous frame's rows are all built: X may be overwritten
       const uint8_t* in = smem + oIn + s * kInBytes;
-      for (int p = bt; p < ((NS_EXP & 2) ? 0 : kIn * kIn); p += 128) {
+      for (int p = bset * 128 + bt; p < ((NS_EXP & 2) ? 0 : kIn * kIn); p += 128 * kBSets) {
         const int y = p / kIn, x = p - kIn * y;
         const uint8_t* px = in + 3 * p;
         X[((x + 1) & 1) * kXPlane + xrow(y + 1) + ((x + 1) >> 1)] =
@@ -541,11 +554,12 @@ conv12_fused_kernel(FusedArgs A) {
                        (uint32_t)lut[512 + px[2]]);
       }
       mbar_arrive(&in_empty[s]);
-      NS_TW(6, nbar_sync(1, 128));  // X complete
+      NS_TW(6, nbar_sync(1, 128 * kBSets));  // X complete
       // One thread = one pool window of group G; its 4 members (dy, dx) are the
       // 4 tiles 4G..4G+3 = A stages 0..3.  The 4x4 padded-pixel neighbourhood
       // (16 cells) serves all 4 members' 3x3 patches.
       for (int G = 0; G < kG1; ++G, u1 += 4) {
+        if (kBSets == 2 && (int)((u1 >> 2) & 1) != bset) continue;   // the other set's group
         const int w = G * 128 + bt;
         const bool valid = w < kP1 * kP1;
         const int yp = valid ? w / kP1 : 0, xp = valid ? w - kP1 * yp : 0;
@@ -707,8 +721,8 @@ conv12_fused_kernel(FusedArgs A) {
   } else if (kConv2) {
     // ===================================================== epilogue 2
     const int lg = (warp & 3) * 32;
-    const int et = tid - wEp2_0 * 32;  // 0..255
-    const int grp2 = et >> 7;          // tiles t with t % 2 == grp2
+    const int et = tid - wEp2_0 * 32;  // 0 .. 128 * kEp2Groups - 1
+    const int grp2 = et >> 7;          // tiles t with t % kEp2Groups == grp2
     // lane -> conv position inside the tile: 4 conv rows x 8 conv columns per warp
     const int rl = (warp & 3) * 4 + (lane >> 3), cl = lane & 7;
     const bool pool_lane = ((lane & 1) == 0) && (((lane >> 3) & 1) == 0);
@@ -716,7 +730,7 @@ conv12_fused_kernel(FusedArgs A) {
     // 13, 169 rows per frame, 14 leading guard rows
     constexpr int kHpool = 12, kWqo = 13, kPo = 13 * 13, kGo = 14;
     if (!A.to_features && blockIdx.x == 0) {  // zero the leading / trailing guards
-      for (int e = et; e < (kC2 / 8) * (kGo + kWqo); e += 256) {
+      for (int e = et; e < (kC2 / 8) * (kGo + kWqo); e += 128 * kEp2Groups) {
         const int c = e / (kGo + kWqo), k = e % (kGo + kWqo);
         const int64_t row = k < kGo ? k : kGo + cnt * kPo + (k - kGo);
         *reinterpret_cast<uint4*>(A.out + ((int64_t)c * A.out_rows + row) * 16) = make_uint4(0, 0, 0, 0);
@@ -725,7 +739,7 @@ conv12_fused_kernel(FusedArgs A) {
     for (int64_t it = 0; it < my_frames; ++it) {
       int64_t i = blockIdx.x + it * gridDim.x;  // chunk-relative frame (queue mode: slot)
       bool stop = false;
-      for (int t = grp2; t < kT2; t += 2) {             // this group's tiles
+      for (int t = grp2; t < kT2; t += kEp2Groups) {    // this group's tiles
         const int b = t2_buf(t);
         NS_TW(10, mbar_wait(&t2_full[b], t2_par(it, t)));
         if (qm && t == grp2) {
