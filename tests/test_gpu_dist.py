@@ -117,3 +117,33 @@ def test_two_ranks_equal_one_rank_and_oracle():
     assert res[0][3] == hist1.tolist() == res[1][3]
     for u in range(N_UNITS):                     # every unit's labels are the oracle cascade's
         assert np.array_equal(lab1[u * UNIT:(u + 1) * UNIT], ref[u]["labels"]), u
+
+
+def test_flat_records_one_sweep_call_equals_per_unit_calls():
+    """bench.py's config X builds one rank's sweep records back to back (run_units
+    writing into flat buffers) and runs one record-builder + one phase-1 call: a
+    unit's first K frames are forced fires (s = +inf), so the labels inherited
+    across a unit boundary only reach the H1 row phase 2 never reads — the best
+    triple equals the per-unit calls'."""
+    from paper_1703_02529_b200 import dist as D
+    from synthgen.gpu import GpuScene, truth_labeller_address
+    N, dd, A, Wt, _ = _setup()
+    lo, hi = -0.1, 0.1
+    _, best_units, _ = _shard(1, 0, lo, hi)
+    units = [dict(id=u, n_frames=UNIT, width=W, height=H) for u in range(N_UNITS)]
+    gs = {u["id"]: GpuScene(_scene(u["id"])) for u in units}
+    buf = torch.empty((CHUNK, sg.frame_pitch(W, H)), dtype=torch.uint8, device="cuda")
+    s_all = torch.empty(N_UNITS * UNIT, dtype=torch.float64, device="cuda")
+    z_all = torch.zeros(N_UNITS * UNIT, dtype=torch.float32, device="cuda")
+    rec = {"flat": (s_all, z_all)}
+    D.run_units(N, units, lambda u, t0, m: gs[u["id"]].render(buf, t0, m)[:m], dd, A, Wt, lo, hi,
+                truth_labeller_address(), lambda u: gs[u["id"]].truth, chunk=CHUNK, device="cuda", records=rec)
+    assert torch.isinf(s_all.view(N_UNITS, UNIT)[:, :K]).all()
+    y_all = torch.cat([gs[u["id"]].truth[:UNIT] for u in units])
+    a_all = N.noscope_sweep_records(s_all, y_all, 1, K, 1)
+    delta = torch.linspace(-3.0, 3.0, 9, dtype=torch.float64, device="cuda")
+    u_c = torch.from_numpy(sg.logit_grid(12)).cuda()
+    hist = torch.zeros(N.sweep_hist_words(9, 12), dtype=torch.int64, device="cuda")
+    N.noscope_threshold_sweep(1, s_all, z_all, y_all, a_all, delta, u_c, hist)
+    best, _ = N.noscope_threshold_sweep(2, None, None, None, None, delta, u_c, hist, (1, 10, 1000), 60, 60)
+    assert best == best_units
