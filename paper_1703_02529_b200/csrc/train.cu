@@ -197,9 +197,33 @@ __global__ void head_grad_kernel(const float* __restrict__ h1, const float* __re
     dh1[e] = h1[e] > 0.0f ? dz[e / D] * w2[e % D] : 0.0f;
 }
 
-__global__ void fill_kernel(float* __restrict__ d, int64_t n, float v) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) d[e] = v;
+// Column sums out[c] = sum_r m[r][c] of a row-major [rows][C] matrix (the bias
+// gradients), deterministic: block b sums the fixed row range [rows*b/nb, rows*(b+1)/nb)
+// with per-thread partials in row order and a fixed smem fold, colsum_final_kernel adds
+// the blocks' partials in block order.  C is a power of two <= 1024.
+constexpr int kCsBlocks = 192;
+__global__ void colsum_partial_kernel(const float* __restrict__ m, int64_t rows, int C, float* __restrict__ part) {
+  extern __shared__ float red[];
+  const int64_t r0 = rows * blockIdx.x / gridDim.x, r1 = rows * (blockIdx.x + 1) / gridDim.x;
+  const int c = threadIdx.x % C, g = threadIdx.x / C, ng = blockDim.x / C;
+  float acc = 0.0f;
+  for (int64_t r = r0 + g; r < r1; r += ng) acc += m[r * C + c];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < C) {
+    float t = 0.0f;
+    for (int k = 0; k < ng; ++k) t += red[k * C + threadIdx.x];
+    part[(int64_t)blockIdx.x * C + threadIdx.x] = t;
+  }
 }
+__global__ void colsum_final_kernel(const float* __restrict__ part, int nb, int C, float* __restrict__ out) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
+    float t = 0.0f;
+    for (int b = 0; b < nb; ++b) t += part[(int64_t)b * C + c];
+    out[c] = t;
+  }
+}
+
 
 __global__ void rmsprop_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ v, int64_t n,
                                float lr, float rho, float eps) {
@@ -256,7 +280,7 @@ noscope_status gemm_rm(bool ta, bool tb, int M, int N, int64_t K, const float* A
 }
 
 struct TWs {
-  float *G, *V, *best, *x[5], *a[4], *cols[4], *dcols, *dx, *dxb, *h1, *dz, *dh1, *ones, *part;
+  float *G, *V, *best, *x[5], *a[4], *cols[4], *dcols, *dx, *dxb, *h1, *dz, *dh1, *part, *cspart;
   uint8_t* arg[4];
   int32_t* idx_tmp;
   double* loss;
@@ -294,7 +318,6 @@ TWs carve_t(const TPlan& p, int B, void* base) {
   w.h1 = (float*)take((size_t)B * p.D * 4);
   w.dz = (float*)take((size_t)B * 4);
   w.dh1 = (float*)take((size_t)B * p.D * 4);
-  w.ones = (float*)take((size_t)B * p.lay[0].H * p.lay[0].W * 4);
   // split-K scratch of the largest GEMM of a step (the weight gradients)
   size_t part = 0;
   auto need = [&](int M, int N, int64_t K) { part = std::max(part, tc_gemm_part_floats(M, N, K)); };
@@ -304,23 +327,27 @@ TWs carve_t(const TPlan& p, int B, void* base) {
     need((int)rows, t.cout, 9 * t.cin);
     need(t.cout, 9 * t.cin, rows);
     need((int)rows, 9 * t.cin, t.cout);
-    need(t.cout, 1, rows);
   }
   need(B, p.D, p.K);
   need(p.D, p.K, B);
   need(B, p.K, p.D);
-  need(p.D, 1, B);
   w.part = (float*)take(std::max<size_t>(part, 1) * 4);
   w.loss = (double*)take(8);
   w.idx_tmp = (int32_t*)take((size_t)B * 4);   // the captured step's batch indices
+  w.cspart = (float*)take((size_t)kCsBlocks * 1024 * 4);   // column-sum partials
   w.total = off;
   return w;
 }
 
-// column sums of a row-major [rows][C] matrix: out[c] = sum_r m[r][c] * 1 (a GEMM with N = 1)
-noscope_status colsum(const float* m, int64_t rows, int C, float* out, const float* ones, float* part,
-                      cudaStream_t st) {
-  return tc_gemm(m, 1, C, ones, 0, 1, out, 1, C, 1, rows, part, st);
+// column sums of a row-major [rows][C] matrix: out[c] = sum_r m[r][c] (the bias gradients;
+// a dedicated reduction: as an N = 1 GEMM it cost a 32-wide tile and a split-K reduce)
+noscope_status colsum(const float* m, int64_t rows, int C, float* out, float* part, cudaStream_t st) {
+  const int threads = C <= 256 ? 256 : C;
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(kCsBlocks, rows));
+  colsum_partial_kernel<<<nb, threads, threads * sizeof(float), st>>>(m, rows, C, part);
+  colsum_final_kernel<<<(C + 255) / 256, 256, 0, st>>>(part, nb, C, out);
+  NS_LAUNCH_CHECK();
+  return NOSCOPE_OK;
 }
 
 // Forward on B frames (idx on device); leaves activations for the backward pass,
@@ -351,7 +378,7 @@ noscope_status backward(const TPlan& p, const float* P, TWs& w, int B, cudaStrea
   float* G = w.G;
   head_grad_kernel<<<1, kT, 0, st>>>(w.h1, P + p.fc2_w, w.dz, B, p.D, G + p.fc2_w, G + p.fc2_b, w.dh1);
   NS_TRY(gemm_rm(true, false, p.D, p.K, B, w.dh1, p.D, w.x[p.L], p.K, G + p.fc1_w, p.K, w.part, st));
-  NS_TRY(colsum(w.dh1, B, p.D, G + p.fc1_b, w.ones, w.part, st));
+  NS_TRY(colsum(w.dh1, B, p.D, G + p.fc1_b, w.cspart, st));
   float* dpool = w.dx;   // gradient w.r.t. the current pooled map
   NS_TRY(gemm_rm(false, false, B, p.K, p.D, w.dh1, p.D, P + p.fc1_w, p.K, dpool, p.K, w.part, st));
   for (int l = p.L - 1; l >= 0; --l) {
@@ -362,7 +389,7 @@ noscope_status backward(const TPlan& p, const float* P, TWs& w, int B, cudaStrea
     // dW = dY^T cols, on this layer's forward im2col rows
     NS_TRY(gemm_rm(true, false, t.cout, 9 * t.cin, rows, w.a[l], t.cout, w.cols[l], 9 * t.cin, G + t.w_off,
                    9 * t.cin, w.part, st));
-    NS_TRY(colsum(w.a[l], rows, t.cout, G + t.b_off, w.ones, w.part, st));
+    NS_TRY(colsum(w.a[l], rows, t.cout, G + t.b_off, w.cspart, st));
     if (l > 0) {
       NS_TRY(gemm_rm(false, false, (int)rows, 9 * t.cin, t.cout, w.a[l], t.cout, P + t.w_off, 9 * t.cin, w.dcols,
                      9 * t.cin, w.part, st));
@@ -438,10 +465,6 @@ noscope_status launch_cnn_train(const noscope_cnn_arch& a, const noscope_train_c
     return ei == cudaSuccess ? NOSCOPE_OK : NOSCOPE_CUDA;
   };
   NS_TRAIN_TRY(cudaMemsetAsync(w.V, 0, p.nparams * 4, st));
-  {
-    const int64_t nr = (int64_t)cfg.batch * p.lay[0].H * p.lay[0].W;
-    fill_kernel<<<grid_for(nr), kT, 0, st>>>(w.ones, nr, 1.0f);
-  }
   NS_TRAIN_TRY(cudaMemcpyAsync(w.best, P, p.nparams * 4, cudaMemcpyDeviceToDevice, st));
   double best_val = INFINITY, prev_tr = INFINITY;
   int run = 0;
