@@ -124,11 +124,9 @@ void run() {
 }
 
 int main() {
-  // A from TMEM (TS mode, conv1 of the fused kernel) vs smem (SS), N = 16 / 32 / 64
-  run<32, 4, false, 128, 0, 0, 128, 0, 1>(); run<32, 4, false, 128, 0, 0, 128, 0, 0>();
-  run<32, 2, false, 128, 0, 0, 128, 0, 1>(); run<32, 8, false, 128, 0, 0, 128, 0, 1>();
-  run<16, 4, false, 128, 0, 0, 128, 0, 1>(); run<16, 4, false, 128, 0, 0, 128, 0, 0>();
-  run<64, 4, false, 128, 0, 0, 128, 0, 1>(); run<64, 2, false, 128, 0, 0, 128, 0, 1>();
-  run<128, 2, false, 128, 0, 0, 128, 0, 1>();
+  // N = 64, SS mode: 1..4 interleaved accumulators (the fused conv2 shape)
+  run<64, 1, false, 128, 0, 0, 128, 0, 0>(); run<64, 2, false, 128, 0, 0, 128, 0, 0>();
+  run<64, 3, false, 128, 0, 0, 128, 0, 0>(); run<64, 4, false, 128, 0, 0, 128, 0, 0>();
+  run<64, 3, false, 432, 0, 16, 128, 0, 0>();
   return 0;
 }
