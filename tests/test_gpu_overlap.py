@@ -111,13 +111,14 @@ def _oracle_samples(sc, out, dd_o, arch, w, k, samples):
     assert np.abs(z_g - z_o).max() <= 2e-2
 
 
-@pytest.mark.parametrize("base_filters,side,chunks", [
-    (32, 8, [24000]),            # the bench's schedule
-    (32, 1, [24000]),            # slow side: most frames left to the tail launch
-    (32, 32, [13000, 11000]),    # wide side; two chunks with carried state (both >= 8,192)
-    (16, 8, [24000]),            # the paper's C = 16 models
+@pytest.mark.parametrize("base_filters,side,chunks,t_skip", [
+    (32, 8, [24000], 1),            # the bench's schedule
+    (32, 1, [24000], 1),            # slow side: most frames left to the tail launch
+    (32, 32, [13000, 11000], 1),    # wide side; two chunks with carried state (both >= 8,192)
+    (16, 8, [24000], 1),            # the paper's C = 16 models
+    (32, 8, [14000, 13001], 3),     # frame skipping: t-30 anchors on checked frames, deferred fires
 ])
-def test_overlap_equals_serial_blocked_lag(base_filters, side, chunks):
+def test_overlap_equals_serial_blocked_lag(base_filters, side, chunks, t_skip):
     nsm = ns()
     n, k = sum(chunks), 30
     sc, gs, frames = _video(n, seed=5, prevalence=0.5)
@@ -125,7 +126,7 @@ def test_overlap_equals_serial_blocked_lag(base_filters, side, chunks):
     arch = sg.CnnArch(2, base_filters, 32)
     w = sg.he_normal_weights(arch, 4)
     delta = 2160.0
-    dd = nsm.DD(mode=1, metric=1, grid=10, t_diff_frames=k, t_skip_frames=1, delta_diff=delta,
+    dd = nsm.DD(mode=1, metric=1, grid=10, t_diff_frames=k, t_skip_frames=t_skip, delta_diff=delta,
                 lr_weights=torch.from_numpy(lr_w).cuda(), lr_bias=float(lr_b))
     lo, hi = 0.0107, 0.1035
     with _env(NOSCOPE_OVERLAP=0):
@@ -133,15 +134,16 @@ def test_overlap_equals_serial_blocked_lag(base_filters, side, chunks):
     with _env(NOSCOPE_OVERLAP=1, NOSCOPE_SIDE_SMS=side):
         ovl = _run(nsm, dd, arch, w, lo, hi, frames, gs, chunks)
     nf = sum(s["n_fired"] for s in ovl["stats"])
-    assert 0.05 * n < nf < 0.95 * n, nf   # a real queue, not a degenerate one
+    assert 0.05 * n / t_skip < nf < 0.95 * n / t_skip, nf   # a real queue, not a degenerate one
     _same(ovl, ser)
     del frames
     torch.cuda.empty_cache()
-    dd_o = O.DDConfig(mode=1, metric=1, grid=10, t_diff_frames=k, t_skip_frames=1, delta_diff=delta,
+    dd_o = O.DDConfig(mode=1, metric=1, grid=10, t_diff_frames=k, t_skip_frames=t_skip, delta_diff=delta,
                       lr_w=lr_w, lr_b=lr_b)
     rng = np.random.default_rng(1)
     samples = sorted(set([k, k + 1, n - 1, chunks[0] - 1, min(chunks[0], n - 1)] +
-                         rng.integers(k, n, 14).tolist()))
+                         rng.integers(k, n, 14 * t_skip).tolist()))
+    samples = [t for t in samples if t % t_skip == 0]   # checked frames (skipped ones have no score)
     _oracle_samples(sc, ovl, dd_o, arch, w, k, samples)
 
 
