@@ -40,7 +40,19 @@ NS_DEV void st_relaxed(unsigned long long* p, unsigned long long v) {
 //            consecutive items, warp scan + block scan give its output position.
 // DRAM traffic per item = the item + 1/4 byte of mask (write + read) + 4 bytes per
 // selected item: within 1.1x of the algorithmic bytes at 15 % selected.
-constexpr int kMThreads = 512, kMWarps = kMThreads / 32;
+// Launch shape: one 1,024-thread CTA per SM for both kernels (A/B at 2^30 dispositions /
+// 2^28 logits: 0.431-0.433 / 0.418-0.422 ms; 512 threads x 3 (compaction) / x 2 (routing)
+// 0.446-0.457 / 0.433-0.446; 768 x 2: 0.431 / 0.422; 256 x 6: 0.477 / 0.441-0.467)
+#ifndef NS_MTHREADS
+#define NS_MTHREADS 1024
+#endif
+#ifndef NS_MCPS
+#define NS_MCPS 1
+#endif
+#ifndef NS_RCPS
+#define NS_RCPS 1
+#endif
+constexpr int kMThreads = NS_MTHREADS, kMWarps = kMThreads / 32;
 constexpr int kMItems = 16, kMRounds = 4;
 constexpr int kMChunk = 32 * kMItems * kMRounds;   // 2048 items per warp-chunk
 constexpr int kMHalf = kMChunk / 16;               // mask halfwords per chunk
@@ -119,7 +131,7 @@ NS_DEV void warp_range(int64_t ch0, int64_t ch1, int warp, int64_t* a, int64_t* 
 // ahead), a warp scan gives each selected item its position in the chunk's run;
 // the warp stages the item offsets (u16) in its own shared-memory slice, then
 // writes the run with coalesced stores: emit(item, pos) for k = lane, lane + 32, ..
-constexpr size_t kMStageBytes = (size_t)kMWarps * kMChunk * 2;   // 64 KB dynamic smem (3 CTAs / SM)
+constexpr size_t kMStageBytes = (size_t)kMWarps * kMChunk * 2;   // 4 KB per warp (128 KB per 1,024-thread CTA)
 
 template <class Emit>
 NS_DEV void emit_selected(MaskWs ws, int64_t wa, int64_t wb, uint64_t off, uint16_t* stage_all, Emit&& emit) {
@@ -155,7 +167,7 @@ NS_DEV void emit_selected(MaskWs ws, int64_t wa, int64_t wb, uint64_t off, uint1
   }
 }
 
-__global__ void __launch_bounds__(kMThreads, 3)
+__global__ void __launch_bounds__(kMThreads, NS_MCPS)
 compact_fired_kernel(uint8_t* disp, double* score, int64_t n, int64_t tau0, int t_skip,
                      int32_t* idx_out, int64_t* count_out, MaskWs ws, int vec, int32_t* pos_pf) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x, c = blockIdx.x;
@@ -288,7 +300,7 @@ NS_DEV uint8_t route_code(float z, float lo, float hi) {
   return z < lo ? NOSCOPE_R_NEG : (z > hi ? NOSCOPE_R_POS : NOSCOPE_R_UNC);
 }
 
-__global__ void __launch_bounds__(kMThreads, 2)
+__global__ void __launch_bounds__(kMThreads, NS_RCPS)
 route_kernel(RouteArgs A, MaskWs ws) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x, c = blockIdx.x;
   const int64_t n = A.n_dev ? min(*A.n_dev, A.n_max) : A.n_max;
