@@ -14,8 +14,11 @@ from gpu_util import hw3, ns, requires_gpu, scene_frames
 pytestmark = [pytest.mark.gpu, requires_gpu]
 
 
-@pytest.mark.parametrize("n", [29, 30, 95, 100_003])
-def test_eval_labels_counts(n):
+@pytest.mark.parametrize("n,shift", [(29, 0), (30, 0), (95, 0), (480, 0), (100_003, 0), (4_800_007, 0),
+                                     (100_003, 1)])
+def test_eval_labels_counts(n, shift):
+    """30-frame windows take the 16-byte-vector kernel (480-frame blocks + a generic tail)
+    when both tracks are 16-byte aligned (shift = 0), the generic kernel otherwise."""
     nsm = ns()
     rng = np.random.default_rng(n)
     ref = (rng.random(n) < 0.3).astype(np.uint8)
@@ -23,7 +26,11 @@ def test_eval_labels_counts(n):
     flip = rng.random(n) < 0.04
     pred[flip] ^= 1
     pred[pred == 1] = rng.integers(1, 255, int((pred == 1).sum()))       # any nonzero = present
-    ev = nsm.noscope_eval_labels(torch.from_numpy(pred).cuda(), torch.from_numpy(ref).cuda())
+    pd = torch.zeros(n + 16, dtype=torch.uint8, device="cuda")
+    rd = torch.zeros(n + 16, dtype=torch.uint8, device="cuda")
+    pd[shift:shift + n] = torch.from_numpy(pred).cuda()
+    rd[shift:shift + n] = torch.from_numpy(ref).cuda()
+    ev = nsm.noscope_eval_labels(pd[shift:shift + n], rd[shift:shift + n])
     fp, fn, tp, tn = O.fp_fn(pred, ref)
     assert (ev["fp"], ev["fn"], ev["tp"], ev["tn"]) == (fp, fn, tp, tn)
     assert ev["windows"] == n // 30
