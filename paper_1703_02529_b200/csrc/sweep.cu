@@ -323,7 +323,23 @@ __global__ void sweep_prefix_kernel(const unsigned long long* __restrict__ G,
   }
 }
 
-// Phase 2b: evaluate every (j, l <= h); thread per (j, l).
+// Phase 2b: evaluate every (j, l <= h).
+// Phase-2 work split: the (l, h >= l) triangle of one delta row is cut into
+// (m + 1) / 2 row pairs {l, m - 1 - l} of m + 1 cells each (one pair of m - l cells
+// when m is odd), dealt round-robin over eval_pieces(m) threads (interleaved, so a
+// warp reads consecutive h: strided pieces would put every lane on one bank).
+__host__ __device__ inline int eval_pieces(int m) {
+  const int p = (m + 1) / 32;
+  return p < 1 ? 1 : (p > 32 ? 32 : p);
+}
+// CTAs per delta row: about 512 cells per thread (each CTA stages the row's FPf and
+// GT columns, so more CTAs per row cost more staging than they save).
+__host__ __device__ inline int eval_ctas_per_row(int m) {
+  const int64_t cells = (int64_t)m * (m + 1) / 2;
+  const int64_t c = (cells + 256 * 512 - 1) / (256 * 512);
+  return (int)(c < 1 ? 1 : (c > 64 ? 64 : c));
+}
+
 struct Cand {
   unsigned long long k0, k1, k2;
   unsigned int j, nl, h, valid;
@@ -338,12 +354,37 @@ NS_DEV bool cand_less(const Cand& x, const Cand& y) {
   return x.h < y.h;
 }
 
+// One (j, l, h) cell of the sweep: cost and constraint keys, kept if it beats the
+// thread's best feasible (bf) or least-violating (bi) candidate.
+NS_DEV void eval_cell(int j, int m, int l, int h, unsigned long long fn, unsigned long long ge,
+                      unsigned long long fp, unsigned long long gth, unsigned long long base_cost,
+                      unsigned long long t_full, unsigned long long fp_lim, unsigned long long fn_lim,
+                      Cand& bf, Cand& bi) {
+  const unsigned long long U = ge - gth;
+  const unsigned long long cost = base_cost + U * t_full;
+  Cand c;
+  c.j = j;
+  c.nl = (unsigned)(m - 1 - l);
+  c.h = h;
+  c.valid = 1;
+  if (fp <= fp_lim && fn <= fn_lim) {
+    c.k0 = cost; c.k1 = U; c.k2 = 0;
+    if (cand_less(c, bf)) bf = c;
+  } else {
+    const unsigned long long vfp = fp > fp_lim ? fp - fp_lim : 0;
+    const unsigned long long vfn = fn > fn_lim ? fn - fn_lim : 0;
+    c.k0 = vfp > vfn ? vfp : vfn; c.k1 = cost; c.k2 = U;
+    if (cand_less(c, bi)) bi = c;
+  }
+}
+
 struct EvalOut {
   Cand feas, infeas;
 };
 
-// One CTA per (j, slice of 256 l values): the j row of FPf and GT (m entries each)
-// staged in shared memory, each thread scans h = l .. m-1 from there.
+// eval_ctas_per_row(m) CTAs per delta row j: the j row of FPf and GT (m entries
+// each) staged in shared memory; the CTAs' threads stride over the row's (pair,
+// piece) items, the pair's FN and GE entries in registers.
 __global__ void __launch_bounds__(256)
 sweep_eval_kernel(Tables T, const unsigned long long* hist, int nd, int m,
                   unsigned long long t_mse, unsigned long long t_snn,
@@ -354,40 +395,36 @@ sweep_eval_kernel(Tables T, const unsigned long long* hist, int nd, int m,
   unsigned long long* gt = fpf + m;                                        // [m]
   __shared__ Cand sf[256], si[256];
   HistLayout L(nd, m);
-  const int lslices = (m + 255) / 256;
-  const int j = blockIdx.x / lslices, l = (blockIdx.x % lslices) * 256 + threadIdx.x;
+  const int cpr = eval_ctas_per_row(m), P = eval_pieces(m);
+  const int j = blockIdx.x / cpr;
   for (int h = threadIdx.x; h < m; h += blockDim.x) {
     fpf[h] = T.FPf[(size_t)j * m + h];
     gt[h] = T.GT[(size_t)j * m + h];
   }
   __syncthreads();
   Cand bf{0, 0, 0, 0, 0, 0, 0}, bi{0, 0, 0, 0, 0, 0, 0};
-  if (l < m) {
-    const unsigned long long checked = hist[L.tail];
-    const unsigned long long F = T.F[j];
-    const unsigned long long fpnf = T.FPnf[j];
-    const unsigned long long fn = T.FNnf[j] + T.FNf[(size_t)j * m + l];
-    const unsigned long long ge = T.GE[(size_t)j * m + l];
-    const unsigned long long base_cost = checked * t_mse + F * t_snn;
-    for (int h = l; h < m; ++h) {
-      const unsigned long long fp = fpnf + fpf[h];
-      const unsigned long long U = ge - gt[h];
-      const unsigned long long cost = base_cost + U * t_full;
-      Cand c;
-      c.j = j;
-      c.nl = (unsigned)(m - 1 - l);
-      c.h = h;
-      c.valid = 1;
-      if (fp <= fp_lim && fn <= fn_lim) {
-        c.k0 = cost; c.k1 = U; c.k2 = 0;
-        if (cand_less(c, bf)) bf = c;
-      } else {
-        const unsigned long long vfp = fp > fp_lim ? fp - fp_lim : 0;
-        const unsigned long long vfn = fn > fn_lim ? fn - fn_lim : 0;
-        c.k0 = vfp > vfn ? vfp : vfn; c.k1 = cost; c.k2 = U;
-        if (cand_less(c, bi)) bi = c;
-      }
-    }
+  const unsigned long long checked = hist[L.tail];
+  const unsigned long long F = T.F[j];
+  const unsigned long long fpnf = T.FPnf[j], fnnf = T.FNnf[j];
+  const unsigned long long base_cost = checked * t_mse + F * t_snn;
+  const unsigned long long* fnf = T.FNf + (size_t)j * m;
+  const unsigned long long* ger = T.GE + (size_t)j * m;
+  const int items = ((m + 1) / 2) * P;   // (pair, piece) work items of this row
+  for (int w = (blockIdx.x - j * cpr) * blockDim.x + threadIdx.x; w < items; w += cpr * blockDim.x) {
+    const int r = w / P, p = w - r * P;
+    const int l1 = r, l2 = m - 1 - r;
+    const int len1 = m - l1, tot = l2 > l1 ? m + 1 : len1;
+    const unsigned long long fn1 = fnnf + fnf[l1], ge1 = ger[l1];
+    const unsigned long long fn2 = fnnf + fnf[l2], ge2 = ger[l2];
+    // lanes on consecutive cells (conflict-free smem reads); the pair's two rows as
+    // two loops, so the cell body carries no per-cell row select
+    int i = p;
+    for (; i < len1; i += P)
+      eval_cell(j, m, l1, l1 + i, fn1, ge1, fpnf + fpf[l1 + i], gt[l1 + i], base_cost, t_full, fp_lim,
+                fn_lim, bf, bi);
+    for (; i < tot; i += P)
+      eval_cell(j, m, l2, l2 + (i - len1), fn2, ge2, fpnf + fpf[l2 + (i - len1)], gt[l2 + (i - len1)],
+                base_cost, t_full, fp_lim, fn_lim, bf, bi);
   }
   sf[threadIdx.x] = bf;
   si[threadIdx.x] = bi;
@@ -457,7 +494,7 @@ __global__ void sweep_final_kernel(const EvalOut* blocks, int nblocks, Tables T,
 size_t sweep_ws_bytes(int32_t nd, int32_t m) {
   size_t tabs = (size_t)nd * 3 + (size_t)nd * m * 4;
   size_t suffix = (size_t)(nd + 1) * (2 * (2 * (size_t)m + 1)) + (size_t)(nd + 1) * 2;
-  size_t blocks = (size_t)nd * ((m + 255) / 256);
+  size_t blocks = (size_t)nd * eval_ctas_per_row(m);
   return 256 + (tabs + suffix) * 8 + blocks * sizeof(EvalOut) + sizeof(noscope_sweep_best) + 256;
 }
 
@@ -515,7 +552,7 @@ noscope_status launch_sweep(int32_t phase, const double* s, const float* z, cons
     }
     unsigned long long* G = take((size_t)(nd + 1) * 2 * L.B);
     unsigned long long* Pn = take((size_t)(nd + 1) * 2);
-    const int nblocks = nd * ((m + 255) / 256);   // one CTA per (j, 256-wide slice of l)
+    const int nblocks = nd * eval_ctas_per_row(m);
     EvalOut* bo = reinterpret_cast<EvalOut*>(p);
     p += (size_t)nblocks * sizeof(EvalOut);
     p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
