@@ -195,10 +195,15 @@ def _best_by_tables(T, timing, fpl, fnl):
     return best
 
 
-@pytest.mark.parametrize("nd,m,n", [(40, 2048, 3000), (2000, 8, 5000)])
+@pytest.mark.parametrize("nd,m,n", [(40, 2048, 3000), (2000, 8, 5000),
+                                    (3, 1, 2000), (7, 33, 4000), (5, 63, 4000), (4, 1001, 3000),
+                                    (3, 1024, 3000)])
 def test_sweep_candidate_limits(nd, m, n):
     """m = 2048 (the largest accepted candidate count: phase 2's per-delta tables
-    use 164 KB of shared memory) and nd = 2,000 (the d-suffix pass is O(nd*m))."""
+    use 164 KB of shared memory) and nd = 2,000 (the d-suffix pass is O(nd*m)); and
+    the evaluation's work split (row pairs {l, m-1-l} dealt to P = (m+1)//32 lanes,
+    1..32): one candidate, odd m (a self-paired middle row) with P = 1, 2 and 31, even
+    m with P = 32."""
     nsm = ns()
     s, z, y, a, _, _ = sg.random_sweep_records(n, 77)
     delta = np.linspace(-7.0, 7.0, nd)                          # distinct, sorted
@@ -217,7 +222,13 @@ def test_sweep_candidate_limits(nd, m, n):
     for k in ("FPf", "FNf", "GE", "GT"):
         assert np.array_equal(tabs[k].reshape(nd, m), T[k]), k
     key = _best_by_tables(T, timing, fpl, fnl)
-    assert key is not None and code == 0
+    if key is None:   # no feasible triple (m = 1): the least-violating one, from the oracle's O9
+        _, best_o = O.sweep(s, z, y, a, delta, u, timing, fpl, fnl)
+        assert code == 7 and not best_o["feasible"]
+        assert (best["j"], best["l"], best["h"], best["cost_ps"]) == \
+            (best_o["j"], best_o["l"], best_o["h"], best_o["cost"])
+        return
+    assert code == 0
     assert (best["cost_ps"], best["uncertain"], best["j"], -best["l"], best["h"]) == key
 
 
@@ -288,3 +299,21 @@ def test_sweep_async_phase2_matches_sync():
     r, code2 = nsm.noscope_threshold_sweep(3, *args, h2, (1, 10, 1000), 200, 200, best_out=out)
     torch.cuda.synchronize()
     assert code2 == 0 and nsm.sweep_best_dict(out) == best_sync
+
+
+@pytest.mark.parametrize("m,seed", [(33, 1), (63, 2), (64, 3), (65, 4)])
+def test_sweep_eval_split_infeasible_and_feasible(m, seed):
+    """The least-violating (no feasible triple) and the feasible argmin at odd and even m
+    across the evaluation's work-split boundaries, against the oracle's O9 sweep."""
+    nsm = ns()
+    s, z, y, a, delta, _ = sg.random_sweep_records(2000, seed + 300, n_delta=9)
+    u = np.linspace(-4.0, 4.0, m).astype(np.float32)            # exactly m distinct candidates
+    hit = np.random.default_rng(seed).random(len(z)) < 0.2
+    z[hit] = np.random.default_rng(seed + 1).choice(u, int(hit.sum()))
+    for fpl, fnl in ((0, 0), (250, 250), (400, 400)):   # infeasible, feasible, feasible
+        T, best_o = O.sweep(s, z, y, a, delta, u, (3, 5, 7), fpl, fnl)
+        best, code, _, _ = _gpu_sweep(nsm, s, z, y, a, delta, u, (3, 5, 7), fpl, fnl)
+        assert (code == 7) == (not best_o["feasible"])
+        for k_g, k_o in [("j", "j"), ("l", "l"), ("h", "h"), ("fp", "fp"), ("fn", "fn"),
+                         ("uncertain", "U"), ("cost_ps", "cost")]:
+            assert best[k_g] == best_o[k_o], (k_g, best, best_o)
