@@ -115,7 +115,7 @@ sweep_hist_kernel(const double* __restrict__ s, const float* __restrict__ z,
   bool bad = false;
   const double ninf = __longlong_as_double(0xFFF0000000000000ll);
   // Each thread takes kU records per step (all loads issued before the searches,
-  // coalesced: record = chunk base + r * blockDim + tid), so the dependent
+  // record = chunk base + tid * kU + r), so the dependent
   // binary-search chains of independent records overlap.
   // The next step's records are prefetched into registers before the current
   // step's searches run (software pipelining: loads overlap the search work).
@@ -124,10 +124,29 @@ sweep_hist_kernel(const double* __restrict__ s, const float* __restrict__ z,
   double sv[kU], sn[kU];
   float zv[kU], zn[kU];
   uint32_t ya[kU], yn[kU];
+  // kU consecutive records per thread: with aligned columns, one 16-byte load per
+  // two s / four z and one 4-byte load of y and of a (a warp still reads contiguous
+  // runs); unaligned columns or the ragged end fall back to per-record loads.
+  const bool vec = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(z)) & 15) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(a)) & 3) == 0;
+  static_assert(kHistU == 4, "vector record loads assume 4 records per thread");
   auto load = [&](int64_t base, double (&sx)[kU], float (&zx)[kU], uint32_t (&yx)[kU]) {
+    const int64_t i0 = base + (int64_t)tid * kU;
+    if (vec && i0 + kU <= n) {
+      const double2 s01 = __ldcs(reinterpret_cast<const double2*>(s + i0));
+      const double2 s23 = __ldcs(reinterpret_cast<const double2*>(s + i0 + 2));
+      const float4 z4 = __ldcs(reinterpret_cast<const float4*>(z + i0));
+      const uint32_t y4 = __ldcs(reinterpret_cast<const unsigned int*>(y + i0));
+      const uint32_t a4 = __ldcs(reinterpret_cast<const unsigned int*>(a + i0));
+      sx[0] = s01.x; sx[1] = s01.y; sx[2] = s23.x; sx[3] = s23.y;
+      zx[0] = z4.x; zx[1] = z4.y; zx[2] = z4.z; zx[3] = z4.w;
+#pragma unroll
+      for (int r = 0; r < kU; ++r) yx[r] = ((y4 >> (8 * r)) & 0xFFu) | (((a4 >> (8 * r)) & 0xFFu) << 8);
+      return;
+    }
 #pragma unroll
     for (int r = 0; r < kU; ++r) {
-      const int64_t i = base + (int64_t)r * blockDim.x + tid;
+      const int64_t i = i0 + r;
       if (i < n) {
         sx[r] = __ldcs(s + i);
         zx[r] = __ldcs(z + i);

@@ -317,3 +317,28 @@ def test_sweep_eval_split_infeasible_and_feasible(m, seed):
         for k_g, k_o in [("j", "j"), ("l", "l"), ("h", "h"), ("fp", "fp"), ("fn", "fn"),
                          ("uncertain", "U"), ("cost_ps", "cost")]:
             assert best[k_g] == best_o[k_o], (k_g, best, best_o)
+
+
+@pytest.mark.parametrize("off,n", [(0, 4099), (1, 4099), (2, 100003), (3, 5), (1, 1), (0, 3)])
+def test_sweep_hist_column_alignment(off, n):
+    """Phase 1 reads 4 consecutive records per thread with 16-byte (s, z) and 4-byte
+    (y, a) loads when every column is aligned, per-record loads otherwise and on the
+    ragged end: record columns starting `off` records into their buffers (views, as a
+    rank's unit slice of the flat record arrays) must give the oracle's tables."""
+    nsm = ns()
+    s, z, y, a, delta, u = sg.random_sweep_records(n + off, 900 + off, n_delta=9, m=8)
+    dev = "cuda"
+    T = lambda x, dt: torch.from_numpy(np.ascontiguousarray(x, dtype=dt)).to(dev)
+    sd, zd, yd, ad = T(s, np.float64), T(z, np.float32), T(y, np.uint8), T(a, np.uint8)
+    dd, uu = T(delta, np.float64), T(u, np.float32)
+    hist = torch.zeros(nsm.sweep_hist_words(len(delta), len(u)), dtype=torch.int64, device=dev)
+    nsm.noscope_threshold_sweep(1, sd[off:], zd[off:], yd[off:], ad[off:], dd, uu, hist)
+    nd, m = len(delta), len(u)
+    tabs = {k: torch.zeros(nd * (m if k in ("FPf", "FNf", "GE", "GT") else 1), dtype=torch.int64,
+                           device=dev) for k in ("F", "FPnf", "FNnf", "FPf", "FNf", "GE", "GT")}
+    nsm.noscope_threshold_sweep(2, None, None, None, None, dd, uu, hist, (1, 10, 1000), 0, 0, tables=tabs)
+    Tor = O.sweep_tables(s[off:], z[off:], y[off:], a[off:], delta, u)
+    for k in ("F", "FPnf", "FNnf"):
+        assert np.array_equal(tabs[k].cpu().numpy().astype(np.uint64), Tor[k]), k
+    for k in ("FPf", "FNf", "GE", "GT"):
+        assert np.array_equal(tabs[k].cpu().numpy().astype(np.uint64).reshape(nd, m), Tor[k]), k
