@@ -17,9 +17,17 @@
 namespace ns {
 
 // 1,024 threads x 4 records in flight per thread (1e9 records: 6.41 ms; 512 x 8: 7.59,
-// 1,024 x 2 / 5 / 6 / 8: 6.51 / 6.43 / 7.31 / 9.08, 768 x 4: 6.67, 512 x 16: 15.15)
-constexpr int kHistThreads = 1024;
-constexpr int kHistU = 4;
+// 1,024 x 2 / 5 / 6 / 8: 6.51 / 6.43 / 7.31 / 9.08, 768 x 4: 6.67, 512 x 16: 15.15);
+// with the vector record loads 5.91 ms (1,024 x 8: 7.08, 512 x 8: 6.41, 512 x 4: 6.82;
+// NS_HIST_T / NS_HIST_U override for such A/Bs, tools/gpu_hist_shape.sh)
+#ifndef NS_HIST_T
+#define NS_HIST_T 1024
+#endif
+#ifndef NS_HIST_U
+#define NS_HIST_U 4
+#endif
+constexpr int kHistThreads = NS_HIST_T;
+constexpr int kHistU = NS_HIST_U;
 constexpr int kMaxCand = 2048;
 
 struct HistLayout {
@@ -129,19 +137,23 @@ sweep_hist_kernel(const double* __restrict__ s, const float* __restrict__ z,
   // runs); unaligned columns or the ragged end fall back to per-record loads.
   const bool vec = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(z)) & 15) == 0 &&
                    ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(a)) & 3) == 0;
-  static_assert(kHistU == 4, "vector record loads assume 4 records per thread");
+  static_assert(kHistU % 4 == 0, "vector record loads take records in fours");
   auto load = [&](int64_t base, double (&sx)[kU], float (&zx)[kU], uint32_t (&yx)[kU]) {
     const int64_t i0 = base + (int64_t)tid * kU;
     if (vec && i0 + kU <= n) {
-      const double2 s01 = __ldcs(reinterpret_cast<const double2*>(s + i0));
-      const double2 s23 = __ldcs(reinterpret_cast<const double2*>(s + i0 + 2));
-      const float4 z4 = __ldcs(reinterpret_cast<const float4*>(z + i0));
-      const uint32_t y4 = __ldcs(reinterpret_cast<const unsigned int*>(y + i0));
-      const uint32_t a4 = __ldcs(reinterpret_cast<const unsigned int*>(a + i0));
-      sx[0] = s01.x; sx[1] = s01.y; sx[2] = s23.x; sx[3] = s23.y;
-      zx[0] = z4.x; zx[1] = z4.y; zx[2] = z4.z; zx[3] = z4.w;
 #pragma unroll
-      for (int r = 0; r < kU; ++r) yx[r] = ((y4 >> (8 * r)) & 0xFFu) | (((a4 >> (8 * r)) & 0xFFu) << 8);
+      for (int q = 0; q < kU / 4; ++q) {
+        const double2 s01 = __ldcs(reinterpret_cast<const double2*>(s + i0 + 4 * q));
+        const double2 s23 = __ldcs(reinterpret_cast<const double2*>(s + i0 + 4 * q + 2));
+        const float4 z4 = __ldcs(reinterpret_cast<const float4*>(z + i0 + 4 * q));
+        const uint32_t y4 = __ldcs(reinterpret_cast<const unsigned int*>(y + i0 + 4 * q));
+        const uint32_t a4 = __ldcs(reinterpret_cast<const unsigned int*>(a + i0 + 4 * q));
+        sx[4 * q] = s01.x; sx[4 * q + 1] = s01.y; sx[4 * q + 2] = s23.x; sx[4 * q + 3] = s23.y;
+        zx[4 * q] = z4.x; zx[4 * q + 1] = z4.y; zx[4 * q + 2] = z4.z; zx[4 * q + 3] = z4.w;
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          yx[4 * q + r] = ((y4 >> (8 * r)) & 0xFFu) | (((a4 >> (8 * r)) & 0xFFu) << 8);
+      }
       return;
     }
 #pragma unroll
