@@ -121,6 +121,7 @@ sweep_hist_kernel(const double* __restrict__ s, const float* __restrict__ z,
   __syncthreads();
   unsigned long long checked = 0;
   bool bad = false;
+  const uint32_t h2o = (uint32_t)L.h2, h1o = (uint32_t)L.h1;
   const double ninf = __longlong_as_double(0xFFF0000000000000ll);
   // Each thread takes kU records per step (all loads issued before the searches,
   // record = chunk base + tid * kU + r), so the dependent
@@ -209,8 +210,9 @@ sweep_hist_kernel(const double* __restrict__ s, const float* __restrict__ z,
       const int d = dj[r];
       const int lt = lj[r];
       const int b = 2 * lt + ((lt < m && uc[lt] == zi) ? 1 : 0);  // #{u<z} + #{u<=z}
-      const size_t w2 = L.h2 + ((size_t)d * L.B + b) * 2 + yi;
-      const size_t w1 = L.h1 + (size_t)d * 4 + ai * 2 + yi;
+      // 32-bit word indices: the histogram has < 2^30 words (nd < 65536, m <= 2048)
+      const uint32_t w2 = h2o + ((uint32_t)d * (uint32_t)L.B + (uint32_t)b) * 2u + (uint32_t)yi;
+      const uint32_t w1 = h1o + (uint32_t)d * 4u + (uint32_t)(ai * 2 + yi);
       // H1 is only ever read at (a, y) = (1, 0) and (0, 1) (the not-fired FP and
       // FN counts), so records with a == y skip that atomic (shared-memory
       // atomics are this kernel's throughput limit).
