@@ -90,7 +90,10 @@ NS_DEV int eytz_sorted_index(int i, int h) {
 }
 
 // Phase 1: block-privatised histogram in shared memory (u32), flushed to the
-// global u64 histogram with one atomic per nonzero bin.
+// global u64 histogram with one atomic per nonzero bin.  HD / HU: the search depths
+// fixed at compile time (fully unrolled searches; the kernel is issue-bound), 0 = the
+// runtime depths.
+template <int HD, int HU>
 __global__ void __launch_bounds__(kHistThreads, 1)
 sweep_hist_kernel(const double* __restrict__ s, const float* __restrict__ z,
                   const uint8_t* __restrict__ y, const uint8_t* __restrict__ a, int64_t n,
@@ -99,7 +102,7 @@ sweep_hist_kernel(const double* __restrict__ s, const float* __restrict__ z,
   extern __shared__ __align__(16) uint8_t smem[];
   HistLayout L(nd, m);
   const int pd = pow2_above(nd), pu = pow2_above(m);
-  const int hd = 31 - __clz(pd), hu = 31 - __clz(pu);
+  const int hd = HD ? HD : 31 - __clz(pd), hu = HU ? HU : 31 - __clz(pu);
   double* dt = reinterpret_cast<double*>(smem);            // [pd] BFS tree of the delta candidates
   float* ut = reinterpret_cast<float*>(dt + pd);            // [pu] BFS tree of the logit candidates
   float* uc = ut + pu;                                      // [pu] sorted logit candidates (equality test)
@@ -186,7 +189,7 @@ sweep_hist_kernel(const double* __restrict__ s, const float* __restrict__ z,
     int dj[kU], lj[kU];
 #pragma unroll
     for (int r = 0; r < kU; ++r) dj[r] = lj[r] = 0;
-    for (int lv = 0; lv < hd; ++lv) {
+    for (int lv = 0; lv < hd; ++lv) {   // constant trip count (fully unrolled) when HD != 0
 #pragma unroll
       for (int r = 0; r < kU; ++r) dj[r] = 2 * dj[r] + 1 + (dt[dj[r]] < sv[r] ? 1 : 0);
     }
@@ -547,12 +550,13 @@ noscope_status launch_sweep(int32_t phase, const double* s, const float* z, cons
       int privatised = priv <= 200 * 1024 ? 1 : 0;
       size_t use = privatised ? priv : smem;
       // set on every call: function attributes are per device context
-      NS_CUDA_TRY(cudaFuncSetAttribute(sweep_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)use));
+      // 100-candidate grids (the bench's, configs[3]) search 7 levels each
+      const bool d7 = pow2_above(nd) == 128 && pow2_above(m) == 128;
+      auto kern = d7 ? sweep_hist_kernel<7, 7> : sweep_hist_kernel<0, 0>;
+      NS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)use));
       int64_t want = (n + kHistThreads * 16 - 1) / (kHistThreads * 16);
       int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, kNumSMs));
-      sweep_hist_kernel<<<grid, kHistThreads, use, st>>>(s, z, y, a, n, delta, nd, u, m, hist,
-                                                         status, privatised);
+      kern<<<grid, kHistThreads, use, st>>>(s, z, y, a, n, delta, nd, u, m, hist, status, privatised);
       NS_LAUNCH_CHECK();
       count_launch();
     }
