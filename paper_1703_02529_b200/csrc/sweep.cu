@@ -550,9 +550,22 @@ noscope_status launch_sweep(int32_t phase, const double* s, const float* z, cons
       int privatised = priv <= 200 * 1024 ? 1 : 0;
       size_t use = privatised ? priv : smem;
       // set on every call: function attributes are per device context
-      // 100-candidate grids (the bench's, configs[3]) search 7 levels each
-      const bool d7 = pow2_above(nd) == 128 && pow2_above(m) == 128;
-      auto kern = d7 ? sweep_hist_kernel<7, 7> : sweep_hist_kernel<0, 0>;
+      // equal search depths 3..11 (8-2047 candidates on both axes; the bench's and
+      // configs[3]'s 100-candidate grids: 7) get a fully unrolled instantiation
+      const int hd = 31 - __builtin_clz(pow2_above(nd)), hu = 31 - __builtin_clz(pow2_above(m));
+      decltype(&sweep_hist_kernel<0, 0>) kern = sweep_hist_kernel<0, 0>;
+      switch (hd == hu ? hd : 0) {
+        case 3: kern = sweep_hist_kernel<3, 3>; break;
+        case 4: kern = sweep_hist_kernel<4, 4>; break;
+        case 5: kern = sweep_hist_kernel<5, 5>; break;
+        case 6: kern = sweep_hist_kernel<6, 6>; break;
+        case 7: kern = sweep_hist_kernel<7, 7>; break;
+        case 8: kern = sweep_hist_kernel<8, 8>; break;
+        case 9: kern = sweep_hist_kernel<9, 9>; break;
+        case 10: kern = sweep_hist_kernel<10, 10>; break;
+        case 11: kern = sweep_hist_kernel<11, 11>; break;
+        default: break;
+      }
       NS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)use));
       int64_t want = (n + kHistThreads * 16 - 1) / (kHistThreads * 16);
       int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, kNumSMs));

@@ -197,14 +197,16 @@ def _best_by_tables(T, timing, fpl, fnl):
 
 @pytest.mark.parametrize("nd,m,n", [(40, 2048, 3000), (2000, 8, 5000),
                                     (3, 1, 2000), (7, 33, 4000), (5, 63, 4000), (4, 1001, 3000),
-                                    (3, 1024, 3000), (100, 101, 20000), (64, 127, 5000), (127, 64, 5000)])
+                                    (3, 1024, 3000), (100, 101, 20000), (64, 127, 5000), (127, 64, 5000),
+                                    (200, 255, 5000), (7, 7, 3000), (1000, 1000, 3000)])
 def test_sweep_candidate_limits(nd, m, n):
     """m = 2048 (the largest accepted candidate count: phase 2's per-delta tables
     use 164 KB of shared memory) and nd = 2,000 (the d-suffix pass is O(nd*m)); and
     the evaluation's work split (row pairs {l, m-1-l} dealt to P = (m+1)//32 lanes,
     1..32): one candidate, odd m (a self-paired middle row) with P = 1, 2 and 31, even
-    m with P = 32; and the histogram's depth-7 instantiation (64 <= nd, m <= 127: the
-    100-candidate grids) at both ends of its range."""
+    m with P = 32; and the histogram's fixed-depth instantiations (equal depths 3..11:
+    depth 7 = 64..127 candidates, the 100-candidate grids, at both ends of its range;
+    depths 8, 3 and 10)."""
     nsm = ns()
     s, z, y, a, _, _ = sg.random_sweep_records(n, 77)
     delta = np.linspace(-7.0, 7.0, nd)                          # distinct, sorted
