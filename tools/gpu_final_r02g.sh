@@ -1,4 +1,4 @@
-# round-2 closing evidence: GPU suite, smoke, default bench (after the histogram vector loads, 32-bit indices and the depth-7 instantiation)
+# round-2 closing evidence: GPU suite, smoke, default bench (final round-2 code: histogram fixed-depth instantiations 3-11)
 python __graft_entry__.py > /dev/null
 timeout 2400 python -m pytest tests -m gpu -q --timeout 1500 -p no:cacheprovider -rf 2>&1 | tail -15 > gpurun_out/gpu_tests_final.log
 tail -3 gpurun_out/gpu_tests_final.log
